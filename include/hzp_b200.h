@@ -1,0 +1,260 @@
+/*
+ * hzp_b200.h — C-ABI of the B200-native AsyncHZP hot path.
+ *
+ * One shared library (paper_2510_20111_b200/libhzp_b200.so) exports these
+ * symbols.  Plain C types only (no torch, no C++); every call returns an
+ * int status (HZP_OK or an HZP_ERR_* code mirroring the reference's C++
+ * exception codes) and hzp_last_error() gives a thread-local message.
+ *
+ * The reference (arxiv 2510.20111 artifact, /root/reference/proj) has no C
+ * ABI; it is a C++ namespace API.  Each entry point below cites the
+ * reference interface it replaces.  The C++ drop-in (same names/types as the
+ * reference) lives in paper_2510_20111_b200/csrc/hzp/{config,sched}.hpp and
+ * is what these wrappers call for the host-side pieces.
+ */
+#ifndef HZP_B200_H_
+#define HZP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+/* Mirrors ValidationError::Code (include/hzp/config.hpp:68-77),
+ * CollectiveError::Code (include/hzp/collective.hpp:18-27),
+ * SchedError::Code (include/hzp/sched.hpp:55-64), MemoryError
+ * (include/hzp/memory.hpp:26-35) and EquivalenceFailure (train.hpp:94-98). */
+enum {
+  HZP_OK = 0,
+  HZP_ERR_NON_DIVISIBLE = 1,     /* ValidationError::NonDivisible */
+  HZP_ERR_EMPTY_MODEL = 2,       /* ValidationError::EmptyModel */
+  HZP_ERR_BAD_FIELD = 3,         /* ValidationError::BadField */
+  HZP_ERR_SHAPE_MISMATCH = 4,    /* CollectiveError::ShapeMismatch */
+  HZP_ERR_DTYPE_UNSUPPORTED = 5, /* CollectiveError::DTypeUnsupported */
+  HZP_ERR_INVALID_POLICY = 6,    /* SchedError::InvalidPolicy */
+  HZP_ERR_DEADLOCK = 7,          /* SchedError::DeadlockDetected */
+  HZP_ERR_MEMORY = 8,            /* MemoryError / device allocation */
+  HZP_ERR_EQUIVALENCE = 9,       /* EquivalenceFailure */
+  HZP_ERR_CUDA = 10,             /* any CUDA runtime / driver failure */
+  HZP_ERR_ARG = 11               /* null pointer / out-of-range argument */
+};
+
+const char* hzp_last_error(void);
+const char* hzp_version(void);
+
+/* ---- domain (include/hzp/config.hpp:16-66) ------------------------------ */
+typedef struct {
+  int dp, z1, z2, z3; /* ParallelConfig: data-parallel size, optimizer /   */
+  int pp, vpp, cp, tp; /* gradient / parameter sharding group sizes, outer */
+} hzp_parallel;        /* dims (pp, vpp, cp, tp >= 1)                       */
+
+typedef struct {
+  int64_t num_layers, params_per_layer, embedding_params;
+  int64_t seq_len, micro_batch_size, num_microbatches;
+  double flops_per_token_per_layer;
+  int64_t hidden_size;
+} hzp_model_spec; /* ModelSpec (config.hpp:16-31) */
+
+typedef struct {
+  int num_nodes, ranks_per_node;
+  double intra_bw, inter_bw, intra_latency, inter_latency;
+  double device_flops;
+} hzp_cost; /* Topology (config.hpp:44-54) + CostModel::device_flops (collective.hpp:63-67) */
+
+enum { HZP_GROUP_Z1 = 0, HZP_GROUP_Z2 = 1, HZP_GROUP_Z3 = 2, HZP_GROUP_DZP = 3 };
+
+/* shard_elems (include/hzp/memory.hpp:37-38): ceil(n / parts). */
+int64_t hzp_shard_elems(int64_t n, int64_t parts);
+
+/* validate_config (include/hzp/config.hpp:89-91). */
+int hzp_validate(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* topo);
+
+/* build_process_groups (include/hzp/config.hpp:96-97) for one GroupKind:
+ * writes groups back to back into ranks_out (cap ints), *group_size and
+ * *n_groups.  Ranks of group g are ranks_out[g*group_size ...]. */
+int hzp_groups(const hzp_parallel* par, int kind, int* ranks_out, int cap, int* group_size,
+               int* n_groups);
+
+/* ---- scheduler (include/hzp/sched.hpp:20-137) --------------------------- */
+/* TaskKind order matches sched.hpp:20-29. */
+enum {
+  HZP_TASK_FWD = 0, HZP_TASK_BWD = 1, HZP_TASK_FWD_RECOMPUTE = 2, HZP_TASK_AG_PARAM = 3,
+  HZP_TASK_RS_GRAD = 4, HZP_TASK_AR_DZP = 5, HZP_TASK_OPT_STEP = 6, HZP_TASK_AG_POST = 7
+};
+enum { HZP_STREAM_COMPUTE = 0, HZP_STREAM_AG = 1, HZP_STREAM_RS = 2 };
+enum { HZP_MODE_VANILLA = 0, HZP_MODE_ASYNC = 1 };
+
+typedef struct hzp_graph hzp_graph;
+
+typedef struct {
+  int id, kind, layer, microbatch, virtual_stage, pass;
+  double duration;
+  int64_t bytes;
+  int num_deps;
+  const int* deps; /* valid until the graph is destroyed */
+} hzp_task;        /* Task (sched.hpp:35-45) */
+
+/* build_task_graph (sched.hpp:90-91).  defer_rs / rank mirror GraphPolicy
+ * (sched.hpp:66-76) with the default one-F-one-B-per-microbatch order. */
+int hzp_graph_build(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* cost,
+                    int defer_rs, int rank, hzp_graph** out);
+void hzp_graph_destroy(hzp_graph* g);
+int hzp_graph_size(const hzp_graph* g);
+int hzp_graph_task(const hzp_graph* g, int i, hzp_task* out);
+int64_t hzp_graph_ag_slot_bytes(const hzp_graph* g); /* TaskGraph::ag_slot_bytes */
+int64_t hzp_graph_grad_buf_bytes(const hzp_graph* g); /* TaskGraph::grad_buf_bytes */
+
+/* derive_prelaunch_depth (sched.hpp:110-112). */
+int hzp_derive_prelaunch_depth(const hzp_graph* g, int64_t free_budget);
+
+/* make_pools (sched.hpp:108): AG pool = depth slots of ag_slot_bytes,
+ * RS pool = rs_slots slots of grad_buf_bytes. */
+typedef struct {
+  int64_t capacity;
+  int slot_count;
+  int64_t slot_bytes;
+} hzp_pool;
+int hzp_make_pools(const hzp_graph* g, int depth, int rs_slots, hzp_pool* ag, hzp_pool* rs);
+
+/* simulate (sched.hpp:137): start/end per task (arrays of hzp_graph_size). */
+typedef struct {
+  double makespan, compute_idle, compute_busy;
+} hzp_sim_summary;
+int hzp_simulate(const hzp_graph* g, int depth, int rs_slots, int mode, double* start,
+                 double* end, hzp_sim_summary* summary);
+
+/* LaunchPlan (new): the per-task issue record the device executor follows.
+ * slot = k % depth for the k-th AG-pool task, k % rs_slots for the k-th RS
+ * task, -1 otherwise; ring_wait = the task whose completion frees that slot
+ * (sched.cpp:285-309 rule), -1 if none. */
+typedef struct {
+  int id, kind, layer, microbatch, stream, slot, ring_wait;
+  int num_waits;
+  const int* waits; /* deps + ring_wait; valid until the graph is destroyed */
+} hzp_plan_entry;
+int hzp_plan_entry_get(const hzp_graph* g, int depth, int rs_slots, int i, hzp_plan_entry* out);
+
+/* ---- device engine ------------------------------------------------------ */
+/* Model families.  HZP_MODEL_MLP is the reference's model (tanh MLP, loss
+ * sum(y^2)/(2*B*out), flat W|b layout per layer, train.cpp:29-150).
+ * HZP_MODEL_GPT is the GPU-scale decoder (pre-LN, GELU MLP, causal MHA,
+ * untied LM head) whose flat layout is documented in DESIGN.md. */
+enum { HZP_MODEL_MLP = 0, HZP_MODEL_GPT = 1 };
+enum { HZP_PREC_FP32 = 0, HZP_PREC_BF16 = 1 };
+
+typedef struct {
+  int model;          /* HZP_MODEL_* */
+  int precision;      /* HZP_PREC_FP32: fp32 working copy + fp32 GEMMs (parity tier B);
+                         HZP_PREC_BF16: bf16 working copy + tcgen05 bf16 GEMMs */
+  int num_dims;       /* MLP: dims[0..num_dims-1] (input width first) */
+  int dims[32];
+  int gpt_layers, gpt_hidden, gpt_heads, gpt_ffn, gpt_vocab, gpt_seq;
+  int batch;          /* MLP: rows per microbatch; GPT: sequences per microbatch */
+  int num_microbatches;
+  hzp_parallel par;
+  int prelaunch_depth; /* AG ring slots (reference default 2, hzpsim.cpp:95) */
+  int rs_slots;        /* RS ring slots (reference default 1, hzpsim.cpp:96) */
+  int wgrad_slots;     /* physical gradient buffers peers pull from (>= 2) */
+  int mode;            /* HZP_MODE_ASYNC or HZP_MODE_VANILLA */
+  double lr, beta1, beta2, eps; /* AdamParams (train.hpp:22-27) */
+  double grad_scale;   /* RS cast/scale factor; 1.0 = reference semantics */
+  int device;          /* CUDA ordinal this process drives */
+  int my_rank;         /* global rank driven by this process, or -1 = emulate all
+                          dp ranks on `device` (single-process parity mode) */
+  int timeline;        /* record per-task CUDA events (measured timeline) */
+} hzp_engine_config;
+
+typedef struct hzp_ctx hzp_ctx;
+
+int hzp_ctx_create(const hzp_engine_config* cfg, hzp_ctx** out);
+void hzp_ctx_destroy(hzp_ctx* ctx);
+
+/* Layout facts of the ctx's model: P, s1, s2, s3, layer count and each
+ * layer's [offset, size) in the flat vector (layer_views, train.cpp:42-53). */
+int hzp_ctx_layout(const hzp_ctx* ctx, int64_t* P, int64_t* s1, int64_t* s2, int64_t* s3,
+                   int* num_layers);
+int hzp_ctx_layer_range(const hzp_ctx* ctx, int layer, int64_t* offset, int64_t* size);
+
+/* Multi-process P2P wiring (one process per GPU): export this rank's
+ * peer-visible arena as an opaque handle, then import every peer's. */
+int hzp_ctx_ipc_handle(hzp_ctx* ctx, void* buf, size_t* len);
+int hzp_ctx_open_peers(hzp_ctx* ctx, const void* handles, size_t handle_len, int n_ranks);
+
+/* ShardedState mirror (train.hpp:73-83).  field: 0 param_shard (working
+ * dtype: fp32 or bf16 bits), 1 grad_shard (fp32), 2 master, 3 momentum,
+ * 4 variance (fp32).  Host buffers; rank must be driven by this ctx. */
+enum { HZP_F_PARAM = 0, HZP_F_GRAD = 1, HZP_F_MASTER = 2, HZP_F_MOM = 3, HZP_F_VAR = 4 };
+int hzp_state_upload(hzp_ctx* ctx, int rank, int field, const void* host, int64_t n);
+int hzp_state_download(hzp_ctx* ctx, int rank, int field, void* host, int64_t n);
+int hzp_state_set_step(hzp_ctx* ctx, int rank, int adam_step);
+/* shard_init (train.cpp:224-253) done on the host by the caller and
+ * uploaded, or seeded on the device for throughput runs: */
+int hzp_state_init_random(hzp_ctx* ctx, uint64_t seed, double scale);
+
+/* train_step_hzp (train.hpp:114-119) on the device, walking the LaunchPlan.
+ * inputs: MLP → fp32 [local_ranks][num_mb][batch][dims0];
+ *         GPT → int32 token ids [local_ranks][num_mb][batch][seq+1].
+ * inputs_on_device != 0: `inputs` is a device pointer; else a host pointer
+ * (copied H2D on the ctx's stream inside the step).  losses_out
+ * (host, [local_ranks], optional) receives per-rank summed losses (D2H). */
+int hzp_step(hzp_ctx* ctx, const void* inputs, int inputs_on_device, float* losses_out);
+int hzp_sync(hzp_ctx* ctx);
+
+/* Launch log: the kernels issued by the last step, in issue order, each with
+ * the reference task ids it covers (SURVEY §7.3-8 parity of launch order). */
+typedef struct {
+  int task_id;   /* reference task id (first covered) */
+  int kind;      /* HZP_TASK_* */
+  int layer, microbatch, stream, slot;
+  int covered_first, covered_last; /* fused kernels cover a task id range */
+} hzp_launch_rec;
+int hzp_launch_log(const hzp_ctx* ctx, hzp_launch_rec* out, int cap, int* n);
+
+/* Measured timeline of the last step (requires cfg.timeline): per task
+ * start/end in ms relative to step start, and the compute-stream idle
+ * (= last compute end - sum compute busy, sched.cpp:341-350). */
+int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, int* n,
+                 double* compute_idle_ms, double* compute_busy_ms, double* makespan_ms);
+
+/* Extra device work counters (kernels launched by the last step). */
+int hzp_ctx_launch_count(const hzp_ctx* ctx, int64_t* kernels);
+
+/* ---- kernel-level entry points (single ctx, its streams) ---------------- */
+/* Layer-wise P2P-pull all-gather of layer `layer` into AG ring slot `slot`
+ * for every rank the ctx drives (collective.cpp:44-67 semantics). */
+int hzp_ag_layer(hzp_ctx* ctx, int layer, int slot);
+/* Read back one rank's AG slot (working dtype bytes, layer size elems). */
+int hzp_ag_slot_download(hzp_ctx* ctx, int rank, int slot, void* host, int64_t n);
+/* Upload a rank's unsharded gradient of `layer` into its gradient ring
+ * buffer `wslot` (fp32 host data, cast to the wire dtype). */
+int hzp_wgrad_upload(hzp_ctx* ctx, int rank, int layer, int wslot, const float* host, int64_t n);
+/* P2P-pull reduce-scatter of `layer` from ring buffer `wslot` into the Z2
+ * grad shards, ascending-rank fp32 sum, cast/scale, += (collective.cpp:69-97
+ * then train.cpp:313-322). */
+int hzp_rs_layer(hzp_ctx* ctx, int layer, int wslot);
+/* Fused Z1 stage: pull-reduce across DZP replicas (collective.cpp:99-115),
+ * Adam (train.cpp:171-189) on the Z1 chunk, round-to-bf16 and P2P-store the
+ * working copy into the Z3 owners (train.cpp:361-379).  grad_out (device
+ * or NULL) optionally receives each driven rank's reduced Z1 gradient chunk. */
+int hzp_z1_adam_step(hzp_ctx* ctx);
+int hzp_zero_grads(hzp_ctx* ctx);
+/* Device-wide barrier over all dp ranks (no-op in emulation mode). */
+int hzp_barrier(hzp_ctx* ctx);
+
+/* Standalone tcgen05 GEMM for tests and benches: C[M,N] = sum_k A[m,k] B[n,k]
+ * with A, B bf16; a_mn / b_mn select MN-major storage (A[k*lda+m],
+ * B[k*ldb+n]) instead of K-major (A[m*lda+k], B[n*ldb+k]).  epi: 0 store
+ * bf16, 1 store fp32, 2 accumulate into fp32 C. stream = cudaStream_t. */
+int hzp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda, int ldb,
+                  int ldc, int a_mn, int b_mn, int epi, void* stream);
+/* Same contract, fp32 operands on the CUDA cores (fp32 parity tier). */
+int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, int lda,
+                 int ldb, int ldc, int a_mn, int b_mn, int epi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HZP_B200_H_ */

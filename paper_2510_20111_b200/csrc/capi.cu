@@ -1,0 +1,578 @@
+// C-ABI of libhzp_b200.so (declared in include/hzp_b200.h).  Thin marshalling
+// over the C++ drop-in (hzp/config.hpp, hzp/sched.hpp) and the device engine;
+// C++ exceptions never cross this boundary: they become HZP_ERR_* codes with
+// a thread-local message (hzp_last_error).
+#include <cstring>
+#include <string>
+
+#include "engine/engine.hpp"
+#include "engine/gemm.cuh"
+#include "hzp_b200.h"
+
+using namespace hzp;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HZP_OK;
+  } catch (const ValidationError& e) {
+    g_err = e.what();
+    return 1 + static_cast<int>(e.code());
+  } catch (const SchedError& e) {
+    g_err = e.what();
+    return e.code() == SchedError::Code::InvalidPolicy ? HZP_ERR_INVALID_POLICY : HZP_ERR_DEADLOCK;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return HZP_ERR_CUDA;
+  } catch (const std::bad_alloc& e) {
+    g_err = e.what();
+    return HZP_ERR_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HZP_ERR_ARG;
+  }
+}
+
+ParallelConfig to_cfg(const hzp_parallel* p) {
+  ParallelConfig c;
+  c.dp = p->dp;
+  c.z1 = p->z1;
+  c.z2 = p->z2;
+  c.z3 = p->z3;
+  c.pp = p->pp > 0 ? p->pp : 1;
+  c.vpp = p->vpp > 0 ? p->vpp : 1;
+  c.cp = p->cp > 0 ? p->cp : 1;
+  c.tp = p->tp > 0 ? p->tp : 1;
+  return c;
+}
+
+ModelSpec to_spec(const hzp_model_spec* s) {
+  ModelSpec m;
+  m.num_layers = s->num_layers;
+  m.params_per_layer = s->params_per_layer;
+  m.embedding_params = s->embedding_params;
+  m.seq_len = s->seq_len;
+  m.micro_batch_size = s->micro_batch_size;
+  m.num_microbatches = s->num_microbatches;
+  m.flops_per_token_per_layer = s->flops_per_token_per_layer;
+  m.hidden_size = s->hidden_size;
+  return m;
+}
+
+Topology to_topo(const hzp_cost* c) {
+  Topology t;
+  t.num_nodes = c->num_nodes;
+  t.ranks_per_node = c->ranks_per_node;
+  t.intra_bw = c->intra_bw;
+  t.inter_bw = c->inter_bw;
+  t.intra_latency = c->intra_latency;
+  t.inter_latency = c->inter_latency;
+  return t;
+}
+
+}  // namespace
+
+struct hzp_graph {
+  TaskGraph g;
+  // LaunchPlans cached per (depth, rs_slots)
+  int plan_depth = -1, plan_rs = -1;
+  LaunchPlan plan;
+};
+
+struct hzp_ctx {
+  Engine* e = nullptr;
+};
+
+extern "C" {
+
+const char* hzp_last_error(void) { return g_err.c_str(); }
+const char* hzp_version(void) { return "hzp-b200 0.1 (sm_100a)"; }
+
+int64_t hzp_shard_elems(int64_t n, int64_t parts) { return shard_elems(n, parts); }
+
+int hzp_validate(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* topo) {
+  if (!spec || !par || !topo) return HZP_ERR_ARG;
+  return guarded([&] { validate_config(to_spec(spec), to_cfg(par), to_topo(topo)); });
+}
+
+int hzp_groups(const hzp_parallel* par, int kind, int* ranks_out, int cap, int* group_size,
+               int* n_groups) {
+  if (!par || !ranks_out || !group_size || !n_groups) return HZP_ERR_ARG;
+  return guarded([&] {
+    Topology t;
+    t.ranks_per_node = par->dp * (par->pp > 0 ? par->pp : 1) * (par->cp > 0 ? par->cp : 1) *
+                       (par->tp > 0 ? par->tp : 1);
+    const GroupMap m = build_process_groups(to_cfg(par), t);
+    static const GroupKind kinds[] = {GroupKind::Z1, GroupKind::Z2, GroupKind::Z3, GroupKind::DzpReplica};
+    if (kind < 0 || kind > 3) throw std::invalid_argument("bad group kind");
+    const auto& gs = m.at(kinds[kind]);
+    int k = 0;
+    for (const auto& g : gs)
+      for (int r : g.ranks) {
+        if (k >= cap) throw std::invalid_argument("ranks_out too small");
+        ranks_out[k++] = r;
+      }
+    *n_groups = static_cast<int>(gs.size());
+    *group_size = gs.empty() ? 0 : gs.front().size();
+  });
+}
+
+int hzp_graph_build(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* cost,
+                    int defer_rs, int rank, hzp_graph** out) {
+  if (!spec || !par || !cost || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    CostModel cm;
+    cm.topo = to_topo(cost);
+    cm.device_flops = cost->device_flops;
+    GraphPolicy pol;
+    pol.defer_rs = defer_rs != 0;
+    pol.rank = rank;
+    auto* g = new hzp_graph();
+    try {
+      g->g = build_task_graph(to_spec(spec), to_cfg(par), cm, pol);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+void hzp_graph_destroy(hzp_graph* g) { delete g; }
+int hzp_graph_size(const hzp_graph* g) { return g ? static_cast<int>(g->g.tasks.size()) : 0; }
+int64_t hzp_graph_ag_slot_bytes(const hzp_graph* g) { return g ? g->g.ag_slot_bytes : 0; }
+int64_t hzp_graph_grad_buf_bytes(const hzp_graph* g) { return g ? g->g.grad_buf_bytes : 0; }
+
+int hzp_graph_task(const hzp_graph* g, int i, hzp_task* out) {
+  if (!g || !out || i < 0 || i >= static_cast<int>(g->g.tasks.size())) return HZP_ERR_ARG;
+  const Task& t = g->g.tasks[i];
+  out->id = t.id;
+  out->kind = static_cast<int>(t.kind);
+  out->layer = t.layer;
+  out->microbatch = t.microbatch;
+  out->virtual_stage = t.virtual_stage;
+  out->pass = static_cast<int>(t.pass);
+  out->duration = t.duration;
+  out->bytes = t.bytes;
+  out->num_deps = static_cast<int>(t.deps.size());
+  out->deps = t.deps.data();
+  return HZP_OK;
+}
+
+int hzp_derive_prelaunch_depth(const hzp_graph* g, int64_t free_budget) {
+  return g ? derive_prelaunch_depth(g->g, free_budget) : 1;
+}
+
+int hzp_make_pools(const hzp_graph* g, int depth, int rs_slots, hzp_pool* ag, hzp_pool* rs) {
+  if (!g || !ag || !rs) return HZP_ERR_ARG;
+  const PoolSet p = make_pools(g->g, depth, rs_slots);
+  *ag = {p.ag.capacity, p.ag.slot_count, p.ag.slot_bytes};
+  *rs = {p.rs.capacity, p.rs.slot_count, p.rs.slot_bytes};
+  return HZP_OK;
+}
+
+int hzp_simulate(const hzp_graph* g, int depth, int rs_slots, int mode, double* start,
+                 double* end, hzp_sim_summary* summary) {
+  if (!g) return HZP_ERR_ARG;
+  return guarded([&] {
+    const Timeline tl = simulate(g->g, make_pools(g->g, depth, rs_slots),
+                                 mode == HZP_MODE_VANILLA ? SchedMode::Vanilla : SchedMode::Async);
+    for (size_t i = 0; i < tl.entries.size(); ++i) {
+      if (start) start[i] = tl.entries[i].start;
+      if (end) end[i] = tl.entries[i].end;
+    }
+    if (summary) *summary = {tl.makespan, tl.compute_idle, tl.compute_busy};
+  });
+}
+
+int hzp_plan_entry_get(const hzp_graph* cg, int depth, int rs_slots, int i, hzp_plan_entry* out) {
+  auto* g = const_cast<hzp_graph*>(cg);
+  if (!g || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    if (g->plan_depth != depth || g->plan_rs != rs_slots) {
+      g->plan = build_launch_plan(g->g, make_pools(g->g, depth, rs_slots));
+      g->plan_depth = depth;
+      g->plan_rs = rs_slots;
+    }
+    if (i < 0 || i >= static_cast<int>(g->plan.entries.size())) throw std::invalid_argument("index");
+    const PlanEntry& e = g->plan.entries[i];
+    out->id = e.id;
+    out->kind = static_cast<int>(e.kind);
+    out->layer = e.layer;
+    out->microbatch = e.microbatch;
+    out->stream = static_cast<int>(e.stream);
+    out->slot = e.slot;
+    out->ring_wait = e.ring_wait;
+    out->num_waits = static_cast<int>(e.waits.size());
+    out->waits = e.waits.data();
+  });
+}
+
+// ---- engine ---------------------------------------------------------------
+int hzp_ctx_create(const hzp_engine_config* cfg, hzp_ctx** out) {
+  if (!cfg || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    auto* c = new hzp_ctx();
+    try {
+      c->e = new Engine(*cfg);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void hzp_ctx_destroy(hzp_ctx* ctx) {
+  if (!ctx) return;
+  delete ctx->e;
+  delete ctx;
+}
+
+int hzp_ctx_layout(const hzp_ctx* ctx, int64_t* P, int64_t* s1, int64_t* s2, int64_t* s3,
+                   int* num_layers) {
+  if (!ctx) return HZP_ERR_ARG;
+  const Engine& e = *ctx->e;
+  if (P) *P = e.geom.P;
+  if (s1) *s1 = e.geom.s1;
+  if (s2) *s2 = e.geom.s2;
+  if (s3) *s3 = e.geom.s3;
+  if (num_layers) *num_layers = static_cast<int>(e.layers.size());
+  return HZP_OK;
+}
+
+int hzp_ctx_layer_range(const hzp_ctx* ctx, int layer, int64_t* offset, int64_t* size) {
+  if (!ctx || layer < 0 || layer >= static_cast<int>(ctx->e->layers.size())) return HZP_ERR_ARG;
+  if (offset) *offset = ctx->e->layers[layer].off;
+  if (size) *size = ctx->e->layers[layer].size;
+  return HZP_OK;
+}
+
+int hzp_ctx_ipc_handle(hzp_ctx* ctx, void* buf, size_t* len) {
+  if (!ctx || !len) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    if (e.emulate) throw std::invalid_argument("emulation ctx has no IPC handle");
+    if (!buf || *len < sizeof(cudaIpcMemHandle_t)) {
+      *len = sizeof(cudaIpcMemHandle_t);
+      throw std::invalid_argument("buffer too small");
+    }
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    cudaIpcMemHandle_t h;
+    HZP_CUDA(cudaIpcGetMemHandle(&h, e.arenas[e.cfg.my_rank].base));
+    std::memcpy(buf, &h, sizeof(h));
+    *len = sizeof(h);
+  });
+}
+
+int hzp_ctx_open_peers(hzp_ctx* ctx, const void* handles, size_t handle_len, int n_ranks) {
+  if (!ctx || !handles) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    if (e.emulate) return;
+    if (n_ranks != e.cfg.par.dp || handle_len != sizeof(cudaIpcMemHandle_t))
+      throw std::invalid_argument("need one cudaIpcMemHandle_t per dp rank");
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    const Arena& mine = e.arenas[e.cfg.my_rank];
+    const size_t p_off = 0;
+    const size_t g_off = static_cast<char*>(static_cast<void*>(mine.grad)) - static_cast<char*>(mine.base);
+    const size_t w_off = mine.wgrad ? static_cast<char*>(mine.wgrad) - static_cast<char*>(mine.base) : 0;
+    const size_t f_off = reinterpret_cast<char*>(mine.flags) - static_cast<char*>(mine.base);
+    for (int r = 0; r < n_ranks; ++r) {
+      if (r == e.cfg.my_rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + r * handle_len, sizeof(h));
+      void* p = nullptr;
+      HZP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      Arena& a = e.arenas[r];
+      a.base = p;
+      a.owned = false;
+      a.bytes = mine.bytes;
+      a.param = static_cast<char*>(p) + p_off;
+      a.grad = reinterpret_cast<float*>(static_cast<char*>(p) + g_off);
+      a.wgrad = mine.wgrad ? static_cast<char*>(p) + w_off : nullptr;
+      a.flags = reinterpret_cast<uint64_t*>(static_cast<char*>(p) + f_off);
+      e.table.param[r] = a.param;
+      e.table.grad[r] = a.grad;
+      e.table.wgrad[r] = a.wgrad;
+      e.table.flags[r] = a.flags;
+    }
+    HZP_CUDA(cudaMemcpy(e.dtable, &e.table, sizeof(RankTable), cudaMemcpyHostToDevice));
+    e.peers_open = true;
+  });
+}
+
+static void* field_ptr(Engine& e, int li, int field, size_t* elem, int64_t* count) {
+  const int r = e.locals[li].rank;
+  switch (field) {
+    case HZP_F_PARAM: *elem = e.bf16 ? 2 : 4; *count = e.geom.s3; return e.arenas[r].param;
+    case HZP_F_GRAD: *elem = 4; *count = e.geom.s2; return e.arenas[r].grad;
+    case HZP_F_MASTER: *elem = 4; *count = e.geom.s1; return e.locals[li].master;
+    case HZP_F_MOM: *elem = 4; *count = e.geom.s1; return e.locals[li].mom;
+    case HZP_F_VAR: *elem = 4; *count = e.geom.s1; return e.locals[li].var;
+    default: throw std::invalid_argument("bad field");
+  }
+}
+
+int hzp_state_upload(hzp_ctx* ctx, int rank, int field, const void* host, int64_t n) {
+  if (!ctx || !host) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    const int li = e.local_index(rank);
+    if (li < 0) throw std::invalid_argument("rank not driven by this ctx");
+    size_t es;
+    int64_t cnt;
+    void* p = field_ptr(e, li, field, &es, &cnt);
+    if (n != cnt) throw std::invalid_argument("element count mismatch");
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    HZP_CUDA(cudaMemcpy(p, host, size_t(n) * es, cudaMemcpyHostToDevice));
+  });
+}
+
+int hzp_state_download(hzp_ctx* ctx, int rank, int field, void* host, int64_t n) {
+  if (!ctx || !host) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    const int li = e.local_index(rank);
+    if (li < 0) throw std::invalid_argument("rank not driven by this ctx");
+    size_t es;
+    int64_t cnt;
+    void* p = field_ptr(e, li, field, &es, &cnt);
+    if (n != cnt) throw std::invalid_argument("element count mismatch");
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    HZP_CUDA(cudaDeviceSynchronize());
+    HZP_CUDA(cudaMemcpy(host, p, size_t(n) * es, cudaMemcpyDeviceToHost));
+  });
+}
+
+int hzp_state_set_step(hzp_ctx* ctx, int rank, int adam_step) {
+  if (!ctx) return HZP_ERR_ARG;
+  const int li = ctx->e->local_index(rank);
+  if (li < 0) return HZP_ERR_ARG;
+  ctx->e->locals[li].adam_step = adam_step;
+  return HZP_OK;
+}
+
+namespace {
+__device__ __forceinline__ float hash_uniform(uint64_t e, uint64_t seed) {
+  uint64_t x = e * 0x9E3779B97F4A7C15ull ^ seed;
+  x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 33;
+  return float(x >> 40) * (1.0f / 16777216.0f) - 0.5f;
+}
+// Device-side shard_init for throughput runs: element e of the flat master
+// copy is hash_uniform(e) * scale; every rank materialises exactly its own
+// Z1 chunk and its Z3 working-copy segment (train.cpp:224-253 layout).
+__global__ void init_rank_kernel(void* param, int bf16, float* master, int64_t s1, int64_t s3,
+                                 int64_t i1, int64_t i3, int64_t P, uint64_t seed, float scale) {
+  const int64_t n = s1 > s3 ? s1 : s3;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if (i < s1) {
+      const int64_t e = i1 * s1 + i;
+      master[i] = e < P ? hash_uniform(e, seed) * scale : 0.f;
+    }
+    if (i < s3) {
+      const int64_t e = i3 * s3 + i;
+      const float w = e < P ? hash_uniform(e, seed) * scale : 0.f;
+      if (bf16) static_cast<uint16_t*>(param)[i] = f32_to_bf16_bits(w);
+      else static_cast<float*>(param)[i] = w;
+    }
+  }
+}
+}  // namespace
+
+int hzp_state_init_random(hzp_ctx* ctx, uint64_t seed, double scale) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    for (auto& l : e.locals) {
+      const int r = l.rank;
+      init_rank_kernel<<<4 * kNumSMs, 256>>>(e.arenas[r].param, e.bf16, l.master, e.geom.s1, e.geom.s3,
+                                              r % e.geom.z1, r % e.geom.z3, e.geom.P, seed, float(scale));
+      HZP_LAUNCH_CHECK();
+      HZP_CUDA(cudaMemset(l.mom, 0, size_t(e.geom.s1) * 4));
+      HZP_CUDA(cudaMemset(l.var, 0, size_t(e.geom.s1) * 4));
+      HZP_CUDA(cudaMemset(e.arenas[r].grad, 0, size_t(e.geom.s2) * 4));
+      l.adam_step = 0;
+    }
+    HZP_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+int hzp_step(hzp_ctx* ctx, const void* inputs, int inputs_on_device, float* losses_out) {
+  if (!ctx || !inputs) return HZP_ERR_ARG;
+  return guarded([&] { ctx->e->step(inputs, inputs_on_device != 0, losses_out); });
+}
+
+int hzp_sync(hzp_ctx* ctx) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    HZP_CUDA(cudaSetDevice(ctx->e->cfg.device));
+    HZP_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+int hzp_launch_log(const hzp_ctx* ctx, hzp_launch_rec* out, int cap, int* n) {
+  if (!ctx || !n) return HZP_ERR_ARG;
+  const auto& log = ctx->e->log;
+  *n = static_cast<int>(log.size());
+  if (out)
+    for (int i = 0; i < *n && i < cap; ++i) out[i] = log[i];
+  return HZP_OK;
+}
+
+int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, int* n,
+                 double* compute_idle_ms, double* compute_busy_ms, double* makespan_ms) {
+  if (!ctx || !n) return HZP_ERR_ARG;
+  return guarded([&] {
+    const Engine& e = *ctx->e;
+    if (!e.cfg.timeline) throw std::invalid_argument("ctx created without timeline");
+    HZP_CUDA(cudaEventSynchronize(e.ev_step1));
+    const int cnt = static_cast<int>(e.plan.entries.size());
+    *n = cnt;
+    double busy = 0, last_c = 0, mk = 0;
+    for (int i = 0; i < cnt; ++i) {
+      float a = 0, b = 0;
+      HZP_CUDA(cudaEventElapsedTime(&a, e.ev_step0, e.tev0[i]));
+      HZP_CUDA(cudaEventElapsedTime(&b, e.ev_step0, e.tev1[i]));
+      if (i < cap) {
+        if (start_ms) start_ms[i] = a;
+        if (end_ms) end_ms[i] = b;
+      }
+      if (e.plan.entries[i].stream == StreamId::Compute) {
+        busy += b - a;
+        last_c = last_c > b ? last_c : b;
+      }
+      mk = mk > b ? mk : b;
+    }
+    if (compute_idle_ms) *compute_idle_ms = last_c - busy;
+    if (compute_busy_ms) *compute_busy_ms = busy;
+    if (makespan_ms) *makespan_ms = mk;
+  });
+}
+
+int hzp_ctx_launch_count(const hzp_ctx* ctx, int64_t* kernels) {
+  if (!ctx || !kernels) return HZP_ERR_ARG;
+  *kernels = ctx->e->launches;
+  return HZP_OK;
+}
+
+int hzp_ag_layer(hzp_ctx* ctx, int layer, int slot) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    if (layer < 0 || layer >= static_cast<int>(e.layers.size()) || slot < 0 || slot >= e.depth)
+      throw std::invalid_argument("layer/slot out of range");
+    e.ag_layer(layer, slot, e.st[1]);
+    HZP_CUDA(cudaStreamSynchronize(e.st[1]));
+  });
+}
+
+int hzp_ag_slot_download(hzp_ctx* ctx, int rank, int slot, void* host, int64_t n) {
+  if (!ctx || !host) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    const int li = e.local_index(rank);
+    if (li < 0 || slot < 0 || slot >= e.depth || n > e.slot_elems) throw std::invalid_argument("bad args");
+    const int es = e.bf16 ? 2 : 4;
+    HZP_CUDA(cudaMemcpy(host, static_cast<char*>(e.locals[li].ag) + int64_t(slot) * e.slot_elems * es,
+                        size_t(n) * es, cudaMemcpyDeviceToHost));
+  });
+}
+
+namespace {
+__global__ void cast_to_wire_kernel(const float* in, void* out, int64_t n, int bf16) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if (bf16) static_cast<uint16_t*>(out)[i] = f32_to_bf16_bits(in[i]);
+    else static_cast<float*>(out)[i] = in[i];
+  }
+}
+}  // namespace
+
+int hzp_wgrad_upload(hzp_ctx* ctx, int rank, int layer, int wslot, const float* host, int64_t n) {
+  if (!ctx || !host) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    const int li = e.local_index(rank);
+    if (li < 0 || e.direct_grad || wslot < 0 || wslot >= e.wslots ||
+        n != e.layers.at(layer).size)
+      throw std::invalid_argument("bad args (z2 == 1 has no gradient ring)");
+    float* tmp = nullptr;
+    HZP_CUDA(cudaMalloc(&tmp, size_t(n) * 4));
+    HZP_CUDA(cudaMemcpy(tmp, host, size_t(n) * 4, cudaMemcpyHostToDevice));
+    const int es = e.bf16 ? 2 : 4;
+    void* dst = static_cast<char*>(e.arenas[rank].wgrad) + int64_t(wslot) * e.slot_elems * es;
+    cast_to_wire_kernel<<<256, 256>>>(tmp, dst, n, e.bf16);
+    HZP_LAUNCH_CHECK();
+    HZP_CUDA(cudaDeviceSynchronize());
+    cudaFree(tmp);
+  });
+}
+
+int hzp_rs_layer(hzp_ctx* ctx, int layer, int wslot) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    if (e.direct_grad) throw std::invalid_argument("z2 == 1: the reduce-scatter is fused into wgrad");
+    e.rs_layer(layer, wslot, false, e.st[2]);
+    HZP_CUDA(cudaStreamSynchronize(e.st[2]));
+  });
+}
+
+int hzp_z1_adam_step(hzp_ctx* ctx) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    e.barrier(e.st[0]);
+    e.z1_adam(e.st[0]);
+    e.barrier(e.st[0]);
+    HZP_CUDA(cudaStreamSynchronize(e.st[0]));
+  });
+}
+
+int hzp_zero_grads(hzp_ctx* ctx) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    for (auto& l : e.locals) HZP_CUDA(cudaMemset(e.arenas[l.rank].grad, 0, size_t(e.geom.s2) * 4));
+  });
+}
+
+int hzp_barrier(hzp_ctx* ctx) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    ctx->e->barrier(ctx->e->st[0]);
+    HZP_CUDA(cudaStreamSynchronize(ctx->e->st[0]));
+  });
+}
+
+int hzp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda, int ldb,
+                  int ldc, int a_mn, int b_mn, int epi, void* stream) {
+  return guarded([&] {
+    GemmShape s{M, N, K, lda, ldb, a_mn, b_mn};
+    Epilogue e;
+    e.ldc = ldc;
+    e.out_bf16 = epi == 0;
+    e.mode = epi == 2 ? kEpiAccum : kEpiStore;
+    gemm_tc_bf16(A, B, C, s, e, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, int lda, int ldb,
+                 int ldc, int a_mn, int b_mn, int epi, void* stream) {
+  return guarded([&] {
+    GemmShape s{M, N, K, lda, ldb, a_mn, b_mn};
+    Epilogue e;
+    e.ldc = ldc;
+    e.out_bf16 = 0;
+    e.mode = epi == 2 ? kEpiAccum : kEpiStore;
+    gemm_f32_ordered(A, B, C, s, e, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,571 @@
+// Device engine: buffers, P2P wiring, tile tables and the stream/event
+// executor that walks the LaunchPlan.
+//
+// Executor contract:
+//  * three CUDA streams per GPU mirror the reference's stream split
+//    (sched.cpp:36-51): compute {FWD, BWD, OPT}, ag {AG-param, AG-post},
+//    rs {RS-grad, AR-dzp}; comm streams run at high priority;
+//  * tasks are issued in task-id order; a task waits (cudaStreamWaitEvent)
+//    for every entry of its plan wait-list that ran on another stream, so
+//    every event is recorded before it is waited on;
+//  * AG-pool slot = k % depth and the ring wait = first consumer of AG-pool
+//    task k-depth (the reference's ring rule), RS ring likewise;
+//  * the tail AR-dzp(l) + OPT + AG-post(l) collapses into ONE fused kernel
+//    (z1_adam: replica pull-reduce + Adam + bf16 P2P store), logged as
+//    covering those task ids.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "engine/engine.hpp"
+#include "engine/gemm.cuh"
+
+namespace hzp {
+namespace {
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Split a contiguous element run whose streams start at offs[] (element
+// offsets into 256-byte aligned buffers of elem bytes ebytes[]) into tiles:
+// scalar head, vector body (aligned for every stream, multiple of vec
+// elements), scalar tail; bodies are cut into pieces of <= max_len.
+template <typename Emit>
+void split_run(const int64_t* offs, const int* ebytes, int nstreams, int64_t len, int vec,
+               int64_t max_len, Emit&& emit) {
+  auto aligned_at = [&](int64_t h) {
+    for (int s = 0; s < nstreams; ++s)
+      if (((offs[s] + h) * ebytes[s]) % 16 != 0) return false;
+    return true;
+  };
+  int64_t head = -1;
+  for (int64_t h = 0; h < 64 && h <= len; ++h)
+    if (aligned_at(h)) { head = h; break; }
+  if (head < 0 || len - head < vec) {
+    for (int64_t p = 0; p < len; p += max_len) emit(p, std::min(max_len, len - p), false);
+    return;
+  }
+  if (head > 0) emit(0, head, false);
+  const int64_t body = (len - head) / vec * vec;
+  const int64_t piece = std::max<int64_t>(vec, max_len / vec * vec);
+  for (int64_t p = 0; p < body; p += piece) emit(head + p, std::min(piece, body - p), true);
+  if (head + body < len) emit(head + body, len - head - body, false);
+}
+
+constexpr int64_t kTileElems = 1 << 15;
+
+uint64_t z1_targets(const ShardGeom& g, int rank, int j3) {
+  uint64_t m = 0;
+  const int base = g.z1_base(rank);
+  for (int q = base; q < base + g.z1; ++q)
+    if (q % g.z3 == j3) m |= 1ull << q;
+  return m;
+}
+
+}  // namespace
+
+Engine::Engine(const hzp_engine_config& c) : cfg(c) {
+  if (c.par.dp < 1 || c.par.dp > kMaxRanks) throw std::invalid_argument("dp must be in [1, 64]");
+  for (int z : {c.par.z1, c.par.z2, c.par.z3})
+    if (z < 1 || c.par.dp % z) throw ValidationError(ValidationError::Code::NonDivisible, "z does not divide dp");
+  bf16 = c.precision == HZP_PREC_BF16;
+  mcfg.kind = c.model;
+  mcfg.bf16 = bf16;
+  mcfg.batch = c.batch;
+  if (c.model == HZP_MODEL_MLP) {
+    if (c.num_dims < 2 || c.num_dims > 32) throw std::invalid_argument("MLP needs 2..32 dims");
+    mcfg.dims.assign(c.dims, c.dims + c.num_dims);
+    model = make_mlp_model(mcfg);
+  } else {
+    mcfg.layers = c.gpt_layers;
+    mcfg.hidden = c.gpt_hidden;
+    mcfg.heads = c.gpt_heads;
+    mcfg.ffn = c.gpt_ffn;
+    mcfg.vocab = c.gpt_vocab;
+    mcfg.seq = c.gpt_seq;
+    if (!bf16) throw std::invalid_argument("the GPT model runs in bf16 only");
+    model = make_gpt_model(mcfg);
+  }
+  HZP_CUDA(cudaSetDevice(c.device));
+  const int L = model->num_layers();
+  for (int l = 0; l < L; ++l) layers.push_back(model->layer(l));
+  geom = ShardGeom(model->param_count(), ParallelConfig{c.par.dp, c.par.z1, c.par.z2, c.par.z3});
+  slot_elems = static_cast<int64_t>(align_up(size_t(model->max_layer_size()), 128));
+  emulate = c.my_rank < 0;
+  depth = std::max(1, c.prelaunch_depth);
+  rs_slots = std::max(1, c.rs_slots);
+  wslots = std::max(2, c.wgrad_slots);
+  direct_grad = geom.z2 == 1;
+  zero_copy_ag = geom.z3 == 1;
+
+  // ---- task graph + plan (the drop-in scheduler) ----
+  ModelSpec spec;
+  spec.num_layers = L;
+  spec.params_per_layer = std::max<int64_t>(1, model->max_layer_size());
+  spec.num_microbatches = std::max(1, c.num_microbatches);
+  spec.seq_len = 1;
+  spec.micro_batch_size = 1;
+  CostModel cost;
+  cost.topo.num_nodes = 1;
+  cost.topo.ranks_per_node = c.par.dp;
+  graph = build_task_graph(spec, ParallelConfig{c.par.dp, c.par.z1, c.par.z2, c.par.z3}, cost, {});
+  pools = make_pools(graph, depth, rs_slots);
+  plan = build_launch_plan(graph, pools);
+
+  // ---- streams / events ----
+  int lo = 0, hi = 0;
+  HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  HZP_CUDA(cudaStreamCreateWithPriority(&st[0], cudaStreamNonBlocking, lo));
+  HZP_CUDA(cudaStreamCreateWithPriority(&st[1], cudaStreamNonBlocking, hi));
+  HZP_CUDA(cudaStreamCreateWithPriority(&st[2], cudaStreamNonBlocking, hi));
+  const int n = static_cast<int>(plan.entries.size());
+  done.resize(n);
+  for (auto& e : done) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (c.timeline) {
+    tev0.resize(n);
+    tev1.resize(n);
+    for (int i = 0; i < n; ++i) {
+      HZP_CUDA(cudaEventCreate(&tev0[i]));
+      HZP_CUDA(cudaEventCreate(&tev1[i]));
+    }
+  }
+  HZP_CUDA(cudaEventCreate(&ev_step0));
+  HZP_CUDA(cudaEventCreate(&ev_step1));
+  HZP_CUDA(cudaEventCreateWithFlags(&ev_opt, cudaEventDisableTiming));
+
+  // ---- per-rank peer-visible arenas ----
+  const int es = bf16 ? 2 : 4;
+  const size_t p_bytes = align_up(size_t(geom.s3) * es, 256);
+  const size_t g_bytes = align_up(size_t(geom.s2) * 4, 256);
+  const size_t w_bytes = direct_grad ? 0 : align_up(size_t(wslots) * slot_elems * es, 256);
+  const size_t f_bytes = align_up(sizeof(uint64_t) * kNumFlagKinds * kMaxRanks, 256);
+  arenas.resize(c.par.dp);
+  std::vector<int> mine;
+  if (emulate) {
+    mine.resize(c.par.dp);
+    std::iota(mine.begin(), mine.end(), 0);
+  } else {
+    if (c.my_rank >= c.par.dp) throw std::invalid_argument("my_rank out of range");
+    mine.push_back(c.my_rank);
+  }
+  for (int r : mine) {
+    Arena& a = arenas[r];
+    a.bytes = p_bytes + g_bytes + w_bytes + f_bytes;
+    HZP_CUDA(cudaMalloc(&a.base, a.bytes));
+    HZP_CUDA(cudaMemset(a.base, 0, a.bytes));
+    a.owned = true;
+  }
+  auto carve = [&](Arena& a) {
+    char* b = static_cast<char*>(a.base);
+    a.param = b;
+    a.grad = reinterpret_cast<float*>(b + p_bytes);
+    a.wgrad = w_bytes ? b + p_bytes + g_bytes : nullptr;
+    a.flags = reinterpret_cast<uint64_t*>(b + p_bytes + g_bytes + w_bytes);
+  };
+  for (int r : mine) carve(arenas[r]);
+
+  // ---- driven ranks ----
+  for (int r : mine) {
+    LocalRank lr;
+    lr.rank = r;
+    HZP_CUDA(cudaMalloc(&lr.ag, size_t(depth) * slot_elems * es));
+    HZP_CUDA(cudaMalloc(&lr.master, size_t(geom.s1) * 4));
+    HZP_CUDA(cudaMalloc(&lr.mom, size_t(geom.s1) * 4));
+    HZP_CUDA(cudaMalloc(&lr.var, size_t(geom.s1) * 4));
+    HZP_CUDA(cudaMemset(lr.master, 0, size_t(geom.s1) * 4));
+    HZP_CUDA(cudaMemset(lr.mom, 0, size_t(geom.s1) * 4));
+    HZP_CUDA(cudaMemset(lr.var, 0, size_t(geom.s1) * 4));
+    if (geom.P < (int64_t(1) << 24)) HZP_CUDA(cudaMalloc(&lr.dbg, size_t(geom.s1) * 4));
+    lr.mbuf = model->alloc_rank_buffers();
+    locals.push_back(lr);
+  }
+  HZP_CUDA(cudaMallocHost(&hloss, sizeof(float) * locals.size()));
+  input_bytes_per_mb = size_t(model->input_elems_per_mb()) * model->input_elem_bytes();
+  HZP_CUDA(cudaMalloc(&dinputs, std::max<size_t>(256, input_bytes_per_mb * locals.size() *
+                                                         std::max(1, c.num_microbatches))));
+
+  // ---- pointer table ----
+  std::memset(&table, 0, sizeof(table));
+  for (int r = 0; r < c.par.dp; ++r) {
+    table.param[r] = arenas[r].param;
+    table.grad[r] = arenas[r].grad;
+    table.wgrad[r] = arenas[r].wgrad;
+    table.flags[r] = arenas[r].flags;
+  }
+  for (size_t i = 0; i < locals.size(); ++i) {
+    table.ag_slots[i] = locals[i].ag;
+    table.master[i] = locals[i].master;
+    table.mom[i] = locals[i].mom;
+    table.var[i] = locals[i].var;
+    table.z1_grad_dbg[i] = locals[i].dbg;
+  }
+  HZP_CUDA(cudaMalloc(&dtable, sizeof(RankTable)));
+  HZP_CUDA(cudaMemcpy(dtable, &table, sizeof(RankTable), cudaMemcpyHostToDevice));
+  peers_open = emulate || c.par.dp == 1;
+  build_tiles();
+}
+
+Engine::~Engine() {
+  cudaDeviceSynchronize();
+  for (auto& l : locals) {
+    cudaFree(l.ag);
+    cudaFree(l.master);
+    cudaFree(l.mom);
+    cudaFree(l.var);
+    cudaFree(l.dbg);
+    model->free_rank_buffers(l.mbuf);
+  }
+  for (auto& a : arenas) {
+    if (a.base && a.owned) cudaFree(a.base);
+    else if (a.base) cudaIpcCloseMemHandle(a.base);
+  }
+  cudaFree(dtable);
+  cudaFree(dtiles);
+  cudaFree(dinputs);
+  cudaFreeHost(hloss);
+  for (auto e : done) cudaEventDestroy(e);
+  for (auto e : tev0) cudaEventDestroy(e);
+  for (auto e : tev1) cudaEventDestroy(e);
+  cudaEventDestroy(ev_step0);
+  cudaEventDestroy(ev_step1);
+  cudaEventDestroy(ev_opt);
+  for (auto s : st) cudaStreamDestroy(s);
+}
+
+int Engine::local_index(int rank) const {
+  for (size_t i = 0; i < locals.size(); ++i)
+    if (locals[i].rank == rank) return int(i);
+  return -1;
+}
+
+void Engine::build_tiles() {
+  std::vector<CommTile> tiles;
+  const int es = bf16 ? 2 : 4;
+  const int L = static_cast<int>(layers.size());
+  const ShardGeom& g = geom;
+  // AG: per layer, per driven rank, owner spans of the layer range.
+  ag_off.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    ag_off[l] = static_cast<int>(tiles.size());
+    for (size_t li = 0; li < locals.size(); ++li) {
+      const int r = locals[li].rank;
+      const int base = g.z3_base(r);
+      int64_t e = layers[l].off;
+      const int64_t end = layers[l].off + layers[l].size;
+      while (e < end) {
+        const int owner = static_cast<int>(e / g.s3);
+        const int64_t stop = std::min(end, (owner + 1) * g.s3);
+        const int64_t offs[2] = {e - layers[l].off, e - owner * g.s3};
+        const int eb[2] = {es, es};
+        split_run(offs, eb, 2, stop - e, 16 / es, kTileElems, [&](int64_t p, int64_t n, bool v) {
+          CommTile t{};
+          t.a_off = offs[0] + p;
+          t.b_off = offs[1] + p;
+          t.len = static_cast<int32_t>(n);
+          t.local = static_cast<int16_t>(li);
+          t.src = static_cast<int16_t>(base + owner);
+          t.vec = v;
+          tiles.push_back(t);
+        });
+        e = stop;
+      }
+    }
+  }
+  ag_off[L] = static_cast<int>(tiles.size());
+  // RS: per layer, per driven rank, intersection with its Z2 segment.
+  rs_off.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    rs_off[l] = static_cast<int>(tiles.size());
+    if (direct_grad) continue;
+    for (size_t li = 0; li < locals.size(); ++li) {
+      const int r = locals[li].rank;
+      const int i2 = r % g.z2;
+      const int64_t e0 = std::max(layers[l].off, i2 * g.s2);
+      const int64_t e1 = std::min(layers[l].off + layers[l].size, (i2 + 1) * g.s2);
+      if (e0 >= e1) continue;
+      const int64_t offs[2] = {e0 - i2 * g.s2, e0 - layers[l].off};
+      const int eb[2] = {4, es};
+      split_run(offs, eb, 2, e1 - e0, bf16 ? 8 : 4, kTileElems, [&](int64_t p, int64_t n, bool v) {
+        CommTile t{};
+        t.a_off = offs[0] + p;
+        t.b_off = offs[1] + p;
+        t.len = static_cast<int32_t>(n);
+        t.local = static_cast<int16_t>(li);
+        t.src = static_cast<int16_t>(g.z2_base(r));
+        t.vec = v;
+        tiles.push_back(t);
+      });
+    }
+  }
+  rs_off[L] = static_cast<int>(tiles.size());
+  // Z1: chunk of each driven rank, cut at Z2 and Z3 segment boundaries.
+  z1_off = static_cast<int>(tiles.size());
+  for (size_t li = 0; li < locals.size(); ++li) {
+    const int r = locals[li].rank;
+    const int i1 = r % g.z1;
+    int64_t e = i1 * g.s1;
+    const int64_t end = std::min(int64_t(i1 + 1) * g.s1, g.P);
+    while (e < end) {
+      const int j2 = static_cast<int>(e / g.s2), j3 = static_cast<int>(e / g.s3);
+      const int64_t stop = std::min({end, (j2 + 1) * g.s2, (j3 + 1) * g.s3});
+      const int64_t offs[3] = {e - i1 * g.s1, e - j2 * g.s2, e - j3 * g.s3};
+      const int eb[3] = {4, 4, bf16 ? 8 : 4};  // param stream: 4 bf16 = 8-byte stores
+      const uint64_t mask = z1_targets(g, r, j3);
+      // bf16 param vector stores are 8 bytes: treat as 16-byte alignment of
+      // 4-element groups by scaling its element size to 4 (offset % 4 == 0).
+      const int64_t offs_al[3] = {offs[0], offs[1], offs[2]};
+      const int eb_al[3] = {4, 4, 4};
+      (void)eb;
+      split_run(offs_al, eb_al, 3, stop - e, 4, kTileElems, [&](int64_t p, int64_t n, bool v) {
+        CommTile t{};
+        t.a_off = offs[0] + p;
+        t.b_off = offs[1] + p;
+        t.c_off = offs[2] + p;
+        t.mask = mask;
+        t.len = static_cast<int32_t>(n);
+        t.local = static_cast<int16_t>(li);
+        t.src = static_cast<int16_t>(j2);
+        t.vec = v;
+        tiles.push_back(t);
+      });
+      e = stop;
+    }
+  }
+  z1_n = static_cast<int>(tiles.size()) - z1_off;
+  if (dtiles) cudaFree(dtiles);
+  HZP_CUDA(cudaMalloc(&dtiles, std::max<size_t>(1, tiles.size()) * sizeof(CommTile)));
+  if (!tiles.empty())
+    HZP_CUDA(cudaMemcpy(dtiles, tiles.data(), tiles.size() * sizeof(CommTile), cudaMemcpyHostToDevice));
+}
+
+void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
+  launch_ag_pull(dtable, dtiles + ag_off[layer], ag_off[layer + 1] - ag_off[layer], slot,
+                 slot_elems, bf16, comm_ctas, s);
+  ++launches;
+}
+
+void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
+  launch_rs_pull(dtable, dtiles + rs_off[layer], rs_off[layer + 1] - rs_off[layer], wslot,
+                 slot_elems, geom.z2, bf16, assign, static_cast<float>(cfg.grad_scale), comm_ctas, s);
+  ++launches;
+}
+
+void Engine::z1_adam(cudaStream_t s) {
+  // Bias corrections exactly as the reference (train.cpp:179-180 with T=float):
+  // (T)1 - (T)std::pow((T)beta, step), std::pow(float, int) promoting to double.
+  LocalRank& l0 = locals.front();
+  for (auto& l : locals) l.adam_step += 1;
+  const int step = l0.adam_step;
+  AdamArgs a;
+  a.lr = static_cast<float>(cfg.lr);
+  a.b1 = static_cast<float>(cfg.beta1);
+  a.b2 = static_cast<float>(cfg.beta2);
+  a.eps = static_cast<float>(cfg.eps);
+  volatile float one = 1.0f;
+  a.omb1 = one - a.b1;
+  a.omb2 = one - a.b2;
+  a.bc1 = one - static_cast<float>(std::pow(static_cast<double>(a.b1), step));
+  a.bc2 = one - static_cast<float>(std::pow(static_cast<double>(a.b2), step));
+  launch_z1_adam(dtable, dtiles + z1_off, z1_n, geom.z2, geom.replicas(), &a, 1, bf16,
+                 l0.dbg != nullptr, std::max(comm_ctas, 2 * kNumSMs), s);
+  ++launches;
+}
+
+void Engine::barrier(cudaStream_t s) {
+  if (emulate || cfg.par.dp == 1) return;
+  ++barrier_epoch;
+  launch_signal(dtable, cfg.my_rank, kFlagBarrier, 0, cfg.par.dp, 1, barrier_epoch, kFlagBarrier,
+                barrier_epoch, s);
+  ++launches;
+}
+
+const void* Engine::layer_params(int li, int layer, int slot) const {
+  const int es = bf16 ? 2 : 4;
+  if (zero_copy_ag)  // z3 == 1: this rank's shard is the whole working copy
+    return static_cast<const char*>(arenas[locals[li].rank].param) + layers[layer].off * es;
+  return static_cast<const char*>(locals[li].ag) + (int64_t(slot) * slot_elems) * es;
+}
+
+GradTarget Engine::grad_target(int li, int layer, int wslot, int mb) const {
+  GradTarget t;
+  const int r = locals[li].rank;
+  if (direct_grad) {  // z2 == 1: the grad shard is the whole flat gradient
+    t.ptr = arenas[r].grad + layers[layer].off;
+    t.bf16 = 0;
+    t.mode = mb == 0 ? kEpiAssign0 : kEpiAccum;
+  } else {
+    const int es = bf16 ? 2 : 4;
+    t.ptr = static_cast<char*>(arenas[r].wgrad) + int64_t(wslot) * slot_elems * es;
+    t.bf16 = bf16;
+    t.mode = kEpiStore;
+  }
+  return t;
+}
+
+void Engine::step(const void* inputs, bool on_device, float* losses_out) {
+  if (!peers_open) throw std::runtime_error("peers not opened (hzp_ctx_open_peers)");
+  HZP_CUDA(cudaSetDevice(cfg.device));
+  log.clear();
+  launches = 0;
+  const int nmb = std::max(1, cfg.num_microbatches);
+  const size_t in_total = input_bytes_per_mb * locals.size() * nmb;
+  cudaStream_t cs = st[0];
+  // Step start: the previous step's tail (fused Z1 kernel + barrier) must be
+  // complete before any stream touches grads or param shards again.
+  HZP_CUDA(cudaEventRecord(ev_step0, cs));
+  HZP_CUDA(cudaStreamWaitEvent(st[1], ev_step0, 0));
+  HZP_CUDA(cudaStreamWaitEvent(st[2], ev_step0, 0));
+  const char* in_dev = static_cast<const char*>(inputs);
+  if (!on_device) {
+    HZP_CUDA(cudaMemcpyAsync(dinputs, inputs, in_total, cudaMemcpyHostToDevice, cs));
+    in_dev = static_cast<const char*>(dinputs);
+  }
+  for (auto& l : locals) model->begin_step(l.mbuf, cs);
+
+  const int n = static_cast<int>(plan.entries.size());
+  std::vector<int> rs_index(n, -1);  // RS sequence index within this step
+  {
+    int k = 0;
+    for (const auto& e : plan.entries)
+      if (e.kind == TaskKind::RsGrad) rs_index[e.id] = k++;
+  }
+  // BWD(l, mb) produces the gradient consumed by RS task rs_of_bwd.
+  std::vector<int> rs_of_bwd(n, -1);
+  for (const auto& t : graph.tasks)
+    if (t.kind == TaskKind::RsGrad)
+      for (int d : t.deps)
+        if (graph.tasks[d].kind == TaskKind::Bwd && graph.tasks[d].layer == t.layer) rs_of_bwd[d] = t.id;
+  std::vector<int> rs_ids;
+  for (const auto& e : plan.entries)
+    if (e.kind == TaskKind::RsGrad) rs_ids.push_back(e.id);
+  const uint64_t seq0 = rs_seq;
+  int last_comm_ev[3] = {-1, -1, -1};
+
+  auto rec_log = [&](const PlanEntry& e, int stream, int cov0, int cov1) {
+    hzp_launch_rec r{};
+    r.task_id = e.id;
+    r.kind = static_cast<int>(e.kind);
+    r.layer = e.layer;
+    r.microbatch = e.microbatch;
+    r.stream = stream;
+    r.slot = e.slot;
+    r.covered_first = cov0;
+    r.covered_last = cov1;
+    log.push_back(r);
+  };
+  int opt_id = -1;
+  for (const auto& e : plan.entries)
+    if (e.kind == TaskKind::OptStep) opt_id = e.id;
+
+  for (const auto& e : plan.entries) {
+    cudaStream_t s = st[static_cast<int>(e.stream)];
+    for (int w : e.waits)
+      if (plan.entries[w].stream != e.stream) HZP_CUDA(cudaStreamWaitEvent(s, done[w], 0));
+    if (cfg.mode == HZP_MODE_VANILLA && e.stream == StreamId::Compute) {
+      // vanilla: compute may not run past any issued collective (sched.cpp:280-284)
+      for (int k = 1; k < 3; ++k)
+        if (last_comm_ev[k] >= 0) HZP_CUDA(cudaStreamWaitEvent(s, done[last_comm_ev[k]], 0));
+    }
+    if (cfg.timeline) HZP_CUDA(cudaEventRecord(tev0[e.id], s));
+    switch (e.kind) {
+      case TaskKind::AgParam:
+        if (zero_copy_ag) {
+          rec_log(e, -1, e.id, e.id);  // identity: layers read the shard in place
+        } else {
+          ag_layer(e.layer, e.slot, s);
+          rec_log(e, int(e.stream), e.id, e.id);
+        }
+        break;
+      case TaskKind::Fwd: {
+        const int slot = plan.entries[e.waits[0]].slot;  // deps[0] = its AG
+        for (size_t li = 0; li < locals.size(); ++li) {
+          const char* in = in_dev + (li * nmb + e.microbatch) * input_bytes_per_mb;
+          model->fwd(locals[li].mbuf, e.layer, in, layer_params(int(li), e.layer, slot), s);
+        }
+        launches += int64_t(locals.size()) * model->launches_per_fwd();
+        rec_log(e, 0, e.id, e.id);
+        break;
+      }
+      case TaskKind::Bwd: {
+        const int slot = plan.entries[e.waits[0]].slot;
+        const int rs = rs_of_bwd[e.id];
+        const int k = rs >= 0 ? rs_index[rs] : 0;
+        const int wslot = static_cast<int>((seq0 + k) % wslots);
+        if (!direct_grad) {
+          // the gradient buffer is free once RS k - wslots finished everywhere
+          if (k >= wslots) HZP_CUDA(cudaStreamWaitEvent(s, done[rs_ids[k - wslots]], 0));
+          if (!emulate && geom.z2 > 1 && seq0 + k >= uint64_t(wslots)) {
+            launch_wait(dtable, cfg.my_rank, kFlagRsDone, geom.z2_base(cfg.my_rank), geom.z2, 1,
+                        seq0 + k + 1 - wslots, s);
+            ++launches;
+          }
+        }
+        for (size_t li = 0; li < locals.size(); ++li)
+          model->bwd(locals[li].mbuf, e.layer, layer_params(int(li), e.layer, slot),
+                     grad_target(int(li), e.layer, wslot, e.microbatch), s);
+        launches += int64_t(locals.size()) * 3;
+        rec_log(e, 0, e.id, e.id);
+        break;
+      }
+      case TaskKind::RsGrad: {
+        const int k = rs_index[e.id];
+        const uint64_t seq = seq0 + k + 1;  // 1-based sequence number of this RS
+        if (direct_grad) {
+          rec_log(e, -1, e.id - 1, e.id);  // fused into the BWD's wgrad epilogue
+        } else {
+          if (!emulate && geom.z2 > 1) {  // publish + wait for every Z2 peer's gradient
+            launch_signal(dtable, cfg.my_rank, kFlagRsReady, geom.z2_base(cfg.my_rank), geom.z2, 1,
+                          seq, kFlagRsReady, seq, s);
+            ++launches;
+          }
+          rs_layer(e.layer, static_cast<int>((seq - 1) % wslots), e.microbatch == 0, s);
+          if (!emulate && geom.z2 > 1) {
+            launch_signal(dtable, cfg.my_rank, kFlagRsDone, geom.z2_base(cfg.my_rank), geom.z2, 1,
+                          seq, -1, 0, s);
+            ++launches;
+          }
+          rec_log(e, int(e.stream), e.id, e.id);
+        }
+        break;
+      }
+      case TaskKind::ArDzp:
+        rec_log(e, -1, opt_id, opt_id);  // folded into the fused Z1 kernel
+        break;
+      case TaskKind::OptStep: {
+        barrier(s);  // every rank's RS complete; nobody reads param shards any more
+        z1_adam(s);
+        barrier(s);  // every push landed, every grad pull done
+        int first = e.id, last = e.id;
+        for (const auto& x : plan.entries)
+          if (x.kind == TaskKind::ArDzp || x.kind == TaskKind::AgPostStep) {
+            first = std::min(first, x.id);
+            last = std::max(last, x.id);
+          }
+        rec_log(e, 0, first, last);
+        break;
+      }
+      case TaskKind::AgPostStep:
+        rec_log(e, -1, opt_id, opt_id);  // done by the fused kernel's P2P stores
+        break;
+      default:
+        break;
+    }
+    if (cfg.timeline) HZP_CUDA(cudaEventRecord(tev1[e.id], s));
+    HZP_CUDA(cudaEventRecord(done[e.id], s));
+    if (e.stream != StreamId::Compute) last_comm_ev[static_cast<int>(e.stream)] = e.id;
+  }
+  rs_seq = seq0 + rs_ids.size();
+  // join the comm streams back into the compute stream
+  for (int k = 1; k < 3; ++k)
+    if (last_comm_ev[k] >= 0) HZP_CUDA(cudaStreamWaitEvent(cs, done[last_comm_ev[k]], 0));
+  for (size_t li = 0; li < locals.size(); ++li)
+    HZP_CUDA(cudaMemcpyAsync(hloss + li, model->loss_device(locals[li].mbuf), sizeof(float),
+                             cudaMemcpyDeviceToHost, cs));
+  HZP_CUDA(cudaEventRecord(ev_step1, cs));
+  if (losses_out) {
+    HZP_CUDA(cudaEventSynchronize(ev_step1));
+    std::memcpy(losses_out, hloss, sizeof(float) * locals.size());
+  }
+}
+
+}  // namespace hzp

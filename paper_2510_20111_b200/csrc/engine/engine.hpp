@@ -1,0 +1,92 @@
+// Device engine: one hzp_ctx drives one GPU and either one dp rank (one
+// process per GPU, peers reached through CUDA IPC over NVLink/NVSwitch) or
+// all dp ranks emulated on that GPU (single-process parity mode).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "hzp/sched.hpp"
+#include "hzp_b200.h"
+#include "engine/comm.cuh"
+#include "engine/model.hpp"
+
+namespace hzp {
+
+struct Arena {
+  void* base = nullptr;
+  size_t bytes = 0;
+  bool owned = false;  // allocated here (else IPC-mapped)
+  void* param = nullptr;
+  float* grad = nullptr;
+  void* wgrad = nullptr;
+  uint64_t* flags = nullptr;
+};
+
+struct LocalRank {
+  int rank = 0;
+  void* ag = nullptr;  // [depth][slot_elems]
+  float* master = nullptr;
+  float* mom = nullptr;
+  float* var = nullptr;
+  float* dbg = nullptr;
+  void* mbuf = nullptr;  // model buffers
+  int adam_step = 0;
+};
+
+struct Engine {
+  hzp_engine_config cfg{};
+  ModelConfig mcfg;
+  std::unique_ptr<Model> model;
+  ShardGeom geom;
+  std::vector<LayerRange> layers;
+  int64_t slot_elems = 0;  // padded max layer size
+  bool emulate = true;
+  bool bf16 = true;
+  int depth = 2, rs_slots = 1, wslots = 2;
+  bool direct_grad = false;  // z2 == 1: wgrad GEMM accumulates into the grad shard
+  bool zero_copy_ag = false; // z3 == 1: layers read straight from the param shard
+
+  TaskGraph graph;
+  PoolSet pools;
+  LaunchPlan plan;
+
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> done;
+  std::vector<cudaEvent_t> tev0, tev1;
+  cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr, ev_opt = nullptr;
+
+  std::vector<Arena> arenas;  // [dp]
+  std::vector<LocalRank> locals;
+  RankTable table{};
+  RankTable* dtable = nullptr;
+
+  CommTile* dtiles = nullptr;
+  std::vector<int> ag_off, rs_off;  // [nlocal_layers + 1] per layer tile ranges
+  int z1_off = 0, z1_n = 0;
+
+  void* dinputs = nullptr;
+  size_t input_bytes_per_mb = 0;
+  float* hloss = nullptr;  // pinned [nlocal]
+
+  uint64_t rs_seq = 0, barrier_epoch = 0;
+  std::vector<hzp_launch_rec> log;
+  int64_t launches = 0;
+  int comm_ctas = 32;
+  bool peers_open = false;
+
+  explicit Engine(const hzp_engine_config& c);
+  ~Engine();
+
+  int local_index(int rank) const;
+  void build_tiles();
+  void step(const void* inputs, bool on_device, float* losses_out);
+  void ag_layer(int layer, int slot, cudaStream_t s);
+  void rs_layer(int layer, int wslot, bool assign, cudaStream_t s);
+  void z1_adam(cudaStream_t s);
+  void barrier(cudaStream_t s);
+  GradTarget grad_target(int li, int layer, int wslot, int mb) const;
+  const void* layer_params(int li, int layer, int slot) const;
+};
+
+}  // namespace hzp

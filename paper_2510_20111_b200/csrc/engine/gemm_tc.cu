@@ -1,0 +1,472 @@
+// tcgen05 GEMM for sm_100a: C = epilogue(A · Bᵀ), bf16 operands, fp32
+// accumulation in TMEM.
+//
+// Structure (one persistent CTA per SM, 6 warps, warp-specialised):
+//   warp 0  : TMA producer — one elected lane streams A/B tiles (128B swizzle)
+//             into a `kStages`-deep shared-memory ring (mbarrier full/empty).
+//   warp 1  : TMEM allocator + MMA issuer — one elected lane issues
+//             tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) and
+//             commits completion to the smem ring / accumulator barriers.
+//   warps 2-5: epilogue — tcgen05.ld 32x32b.x32 from TMEM, bias/activation/
+//             accumulate, vectorised global stores.
+// Two TMEM accumulators (2 x BN fp32 columns) let the epilogue of tile i
+// overlap the MMAs of tile i+1.
+//
+// Operands may be K-major or MN-major in global memory; MN-major tiles are
+// loaded as 64-wide boxes and described to the tensor core with the MN-major
+// SW128 canonical layout (LBO = 64-wide block stride, SBO = 8-row K-group
+// stride), so dgrad / wgrad never materialise a transpose.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "engine/gemm.cuh"
+
+namespace hzp {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int kThreadsTC = 192;
+
+int g_sm_budget = kNumSMs;
+
+// ---- PTX wrappers ---------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// SM100 shared-memory matrix descriptor, SWIZZLE_128B (layout type 2,
+// bits 61-63), version 1 (bits 46-47).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k = 0.7978845608028654f;
+  return 0.5f * x * (1.f + tanhf(k * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k = 0.7978845608028654f;
+  const float u = k * (x + 0.044715f * x * x * x);
+  const float t = tanhf(u);
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k * (1.f + 3.f * 0.044715f * x * x);
+}
+
+struct TcParams {
+  int M, N, K;
+  int tiles_m, tiles_n, num_tiles;
+  Epilogue e;
+  void* C;
+};
+
+template <int BN, int A_MN, int B_MN, int STAGES>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const TcParams p) {
+  constexpr uint32_t A_BYTES = BM * BK * 2;
+  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  constexpr uint32_t IDESC = make_idesc(BM, BN, A_MN, B_MN);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int m0 = (t % p.tiles_m) * BM, n0 = (t / p.tiles_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (BK * 128), &tmA, &full[stage], m0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (BK * 128), &tmB, &full[stage], n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 32 bytes inside the swizzled row; MN-major:
+            // advance 16 K-rows = 2 eight-row groups = 2048 bytes.
+            const uint64_t ad = A_MN ? smem_desc(sa + k * 2048, BK * 128, 1024)
+                                     : smem_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(sb + k * 2048, BK * 128, 1024)
+                                     : smem_desc(sb + k * 32, 16, 1024);
+            tc_mma(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);  // frees this smem stage when the MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4 ----
+    const int quarter = warp & 3;
+    const Epilogue& e = p.e;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int m0 = (t % p.tiles_m) * BM, n0 = (t / p.tiles_m) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int m = m0 + quarter * 32 + lane;
+      const bool row_ok = m < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + acc * BN + c * 32, r);
+        const int nb = n0 + c * 32;
+        if (!row_ok || nb >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const bool full_chunk = nb + 32 <= p.N;
+        if (e.bias_any) {
+          const uint16_t* b = static_cast<const uint16_t*>(e.bias_any) + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (full_chunk || nb + j < p.N) v[j] += bf16_bits_to_f32(b[j]);
+        } else if (e.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (full_chunk || nb + j < p.N) v[j] += e.bias[nb + j];
+        }
+        if (e.act == kActTanh) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = tanhf(v[j]);
+        } else if (e.act == kActGelu) {
+          uint16_t* aux = static_cast<uint16_t*>(e.aux) + int64_t(m) * e.ldaux + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (full_chunk || nb + j < p.N) aux[j] = f32_to_bf16_bits(v[j]);
+            v[j] = gelu_tanh(v[j]);
+          }
+        } else if (e.act == kActTanhGrad || e.act == kActGeluGrad) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (!(full_chunk || nb + j < p.N)) continue;
+            const int64_t ai = int64_t(m) * e.ldaux + nb + j;
+            const float a = e.aux_bf16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(e.aux)[ai])
+                                       : static_cast<const float*>(e.aux)[ai];
+            v[j] *= e.act == kActTanhGrad ? (1.f - a * a) : gelu_tanh_grad(a);
+          }
+        }
+        const int64_t ci = int64_t(m) * e.ldc + nb;
+        if (e.out_bf16) {
+          uint16_t* out = static_cast<uint16_t*>(p.C) + ci;
+          if (full_chunk && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 w;
+              w.x = uint32_t(f32_to_bf16_bits(v[8 * q + 0])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 1])) << 16);
+              w.y = uint32_t(f32_to_bf16_bits(v[8 * q + 2])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 3])) << 16);
+              w.z = uint32_t(f32_to_bf16_bits(v[8 * q + 4])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 5])) << 16);
+              w.w = uint32_t(f32_to_bf16_bits(v[8 * q + 6])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 7])) << 16);
+              reinterpret_cast<uint4*>(out)[q] = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && nb + j < p.N; ++j) out[j] = f32_to_bf16_bits(v[j]);
+          }
+        } else {
+          float* out = static_cast<float*>(p.C) + ci;
+          if (full_chunk && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              if (e.mode == kEpiAccum) {
+                const float4 o = reinterpret_cast<const float4*>(out)[q];
+                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+              } else if (e.mode == kEpiAssign0) {
+                w.x = __fadd_rn(0.f, w.x); w.y = __fadd_rn(0.f, w.y); w.z = __fadd_rn(0.f, w.z); w.w = __fadd_rn(0.f, w.w);
+              }
+              reinterpret_cast<float4*>(out)[q] = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && nb + j < p.N; ++j) {
+              float w = v[j];
+              if (e.mode == kEpiAccum) w += out[j];
+              else if (e.mode == kEpiAssign0) w = __fadd_rn(0.f, w);
+              out[j] = w;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---- SIMT fallback for shapes TMA cannot describe (unaligned leading dims)
+__global__ void gemm_bf16_simt_kernel(const uint16_t* __restrict__ A, const uint16_t* __restrict__ B,
+                                      void* C, GemmShape s, Epilogue e) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (n >= s.N || m >= s.M) return;
+  float acc = 0.f;
+  for (int k = 0; k < s.K; ++k) {
+    const float a = bf16_bits_to_f32(s.a_mn ? A[int64_t(k) * s.lda + m] : A[int64_t(m) * s.lda + k]);
+    const float b = bf16_bits_to_f32(s.b_mn ? B[int64_t(k) * s.ldb + n] : B[int64_t(n) * s.ldb + k]);
+    acc += a * b;
+  }
+  if (e.bias_any) acc += bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias_any)[n]);
+  else if (e.bias) acc += e.bias[n];
+  float v = acc;
+  if (e.act == kActTanh) v = tanhf(acc);
+  else if (e.act == kActGelu) {
+    static_cast<uint16_t*>(e.aux)[int64_t(m) * e.ldaux + n] = f32_to_bf16_bits(acc);
+    v = gelu_tanh(acc);
+  } else if (e.act == kActTanhGrad || e.act == kActGeluGrad) {
+    const int64_t ai = int64_t(m) * e.ldaux + n;
+    const float a = e.aux_bf16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(e.aux)[ai])
+                               : static_cast<const float*>(e.aux)[ai];
+    v = acc * (e.act == kActTanhGrad ? (1.f - a * a) : gelu_tanh_grad(a));
+  }
+  const int64_t ci = int64_t(m) * e.ldc + n;
+  if (e.out_bf16) {
+    static_cast<uint16_t*>(C)[ci] = f32_to_bf16_bits(v);
+  } else {
+    float* o = static_cast<float*>(C) + ci;
+    *o = e.mode == kEpiAccum ? *o + v : (e.mode == kEpiAssign0 ? __fadd_rn(0.f, v) : v);
+  }
+}
+
+// ---- host side --------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner extent `inner` (contiguous), outer extent
+// `outer`, row pitch `ld` elements, box {64, box_outer}, 128-byte swizzle.
+CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+  cuuint32_t box[2] = {64, cuuint32_t(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+template <int BN, int A_MN, int B_MN>
+void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
+               cudaStream_t stream) {
+  constexpr int STAGES = BN == 256 ? 4 : 6;
+  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    HZP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
+    attr_set = true;
+  }
+  const CUtensorMap ta = A_MN ? make_map(A, s.M, s.K, s.lda, BK) : make_map(A, s.K, s.M, s.lda, BM);
+  const CUtensorMap tb = B_MN ? make_map(B, s.N, s.K, s.ldb, BK) : make_map(B, s.K, s.N, s.ldb, BN);
+  TcParams p;
+  p.M = s.M;
+  p.N = s.N;
+  p.K = s.K;
+  p.tiles_m = (s.M + BM - 1) / BM;
+  p.tiles_n = (s.N + BN - 1) / BN;
+  p.num_tiles = p.tiles_m * p.tiles_n;
+  p.e = e;
+  p.C = C;
+  const int grid = p.num_tiles < g_sm_budget ? p.num_tiles : g_sm_budget;
+  kern<<<grid, kThreadsTC, SMEM, stream>>>(ta, tb, p);
+  HZP_LAUNCH_CHECK();
+}
+
+template <int BN>
+void dispatch_major(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
+                    cudaStream_t st) {
+  if (s.a_mn) {
+    if (s.b_mn) launch_tc<BN, 1, 1>(A, B, C, s, e, st);
+    else launch_tc<BN, 1, 0>(A, B, C, s, e, st);
+  } else {
+    if (s.b_mn) launch_tc<BN, 0, 1>(A, B, C, s, e, st);
+    else launch_tc<BN, 0, 0>(A, B, C, s, e, st);
+  }
+}
+
+}  // namespace
+
+void gemm_set_sm_budget(int sms) { g_sm_budget = sms < 1 ? 1 : (sms > kNumSMs ? kNumSMs : sms); }
+
+void gemm_tc_bf16(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
+                  cudaStream_t stream) {
+  if (s.M <= 0 || s.N <= 0) return;
+  const bool tma_ok = s.K > 0 && (s.lda % 8 == 0) && (s.ldb % 8 == 0) &&
+                      (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+  if (!tma_ok) {
+    dim3 grid((s.N + 127) / 128, s.M);
+    gemm_bf16_simt_kernel<<<grid, 128, 0, stream>>>(static_cast<const uint16_t*>(A),
+                                                    static_cast<const uint16_t*>(B), C, s, e);
+    HZP_LAUNCH_CHECK();
+    return;
+  }
+  if (s.N > 128) dispatch_major<256>(A, B, C, s, e, stream);
+  else dispatch_major<128>(A, B, C, s, e, stream);
+}
+
+}  // namespace hzp

@@ -1,0 +1,343 @@
+// Scheduler host code: launch order, pools, ring-slot simulation, LaunchPlan.
+// Semantics follow /root/reference/proj/src/sched.cpp:75-387 and are checked
+// bit-exactly (task list, deps, simulated start/end doubles) against
+// tests/golden/sched.json by tests/test_host.py.
+#include "hzp/sched.hpp"
+
+#include <algorithm>
+#include <map>
+
+namespace hzp {
+
+double collective_cost(CollectiveKind kind, const ProcessGroup& group, std::int64_t bytes,
+                       const CostModel& model) {
+  const int g = group.size();
+  if (g <= 1 || bytes < 0) return 0.0;
+  const bool x = group.spans_nodes;
+  const double bw = x ? model.topo.inter_bw : model.topo.intra_bw;
+  const double lat = x ? model.topo.inter_latency : model.topo.intra_latency;
+  const double hops = static_cast<double>(g - 1);
+  const double t = hops * (static_cast<double>(bytes) / g) / bw + hops * lat;
+  return kind == CollectiveKind::AllReduce ? 2.0 * t : t;
+}
+
+const char* to_string(TaskKind kind) {
+  static const char* const names[] = {"FWD",    "BWD",    "FWD-recompute", "AG-param",
+                                      "RS-grad", "AR-dzp", "OPT-step",      "AG-post-step"};
+  const int i = static_cast<int>(kind);
+  return (i >= 0 && i < 8) ? names[i] : "?";
+}
+
+int TaskGraph::count(TaskKind kind) const {
+  return static_cast<int>(std::count_if(tasks.begin(), tasks.end(),
+                                        [kind](const Task& t) { return t.kind == kind; }));
+}
+
+StreamId stream_of(TaskKind kind) {
+  switch (kind) {
+    case TaskKind::AgParam:
+    case TaskKind::AgPostStep:
+      return StreamId::Ag;
+    case TaskKind::RsGrad:
+    case TaskKind::ArDzp:
+      return StreamId::Rs;
+    default:
+      return StreamId::Compute;  // FWD, BWD, recompute, OPT
+  }
+}
+
+bool uses_ag_pool(TaskKind kind) {
+  return kind == TaskKind::AgParam || kind == TaskKind::AgPostStep;
+}
+
+bool is_comm(TaskKind kind) { return stream_of(kind) != StreamId::Compute; }
+
+namespace {
+
+// Emits tasks in issue order; the id of a task is its position.
+class GraphWriter {
+ public:
+  explicit GraphWriter(TaskGraph& g) : g_(g) {}
+  int emit(TaskKind kind, int layer, int mb, int vstage, Pass pass, double dur,
+           std::int64_t bytes, std::vector<int> deps) {
+    Task t;
+    t.id = static_cast<int>(g_.tasks.size());
+    t.kind = kind;
+    t.layer = layer;
+    t.microbatch = mb;
+    t.virtual_stage = vstage;
+    t.pass = pass;
+    t.duration = dur;
+    t.bytes = bytes;
+    t.deps = std::move(deps);
+    g_.tasks.push_back(std::move(t));
+    return g_.tasks.back().id;
+  }
+
+ private:
+  TaskGraph& g_;
+};
+
+}  // namespace
+
+TaskGraph build_task_graph(const ModelSpec& spec, const ParallelConfig& cfg,
+                           const CostModel& cost, const GraphPolicy& policy) {
+  using E = SchedError::Code;
+  if (cfg.tp != 1) throw SchedError(E::InvalidPolicy, "task graphs model the sharded path; tp must be 1");
+  const std::int64_t chunks = std::int64_t(cfg.pp) * cfg.vpp;
+  if (spec.num_layers % chunks != 0)
+    throw SchedError(E::InvalidPolicy, "num_layers must divide evenly into pp*vpp chunks");
+  if (policy.rank < 0 || policy.rank >= cfg.pp) throw SchedError(E::InvalidPolicy, "rank out of range");
+
+  std::vector<ScheduleSlot> order = policy.order;
+  if (order.empty()) {
+    for (int mb = 0; mb < spec.num_microbatches; ++mb) {
+      order.push_back({Pass::Forward, mb, 0});
+      order.push_back({Pass::Backward, mb, 0});
+    }
+  }
+  for (const auto& s : order)
+    if (s.virtual_stage < 0 || s.virtual_stage >= cfg.vpp || s.microbatch < 0 ||
+        s.microbatch >= spec.num_microbatches)
+      throw SchedError(E::InvalidPolicy, "schedule slot outside configured ranges");
+
+  const GroupMap groups = build_process_groups(cfg, cost.topo);
+  const ProcessGroup& z3 = groups.at(GroupKind::Z3).front();
+  const ProcessGroup& z2 = groups.at(GroupKind::Z2).front();
+  const ProcessGroup& dzp = groups.at(GroupKind::DzpReplica).front();
+
+  TaskGraph g;
+  g.spec = spec;
+  g.cfg = cfg;
+  g.rank = policy.rank;
+  g.ag_slot_bytes = 2 * spec.params_per_layer;   // bf16 working copy of one layer
+  g.grad_buf_bytes = 4 * spec.params_per_layer;  // fp32 gradient of one layer
+  g.compute_flops_per_sec = cost.device_flops;
+  const double t_ag = collective_cost(CollectiveKind::AllGather, z3, g.ag_slot_bytes, cost);
+  const double t_rs = collective_cost(CollectiveKind::ReduceScatter, z2, g.grad_buf_bytes, cost);
+  const double t_fwd = spec.flops_per_token_per_layer * static_cast<double>(spec.seq_len) *
+                       static_cast<double>(spec.micro_batch_size) / cost.device_flops;
+  const double t_bwd = 2.0 * t_fwd;
+
+  const std::int64_t per_chunk = spec.num_layers / chunks;
+  auto layers_of = [&](int vstage) {
+    const std::int64_t c = std::int64_t(vstage) * cfg.pp + policy.rank;
+    std::vector<int> ls;
+    for (std::int64_t l = c * per_chunk; l < (c + 1) * per_chunk; ++l) ls.push_back(int(l));
+    return ls;
+  };
+
+  GraphWriter w(g);
+  int prev_compute = -1, last_bwd = -1;
+  std::vector<int> rs_all;
+  std::map<int, std::vector<int>> rs_of_layer;  // ascending layer iteration
+  struct Deferred { int layer, mb, vstage, bwd; };
+  std::vector<Deferred> deferred;
+
+  auto gathered_compute = [&](TaskKind kind, int l, const ScheduleSlot& s, double dur) {
+    const int ag = w.emit(TaskKind::AgParam, l, s.microbatch, s.virtual_stage, s.pass, t_ag,
+                          g.ag_slot_bytes, {});
+    std::vector<int> deps{ag};
+    if (prev_compute >= 0) deps.push_back(prev_compute);
+    prev_compute = w.emit(kind, l, s.microbatch, s.virtual_stage, s.pass, dur, 0, std::move(deps));
+    return prev_compute;
+  };
+
+  for (const auto& s : order) {
+    std::vector<int> ls = layers_of(s.virtual_stage);
+    if (s.pass == Pass::Forward) {
+      for (int l : ls) gathered_compute(TaskKind::Fwd, l, s, t_fwd);
+      continue;
+    }
+    std::reverse(ls.begin(), ls.end());
+    for (int l : ls) {
+      const int bwd = gathered_compute(TaskKind::Bwd, l, s, t_bwd);
+      last_bwd = bwd;
+      if (policy.defer_rs) {
+        deferred.push_back({l, s.microbatch, s.virtual_stage, bwd});
+        continue;
+      }
+      const int rs = w.emit(TaskKind::RsGrad, l, s.microbatch, s.virtual_stage, Pass::Backward,
+                            t_rs, g.grad_buf_bytes, {bwd});
+      rs_all.push_back(rs);
+      rs_of_layer[l].push_back(rs);
+    }
+  }
+  for (const auto& d : deferred) {
+    std::vector<int> deps{d.bwd};
+    if (last_bwd >= 0 && last_bwd != d.bwd) deps.push_back(last_bwd);
+    const int rs = w.emit(TaskKind::RsGrad, d.layer, d.mb, d.vstage, Pass::Backward, t_rs,
+                          g.grad_buf_bytes, std::move(deps));
+    rs_all.push_back(rs);
+    rs_of_layer[d.layer].push_back(rs);
+  }
+
+  // Tail: per-layer DZP all-reduce (only with >1 replica), one optimizer
+  // step, per-layer post-step all-gather of the rebuilt working copy.
+  std::vector<int> opt_deps = rs_all;
+  if (cfg.dp / cfg.z2 > 1) {
+    opt_deps.clear();
+    const std::int64_t shard_bytes = 4 * shard_elems(spec.params_per_layer, cfg.z2);
+    const double t_ar = collective_cost(CollectiveKind::AllReduce, dzp, shard_bytes, cost);
+    for (const auto& [layer, ids] : rs_of_layer)
+      opt_deps.push_back(
+          w.emit(TaskKind::ArDzp, layer, -1, 0, Pass::None, t_ar, shard_bytes, ids));
+  }
+  const int opt = w.emit(TaskKind::OptStep, -1, -1, 0, Pass::None, 0.0, 0, std::move(opt_deps));
+  for (const auto& kv : rs_of_layer)
+    w.emit(TaskKind::AgPostStep, kv.first, -1, 0, Pass::None, t_ag, g.ag_slot_bytes, {opt});
+  return g;
+}
+
+PoolSet make_pools(const TaskGraph& graph, int prelaunch_depth, int rs_slots) {
+  PoolSet p;
+  p.ag.slot_count = std::max(1, prelaunch_depth);
+  p.ag.slot_bytes = graph.ag_slot_bytes;
+  p.ag.capacity = p.ag.slot_bytes * p.ag.slot_count;
+  p.rs.slot_count = std::max(1, rs_slots);
+  p.rs.slot_bytes = graph.grad_buf_bytes;
+  p.rs.capacity = p.rs.slot_bytes * p.rs.slot_count;
+  return p;
+}
+
+int derive_prelaunch_depth(const TaskGraph& graph, std::int64_t free_budget) {
+  if (graph.ag_slot_bytes <= 0) return 1;
+  const std::int64_t hi = std::max<std::int64_t>(1, graph.spec.num_layers);
+  return static_cast<int>(std::clamp<std::int64_t>(free_budget / graph.ag_slot_bytes, 1, hi));
+}
+
+namespace {
+
+std::vector<int> first_consumers(const TaskGraph& g) {
+  std::vector<int> fc(g.tasks.size(), -1);
+  for (const auto& t : g.tasks)
+    for (int d : t.deps)
+      if (fc[d] < 0) fc[d] = t.id;
+  return fc;
+}
+
+// The ring rule shared by simulate() and the LaunchPlan: which earlier task
+// must finish before task `t` may occupy its pool slot.
+struct RingState {
+  std::vector<int> ag_order, rs_order;
+  int depth, rs_slots;
+  const std::vector<int>& fc;
+  RingState(int d, int r, const std::vector<int>& f) : depth(d), rs_slots(r), fc(f) {}
+  // returns {slot, blocking task whose end frees it (or -1), blocking AG}
+  std::pair<int, int> admit(const Task& t, int* ag_blocker) {
+    *ag_blocker = -1;
+    if (uses_ag_pool(t.kind)) {
+      const int k = static_cast<int>(ag_order.size());
+      int wait = -1;
+      if (k >= depth) {
+        const int blocking = ag_order[k - depth];
+        *ag_blocker = blocking;
+        wait = fc[blocking] >= 0 ? fc[blocking] : blocking;
+      }
+      ag_order.push_back(t.id);
+      return {k % depth, wait};
+    }
+    if (t.kind == TaskKind::RsGrad) {
+      const int k = static_cast<int>(rs_order.size());
+      const int wait = k >= rs_slots ? rs_order[k - rs_slots] : -1;
+      rs_order.push_back(t.id);
+      return {k % rs_slots, wait};
+    }
+    return {-1, -1};
+  }
+};
+
+}  // namespace
+
+Timeline simulate(const TaskGraph& graph, const PoolSet& pools, SchedMode mode) {
+  using E = SchedError::Code;
+  if (pools.ag.slot_count < 1 || pools.rs.slot_count < 1)
+    throw SchedError(E::InvalidPolicy, "pools need at least one slot each");
+  const int n = static_cast<int>(graph.tasks.size());
+  const std::vector<int> fc = first_consumers(graph);
+  RingState ring(pools.ag.slot_count, pools.rs.slot_count, fc);
+  std::vector<double> t0(n, 0.0), t1(n, 0.0);
+  double free_at[3] = {0.0, 0.0, 0.0};
+  double comm_horizon = 0.0;  // vanilla: compute may not pass issued comm
+
+  Timeline tl;
+  tl.mode = mode;
+  tl.entries.resize(n);
+  for (int id = 0; id < n; ++id) {
+    const Task& t = graph.tasks[id];
+    const StreamId sid = stream_of(t.kind);
+    double at = free_at[int(sid)];
+    for (int d : t.deps) {
+      if (d >= id) throw SchedError(E::DeadlockDetected, "dependency on a later task in issue order");
+      at = std::max(at, t1[d]);
+    }
+    if (mode == SchedMode::Vanilla && sid == StreamId::Compute) at = std::max(at, comm_horizon);
+    int ag_blocker = -1;
+    const auto [slot, wait] = ring.admit(t, &ag_blocker);
+    (void)slot;
+    if (wait >= 0) {
+      if (ag_blocker >= 0 && fc[ag_blocker] >= id)
+        throw SchedError(E::DeadlockDetected, "pool slot held by an unscheduled consumer");
+      at = std::max(at, t1[wait]);
+    }
+    t0[id] = at;
+    t1[id] = at + t.duration;
+    free_at[int(sid)] = t1[id];
+    if (mode == SchedMode::Vanilla && is_comm(t.kind)) comm_horizon = std::max(comm_horizon, t1[id]);
+    auto& e = tl.entries[id];
+    e.task_id = id;
+    e.kind = t.kind;
+    e.layer = t.layer;
+    e.microbatch = t.microbatch;
+    e.stream = sid;
+    e.start = t0[id];
+    e.end = t1[id];
+    e.bytes = t.bytes;
+  }
+  std::vector<double> last_use(n, 0.0);
+  for (const auto& t : graph.tasks)
+    for (int d : t.deps) last_use[d] = std::max(last_use[d], t1[t.id]);
+  double last_compute = 0.0;
+  for (int id = 0; id < n; ++id) {
+    auto& e = tl.entries[id];
+    e.buffer_release = std::max(t1[id], last_use[id]);
+    e.pool_release = fc[id] >= 0 ? t1[fc[id]] : t1[id];
+    tl.makespan = std::max(tl.makespan, t1[id]);
+    if (e.stream == StreamId::Compute) {
+      tl.compute_busy += graph.tasks[id].duration;
+      last_compute = std::max(last_compute, t1[id]);
+    }
+  }
+  tl.compute_idle = last_compute - tl.compute_busy;
+  return tl;
+}
+
+LaunchPlan build_launch_plan(const TaskGraph& graph, const PoolSet& pools) {
+  const std::vector<int> fc = first_consumers(graph);
+  RingState ring(pools.ag.slot_count, pools.rs.slot_count, fc);
+  LaunchPlan plan;
+  plan.depth = pools.ag.slot_count;
+  plan.rs_slots = pools.rs.slot_count;
+  plan.entries.reserve(graph.tasks.size());
+  for (const Task& t : graph.tasks) {
+    PlanEntry e;
+    e.id = t.id;
+    e.kind = t.kind;
+    e.layer = t.layer;
+    e.microbatch = t.microbatch;
+    e.stream = stream_of(t.kind);
+    int ag_blocker = -1;
+    const auto [slot, wait] = ring.admit(t, &ag_blocker);
+    if (wait >= t.id)
+      throw SchedError(SchedError::Code::DeadlockDetected, "pool slot held by an unscheduled consumer");
+    e.slot = slot;
+    e.ring_wait = wait;
+    e.waits = t.deps;
+    if (wait >= 0 && std::find(e.waits.begin(), e.waits.end(), wait) == e.waits.end())
+      e.waits.push_back(wait);
+    plan.entries.push_back(std::move(e));
+  }
+  return plan;
+}
+
+}  // namespace hzp

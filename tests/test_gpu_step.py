@@ -1,0 +1,94 @@
+"""Full train_step_hzp on the device vs the oracle (SURVEY §7.4 tiers B/C),
+plus launch-order / slot parity of the executor against the LaunchPlan.
+
+fp32 engine: ordered fp32 GEMMs (the reference's summation order) — params,
+  grads and optimizer state within 1e-5 relative (max-norm, the reference's
+  rel_diff definition, train.cpp:519-527) after N steps.
+bf16 engine: tcgen05 bf16 GEMMs with fp32 accumulation vs the reference's
+  mixed mode — within 1e-2 relative.
+"""
+import numpy as np
+import pytest
+
+from paper_2510_20111_b200 import hzp as H
+
+pytestmark = pytest.mark.gpu
+
+STEP_CONFIGS = [
+    # dims, dp, z1, z2, z3, mbs, batch, steps
+    ([12, 20, 8], 4, 4, 2, 2, 1, 4, 10),   # the CPU reference config
+    ([12, 20, 8], 4, 4, 2, 2, 2, 4, 10),
+    ([12, 20, 8], 8, 8, 4, 4, 2, 4, 5),
+    ([12, 20, 8], 8, 2, 4, 8, 1, 4, 5),
+    ([12, 20, 8], 1, 1, 1, 1, 2, 4, 5),
+    ([64, 128, 128, 64], 8, 8, 2, 2, 2, 16, 5),
+    ([64, 128, 64], 8, 8, 8, 8, 1, 32, 5),
+]
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def _run(oracle, cfg, prec, mode=1, timeline=0):
+    from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
+    dims, dp, z1, z2, z3, mbs, batch, steps = cfg
+    bf16 = bool(prec)
+    st = oracle.shard_init(dims, dp, z1, z2, z3, 2024, bf16)
+    eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=batch,
+                                 num_microbatches=mbs, par=ParallelConfig(dp=dp, z1=z1, z2=z2, z3=z3),
+                                 mode=mode, timeline=timeline))
+    eng.load_state(st)
+    for step in range(steps):
+        x = oracle.make_inputs(dims, dp, mbs, batch, 2024, step)
+        ref_losses, _ = oracle.train_step_hzp(st, x, batch, bf16)
+        losses = eng.step(x)
+    return eng, st, losses, ref_losses
+
+
+@pytest.mark.parametrize("cfg", STEP_CONFIGS, ids=lambda c: "{}-dp{}-z{}{}{}-mb{}".format("x".join(map(str, c[0])), *c[1:6]))
+def test_fp32_step_matches_oracle(gpu, oracle, cfg):
+    eng, st, losses, ref_losses = _run(oracle, cfg, 0)
+    dp = cfg[1]
+    for r in range(dp):
+        assert rel(eng.param_f32(r), st.param[r]) <= 1e-5, r
+        assert rel(eng.download(r, 2), st.master[r]) <= 1e-5, r
+        assert rel(eng.download(r, 3), st.mom[r]) <= 1e-5, r
+        assert rel(eng.download(r, 4), st.var[r]) <= 1e-5, r
+    assert rel(losses, ref_losses) <= 1e-5
+    eng.close()
+
+
+@pytest.mark.parametrize("cfg", STEP_CONFIGS, ids=lambda c: "{}-dp{}-z{}{}{}-mb{}".format("x".join(map(str, c[0])), *c[1:6]))
+def test_bf16_step_matches_oracle_mixed(gpu, oracle, cfg):
+    eng, st, losses, ref_losses = _run(oracle, cfg, 1)
+    for r in range(cfg[1]):
+        assert rel(eng.param_f32(r), st.param[r]) <= 1e-2, r
+        assert rel(eng.download(r, 2), st.master[r]) <= 1e-2, r
+    assert rel(losses, ref_losses) <= 1e-2
+    eng.close()
+
+
+@pytest.mark.parametrize("mode", [1, 0], ids=["async", "vanilla"])
+def test_launch_log_follows_plan(gpu, oracle, mode):
+    cfg = ([64, 128, 64], 8, 8, 4, 4, 2, 16, 1)
+    eng, st, _, _ = _run(oracle, cfg, 1, mode=mode, timeline=1)
+    log = eng.launch_log()
+    g = H.build_task_graph(H.ModelSpec(num_layers=2, params_per_layer=1, num_microbatches=2),
+                           H.ParallelConfig(dp=8, z1=8, z2=4, z3=4), H.CostModel(ranks_per_node=8))
+    plan = H.launch_plan(g, 2, 1)
+    assert [r[0] for r in log] == [p.id for p in plan]           # issue order == task-id order
+    assert [r[1] for r in log] == [p.kind for p in plan]
+    assert [r[5] for r in log] == [p.slot for p in plan]          # ring slots bit-exact
+    fused = [r for r in log if r[1] == H.OPT_STEP][0]
+    ids = [p.id for p in plan if p.kind in (H.AR_DZP, H.AG_POST_STEP)]
+    assert (fused[6], fused[7]) == (min(ids + [fused[0]]), max(ids + [fused[0]]))
+    tl = eng.timeline()
+    assert tl["makespan_ms"] > 0 and tl["compute_busy_ms"] > 0
+    # every task starts after each of its waits ended (device clock)
+    for p in plan:
+        for w in p.waits:
+            assert tl["start_ms"][p.id] >= tl["end_ms"][w] - 1e-3
+    eng.close()
