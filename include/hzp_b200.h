@@ -137,6 +137,24 @@ typedef struct {
 } hzp_plan_entry;
 int hzp_plan_entry_get(const hzp_graph* g, int depth, int rs_slots, int i, hzp_plan_entry* out);
 
+/* Host-side work decomposition of the P2P passes for one rank (no GPU):
+ * tiles of the layer-wise AG (per layer), the RS (per layer) and the fused
+ * Z1 stage, exactly as the device kernels consume them.  layer_off/size: the
+ * model's flat layer ranges (train.cpp:42-53 layout); working_bytes 2|4.
+ * ag_off/rs_off receive L+1 prefix offsets into `out`; *z1_off / *z1_n the
+ * Z1 range.  *n_out = total tiles (call with out=NULL to size). */
+typedef struct {
+  int64_t a_off, b_off, c_off;
+  uint64_t mask;
+  int32_t len;
+  int16_t local, src;
+  int32_t vec, pad_;
+} hzp_comm_tile;
+int hzp_comm_tiles(const hzp_parallel* par, int64_t P, const int64_t* layer_off,
+                   const int64_t* layer_size, int num_layers, int rank, int working_bytes,
+                   hzp_comm_tile* out, int cap, int* n_out, int* ag_off, int* rs_off,
+                   int* z1_off, int* z1_n);
+
 /* ---- device engine ------------------------------------------------------ */
 /* Model families.  HZP_MODEL_MLP is the reference's model (tanh MLP, loss
  * sum(y^2)/(2*B*out), flat W|b layout per layer, train.cpp:29-150).

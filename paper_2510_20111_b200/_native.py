@@ -57,6 +57,12 @@ class hzp_plan_entry(C.Structure):
                 ("num_waits", C.c_int), ("waits", C.POINTER(C.c_int))]
 
 
+class hzp_comm_tile(C.Structure):
+    _fields_ = [("a_off", C.c_int64), ("b_off", C.c_int64), ("c_off", C.c_int64),
+                ("mask", C.c_uint64), ("len", C.c_int32), ("local", C.c_int16),
+                ("src", C.c_int16), ("vec", C.c_int32), ("pad_", C.c_int32)]
+
+
 class hzp_engine_config(C.Structure):
     _fields_ = [("model", C.c_int), ("precision", C.c_int), ("num_dims", C.c_int),
                 ("dims", C.c_int * 32), ("gpt_layers", C.c_int), ("gpt_hidden", C.c_int),
@@ -97,6 +103,9 @@ SIGNATURES = [
     ("hzp_simulate", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_double), _P(C.c_double),
                                _P(hzp_sim_summary)]),
     ("hzp_plan_entry_get", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(hzp_plan_entry)]),
+    ("hzp_comm_tiles", C.c_int, [_P(hzp_parallel), C.c_int64, _P(C.c_int64), _P(C.c_int64), C.c_int,
+                                 C.c_int, C.c_int, _P(hzp_comm_tile), C.c_int, _P(C.c_int),
+                                 _P(C.c_int), _P(C.c_int), _P(C.c_int), _P(C.c_int)]),
     ("hzp_ctx_create", C.c_int, [_P(hzp_engine_config), _P(_vp)]),
     ("hzp_ctx_destroy", None, [_vp]),
     ("hzp_ctx_layout", C.c_int, [_vp, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64), _P(C.c_int64),

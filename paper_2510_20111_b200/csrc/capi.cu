@@ -2,6 +2,7 @@
 // over the C++ drop-in (hzp/config.hpp, hzp/sched.hpp) and the device engine;
 // C++ exceptions never cross this boundary: they become HZP_ERR_* codes with
 // a thread-local message (hzp_last_error).
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -210,6 +211,27 @@ int hzp_plan_entry_get(const hzp_graph* cg, int depth, int rs_slots, int i, hzp_
     out->ring_wait = e.ring_wait;
     out->num_waits = static_cast<int>(e.waits.size());
     out->waits = e.waits.data();
+  });
+}
+
+int hzp_comm_tiles(const hzp_parallel* par, int64_t P, const int64_t* layer_off,
+                   const int64_t* layer_size, int num_layers, int rank, int working_bytes,
+                   hzp_comm_tile* out, int cap, int* n_out, int* ag_off, int* rs_off,
+                   int* z1_off, int* z1_n) {
+  static_assert(sizeof(hzp_comm_tile) == sizeof(CommTile), "tile ABI");
+  if (!par || !layer_off || !layer_size || !n_out) return HZP_ERR_ARG;
+  return guarded([&] {
+    const ParallelConfig c = to_cfg(par);
+    if (rank < 0 || rank >= c.dp || c.dp > kMaxRanks) throw std::invalid_argument("rank / dp out of range");
+    std::vector<Range64> lr;
+    for (int l = 0; l < num_layers; ++l) lr.push_back({layer_off[l], layer_size[l]});
+    const TileTables T = build_comm_tiles(ShardGeom(P, c), lr, {rank}, working_bytes, c.z2 == 1);
+    *n_out = static_cast<int>(T.tiles.size());
+    if (out) std::memcpy(out, T.tiles.data(), sizeof(CommTile) * std::min<size_t>(cap, T.tiles.size()));
+    if (ag_off) std::copy(T.ag_off.begin(), T.ag_off.end(), ag_off);
+    if (rs_off) std::copy(T.rs_off.begin(), T.rs_off.end(), rs_off);
+    if (z1_off) *z1_off = T.z1_off;
+    if (z1_n) *z1_n = T.z1_n;
   });
 }
 

@@ -21,22 +21,13 @@
 #include <cstdint>
 
 #include "engine/common.cuh"
+#include "hzp/tiles.hpp"
 
 namespace hzp {
 
 constexpr int kMaxRanks = 64;
 
-struct CommTile {
-  int64_t a_off;   // AG: dst (slot) offset | RS: grad offset | Z1: chunk offset
-  int64_t b_off;   // AG: src (shard) offset | RS: gradient-buffer offset | Z1: grad-shard offset
-  int64_t c_off;   // Z1: param-shard offset
-  uint64_t mask;   // Z1: push targets, bit q = global rank q
-  int32_t len;     // elements
-  int16_t local;   // index of the destination rank among the ctx's driven ranks
-  int16_t src;     // AG: owner rank | RS: Z2 group base | Z1: Z2 segment index j
-  int32_t vec;     // 1 = every address 16-byte aligned and len a multiple of the vector
-  int32_t pad_;
-};
+// CommTile: see hzp/tiles.hpp (host-built work table).
 
 // Device-visible pointer table (one per ctx).
 struct RankTable {

@@ -26,42 +26,6 @@ namespace {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Split a contiguous element run whose streams start at offs[] (element
-// offsets into 256-byte aligned buffers of elem bytes ebytes[]) into tiles:
-// scalar head, vector body (aligned for every stream, multiple of vec
-// elements), scalar tail; bodies are cut into pieces of <= max_len.
-template <typename Emit>
-void split_run(const int64_t* offs, const int* ebytes, int nstreams, int64_t len, int vec,
-               int64_t max_len, Emit&& emit) {
-  auto aligned_at = [&](int64_t h) {
-    for (int s = 0; s < nstreams; ++s)
-      if (((offs[s] + h) * ebytes[s]) % 16 != 0) return false;
-    return true;
-  };
-  int64_t head = -1;
-  for (int64_t h = 0; h < 64 && h <= len; ++h)
-    if (aligned_at(h)) { head = h; break; }
-  if (head < 0 || len - head < vec) {
-    for (int64_t p = 0; p < len; p += max_len) emit(p, std::min(max_len, len - p), false);
-    return;
-  }
-  if (head > 0) emit(0, head, false);
-  const int64_t body = (len - head) / vec * vec;
-  const int64_t piece = std::max<int64_t>(vec, max_len / vec * vec);
-  for (int64_t p = 0; p < body; p += piece) emit(head + p, std::min(piece, body - p), true);
-  if (head + body < len) emit(head + body, len - head - body, false);
-}
-
-constexpr int64_t kTileElems = 1 << 15;
-
-uint64_t z1_targets(const ShardGeom& g, int rank, int j3) {
-  uint64_t m = 0;
-  const int base = g.z1_base(rank);
-  for (int q = base; q < base + g.z1; ++q)
-    if (q % g.z3 == j3) m |= 1ull << q;
-  return m;
-}
-
 }  // namespace
 
 Engine::Engine(const hzp_engine_config& c) : cfg(c) {
@@ -239,103 +203,19 @@ int Engine::local_index(int rank) const {
 }
 
 void Engine::build_tiles() {
-  std::vector<CommTile> tiles;
-  const int es = bf16 ? 2 : 4;
-  const int L = static_cast<int>(layers.size());
-  const ShardGeom& g = geom;
-  // AG: per layer, per driven rank, owner spans of the layer range.
-  ag_off.assign(L + 1, 0);
-  for (int l = 0; l < L; ++l) {
-    ag_off[l] = static_cast<int>(tiles.size());
-    for (size_t li = 0; li < locals.size(); ++li) {
-      const int r = locals[li].rank;
-      const int base = g.z3_base(r);
-      int64_t e = layers[l].off;
-      const int64_t end = layers[l].off + layers[l].size;
-      while (e < end) {
-        const int owner = static_cast<int>(e / g.s3);
-        const int64_t stop = std::min(end, (owner + 1) * g.s3);
-        const int64_t offs[2] = {e - layers[l].off, e - owner * g.s3};
-        const int eb[2] = {es, es};
-        split_run(offs, eb, 2, stop - e, 16 / es, kTileElems, [&](int64_t p, int64_t n, bool v) {
-          CommTile t{};
-          t.a_off = offs[0] + p;
-          t.b_off = offs[1] + p;
-          t.len = static_cast<int32_t>(n);
-          t.local = static_cast<int16_t>(li);
-          t.src = static_cast<int16_t>(base + owner);
-          t.vec = v;
-          tiles.push_back(t);
-        });
-        e = stop;
-      }
-    }
-  }
-  ag_off[L] = static_cast<int>(tiles.size());
-  // RS: per layer, per driven rank, intersection with its Z2 segment.
-  rs_off.assign(L + 1, 0);
-  for (int l = 0; l < L; ++l) {
-    rs_off[l] = static_cast<int>(tiles.size());
-    if (direct_grad) continue;
-    for (size_t li = 0; li < locals.size(); ++li) {
-      const int r = locals[li].rank;
-      const int i2 = r % g.z2;
-      const int64_t e0 = std::max(layers[l].off, i2 * g.s2);
-      const int64_t e1 = std::min(layers[l].off + layers[l].size, (i2 + 1) * g.s2);
-      if (e0 >= e1) continue;
-      const int64_t offs[2] = {e0 - i2 * g.s2, e0 - layers[l].off};
-      const int eb[2] = {4, es};
-      split_run(offs, eb, 2, e1 - e0, bf16 ? 8 : 4, kTileElems, [&](int64_t p, int64_t n, bool v) {
-        CommTile t{};
-        t.a_off = offs[0] + p;
-        t.b_off = offs[1] + p;
-        t.len = static_cast<int32_t>(n);
-        t.local = static_cast<int16_t>(li);
-        t.src = static_cast<int16_t>(g.z2_base(r));
-        t.vec = v;
-        tiles.push_back(t);
-      });
-    }
-  }
-  rs_off[L] = static_cast<int>(tiles.size());
-  // Z1: chunk of each driven rank, cut at Z2 and Z3 segment boundaries.
-  z1_off = static_cast<int>(tiles.size());
-  for (size_t li = 0; li < locals.size(); ++li) {
-    const int r = locals[li].rank;
-    const int i1 = r % g.z1;
-    int64_t e = i1 * g.s1;
-    const int64_t end = std::min(int64_t(i1 + 1) * g.s1, g.P);
-    while (e < end) {
-      const int j2 = static_cast<int>(e / g.s2), j3 = static_cast<int>(e / g.s3);
-      const int64_t stop = std::min({end, (j2 + 1) * g.s2, (j3 + 1) * g.s3});
-      const int64_t offs[3] = {e - i1 * g.s1, e - j2 * g.s2, e - j3 * g.s3};
-      const int eb[3] = {4, 4, bf16 ? 8 : 4};  // param stream: 4 bf16 = 8-byte stores
-      const uint64_t mask = z1_targets(g, r, j3);
-      // bf16 param vector stores are 8 bytes: treat as 16-byte alignment of
-      // 4-element groups by scaling its element size to 4 (offset % 4 == 0).
-      const int64_t offs_al[3] = {offs[0], offs[1], offs[2]};
-      const int eb_al[3] = {4, 4, 4};
-      (void)eb;
-      split_run(offs_al, eb_al, 3, stop - e, 4, kTileElems, [&](int64_t p, int64_t n, bool v) {
-        CommTile t{};
-        t.a_off = offs[0] + p;
-        t.b_off = offs[1] + p;
-        t.c_off = offs[2] + p;
-        t.mask = mask;
-        t.len = static_cast<int32_t>(n);
-        t.local = static_cast<int16_t>(li);
-        t.src = static_cast<int16_t>(j2);
-        t.vec = v;
-        tiles.push_back(t);
-      });
-      e = stop;
-    }
-  }
-  z1_n = static_cast<int>(tiles.size()) - z1_off;
+  std::vector<Range64> lr;
+  for (const auto& l : layers) lr.push_back({l.off, l.size});
+  std::vector<int> ranks;
+  for (const auto& l : locals) ranks.push_back(l.rank);
+  TileTables T = build_comm_tiles(geom, lr, ranks, bf16 ? 2 : 4, direct_grad);
+  ag_off = T.ag_off;
+  rs_off = T.rs_off;
+  z1_off = T.z1_off;
+  z1_n = T.z1_n;
   if (dtiles) cudaFree(dtiles);
-  HZP_CUDA(cudaMalloc(&dtiles, std::max<size_t>(1, tiles.size()) * sizeof(CommTile)));
-  if (!tiles.empty())
-    HZP_CUDA(cudaMemcpy(dtiles, tiles.data(), tiles.size() * sizeof(CommTile), cudaMemcpyHostToDevice));
+  HZP_CUDA(cudaMalloc(&dtiles, std::max<size_t>(1, T.tiles.size()) * sizeof(CommTile)));
+  if (!T.tiles.empty())
+    HZP_CUDA(cudaMemcpy(dtiles, T.tiles.data(), T.tiles.size() * sizeof(CommTile), cudaMemcpyHostToDevice));
 }
 
 void Engine::ag_layer(int layer, int slot, cudaStream_t s) {

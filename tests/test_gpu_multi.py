@@ -1,0 +1,35 @@
+"""Multi-GPU (one process per GPU, CUDA IPC peers over NVLink) parity runs.
+Skipped unless the box has >= 2 GPUs; the host-side logic of the same path
+is covered on CPU by tests/test_multiproc_cpu.py (gloo, world_size 2)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _ngpu():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.parametrize("n,z", [(2, (2, 2, 2)), (2, (2, 1, 2)), (2, (2, 2, 1)), (4, (4, 2, 2)),
+                                 (4, (4, 4, 4)), (4, (2, 4, 2))])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_multiprocess_step_matches_oracle(n, z, prec):
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n * 10 + prec),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *map(str, z), str(prec)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count(": OK") == n

@@ -1,0 +1,76 @@
+"""Kernel microbenchmarks (CUDA-event timed, warm, inputs > L2 where it matters).
+
+  python tools/bench_kernels.py gemm        # tcgen05 GEMM TFLOP/s per layout
+  python tools/bench_kernels.py comm        # AG/RS/Z1 GB/s (emulated ranks = HBM)
+Prints one JSON object per line.
+"""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2510_20111_b200.engine import gemm_bf16  # noqa: E402
+
+
+def timeit(fn, iters=20, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def bench_gemm():
+    dev = torch.device("cuda:0")
+    shapes = [(8192, 8192, 8192), (8192, 6144, 2048), (8192, 2048, 2048), (8192, 8192, 2048),
+              (8192, 2048, 8192), (2048, 8192, 8192), (6144, 2048, 8192)]
+    for (M, N, K) in shapes:
+        for a_mn, b_mn in ((0, 0), (0, 1), (1, 1)):
+            A = torch.randn(K, M, device=dev).to(torch.bfloat16) if a_mn else torch.randn(M, K, device=dev).to(torch.bfloat16)
+            B = torch.randn(K, N, device=dev).to(torch.bfloat16) if b_mn else torch.randn(N, K, device=dev).to(torch.bfloat16)
+            C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            lda = M if a_mn else K
+            ldb = N if b_mn else K
+            ms = timeit(lambda: gemm_bf16(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, lda, ldb, N,
+                                          a_mn, b_mn, 0, torch.cuda.current_stream().cuda_stream))
+            At = A.t() if a_mn else A
+            Bt = B if b_mn else B.t()
+            ms_t = timeit(lambda: torch.matmul(At, Bt))
+            tf = 2 * M * N * K / ms / 1e9
+            print(json.dumps({"kernel": "gemm_tc_bf16", "M": M, "N": N, "K": K, "a_mn": a_mn,
+                              "b_mn": b_mn, "ms": round(ms, 4), "tflops": round(tf, 1),
+                              "cublas_tflops": round(2 * M * N * K / ms_t / 1e9, 1)}), flush=True)
+
+
+def bench_comm():
+    from oracle import load_oracle  # noqa: F401  (not used for timing)
+    from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
+    # emulated dp ranks on one GPU: peer loads hit local HBM; measures the
+    # kernels' memory-level parallelism, not NVLink
+    for dims, dp in (([4096, 16384, 4096], 4), ([4096, 16384, 4096], 8)):
+        for prec in (1,):
+            eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=8,
+                                         par=ParallelConfig(dp=dp, z1=dp, z2=dp, z3=dp)))
+            eng.init_random()
+            off, n = eng.layers[0]
+            es = 2 if prec else 4
+            ms = timeit(lambda: eng.ag_layer(0, 0), iters=10)
+            # bytes moved per rank = full layer (dst) read from peers; dp ranks per launch
+            gbs = n * es * dp * 2 / ms / 1e6  # read + write
+            print(json.dumps({"kernel": "ag_pull", "dp": dp, "layer_elems": n, "ms": round(ms, 4),
+                              "GBps_hbm_rw": round(gbs, 1)}), flush=True)
+            eng.close()
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "gemm"
+    {"gemm": bench_gemm, "comm": bench_comm}[what]()
