@@ -27,6 +27,7 @@ enum EpiAct : int {
   kActGelu = 2,       // C = gelu_tanh(acc + bias), aux <- acc + bias (pre-activation)
   kActTanhGrad = 3,   // C = acc * (1 - a*a), a = aux[m, n]   (MLP dgrad, train.cpp:142-143)
   kActGeluGrad = 4,   // C = acc * gelu'(aux[m, n])           (GPT FC1 dgrad)
+  kActSoftmaxGrad = 5,  // C = alpha * aux[m, n] * (acc - rowvec[m])  (attention dS)
 };
 
 struct Epilogue {
@@ -39,13 +40,26 @@ struct Epilogue {
   void* aux = nullptr;        // [M, ldaux] pre-activation out (Gelu) / activation in (grads)
   int aux_bf16 = 1;
   int ldaux = 0;
-  float* rowsum = nullptr;    // unused placeholder for future fused reductions
+  float alpha = 1.f;          // acc *= alpha before bias / activation
+  const void* resid = nullptr;  // bf16 [M, ldres]: C = resid + f(acc)  (residual stream)
+  int ldres = 0;
+  const float* rowvec = nullptr;  // fp32 per-row vector (softmax-grad D), batch strides below
+  int64_t rv_sh = 0, rv_sb = 0;
 };
 
 struct GemmShape {
   int M, N, K;
   int lda, ldb;
   int a_mn, b_mn;  // 1 = MN-major storage
+  // Batched (attention): z = zb * nh + zh; operand X of batch z starts at
+  // X + zh * x_sh + zb * x_sb elements.  C, aux and resid share C's strides.
+  int nh = 1, nb = 1;
+  int64_t a_sh = 0, a_sb = 0, b_sh = 0, b_sb = 0, c_sh = 0, c_sb = 0;
+  // Causal structure of the attention products (M = query or key rows):
+  //  1: skip tiles entirely above the diagonal (n0 >= m0 + 128)  S, dP
+  //  2: K range [0, m0 + 128)                                      O = PV, dQ
+  //  3: K range [m0, K)                                            dV, dK
+  int causal = 0;
 };
 
 // bf16 x bf16 -> fp32 accumulate on the 5th-gen tensor cores (tcgen05.mma,

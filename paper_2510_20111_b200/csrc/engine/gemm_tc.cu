@@ -64,6 +64,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -128,10 +136,31 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
 
 struct TcParams {
   int M, N, K;
-  int tiles_m, tiles_n, num_tiles;
+  int tiles_m, tiles_n, tiles_mn, num_tiles;
+  int nh, causal;
+  int64_t c_sh, c_sb;
   Epilogue e;
   void* C;
 };
+
+// Tile t -> (m0, n0, zh, zb); z slowest so concurrent CTAs share operands.
+struct TileCoord {
+  int m0, n0, zh, zb;
+};
+__device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int t, int bn) {
+  const int z = t / p.tiles_mn;
+  const int r = t - z * p.tiles_mn;
+  return {(r % p.tiles_m) * BM, (r / p.tiles_m) * bn, z % p.nh, z / p.nh};
+}
+// K-block range of a tile under the causal mode (see GemmShape::causal).
+__device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int& kb0, int& kb1) {
+  const int nkb = (p.K + BK - 1) / BK;
+  kb0 = 0;
+  kb1 = nkb;
+  if (p.causal == 1 && n0 >= m0 + BM) kb1 = 0;  // fully masked tile: no work
+  else if (p.causal == 2) kb1 = min(nkb, (m0 + BM + BK - 1) / BK);
+  else if (p.causal == 3) kb0 = min(nkb, m0 / BK);
+}
 
 template <int BN, int A_MN, int B_MN, int STAGES>
 __global__ void __launch_bounds__(kThreadsTC, 1)
@@ -175,15 +204,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
-  const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int m0 = (t % p.tiles_m) * BM, n0 = (t / p.tiles_m) * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const TileCoord tc = tile_coord(p, t, BN);
+        int kb0, kb1;
+        kb_range(p, tc.m0, tc.n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -191,15 +221,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const int k0 = kb * BK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (BK * 128), &tmA, &full[stage], m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_4d(sa + j * (BK * 128), &tmA, &full[stage], tc.m0 + 64 * j, k0, tc.zh, tc.zb);
           } else {
-            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+            tma_load_4d(sa, &tmA, &full[stage], k0, tc.m0, tc.zh, tc.zb);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (BK * 128), &tmB, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_4d(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, tc.zh, tc.zb);
           } else {
-            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            tma_load_4d(sb, &tmB, &full[stage], k0, tc.n0, tc.zh, tc.zb);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -212,10 +244,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(p, t, BN);
+        int kb0, kb1;
+        kb_range(p, tc.m0, tc.n0, kb0, kb1);
+        if (kb1 <= kb0) continue;  // skipped tile: the epilogue skips it too
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
@@ -228,7 +264,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                      : smem_desc(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc(sb + k * 2048, BK * 128, 1024)
                                      : smem_desc(sb + k * 32, 16, 1024);
-            tc_mma(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+            tc_mma(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);  // frees this smem stage when the MMAs retire
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -244,11 +280,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int m0 = (t % p.tiles_m) * BM, n0 = (t / p.tiles_m) * BN;
+      const TileCoord tc = tile_coord(p, t, BN);
+      int kb0, kb1;
+      kb_range(p, tc.m0, tc.n0, kb0, kb1);
+      if (kb1 <= kb0) continue;
+      const int m0 = tc.m0, n0 = tc.n0;
+      const int64_t zoff = int64_t(tc.zh) * p.c_sh + int64_t(tc.zb) * p.c_sb;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int m = m0 + quarter * 32 + lane;
       const bool row_ok = m < p.M;
+      float rv = 0.f;
+      if (e.act == kActSoftmaxGrad && row_ok)
+        rv = e.rowvec[int64_t(tc.zh) * e.rv_sh + int64_t(tc.zb) * e.rv_sb + m];
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -257,7 +301,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         if (!row_ok || nb >= p.N) continue;
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * e.alpha;
         const bool full_chunk = nb + 32 <= p.N;
         if (e.bias_any) {
           const uint16_t* b = static_cast<const uint16_t*>(e.bias_any) + nb;
@@ -273,23 +317,62 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = tanhf(v[j]);
         } else if (e.act == kActGelu) {
-          uint16_t* aux = static_cast<uint16_t*>(e.aux) + int64_t(m) * e.ldaux + nb;
+          uint16_t* aux = static_cast<uint16_t*>(e.aux) + zoff + int64_t(m) * e.ldaux + nb;
+          if (full_chunk) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (full_chunk || nb + j < p.N) aux[j] = f32_to_bf16_bits(v[j]);
-            v[j] = gelu_tanh(v[j]);
+            for (int q = 0; q < 4; ++q) {
+              uint4 w;
+              w.x = uint32_t(f32_to_bf16_bits(v[8 * q + 0])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 1])) << 16);
+              w.y = uint32_t(f32_to_bf16_bits(v[8 * q + 2])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 3])) << 16);
+              w.z = uint32_t(f32_to_bf16_bits(v[8 * q + 4])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 5])) << 16);
+              w.w = uint32_t(f32_to_bf16_bits(v[8 * q + 6])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 7])) << 16);
+              reinterpret_cast<uint4*>(aux)[q] = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && nb + j < p.N; ++j) aux[j] = f32_to_bf16_bits(v[j]);
           }
-        } else if (e.act == kActTanhGrad || e.act == kActGeluGrad) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (!(full_chunk || nb + j < p.N)) continue;
-            const int64_t ai = int64_t(m) * e.ldaux + nb + j;
-            const float a = e.aux_bf16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(e.aux)[ai])
-                                       : static_cast<const float*>(e.aux)[ai];
-            v[j] *= e.act == kActTanhGrad ? (1.f - a * a) : gelu_tanh_grad(a);
+          for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+        } else if (e.act == kActTanhGrad || e.act == kActGeluGrad || e.act == kActSoftmaxGrad) {
+          const int64_t ab = zoff + int64_t(m) * e.ldaux + nb;
+          float a[32];
+          if (e.aux_bf16 && full_chunk) {
+            const uint4* ap = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.aux) + ab);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 w = ap[q];
+              a[8 * q + 0] = __uint_as_float(w.x << 16); a[8 * q + 1] = __uint_as_float(w.x & 0xFFFF0000u);
+              a[8 * q + 2] = __uint_as_float(w.y << 16); a[8 * q + 3] = __uint_as_float(w.y & 0xFFFF0000u);
+              a[8 * q + 4] = __uint_as_float(w.z << 16); a[8 * q + 5] = __uint_as_float(w.z & 0xFFFF0000u);
+              a[8 * q + 6] = __uint_as_float(w.w << 16); a[8 * q + 7] = __uint_as_float(w.w & 0xFFFF0000u);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              a[j] = (full_chunk || nb + j < p.N)
+                         ? (e.aux_bf16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(e.aux)[ab + j])
+                                       : static_cast<const float*>(e.aux)[ab + j])
+                         : 0.f;
+          }
+          if (e.act == kActTanhGrad) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= 1.f - a[j] * a[j];
+          } else if (e.act == kActGeluGrad) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= gelu_tanh_grad(a[j]);
+          } else {
+            // v = alpha * acc already; dS = P * (alpha*dP - alpha*D) with alpha folded
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = a[j] * (v[j] - e.alpha * rv);
           }
         }
-        const int64_t ci = int64_t(m) * e.ldc + nb;
+        if (e.resid) {
+          const uint16_t* rp = static_cast<const uint16_t*>(e.resid) + zoff + int64_t(m) * e.ldres + nb;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (full_chunk || nb + j < p.N) v[j] += bf16_bits_to_f32(rp[j]);
+        }
+        const int64_t ci = zoff + int64_t(m) * e.ldc + nb;
         if (e.out_bf16) {
           uint16_t* out = static_cast<uint16_t*>(p.C) + ci;
           if (full_chunk && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
@@ -357,6 +440,7 @@ __global__ void gemm_bf16_simt_kernel(const uint16_t* __restrict__ A, const uint
   }
   if (e.bias_any) acc += bf16_bits_to_f32(static_cast<const uint16_t*>(e.bias_any)[n]);
   else if (e.bias) acc += e.bias[n];
+  acc *= e.alpha;
   float v = acc;
   if (e.act == kActTanh) v = tanhf(acc);
   else if (e.act == kActGelu) {
@@ -393,15 +477,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D bf16 tensor map: inner extent `inner` (contiguous), outer extent
-// `outer`, row pitch `ld` elements, box {64, box_outer}, 128-byte swizzle.
-CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+// 4-D bf16 tensor map {inner, outer, nh, nb}: row pitch `ld` elements, batch
+// strides sh / sb elements, box {64, box_outer, 1, 1}, 128-byte swizzle.
+CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer,
+                     int nh, int nb, int64_t sh, int64_t sb) {
   CUtensorMap m;
-  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
-  cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
-  cuuint32_t box[2] = {64, cuuint32_t(box_outer)};
-  cuuint32_t estr[2] = {1, 1};
-  const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+  if (nh <= 1) sh = ld * outer;
+  if (nb <= 1) sb = sh * nh;
+  cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(nh), cuuint64_t(nb)};
+  cuuint64_t strides[3] = {cuuint64_t(ld) * 2, cuuint64_t(sh) * 2, cuuint64_t(sb) * 2};
+  cuuint32_t box[4] = {64, cuuint32_t(box_outer), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -420,15 +507,22 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
     HZP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
     attr_set = true;
   }
-  const CUtensorMap ta = A_MN ? make_map(A, s.M, s.K, s.lda, BK) : make_map(A, s.K, s.M, s.lda, BM);
-  const CUtensorMap tb = B_MN ? make_map(B, s.N, s.K, s.ldb, BK) : make_map(B, s.K, s.N, s.ldb, BN);
+  const CUtensorMap ta = A_MN ? make_map(A, s.M, s.K, s.lda, BK, s.nh, s.nb, s.a_sh, s.a_sb)
+                              : make_map(A, s.K, s.M, s.lda, BM, s.nh, s.nb, s.a_sh, s.a_sb);
+  const CUtensorMap tb = B_MN ? make_map(B, s.N, s.K, s.ldb, BK, s.nh, s.nb, s.b_sh, s.b_sb)
+                              : make_map(B, s.K, s.N, s.ldb, BN, s.nh, s.nb, s.b_sh, s.b_sb);
   TcParams p;
   p.M = s.M;
   p.N = s.N;
   p.K = s.K;
   p.tiles_m = (s.M + BM - 1) / BM;
   p.tiles_n = (s.N + BN - 1) / BN;
-  p.num_tiles = p.tiles_m * p.tiles_n;
+  p.tiles_mn = p.tiles_m * p.tiles_n;
+  p.num_tiles = p.tiles_mn * s.nh * s.nb;
+  p.nh = s.nh;
+  p.causal = s.causal;
+  p.c_sh = s.c_sh;
+  p.c_sb = s.c_sb;
   p.e = e;
   p.C = C;
   const int grid = p.num_tiles < g_sm_budget ? p.num_tiles : g_sm_budget;
@@ -459,6 +553,8 @@ void gemm_tc_bf16(const void* A, const void* B, void* C, const GemmShape& s, con
                       (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                       (reinterpret_cast<uintptr_t>(B) % 16 == 0);
   if (!tma_ok) {
+    if (s.nh * s.nb != 1 || s.causal || e.resid || e.act == kActSoftmaxGrad)
+      throw std::invalid_argument("batched/causal GEMMs need TMA-compatible (16-byte) layouts");
     dim3 grid((s.N + 127) / 128, s.M);
     gemm_bf16_simt_kernel<<<grid, 128, 0, stream>>>(static_cast<const uint16_t*>(A),
                                                     static_cast<const uint16_t*>(B), C, s, e);

@@ -1,0 +1,389 @@
+// Non-GEMM kernels of the GPT decoder.  See gpt_ops.cuh.
+#include <cmath>
+
+#include "engine/gemm.cuh"
+#include "engine/gpt_ops.cuh"
+
+namespace hzp {
+namespace {
+
+constexpr int kT = 256;       // threads per row-CTA
+constexpr int kMaxVec = 4;    // <= 4 x 8 bf16 per thread  -> h <= 8192
+
+__device__ __forceinline__ void unpack8(uint4 v, float* f) {
+  f[0] = __uint_as_float(v.x << 16); f[1] = __uint_as_float(v.x & 0xFFFF0000u);
+  f[2] = __uint_as_float(v.y << 16); f[3] = __uint_as_float(v.y & 0xFFFF0000u);
+  f[4] = __uint_as_float(v.z << 16); f[5] = __uint_as_float(v.z & 0xFFFF0000u);
+  f[6] = __uint_as_float(v.w << 16); f[7] = __uint_as_float(v.w & 0xFFFF0000u);
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 v;
+  v.x = uint32_t(f32_to_bf16_bits(f[0])) | (uint32_t(f32_to_bf16_bits(f[1])) << 16);
+  v.y = uint32_t(f32_to_bf16_bits(f[2])) | (uint32_t(f32_to_bf16_bits(f[3])) << 16);
+  v.z = uint32_t(f32_to_bf16_bits(f[4])) | (uint32_t(f32_to_bf16_bits(f[5])) << 16);
+  v.w = uint32_t(f32_to_bf16_bits(f[6])) | (uint32_t(f32_to_bf16_bits(f[7])) << 16);
+  return v;
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int i = 0; i < int(blockDim.x >> 5); ++i) s += red[i];
+  return s;
+}
+__device__ __forceinline__ float block_max(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = -INFINITY;
+  for (int i = 0; i < int(blockDim.x >> 5); ++i) s = fmaxf(s, red[i]);
+  return s;
+}
+
+__global__ void __launch_bounds__(kT) embed_fwd_kernel(const int* __restrict__ tok,
+                                                       const uint16_t* __restrict__ wte,
+                                                       const uint16_t* __restrict__ wpe,
+                                                       uint16_t* __restrict__ x, int S, int h) {
+  const int t = blockIdx.x;
+  const int bi = t / S, s = t % S;
+  const int id = tok[bi * (S + 1) + s];
+  const uint4* a = reinterpret_cast<const uint4*>(wte + int64_t(id) * h);
+  const uint4* p = reinterpret_cast<const uint4*>(wpe + int64_t(s) * h);
+  uint4* o = reinterpret_cast<uint4*>(x + int64_t(t) * h);
+  for (int v = threadIdx.x; v < h / 8; v += blockDim.x) {
+    float fa[8], fp[8];
+    unpack8(a[v], fa);
+    unpack8(p[v], fp);
+    for (int j = 0; j < 8; ++j) fa[j] += fp[j];
+    o[v] = pack8(fa);
+  }
+}
+
+__global__ void __launch_bounds__(kT) embed_bwd_kernel(const int* __restrict__ tok,
+                                                       const uint16_t* __restrict__ dx,
+                                                       float* __restrict__ dwte,
+                                                       float* __restrict__ dwpe, int S, int h) {
+  const int t = blockIdx.x;
+  const int bi = t / S, s = t % S;
+  const int id = tok[bi * (S + 1) + s];
+  const uint4* d = reinterpret_cast<const uint4*>(dx + int64_t(t) * h);
+  for (int v = threadIdx.x; v < h / 8; v += blockDim.x) {
+    float f[8];
+    unpack8(d[v], f);
+    float4* a = reinterpret_cast<float4*>(dwte + int64_t(id) * h + 8 * v);
+    float4* p = reinterpret_cast<float4*>(dwpe + int64_t(s) * h + 8 * v);
+    atomicAdd(a, make_float4(f[0], f[1], f[2], f[3]));
+    atomicAdd(a + 1, make_float4(f[4], f[5], f[6], f[7]));
+    atomicAdd(p, make_float4(f[0], f[1], f[2], f[3]));
+    atomicAdd(p + 1, make_float4(f[4], f[5], f[6], f[7]));
+  }
+}
+
+__global__ void __launch_bounds__(kT) layernorm_fwd_kernel(const uint16_t* __restrict__ x,
+                                                           const uint16_t* __restrict__ g,
+                                                           const uint16_t* __restrict__ be,
+                                                           uint16_t* __restrict__ y,
+                                                           float* __restrict__ mu,
+                                                           float* __restrict__ rs, int h) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+  float v[kMaxVec][8];
+  float s = 0.f;
+  const int nv = h / 8;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kT;
+    if (i < nv) {
+      unpack8(xr[i], v[k]);
+      for (int j = 0; j < 8; ++j) s += v[k][j];
+    }
+  }
+  const float mean = block_sum(s, red) / h;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k)
+    if (threadIdx.x + k * kT < nv)
+      for (int j = 0; j < 8; ++j) {
+        const float d = v[k][j] - mean;
+        q += d * d;
+      }
+  const float rstd = rsqrtf(block_sum(q, red) / h + 1e-5f);
+  if (threadIdx.x == 0) {
+    mu[r] = mean;
+    rs[r] = rstd;
+  }
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  const uint4* br = reinterpret_cast<const uint4*>(be);
+  uint4* yr = reinterpret_cast<uint4*>(y + int64_t(r) * h);
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kT;
+    if (i < nv) {
+      float gg[8], bb[8], o[8];
+      unpack8(gr[i], gg);
+      unpack8(br[i], bb);
+      for (int j = 0; j < 8; ++j) o[j] = (v[k][j] - mean) * rstd * gg[j] + bb[j];
+      yr[i] = pack8(o);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT) layernorm_bwd_kernel(
+    const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
+    const float* __restrict__ mu, const float* __restrict__ rs, const uint16_t* __restrict__ resid,
+    uint16_t* __restrict__ dx, float* __restrict__ part, int chunks, int rows, int h) {
+  __shared__ float red[32];
+  const int nv = h / 8;
+  const int per = (rows + chunks - 1) / chunks;
+  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float pg[kMaxVec][8], pb[kMaxVec][8], gg[kMaxVec][8];
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kT;
+    for (int j = 0; j < 8; ++j) pg[k][j] = pb[k][j] = 0.f;
+    if (i < nv) unpack8(reinterpret_cast<const uint4*>(g)[i], gg[k]);
+  }
+  for (int r = r0; r < r1; ++r) {
+    const float m = mu[r], rstd = rs[r];
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+    float xh[kMaxVec][8], dg[kMaxVec][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = threadIdx.x + k * kT;
+      if (i < nv) {
+        float d[8];
+        unpack8(dyr[i], d);
+        unpack8(xr[i], xh[k]);
+        for (int j = 0; j < 8; ++j) {
+          xh[k][j] = (xh[k][j] - m) * rstd;
+          dg[k][j] = d[j] * gg[k][j];
+          s1 += dg[k][j];
+          s2 += dg[k][j] * xh[k][j];
+          pg[k][j] += d[j] * xh[k][j];
+          pb[k][j] += d[j];
+        }
+      }
+    }
+    const float a1 = block_sum(s1, red) / h;
+    const float a2 = block_sum(s2, red) / h;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
+    const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + int64_t(r) * h) : nullptr;
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = threadIdx.x + k * kT;
+      if (i < nv) {
+        float o[8], rv[8];
+        if (rr) unpack8(rr[i], rv);
+        for (int j = 0; j < 8; ++j) {
+          o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
+          if (rr) o[j] += rv[j];
+        }
+        dxr[i] = pack8(o);
+      }
+    }
+  }
+  float* pgo = part + int64_t(blockIdx.x) * h;
+  float* pbo = part + int64_t(chunks + blockIdx.x) * h;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kT;
+    if (i < nv)
+      for (int j = 0; j < 8; ++j) {
+        pgo[8 * i + j] = pg[k][j];
+        pbo[8 * i + j] = pb[k][j];
+      }
+  }
+}
+
+__global__ void colsum_partial_kernel(const uint16_t* __restrict__ d, int rows, int cols,
+                                      float* __restrict__ part, int chunks) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column vector index
+  if (v * 8 >= cols) return;
+  const int per = (rows + chunks - 1) / chunks;
+  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = r0; r < r1; ++r) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(d + int64_t(r) * cols)[v], f);
+    for (int j = 0; j < 8; ++j) acc[j] += f[j];
+  }
+  float4* o = reinterpret_cast<float4*>(part + int64_t(blockIdx.y) * cols + 8 * v);
+  o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+__device__ __forceinline__ void write_mode(void* out, int64_t i, float v, int out_bf16, int mode) {
+  if (out_bf16) {
+    static_cast<uint16_t*>(out)[i] = f32_to_bf16_bits(v);
+  } else {
+    float* p = static_cast<float*>(out) + i;
+    *p = mode == kEpiAccum ? *p + v : (mode == kEpiAssign0 ? __fadd_rn(0.f, v) : v);
+  }
+}
+
+__global__ void colsum_finalize_kernel(const float* __restrict__ part, int chunks, int cols,
+                                       void* out, int out_bf16, int mode) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int k = 0; k < chunks; ++k) s += part[int64_t(k) * cols + c];
+  write_mode(out, c, s, out_bf16, mode);
+}
+
+__global__ void grad_write_kernel(const float* __restrict__ src, int64_t n, void* out, int out_bf16,
+                                  int mode) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    write_mode(out, i, src[i], out_bf16, mode);
+}
+
+// one warp per (z, q) row
+__global__ void softmax_causal_kernel(const float* __restrict__ S, uint16_t* __restrict__ P, int Z,
+                                      int Sq) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= Z * Sq) return;
+  const int q = row % Sq;
+  const float* s = S + int64_t(row) * Sq;
+  uint16_t* p = P + int64_t(row) * Sq;
+  const int n = q + 1;
+  const float kL2E = 1.4426950408889634f;
+  float mx = -INFINITY;
+  for (int k = lane; k < n; k += 32) mx = fmaxf(mx, s[k]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+  for (int k = lane; k < n; k += 32) sum += exp2f((s[k] - mx) * kL2E);
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = 1.f / sum;
+  const int zend = min(Sq, (q / 128 + 1) * 128);
+  for (int k = lane; k < zend; k += 32)
+    p[k] = f32_to_bf16_bits(k < n ? exp2f((s[k] - mx) * kL2E) * inv : 0.f);
+}
+
+// one warp per (token, head)
+__global__ void attn_rowdot_kernel(const uint16_t* __restrict__ dO, const uint16_t* __restrict__ O,
+                                   float* __restrict__ D, int b, int nh, int S, int hd) {
+  const int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (w >= b * S * nh) return;
+  const int hh = w % nh, t = w / nh;
+  const int bi = t / S, s = t % S;
+  const int64_t base = int64_t(t) * nh * hd + int64_t(hh) * hd;
+  float acc = 0.f;
+  for (int d = lane * 2; d < hd; d += 64) {
+    const uint32_t a = *reinterpret_cast<const uint32_t*>(dO + base + d);
+    const uint32_t c = *reinterpret_cast<const uint32_t*>(O + base + d);
+    acc += __uint_as_float(a << 16) * __uint_as_float(c << 16) +
+           __uint_as_float(a & 0xFFFF0000u) * __uint_as_float(c & 0xFFFF0000u);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) D[(int64_t(bi) * nh + hh) * S + s] = acc;
+}
+
+// one CTA per token row of the logits
+__global__ void __launch_bounds__(kT) cross_entropy_kernel(uint16_t* __restrict__ logits,
+                                                           const int* __restrict__ tok, int S,
+                                                           int V, float inv_T,
+                                                           float* __restrict__ loss) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const int bi = t / S, s = t % S;
+  const int target = tok[bi * (S + 1) + s + 1];
+  uint16_t* row = logits + int64_t(t) * V;
+  const int nv = V / 8;
+  const float kL2E = 1.4426950408889634f;
+  float mx = -INFINITY, sum = 0.f;  // online softmax per thread
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(row)[v], f);
+    float m2 = mx;
+    for (int j = 0; j < 8; ++j) m2 = fmaxf(m2, f[j]);
+    sum *= exp2f((mx - m2) * kL2E);
+    for (int j = 0; j < 8; ++j) sum += exp2f((f[j] - m2) * kL2E);
+    mx = m2;
+  }
+  const float gmax = block_max(mx, red);
+  sum = mx == -INFINITY ? 0.f : sum * exp2f((mx - gmax) * kL2E);
+  const float gsum = block_sum(sum, red);
+  const float lse = gmax + logf(gsum);
+  const float xt = bf16_bits_to_f32(row[target]);
+  __syncthreads();
+  const float inv = 1.f / gsum;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    float f[8];
+    unpack8(reinterpret_cast<const uint4*>(row)[v], f);
+    for (int j = 0; j < 8; ++j) {
+      const float p = exp2f((f[j] - gmax) * kL2E) * inv;
+      f[j] = (p - ((8 * v + j) == target ? 1.f : 0.f)) * inv_T;
+    }
+    reinterpret_cast<uint4*>(row)[v] = pack8(f);
+  }
+  if (threadIdx.x == 0) atomicAdd(loss, (lse - xt) * inv_T);
+}
+
+}  // namespace
+
+void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int b, int S,
+               int h, cudaStream_t s) {
+  embed_fwd_kernel<<<b * S, kT, 0, s>>>(tokens, wte, wpe, x, S, h);
+  HZP_LAUNCH_CHECK();
+}
+void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, int b, int S, int h,
+               cudaStream_t s) {
+  embed_bwd_kernel<<<b * S, kT, 0, s>>>(tokens, dx, dwte, dwpe, S, h);
+  HZP_LAUNCH_CHECK();
+}
+void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
+                   float* mu, float* rstd, int rows, int h, cudaStream_t s) {
+  if (h % 8 || h > 8 * kT * kMaxVec) throw std::invalid_argument("layernorm: h % 8 != 0 or > 8192");
+  layernorm_fwd_kernel<<<rows, kT, 0, s>>>(x, g, beta, y, mu, rstd, h);
+  HZP_LAUNCH_CHECK();
+}
+void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
+                   const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
+                   int rows, int h, cudaStream_t s) {
+  layernorm_bwd_kernel<<<chunks, kT, 0, s>>>(dy, x, g, mu, rstd, resid, dx, part, chunks, rows, h);
+  HZP_LAUNCH_CHECK();
+}
+void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s) {
+  dim3 grid((cols / 8 + 127) / 128, chunks);
+  colsum_partial_kernel<<<grid, 128, 0, s>>>(d, rows, cols, part, chunks);
+  HZP_LAUNCH_CHECK();
+}
+void colsum_finalize(const float* part, int chunks, int cols, void* out, int out_bf16, int mode,
+                     cudaStream_t s) {
+  colsum_finalize_kernel<<<(cols + 255) / 256, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
+  HZP_LAUNCH_CHECK();
+}
+void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s) {
+  grad_write_kernel<<<4 * kNumSMs, 256, 0, s>>>(src, n, out, out_bf16, mode);
+  HZP_LAUNCH_CHECK();
+}
+void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s) {
+  const int rows = Z * Sq;
+  softmax_causal_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
+  HZP_LAUNCH_CHECK();
+}
+void attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int b, int nh, int S, int hd,
+                 cudaStream_t s) {
+  const int warps = b * S * nh;
+  attn_rowdot_kernel<<<(warps + 7) / 8, 256, 0, s>>>(dO, O, D, b, nh, S, hd);
+  HZP_LAUNCH_CHECK();
+}
+void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* loss,
+                   cudaStream_t s) {
+  if (V % 8) throw std::invalid_argument("vocab must be a multiple of 8");
+  cross_entropy_kernel<<<b * S, kT, 0, s>>>(logits, tokens, S, V, 1.f / float(b * S), loss);
+  HZP_LAUNCH_CHECK();
+}
+
+}  // namespace hzp

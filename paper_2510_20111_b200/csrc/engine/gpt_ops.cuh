@@ -1,0 +1,48 @@
+// Non-GEMM kernels of the GPT decoder (bf16 activations, fp32 statistics).
+// All are HBM-bound row/column passes: 16-byte vector access, one CTA (or
+// warp) per row, grids sized in multiples of the 148 SMs.
+#pragma once
+
+#include <cstdint>
+
+#include "engine/common.cuh"
+
+namespace hzp {
+
+// x[t] = wte[tok[t]] + wpe[t % S]; tokens laid out [b][S+1] (inputs = [:, :S]).
+void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int b, int S,
+               int h, cudaStream_t s);
+// Scatter-add dx rows into fp32 scratch: dwte[tok[t]] += dx[t], dwpe[s] += dx[t].
+void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, int b, int S, int h,
+               cudaStream_t s);
+
+// LayerNorm over h (eps 1e-5): y = (x - mu) * rstd * g + beta; saves mu, rstd.
+void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
+                   float* mu, float* rstd, int rows, int h, cudaStream_t s);
+// dx = resid + rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)); per-chunk
+// partial column sums of dy*xhat (dg) and dy (dbeta) into part[2][chunks][h].
+void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
+                   const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
+                   int rows, int h, cudaStream_t s);
+
+// Column sums of a bf16 [rows, cols] matrix into fp32 partials [chunks][cols].
+void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s);
+// out[c] (mode, dtype) <- sum over chunks of part[k][c]  (+ optional 2nd slab)
+void colsum_finalize(const float* part, int chunks, int cols, void* out, int out_bf16, int mode,
+                     cudaStream_t s);
+// out[i] (mode, dtype) <- src[i] (fp32 scratch -> gradient target)
+void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s);
+
+// Causal softmax of fp32 scores S[z][q][k] (already scaled): P = exp(S - lse)
+// for k <= q, 0 for q < k < 128*ceil((q+1)/128); P bf16, same layout.
+void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s);
+// D[z][q] = sum_d dO[b, q, head, d] * O[b, q, head, d]  (rows of [T, h] head slices)
+void attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int b, int nh, int S, int hd,
+                 cudaStream_t s);
+
+// Fused softmax cross-entropy over rows of bf16 logits [T, V]: loss +=
+// sum_t (lse - logit[target]) / T; logits <- (softmax - onehot) / T in place.
+void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* loss,
+                   cudaStream_t s);
+
+}  // namespace hzp

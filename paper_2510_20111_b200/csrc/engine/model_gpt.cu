@@ -1,10 +1,421 @@
-// GPT decoder model (filled in by a later milestone).
-#include <stdexcept>
+// GPT-style decoder on the engine (BASELINE configs[1]: 1.3B-class, seq 2048).
+//
+// Task-graph layers (the unit of layer-wise AG / RS):
+//   layer 0        embedding: wte [V, h] | wpe [S, h]
+//   layer 1..L     decoder block (pre-LN):
+//                  ln1_g ln1_b [h] | w_qkv [3h, h] | b_qkv [3h] | w_o [h, h] | b_o [h] |
+//                  ln2_g ln2_b [h] | w_fc1 [f, h] | b_fc1 [f] | w_fc2 [h, f] | b_fc2 [h]
+//   layer L+1      head: lnf_g lnf_b [h] | w_head [V, h]  (untied)
+// Every matrix is row-major [out, in] like the reference's W (train.cpp:42-53),
+// so all three products of each linear layer map onto the tcgen05 GEMM
+// without transposes (gemm.cuh).  Attention runs as batched causal tcgen05
+// GEMMs over (sequence, head): S = QK^T * d^-1/2 (fp32, upper tiles skipped),
+// causal softmax, O = PV; backward dS = P * (dP - rowdot(dO, O)), dQ, dK, dV.
+#include <cmath>
+#include <vector>
 
+#include "engine/gemm.cuh"
+#include "engine/gpt_ops.cuh"
 #include "engine/model.hpp"
 
 namespace hzp {
-std::unique_ptr<Model> make_gpt_model(const ModelConfig&) {
-  throw std::invalid_argument("GPT model not built yet");
-}
+namespace {
+
+struct BlockOff {  // element offsets inside a block's parameter range
+  int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2, size;
+};
+
+struct LayerActs {  // saved activations of one block (one microbatch)
+  uint16_t *ln1, *qkv, *P, *attn, *xm, *ln2, *fpre, *fact;
+  float *mu1, *rs1, *mu2, *rs2;
+};
+
+struct GptBuffers {
+  std::vector<uint16_t*> x;  // x[0..L+1]: x[l] = input of task-layer l (x[1] = embedding out)
+  std::vector<LayerActs> acts;  // [L+2] (only 1..L used)
+  uint16_t* lnf = nullptr;
+  float *muf = nullptr, *rsf = nullptr;
+  uint16_t* logits = nullptr;  // [T, V]; dlogits in place after the fused CE
+  float* S = nullptr;          // [Z, S, S] fp32 scores
+  uint16_t* dS = nullptr;      // [Z, S, S]
+  float* D = nullptr;          // [Z, S]
+  uint16_t* dx[2] = {nullptr, nullptr};
+  int cur = 0;
+  uint16_t *dln = nullptr, *dqkv = nullptr, *dattn = nullptr, *dfc1 = nullptr, *dxm = nullptr;
+  float* part = nullptr;       // column-sum partials
+  float* emb = nullptr;        // fp32 scratch for the embedding gradient [V*h + S*h]
+  float* loss = nullptr;
+  const int* tokens = nullptr;  // current microbatch
+};
+
+constexpr int kChunks = 2 * kNumSMs;
+
+class GptModel final : public Model {
+ public:
+  explicit GptModel(const ModelConfig& c) : c_(c) {
+    h_ = c.hidden;
+    nh_ = c.heads;
+    hd_ = h_ / nh_;
+    f_ = c.ffn;
+    V_ = c.vocab;
+    S_ = c.seq;
+    b_ = c.batch;
+    T_ = int64_t(b_) * S_;
+    L_ = c.layers;
+    if (h_ % 64 || f_ % 64 || V_ % 64 || S_ % 128 || hd_ % 64 || h_ % nh_)
+      throw std::invalid_argument("GPT dims must be multiples of 64 (seq of 128, head dim of 64)");
+    int64_t o = 0;
+    auto take = [&](int64_t n) {
+      const int64_t r = o;
+      o += n;
+      return r;
+    };
+    bo_.ln1_g = take(h_);
+    bo_.ln1_b = take(h_);
+    bo_.w_qkv = take(3 * int64_t(h_) * h_);
+    bo_.b_qkv = take(3 * h_);
+    bo_.w_o = take(int64_t(h_) * h_);
+    bo_.b_o = take(h_);
+    bo_.ln2_g = take(h_);
+    bo_.ln2_b = take(h_);
+    bo_.w_fc1 = take(int64_t(f_) * h_);
+    bo_.b_fc1 = take(f_);
+    bo_.w_fc2 = take(int64_t(h_) * f_);
+    bo_.b_fc2 = take(h_);
+    bo_.size = o;
+    int64_t off = 0;
+    ranges_.push_back({off, int64_t(V_) * h_ + int64_t(S_) * h_});
+    off += ranges_.back().size;
+    for (int l = 0; l < L_; ++l) {
+      ranges_.push_back({off, bo_.size});
+      off += bo_.size;
+    }
+    ranges_.push_back({off, 2 * int64_t(h_) + int64_t(V_) * h_});
+    off += ranges_.back().size;
+    P_ = off;
+  }
+
+  int num_layers() const override { return L_ + 2; }
+  LayerRange layer(int l) const override { return ranges_[l]; }
+  int64_t param_count() const override { return P_; }
+  int64_t input_elems_per_mb() const override { return int64_t(b_) * (S_ + 1); }
+  int input_elem_bytes() const override { return 4; }
+  int64_t tokens_per_mb() const override { return T_; }
+  double flops_per_mb() const override {
+    // 6 * dense params * tokens + causal attention (QK^T and PV, fwd + bwd = 3x):
+    // 3 * 2 * 2 * S^2/2 * h * b * L
+    const double dense = double(L_) * (4.0 * h_ * h_ + 2.0 * h_ * f_) + double(V_) * h_;
+    return 6.0 * dense * double(T_) + 6.0 * double(S_) * S_ * h_ * b_ * L_;
+  }
+  int64_t launches_per_fwd() const override { return 9; }
+
+  void* alloc_rank_buffers() override {
+    auto* B = new GptBuffers();
+    auto bf = [](int64_t n) {
+      uint16_t* p = nullptr;
+      HZP_CUDA(cudaMalloc(&p, size_t(n) * 2));
+      return p;
+    };
+    auto f32 = [](int64_t n) {
+      float* p = nullptr;
+      HZP_CUDA(cudaMalloc(&p, size_t(n) * 4));
+      return p;
+    };
+    const int64_t Z = int64_t(b_) * nh_;
+    const int64_t SS = Z * S_ * S_;
+    B->x.assign(L_ + 2, nullptr);
+    for (int l = 1; l <= L_ + 1; ++l) B->x[l] = bf(T_ * h_);
+    B->acts.resize(L_ + 2);
+    for (int l = 1; l <= L_; ++l) {
+      LayerActs& a = B->acts[l];
+      a.ln1 = bf(T_ * h_);
+      a.qkv = bf(T_ * 3 * h_);
+      a.P = bf(SS);
+      a.attn = bf(T_ * h_);
+      a.xm = bf(T_ * h_);
+      a.ln2 = bf(T_ * h_);
+      a.fpre = bf(T_ * f_);
+      a.fact = bf(T_ * f_);
+      a.mu1 = f32(T_);
+      a.rs1 = f32(T_);
+      a.mu2 = f32(T_);
+      a.rs2 = f32(T_);
+    }
+    B->lnf = bf(T_ * h_);
+    B->muf = f32(T_);
+    B->rsf = f32(T_);
+    B->logits = bf(T_ * V_);
+    B->S = f32(SS);
+    B->dS = bf(SS);
+    B->D = f32(Z * S_);
+    B->dx[0] = bf(T_ * h_);
+    B->dx[1] = bf(T_ * h_);
+    B->dln = bf(T_ * h_);
+    B->dqkv = bf(T_ * 3 * h_);
+    B->dattn = bf(T_ * h_);
+    B->dfc1 = bf(T_ * f_);
+    B->dxm = bf(T_ * h_);
+    B->part = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
+    B->emb = f32(int64_t(V_) * h_ + int64_t(S_) * h_);
+    B->loss = f32(1);
+    HZP_CUDA(cudaMemset(B->loss, 0, 4));
+    return B;
+  }
+  void free_rank_buffers(void* p) override {
+    auto* B = static_cast<GptBuffers*>(p);
+    for (auto* x : B->x) cudaFree(x);
+    for (auto& a : B->acts) {
+      for (void* q : {(void*)a.ln1, (void*)a.qkv, (void*)a.P, (void*)a.attn, (void*)a.xm,
+                      (void*)a.ln2, (void*)a.fpre, (void*)a.fact, (void*)a.mu1, (void*)a.rs1,
+                      (void*)a.mu2, (void*)a.rs2})
+        cudaFree(q);
+    }
+    for (void* q : {(void*)B->lnf, (void*)B->muf, (void*)B->rsf, (void*)B->logits, (void*)B->S,
+                    (void*)B->dS, (void*)B->D, (void*)B->dx[0], (void*)B->dx[1], (void*)B->dln,
+                    (void*)B->dqkv, (void*)B->dattn, (void*)B->dfc1, (void*)B->dxm, (void*)B->part,
+                    (void*)B->emb, (void*)B->loss})
+      cudaFree(q);
+    delete B;
+  }
+  void begin_step(void* p, cudaStream_t s) override {
+    HZP_CUDA(cudaMemsetAsync(static_cast<GptBuffers*>(p)->loss, 0, 4, s));
+  }
+  const float* loss_device(void* p) const override { return static_cast<GptBuffers*>(p)->loss; }
+
+  // ---- helpers ---------------------------------------------------------------
+  // y[T, N] (+)= x[T, K] W[N, K]^T with epilogue e
+  void linear_fwd(const uint16_t* x, const uint16_t* w, void* y, int N, int K, Epilogue e,
+                  cudaStream_t s) const {
+    GemmShape sh{int(T_), N, K, K, K, 0, 0};
+    e.ldc = N;
+    gemm_tc_bf16(x, w, y, sh, e, s);
+  }
+  // dW[N, K] = dy[T, N]^T x[T, K] -> grad target (+ bias grad colsum(dy) if db_off >= 0)
+  void linear_wgrad(const uint16_t* dy, const uint16_t* x, int N, int K, const GradTarget& g,
+                    int64_t w_off, int64_t b_off, GptBuffers* B, cudaStream_t s) const {
+    GemmShape sh{N, K, int(T_), N, K, 1, 1};
+    Epilogue e;
+    e.mode = g.mode;
+    e.out_bf16 = g.bf16;
+    e.ldc = K;
+    gemm_tc_bf16(dy, x, gptr(g, w_off), sh, e, s);
+    if (b_off >= 0) {
+      colsum_partial(dy, int(T_), N, B->part, kChunks, s);
+      colsum_finalize(B->part, kChunks, N, gptr(g, b_off), g.bf16, g.mode, s);
+    }
+  }
+  // dx[T, K] = dy[T, N] W[N, K]   (+ epilogue)
+  void linear_dgrad(const uint16_t* dy, const uint16_t* w, uint16_t* dx, int N, int K, Epilogue e,
+                    cudaStream_t s) const {
+    GemmShape sh{int(T_), K, N, N, K, 0, 1};
+    e.ldc = K;
+    gemm_tc_bf16(dy, w, dx, sh, e, s);
+  }
+  static void* gptr(const GradTarget& g, int64_t off) {
+    return g.bf16 ? static_cast<void*>(static_cast<uint16_t*>(g.ptr) + off)
+                  : static_cast<void*>(static_cast<float*>(g.ptr) + off);
+  }
+  void ln_param_grads(GptBuffers* B, const GradTarget& g, int64_t g_off, int64_t b_off,
+                      cudaStream_t s) const {
+    colsum_finalize(B->part, kChunks, h_, gptr(g, g_off), g.bf16, g.mode, s);
+    colsum_finalize(B->part + int64_t(kChunks) * h_, kChunks, h_, gptr(g, b_off), g.bf16, g.mode, s);
+  }
+  // batched attention shapes over z = (sequence b, head)
+  GemmShape attn_shape(int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int64_t a_sh,
+                       int64_t a_sb, int64_t b_sh, int64_t b_sb, int64_t c_sh, int64_t c_sb,
+                       int causal) const {
+    GemmShape sh{M, N, K, lda, ldb, a_mn, b_mn};
+    sh.nh = nh_;
+    sh.nb = b_;
+    sh.a_sh = a_sh;
+    sh.a_sb = a_sb;
+    sh.b_sh = b_sh;
+    sh.b_sb = b_sb;
+    sh.c_sh = c_sh;
+    sh.c_sb = c_sb;
+    sh.causal = causal;
+    return sh;
+  }
+
+  // ---- forward ---------------------------------------------------------------
+  void fwd(void* p, int l, const void* input_mb, const void* params, cudaStream_t s) override {
+    auto* B = static_cast<GptBuffers*>(p);
+    const auto* W = static_cast<const uint16_t*>(params);
+    if (l == 0) {
+      B->tokens = static_cast<const int*>(input_mb);
+      embed_fwd(B->tokens, W, W + int64_t(V_) * h_, B->x[1], b_, S_, h_, s);
+      return;
+    }
+    if (l == L_ + 1) {
+      layernorm_fwd(B->x[l], W, W + h_, B->lnf, B->muf, B->rsf, int(T_), h_, s);
+      Epilogue e;
+      e.out_bf16 = 1;
+      linear_fwd(B->lnf, W + 2 * h_, B->logits, V_, h_, e, s);
+      cross_entropy(B->logits, B->tokens, b_, S_, V_, B->loss, s);
+      return;
+    }
+    const LayerActs& a = B->acts[l];
+    const BlockOff& o = bo_;
+    const int64_t h3 = 3 * int64_t(h_);
+    layernorm_fwd(B->x[l], W + o.ln1_g, W + o.ln1_b, a.ln1, a.mu1, a.rs1, int(T_), h_, s);
+    {
+      Epilogue e;
+      e.bias_any = W + o.b_qkv;
+      linear_fwd(a.ln1, W + o.w_qkv, a.qkv, int(h3), h_, e, s);
+    }
+    const int64_t SS = int64_t(S_) * S_;
+    {  // S = Q K^T / sqrt(d)  (fp32, causal tile skip)
+      GemmShape sh = attn_shape(S_, S_, hd_, int(h3), int(h3), 0, 0, hd_, S_ * h3, hd_, S_ * h3, SS,
+                                SS * nh_, 1);
+      Epilogue e;
+      e.out_bf16 = 0;
+      e.ldc = S_;
+      e.alpha = 1.f / std::sqrt(float(hd_));
+      gemm_tc_bf16(a.qkv, a.qkv + h_, B->S, sh, e, s);
+    }
+    softmax_causal(B->S, a.P, b_ * nh_, S_, s);
+    {  // O = P V  -> attn [T, h] head slices
+      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 0, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
+                                int64_t(S_) * h_, 2);
+      Epilogue e;
+      e.ldc = h_;
+      gemm_tc_bf16(a.P, a.qkv + 2 * h_, a.attn, sh, e, s);
+    }
+    {
+      Epilogue e;
+      e.bias_any = W + o.b_o;
+      e.resid = B->x[l];
+      e.ldres = h_;
+      linear_fwd(a.attn, W + o.w_o, a.xm, h_, h_, e, s);
+    }
+    layernorm_fwd(a.xm, W + o.ln2_g, W + o.ln2_b, a.ln2, a.mu2, a.rs2, int(T_), h_, s);
+    {
+      Epilogue e;
+      e.bias_any = W + o.b_fc1;
+      e.act = kActGelu;
+      e.aux = a.fpre;
+      e.ldaux = f_;
+      linear_fwd(a.ln2, W + o.w_fc1, a.fact, f_, h_, e, s);
+    }
+    {
+      Epilogue e;
+      e.bias_any = W + o.b_fc2;
+      e.resid = a.xm;
+      e.ldres = h_;
+      linear_fwd(a.fact, W + o.w_fc2, B->x[l + 1], h_, f_, e, s);
+    }
+  }
+
+  // ---- backward --------------------------------------------------------------
+  void bwd(void* p, int l, const void* params, const GradTarget& g, cudaStream_t s) override {
+    auto* B = static_cast<GptBuffers*>(p);
+    const auto* W = static_cast<const uint16_t*>(params);
+    if (l == L_ + 1) {  // head: dlogits already in B->logits
+      linear_wgrad(B->logits, B->lnf, V_, h_, g, 2 * h_, -1, B, s);
+      Epilogue e;
+      linear_dgrad(B->logits, W + 2 * h_, B->dln, V_, h_, e, s);
+      B->cur = 0;
+      layernorm_bwd(B->dln, B->x[l], W, B->muf, B->rsf, nullptr, B->dx[0], B->part, kChunks,
+                    int(T_), h_, s);
+      ln_param_grads(B, g, 0, h_, s);
+      return;
+    }
+    if (l == 0) {
+      const int64_t nw = int64_t(V_) * h_, np = int64_t(S_) * h_;
+      HZP_CUDA(cudaMemsetAsync(B->emb, 0, size_t(nw + np) * 4, s));
+      embed_bwd(B->tokens, B->dx[B->cur], B->emb, B->emb + nw, b_, S_, h_, s);
+      grad_write(B->emb, nw + np, g.ptr, g.bf16, g.mode, s);
+      return;
+    }
+    const LayerActs& a = B->acts[l];
+    const BlockOff& o = bo_;
+    const int64_t h3 = 3 * int64_t(h_);
+    uint16_t* dout = B->dx[B->cur];
+    uint16_t* din = B->dx[B->cur ^ 1];
+    // MLP
+    linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, o.b_fc2, B, s);
+    {
+      Epilogue e;
+      e.act = kActGeluGrad;
+      e.aux = a.fpre;
+      e.ldaux = f_;
+      linear_dgrad(dout, W + o.w_fc2, B->dfc1, h_, f_, e, s);
+    }
+    linear_wgrad(B->dfc1, a.ln2, f_, h_, g, o.w_fc1, o.b_fc1, B, s);
+    {
+      Epilogue e;
+      linear_dgrad(B->dfc1, W + o.w_fc1, B->dln, f_, h_, e, s);
+    }
+    layernorm_bwd(B->dln, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_),
+                  h_, s);
+    ln_param_grads(B, g, o.ln2_g, o.ln2_b, s);
+    // attention output projection
+    linear_wgrad(B->dxm, a.attn, h_, h_, g, o.w_o, o.b_o, B, s);
+    {
+      Epilogue e;
+      linear_dgrad(B->dxm, W + o.w_o, B->dattn, h_, h_, e, s);
+    }
+    // attention core
+    const int64_t SS = int64_t(S_) * S_;
+    const float scale = 1.f / std::sqrt(float(hd_));
+    attn_rowdot(B->dattn, a.attn, B->D, b_, nh_, S_, hd_, s);
+    {  // dS = scale * P * (dO V^T - D)
+      GemmShape sh = attn_shape(S_, S_, hd_, h_, int(h3), 0, 0, hd_, int64_t(S_) * h_, hd_, S_ * h3,
+                                SS, SS * nh_, 1);
+      Epilogue e;
+      e.ldc = S_;
+      e.act = kActSoftmaxGrad;
+      e.aux = a.P;
+      e.ldaux = S_;
+      e.alpha = scale;
+      e.rowvec = B->D;
+      e.rv_sh = S_;
+      e.rv_sb = int64_t(S_) * nh_;
+      gemm_tc_bf16(B->dattn, a.qkv + 2 * h_, B->dS, sh, e, s);
+    }
+    {  // dQ = dS K
+      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 0, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
+                                S_ * h3, 2);
+      Epilogue e;
+      e.ldc = int(h3);
+      gemm_tc_bf16(B->dS, a.qkv + h_, B->dqkv, sh, e, s);
+    }
+    {  // dK = dS^T Q
+      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 1, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
+                                S_ * h3, 3);
+      Epilogue e;
+      e.ldc = int(h3);
+      gemm_tc_bf16(B->dS, a.qkv, B->dqkv + h_, sh, e, s);
+    }
+    {  // dV = P^T dO
+      GemmShape sh = attn_shape(S_, hd_, S_, S_, h_, 1, 1, SS, SS * nh_, hd_, int64_t(S_) * h_, hd_,
+                                S_ * h3, 3);
+      Epilogue e;
+      e.ldc = int(h3);
+      gemm_tc_bf16(a.P, B->dattn, B->dqkv + 2 * h_, sh, e, s);
+    }
+    linear_wgrad(B->dqkv, a.ln1, int(h3), h_, g, o.w_qkv, o.b_qkv, B, s);
+    {
+      Epilogue e;
+      linear_dgrad(B->dqkv, W + o.w_qkv, B->dln, int(h3), h_, e, s);
+    }
+    layernorm_bwd(B->dln, B->x[l], W + o.ln1_g, a.mu1, a.rs1, B->dxm, din, B->part, kChunks,
+                  int(T_), h_, s);
+    ln_param_grads(B, g, o.ln1_g, o.ln1_b, s);
+    B->cur ^= 1;
+  }
+
+ private:
+  ModelConfig c_;
+  int h_, nh_, hd_, f_, V_, S_, b_, L_;
+  int64_t T_;
+  BlockOff bo_;
+  std::vector<LayerRange> ranges_;
+  int64_t P_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<Model> make_gpt_model(const ModelConfig& c) { return std::make_unique<GptModel>(c); }
+
 }  // namespace hzp
