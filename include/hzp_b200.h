@@ -239,6 +239,17 @@ int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, 
 
 /* Extra device work counters (kernels launched by the last step). */
 int hzp_ctx_launch_count(const hzp_ctx* ctx, int64_t* kernels);
+/* Total kernels this library has launched in the process (every launch site
+ * counts itself) — the bench's gpu_launches evidence. */
+uint64_t hzp_kernel_launches(void);
+/* The ctx's CUDA streams (which: HZP_STREAM_*) as cudaStream_t, so callers
+ * can time the step with events on the stream the work runs on. */
+int hzp_ctx_stream(const hzp_ctx* ctx, int which, void** stream);
+/* Per-GEMM timing for the roofline: while on, every tcgen05 GEMM launch is
+ * bracketed by CUDA events; read returns (and clears) the summed algorithmic
+ * FLOPs, summed kernel milliseconds and launch count. */
+int hzp_gemm_profile(int on);
+int hzp_gemm_profile_read(double* flops, double* ms, int* launches);
 
 /* ---- kernel-level entry points (single ctx, its streams) ---------------- */
 /* Layer-wise P2P-pull all-gather of layer `layer` into AG ring slot `slot`

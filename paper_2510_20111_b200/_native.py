@@ -123,6 +123,10 @@ SIGNATURES = [
     ("hzp_timeline", C.c_int, [_vp, _P(C.c_double), _P(C.c_double), C.c_int, _P(C.c_int),
                                _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     ("hzp_ctx_launch_count", C.c_int, [_vp, _P(C.c_int64)]),
+    ("hzp_kernel_launches", C.c_uint64, []),
+    ("hzp_ctx_stream", C.c_int, [_vp, C.c_int, _P(_vp)]),
+    ("hzp_gemm_profile", C.c_int, [C.c_int]),
+    ("hzp_gemm_profile_read", C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_int)]),
     ("hzp_ag_layer", C.c_int, [_vp, C.c_int, C.c_int]),
     ("hzp_ag_slot_download", C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64]),
     ("hzp_wgrad_upload", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_float), C.c_int64]),

@@ -484,6 +484,40 @@ int hzp_ctx_launch_count(const hzp_ctx* ctx, int64_t* kernels) {
   return HZP_OK;
 }
 
+uint64_t hzp_kernel_launches(void) { return launch_counter(); }
+
+int hzp_ctx_stream(const hzp_ctx* ctx, int which, void** stream) {
+  if (!ctx || !stream || which < 0 || which > 2) return HZP_ERR_ARG;
+  *stream = ctx->e->st[which];
+  return HZP_OK;
+}
+
+int hzp_gemm_profile(int on) {
+  gemm_profile().on = on != 0;
+  return HZP_OK;
+}
+
+int hzp_gemm_profile_read(double* flops, double* ms, int* launches) {
+  return guarded([&] {
+    GemmProfile& p = gemm_profile();
+    double f = 0, t = 0;
+    for (size_t i = 0; i < p.ev.size(); ++i) {
+      HZP_CUDA(cudaEventSynchronize(p.ev[i].second));
+      float x = 0;
+      HZP_CUDA(cudaEventElapsedTime(&x, p.ev[i].first, p.ev[i].second));
+      t += x;
+      f += p.flops[i];
+      cudaEventDestroy(p.ev[i].first);
+      cudaEventDestroy(p.ev[i].second);
+    }
+    if (flops) *flops = f;
+    if (ms) *ms = t;
+    if (launches) *launches = static_cast<int>(p.ev.size());
+    p.ev.clear();
+    p.flops.clear();
+  });
+}
+
 int hzp_ag_layer(hzp_ctx* ctx, int layer, int slot) {
   if (!ctx) return HZP_ERR_ARG;
   return guarded([&] {

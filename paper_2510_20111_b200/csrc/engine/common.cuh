@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 namespace hzp {
 
@@ -24,7 +26,23 @@ struct CudaError : std::runtime_error {
                              __FILE__ + ":" + std::to_string(__LINE__));                 \
   } while (0)
 
-#define HZP_LAUNCH_CHECK() HZP_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by HZP_LAUNCH_CHECK(), which
+// also counts it (hzp_kernel_launches(): the bench's gpu_launches evidence).
+uint64_t& launch_counter();
+#define HZP_LAUNCH_CHECK()                \
+  do {                                    \
+    HZP_CUDA(cudaGetLastError());         \
+    ++::hzp::launch_counter();            \
+  } while (0)
+
+// Optional per-GEMM timing (bench roofline): when enabled, every tcgen05 GEMM
+// launch is bracketed by CUDA events on its stream and its FLOPs recorded.
+struct GemmProfile {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> flops;
+};
+GemmProfile& gemm_profile();
 
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
 

@@ -544,6 +544,15 @@ void dispatch_major(const void* A, const void* B, void* C, const GemmShape& s, c
 
 }  // namespace
 
+uint64_t& launch_counter() {
+  static uint64_t n = 0;
+  return n;
+}
+GemmProfile& gemm_profile() {
+  static GemmProfile p;
+  return p;
+}
+
 void gemm_set_sm_budget(int sms) { g_sm_budget = sms < 1 ? 1 : (sms > kNumSMs ? kNumSMs : sms); }
 
 void gemm_tc_bf16(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
@@ -561,8 +570,22 @@ void gemm_tc_bf16(const void* A, const void* B, void* C, const GemmShape& s, con
     HZP_LAUNCH_CHECK();
     return;
   }
+  GemmProfile& prof = gemm_profile();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof.on) {
+    HZP_CUDA(cudaEventCreate(&e0));
+    HZP_CUDA(cudaEventCreate(&e1));
+    HZP_CUDA(cudaEventRecord(e0, stream));
+  }
   if (s.N > 128) dispatch_major<256>(A, B, C, s, e, stream);
   else dispatch_major<128>(A, B, C, s, e, stream);
+  if (prof.on) {
+    HZP_CUDA(cudaEventRecord(e1, stream));
+    // algorithmic FLOPs: 2MNK per batch; the causal attention products do half
+    const double f = 2.0 * s.M * s.N * double(s.K) * s.nh * s.nb * (s.causal ? 0.5 : 1.0);
+    prof.ev.emplace_back(e0, e1);
+    prof.flops.push_back(f);
+  }
 }
 
 }  // namespace hzp

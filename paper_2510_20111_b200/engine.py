@@ -195,6 +195,11 @@ class HzpEngine:
                 "compute_idle_ms": idle.value, "compute_busy_ms": busy.value,
                 "makespan_ms": mk.value}
 
+    def stream(self, which: int = 0) -> int:
+        p = C.c_void_p()
+        N.check(N.lib.hzp_ctx_stream(self._h, which, C.byref(p)))
+        return p.value or 0
+
     def launch_count(self) -> int:
         k = C.c_int64()
         N.check(N.lib.hzp_ctx_launch_count(self._h, C.byref(k)))
@@ -226,6 +231,20 @@ class HzpEngine:
 
     def barrier(self) -> None:
         N.check(N.lib.hzp_barrier(self._h))
+
+
+def kernel_launches() -> int:
+    return int(N.lib.hzp_kernel_launches())
+
+
+def gemm_profile(on: bool) -> None:
+    N.check(N.lib.hzp_gemm_profile(int(on)))
+
+
+def gemm_profile_read():
+    f, ms, n = C.c_double(), C.c_double(), C.c_int()
+    N.check(N.lib.hzp_gemm_profile_read(C.byref(f), C.byref(ms), C.byref(n)))
+    return f.value, ms.value, n.value
 
 
 def gemm_bf16(A, B, C_, M, N_, K, lda, ldb, ldc, a_mn=0, b_mn=0, epi=0, stream=0):
