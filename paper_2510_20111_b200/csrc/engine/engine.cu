@@ -15,6 +15,7 @@
 //    covering those task ids.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -166,6 +167,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   HZP_CUDA(cudaMalloc(&dtable, sizeof(RankTable)));
   HZP_CUDA(cudaMemcpy(dtable, &table, sizeof(RankTable), cudaMemcpyHostToDevice));
   peers_open = emulate || c.par.dp == 1;
+  debug_sync = std::getenv("HZP_DEBUG_SYNC") != nullptr;
   build_tiles();
 }
 
@@ -433,6 +435,11 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
     if (cfg.timeline) HZP_CUDA(cudaEventRecord(tev1[e.id], s));
     HZP_CUDA(cudaEventRecord(done[e.id], s));
     if (e.stream != StreamId::Compute) last_comm_ev[static_cast<int>(e.stream)] = e.id;
+    if (debug_sync) {  // HZP_DEBUG_SYNC=1: serialise every task across all ranks
+      HZP_CUDA(cudaDeviceSynchronize());
+      barrier(cs);
+      HZP_CUDA(cudaDeviceSynchronize());
+    }
   }
   rs_seq = seq0 + rs_ids.size();
   // join the comm streams back into the compute stream

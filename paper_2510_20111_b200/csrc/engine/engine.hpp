@@ -74,6 +74,7 @@ struct Engine {
   int64_t launches = 0;
   int comm_ctas = 32;
   bool peers_open = false;
+  bool debug_sync = false;
 
   explicit Engine(const hzp_engine_config& c);
   ~Engine();

@@ -20,9 +20,58 @@ from oracle import load_oracle  # noqa: E402
 from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig  # noqa: E402
 
 
+def kernels(z1, z2, z3, prec):
+    """Kernel-level multi-process parity: AG and RS through the test entry
+    points (host barriers between phases, no device flags)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dims = [64, 128, 128, 64]
+    o = load_oracle()
+    st = o.shard_init(dims, world, z1, z2, z3, 7, bool(prec))
+    eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=16, num_microbatches=1,
+                                 par=ParallelConfig(dp=world, z1=z1, z2=z2, z3=z3), device=local,
+                                 my_rank=rank))
+    eng.connect()
+    eng.load_state(st)
+    dist.barrier()
+    ok = True
+    for l, (off, n) in enumerate(eng.layers):
+        eng.ag_layer(l, 0)
+        g0 = rank - rank % z3
+        want = o.all_gather(st.param[g0:g0 + z3])[off:off + n]
+        got = eng.ag_slot(rank, 0, n)
+        if prec:
+            got = (got.astype(np.uint32) << 16).view(np.float32)
+        ok &= bool(np.array_equal(got, want))
+    if z2 > 1 and prec == 0:
+        rng = np.random.default_rng(5)
+        grads = rng.standard_normal((world, st.s2 * z2)).astype(np.float32)
+        eng.zero_grads()
+        for l, (off, n) in enumerate(eng.layers):
+            eng.wgrad_upload(rank, l, 0, grads[rank, off:off + n])
+            torch.cuda.synchronize()
+            dist.barrier()
+            eng.rs_layer(l, 0)
+            torch.cuda.synchronize()
+            dist.barrier()
+        g0 = rank - rank % z2
+        seg = o.reduce_scatter(grads[g0:g0 + z2])[rank % z2]
+        got = eng.download(rank, 1)
+        ok &= bool(np.array_equal(got, 0 + seg))
+    print(f"rank {rank}: {'OK' if ok else 'FAIL'} kernels", flush=True)
+    dist.barrier()
+    eng.close()
+    return ok
+
+
 def main():
     z1, z2, z3, prec = (int(x) for x in sys.argv[1:5])
     dist.init_process_group("gloo")
+    if len(sys.argv) > 5 and sys.argv[5] == "kernels":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", dist.get_rank())))
+        ok = kernels(z1, z2, z3, prec)
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)

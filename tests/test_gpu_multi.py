@@ -20,6 +20,20 @@ def _ngpu():
         return 0
 
 
+@pytest.mark.parametrize("n,z", [(2, (2, 2, 2)), (2, (2, 2, 1)), (4, (4, 2, 2)), (4, (4, 4, 4))])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_multiprocess_kernels_match_oracle(n, z, prec):
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + n * 10 + prec),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *map(str, z), str(prec), "kernels"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count(": OK") == n
+
+
 @pytest.mark.parametrize("n,z", [(2, (2, 2, 2)), (2, (2, 1, 2)), (2, (2, 2, 1)), (4, (4, 2, 2)),
                                  (4, (4, 4, 4)), (4, (2, 4, 2))])
 @pytest.mark.parametrize("prec", [0, 1])
