@@ -250,6 +250,8 @@ int hzp_ctx_stream(const hzp_ctx* ctx, int which, void** stream);
  * FLOPs, summed kernel milliseconds and launch count. */
 int hzp_gemm_profile(int on);
 int hzp_gemm_profile_read(double* flops, double* ms, int* launches);
+/* Same, plus a per-shape text table (count, ms, TFLOP/s) into text[cap]. */
+int hzp_gemm_profile_dump(double* flops, double* ms, int* launches, char* text, int cap);
 
 /* ---- kernel-level entry points (single ctx, its streams) ---------------- */
 /* Layer-wise P2P-pull all-gather of layer `layer` into AG ring slot `slot`

@@ -3,6 +3,9 @@
 // C++ exceptions never cross this boundary: they become HZP_ERR_* codes with
 // a thread-local message (hzp_last_error).
 #include <algorithm>
+#include <array>
+#include <cstdio>
+#include <map>
 #include <cstring>
 #include <string>
 
@@ -498,8 +501,13 @@ int hzp_gemm_profile(int on) {
 }
 
 int hzp_gemm_profile_read(double* flops, double* ms, int* launches) {
+  return hzp_gemm_profile_dump(flops, ms, launches, nullptr, 0);
+}
+
+int hzp_gemm_profile_dump(double* flops, double* ms, int* launches, char* text, int cap) {
   return guarded([&] {
     GemmProfile& p = gemm_profile();
+    std::map<std::string, std::array<double, 3>> agg;  // shape -> {count, ms, flops}
     double f = 0, t = 0;
     for (size_t i = 0; i < p.ev.size(); ++i) {
       HZP_CUDA(cudaEventSynchronize(p.ev[i].second));
@@ -507,6 +515,12 @@ int hzp_gemm_profile_read(double* flops, double* ms, int* launches) {
       HZP_CUDA(cudaEventElapsedTime(&x, p.ev[i].first, p.ev[i].second));
       t += x;
       f += p.flops[i];
+      if (i < p.shape.size()) {
+        auto& a = agg[p.shape[i]];
+        a[0] += 1;
+        a[1] += x;
+        a[2] += p.flops[i];
+      }
       cudaEventDestroy(p.ev[i].first);
       cudaEventDestroy(p.ev[i].second);
     }
@@ -515,6 +529,17 @@ int hzp_gemm_profile_read(double* flops, double* ms, int* launches) {
     if (launches) *launches = static_cast<int>(p.ev.size());
     p.ev.clear();
     p.flops.clear();
+    p.shape.clear();
+    if (text && cap > 0) {
+      std::string out;
+      for (const auto& [k, a] : agg) {
+        char line[256];
+        std::snprintf(line, sizeof line, "%-48s n=%4.0f ms=%9.3f TF/s=%7.1f\n", k.c_str(), a[0], a[1],
+                      a[1] > 0 ? a[2] / (a[1] * 1e9) : 0.0);
+        out += line;
+      }
+      std::snprintf(text, size_t(cap), "%s", out.c_str());
+    }
   });
 }
 

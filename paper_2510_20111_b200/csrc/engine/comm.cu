@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads) rs_pull_kernel(const RankTable* __re
   const bool do_scale = scale != 1.0f;
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
-    float* g = T->grad[t.local] + t.a_off;
+    float* g = T->grad[T->global_rank[t.local]] + t.a_off;  // local index -> global rank
     const int64_t woff = (int64_t(wslot) * wslot_elems + t.b_off) * kEB;
     if (t.vec) {
       constexpr int kPer = kBf16Wire ? 8 : 4;  // elements per 16-byte load

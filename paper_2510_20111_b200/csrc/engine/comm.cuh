@@ -41,6 +41,7 @@ struct RankTable {
   float* mom[kMaxRanks];
   float* var[kMaxRanks];
   float* z1_grad_dbg[kMaxRanks];  // optional reduced-gradient dump [s1]
+  int global_rank[kMaxRanks];     // driven-rank index -> global dp rank
 };
 
 struct AdamArgs {

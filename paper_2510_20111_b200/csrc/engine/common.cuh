@@ -41,6 +41,7 @@ struct GemmProfile {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> flops;
+  std::vector<std::string> shape;  // "MxNxK z=.. a_mn b_mn causal"
 };
 GemmProfile& gemm_profile();
 

@@ -163,6 +163,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     table.mom[i] = locals[i].mom;
     table.var[i] = locals[i].var;
     table.z1_grad_dbg[i] = locals[i].dbg;
+    table.global_rank[i] = locals[i].rank;
   }
   HZP_CUDA(cudaMalloc(&dtable, sizeof(RankTable)));
   HZP_CUDA(cudaMemcpy(dtable, &table, sizeof(RankTable), cudaMemcpyHostToDevice));

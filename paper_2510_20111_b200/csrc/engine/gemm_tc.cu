@@ -585,6 +585,10 @@ void gemm_tc_bf16(const void* A, const void* B, void* C, const GemmShape& s, con
     const double f = 2.0 * s.M * s.N * double(s.K) * s.nh * s.nb * (s.causal ? 0.5 : 1.0);
     prof.ev.emplace_back(e0, e1);
     prof.flops.push_back(f);
+    prof.shape.push_back(std::to_string(s.M) + "x" + std::to_string(s.N) + "x" + std::to_string(s.K) +
+                         " z" + std::to_string(s.nh * s.nb) + " mn" + std::to_string(s.a_mn) +
+                         std::to_string(s.b_mn) + " c" + std::to_string(s.causal) +
+                         " act" + std::to_string(e.act) + " bf" + std::to_string(e.out_bf16));
   }
 }
 

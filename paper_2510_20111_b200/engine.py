@@ -247,6 +247,13 @@ def gemm_profile_read():
     return f.value, ms.value, n.value
 
 
+def gemm_profile_dump():
+    f, ms, n = C.c_double(), C.c_double(), C.c_int()
+    buf = C.create_string_buffer(1 << 16)
+    N.check(N.lib.hzp_gemm_profile_dump(C.byref(f), C.byref(ms), C.byref(n), buf, 1 << 16))
+    return f.value, ms.value, n.value, buf.value.decode()
+
+
 def gemm_bf16(A, B, C_, M, N_, K, lda, ldb, ldc, a_mn=0, b_mn=0, epi=0, stream=0):
     """Standalone tcgen05 GEMM on raw device pointers (tests / benches)."""
     N.check(N.lib.hzp_gemm_bf16(C.c_void_p(A), C.c_void_p(B), C.c_void_p(C_), M, N_, K, lda, ldb,
