@@ -281,6 +281,14 @@ int hzp_barrier(hzp_ctx* ctx);
  * bf16, 1 store fp32, 2 accumulate into fp32 C. stream = cudaStream_t. */
 int hzp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda, int ldb,
                   int ldc, int a_mn, int b_mn, int epi, void* stream);
+/* Extended epilogue (tests): mode 0 store / 1 accumulate (fp32 C) / 2 assign 0+acc;
+ * act 0 none, 1 tanh, 2 gelu (aux <- pre-activation, bf16), 3 tanh' (aux in),
+ * 4 gelu' (aux in), 5 softmax-grad alpha*aux*(acc - rowvec[m]); bias bf16 [N]
+ * or NULL; resid bf16 [M, ldres] added last or NULL; alpha scales acc. */
+int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K, int lda, int ldb,
+                     int ldc, int a_mn, int b_mn, int mode, int out_bf16, int act,
+                     const void* bias_bf16, void* aux, int ldaux, const void* resid, int ldres,
+                     const float* rowvec, float alpha, void* stream);
 /* Same contract, fp32 operands on the CUDA cores (fp32 parity tier). */
 int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                  int ldb, int ldc, int a_mn, int b_mn, int epi, void* stream);

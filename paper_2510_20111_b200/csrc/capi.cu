@@ -644,6 +644,29 @@ int hzp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, in
   });
 }
 
+int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K, int lda, int ldb,
+                     int ldc, int a_mn, int b_mn, int mode, int out_bf16, int act,
+                     const void* bias_bf16, void* aux, int ldaux, const void* resid, int ldres,
+                     const float* rowvec, float alpha, void* stream) {
+  return guarded([&] {
+    GemmShape s{M, N, K, lda, ldb, a_mn, b_mn};
+    Epilogue e;
+    e.ldc = ldc;
+    e.out_bf16 = out_bf16;
+    e.mode = mode;
+    e.act = act;
+    e.bias_any = bias_bf16;
+    e.aux = aux;
+    e.ldaux = ldaux;
+    e.aux_bf16 = 1;
+    e.resid = resid;
+    e.ldres = ldres;
+    e.rowvec = rowvec;
+    e.alpha = alpha;
+    gemm_tc_bf16(A, B, C, s, e, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, int lda, int ldb,
                  int ldc, int a_mn, int b_mn, int epi, void* stream) {
   return guarded([&] {

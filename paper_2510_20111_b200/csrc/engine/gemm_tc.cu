@@ -72,6 +72,36 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_4d(const CUtensorMap* map, const void* src, int c0,
+                                                  int c1, int c2, int c3) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ uint4 pack8f(const float* f) {
+  uint4 w;
+  w.x = uint32_t(f32_to_bf16_bits(f[0])) | (uint32_t(f32_to_bf16_bits(f[1])) << 16);
+  w.y = uint32_t(f32_to_bf16_bits(f[2])) | (uint32_t(f32_to_bf16_bits(f[3])) << 16);
+  w.z = uint32_t(f32_to_bf16_bits(f[4])) | (uint32_t(f32_to_bf16_bits(f[5])) << 16);
+  w.w = uint32_t(f32_to_bf16_bits(f[6])) | (uint32_t(f32_to_bf16_bits(f[7])) << 16);
+  return w;
+}
+__device__ __forceinline__ void unpack8f(uint4 w, float* a) {
+  a[0] = __uint_as_float(w.x << 16); a[1] = __uint_as_float(w.x & 0xFFFF0000u);
+  a[2] = __uint_as_float(w.y << 16); a[3] = __uint_as_float(w.y & 0xFFFF0000u);
+  a[4] = __uint_as_float(w.z << 16); a[5] = __uint_as_float(w.z & 0xFFFF0000u);
+  a[6] = __uint_as_float(w.w << 16); a[7] = __uint_as_float(w.w & 0xFFFF0000u);
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -135,6 +165,8 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
 }
 
 struct TcParams {
+  CUtensorMap tmC;    // output (STORE != 0)
+  CUtensorMap tmAux;  // GELU pre-activation output (STORE == 1, act == Gelu)
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
   int nh, causal;
@@ -162,10 +194,10 @@ __device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int&
   else if (p.causal == 3) kb0 = min(nkb, m0 / BK);
 }
 
-template <int BN, int A_MN, int B_MN, int STAGES>
+template <int BN, int A_MN, int B_MN, int STAGES, int STORE>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const TcParams p) {
+                   const __grid_constant__ TcParams p) {
   constexpr uint32_t A_BYTES = BM * BK * 2;
   constexpr uint32_t B_BYTES = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -275,9 +307,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
   } else {
     // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4 ----
+    // Thread `lane` of warp quarter q owns accumulator row q*32 + lane.  Each
+    // 32-column chunk is computed in registers; with STORE != 0 it is staged
+    // in the warp's 128B/64B-swizzled smem buffer and written by a single
+    // TMA bulk tensor store (reduce-add for fp32 accumulation), so global
+    // writes are full-line and coalesced whatever the row pitch.
     const int quarter = warp & 3;
     const Epilogue& e = p.e;
-    int acc = 0;
+    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + (quarter * 2) * 4096;
+    int acc = 0, nchunk = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       const TileCoord tc = tile_coord(p, t, BN);
@@ -298,61 +336,62 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + acc * BN + c * 32, r);
         const int nb = n0 + c * 32;
-        if (!row_ok || nb >= p.N) continue;
+        if (nb >= p.N) continue;                 // warp-uniform
+        if (STORE == 0 && !row_ok) continue;
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * e.alpha;
         const bool full_chunk = nb + 32 <= p.N;
-        if (e.bias_any) {
-          const uint16_t* b = static_cast<const uint16_t*>(e.bias_any) + nb;
+        if (row_ok) {
+          if (e.bias_any) {
+            const uint16_t* bp = static_cast<const uint16_t*>(e.bias_any) + nb;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (full_chunk || nb + j < p.N) v[j] += bf16_bits_to_f32(b[j]);
-        } else if (e.bias) {
+            for (int j = 0; j < 32; ++j)
+              if (full_chunk || nb + j < p.N) v[j] += bf16_bits_to_f32(bp[j]);
+          } else if (e.bias) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (full_chunk || nb + j < p.N) v[j] += e.bias[nb + j];
+            for (int j = 0; j < 32; ++j)
+              if (full_chunk || nb + j < p.N) v[j] += e.bias[nb + j];
+          }
         }
+        float pre[32];  // GELU pre-activation (aux output)
         if (e.act == kActTanh) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = tanhf(v[j]);
         } else if (e.act == kActGelu) {
-          uint16_t* aux = static_cast<uint16_t*>(e.aux) + zoff + int64_t(m) * e.ldaux + nb;
-          if (full_chunk) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w;
-              w.x = uint32_t(f32_to_bf16_bits(v[8 * q + 0])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 1])) << 16);
-              w.y = uint32_t(f32_to_bf16_bits(v[8 * q + 2])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 3])) << 16);
-              w.z = uint32_t(f32_to_bf16_bits(v[8 * q + 4])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 5])) << 16);
-              w.w = uint32_t(f32_to_bf16_bits(v[8 * q + 6])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 7])) << 16);
-              reinterpret_cast<uint4*>(aux)[q] = w;
-            }
-          } else {
-            for (int j = 0; j < 32 && nb + j < p.N; ++j) aux[j] = f32_to_bf16_bits(v[j]);
+          for (int j = 0; j < 32; ++j) {
+            pre[j] = v[j];
+            v[j] = gelu_tanh(v[j]);
           }
+          if (STORE == 0) {
+            uint16_t* aux = static_cast<uint16_t*>(e.aux) + zoff + int64_t(m) * e.ldaux + nb;
+            if (full_chunk) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+              for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(aux)[q] = pack8f(pre + 8 * q);
+            } else {
+              for (int j = 0; j < 32 && nb + j < p.N; ++j) aux[j] = f32_to_bf16_bits(pre[j]);
+            }
+          }
         } else if (e.act == kActTanhGrad || e.act == kActGeluGrad || e.act == kActSoftmaxGrad) {
-          const int64_t ab = zoff + int64_t(m) * e.ldaux + nb;
           float a[32];
-          if (e.aux_bf16 && full_chunk) {
-            const uint4* ap = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.aux) + ab);
+          if (row_ok) {
+            const int64_t ab = zoff + int64_t(m) * e.ldaux + nb;
+            if (e.aux_bf16 && full_chunk) {
+              const uint4* ap = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.aux) + ab);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 w = ap[q];
-              a[8 * q + 0] = __uint_as_float(w.x << 16); a[8 * q + 1] = __uint_as_float(w.x & 0xFFFF0000u);
-              a[8 * q + 2] = __uint_as_float(w.y << 16); a[8 * q + 3] = __uint_as_float(w.y & 0xFFFF0000u);
-              a[8 * q + 4] = __uint_as_float(w.z << 16); a[8 * q + 5] = __uint_as_float(w.z & 0xFFFF0000u);
-              a[8 * q + 6] = __uint_as_float(w.w << 16); a[8 * q + 7] = __uint_as_float(w.w & 0xFFFF0000u);
+              for (int q = 0; q < 4; ++q) unpack8f(ap[q], a + 8 * q);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                a[j] = (full_chunk || nb + j < p.N)
+                           ? (e.aux_bf16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(e.aux)[ab + j])
+                                         : static_cast<const float*>(e.aux)[ab + j])
+                           : 0.f;
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              a[j] = (full_chunk || nb + j < p.N)
-                         ? (e.aux_bf16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(e.aux)[ab + j])
-                                       : static_cast<const float*>(e.aux)[ab + j])
-                         : 0.f;
+            for (int j = 0; j < 32; ++j) a[j] = 0.f;
           }
           if (e.act == kActTanhGrad) {
 #pragma unroll
@@ -361,54 +400,79 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] *= gelu_tanh_grad(a[j]);
           } else {
-            // v = alpha * acc already; dS = P * (alpha*dP - alpha*D) with alpha folded
+            // dS = P * (alpha*dP - alpha*D), alpha already applied to acc
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = a[j] * (v[j] - e.alpha * rv);
           }
         }
-        if (e.resid) {
+        if (e.resid && row_ok) {
           const uint16_t* rp = static_cast<const uint16_t*>(e.resid) + zoff + int64_t(m) * e.ldres + nb;
+          if (full_chunk) {
+            float rr[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (full_chunk || nb + j < p.N) v[j] += bf16_bits_to_f32(rp[j]);
+            for (int q = 0; q < 4; ++q) unpack8f(reinterpret_cast<const uint4*>(rp)[q], rr + 8 * q);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += rr[j];
+          } else {
+            for (int j = 0; j < 32 && nb + j < p.N; ++j) v[j] += bf16_bits_to_f32(rp[j]);
+          }
         }
+        if (STORE != 0) {
+          // ---- stage in smem (swizzled) and TMA-store the 32x32 chunk ----
+          uint8_t* buf = stage_base + (nchunk & 1) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          if (STORE == 1) {  // bf16: 32 rows x 64 B, SWIZZLE_64B; GELU aux in the 2nd half
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int pc = q ^ ((lane >> 1) & 3);
+              *reinterpret_cast<uint4*>(buf + lane * 64 + pc * 16) = pack8f(v + 8 * q);
+              if (e.act == kActGelu)
+                *reinterpret_cast<uint4*>(buf + 2048 + lane * 64 + pc * 16) = pack8f(pre + 8 * q);
+            }
+          } else {  // fp32: 32 rows x 128 B, SWIZZLE_128B
+            if (e.mode == kEpiAssign0) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(0.f, v[j]);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int pc = q ^ (lane & 7);
+              *reinterpret_cast<float4*>(buf + lane * 128 + pc * 16) =
+                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int mr = m0 + quarter * 32;
+            if (STORE == 2 && e.mode == kEpiAccum)
+              tma_reduce_add_4d(&p.tmC, buf, nb, mr, tc.zh, tc.zb);
+            else
+              tma_store_4d(&p.tmC, buf, nb, mr, tc.zh, tc.zb);
+            if (STORE == 1 && e.act == kActGelu) tma_store_4d(&p.tmAux, buf + 2048, nb, mr, tc.zh, tc.zb);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++nchunk;
+          continue;
+        }
+        // ---- direct stores (fallback for TMA-incompatible C layouts) ----
         const int64_t ci = zoff + int64_t(m) * e.ldc + nb;
         if (e.out_bf16) {
           uint16_t* out = static_cast<uint16_t*>(p.C) + ci;
           if (full_chunk && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w;
-              w.x = uint32_t(f32_to_bf16_bits(v[8 * q + 0])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 1])) << 16);
-              w.y = uint32_t(f32_to_bf16_bits(v[8 * q + 2])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 3])) << 16);
-              w.z = uint32_t(f32_to_bf16_bits(v[8 * q + 4])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 5])) << 16);
-              w.w = uint32_t(f32_to_bf16_bits(v[8 * q + 6])) | (uint32_t(f32_to_bf16_bits(v[8 * q + 7])) << 16);
-              reinterpret_cast<uint4*>(out)[q] = w;
-            }
+            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(out)[q] = pack8f(v + 8 * q);
           } else {
             for (int j = 0; j < 32 && nb + j < p.N; ++j) out[j] = f32_to_bf16_bits(v[j]);
           }
         } else {
           float* out = static_cast<float*>(p.C) + ci;
-          if (full_chunk && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-              if (e.mode == kEpiAccum) {
-                const float4 o = reinterpret_cast<const float4*>(out)[q];
-                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
-              } else if (e.mode == kEpiAssign0) {
-                w.x = __fadd_rn(0.f, w.x); w.y = __fadd_rn(0.f, w.y); w.z = __fadd_rn(0.f, w.z); w.w = __fadd_rn(0.f, w.w);
-              }
-              reinterpret_cast<float4*>(out)[q] = w;
-            }
-          } else {
-            for (int j = 0; j < 32 && nb + j < p.N; ++j) {
-              float w = v[j];
-              if (e.mode == kEpiAccum) w += out[j];
-              else if (e.mode == kEpiAssign0) w = __fadd_rn(0.f, w);
-              out[j] = w;
-            }
+          for (int j = 0; j < 32 && nb + j < p.N; ++j) {
+            float w = v[j];
+            if (e.mode == kEpiAccum) w += out[j];
+            else if (e.mode == kEpiAssign0) w = __fadd_rn(0.f, w);
+            out[j] = w;
           }
         }
       }
@@ -417,6 +481,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (STORE != 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (warp == 1) {
@@ -496,12 +561,39 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
   return m;
 }
 
-template <int BN, int A_MN, int B_MN>
+// Output map for the TMA-store epilogue: {N, M, nh, nb}, box {32, 32, 1, 1};
+// bf16 rows of 64 B use SWIZZLE_64B, fp32 rows of 128 B SWIZZLE_128B.
+CUtensorMap make_out_map(const void* base, bool f32, int64_t N, int64_t M, int64_t ld, int nh, int nb,
+                         int64_t sh, int64_t sb) {
+  CUtensorMap m;
+  const int es = f32 ? 4 : 2;
+  if (nh <= 1) sh = ld * M;
+  if (nb <= 1) sb = sh * nh;
+  cuuint64_t dims[4] = {cuuint64_t(N), cuuint64_t(M), cuuint64_t(nh), cuuint64_t(nb)};
+  cuuint64_t strides[3] = {cuuint64_t(ld) * es, cuuint64_t(sh) * es, cuuint64_t(sb) * es};
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = get_encode()(
+      &m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base),
+      dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (out) failed: " + std::to_string(int(r)));
+  return m;
+}
+
+bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
+  return (reinterpret_cast<uintptr_t>(p) % 16) == 0 && (ld * es) % 16 == 0 && (sh * es) % 16 == 0 &&
+         (sb * es) % 16 == 0;
+}
+
+template <int BN, int A_MN, int B_MN, int STORE>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
   constexpr int STAGES = BN == 256 ? 4 : 6;
-  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES>;
+  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 + 8 * 4096;
+  static_assert(SMEM <= 232448, "smem budget");
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     HZP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
@@ -512,6 +604,11 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   const CUtensorMap tb = B_MN ? make_map(B, s.N, s.K, s.ldb, BK, s.nh, s.nb, s.b_sh, s.b_sb)
                               : make_map(B, s.K, s.N, s.ldb, BN, s.nh, s.nb, s.b_sh, s.b_sb);
   TcParams p;
+  if (STORE != 0) {
+    p.tmC = make_out_map(C, STORE == 2, s.N, s.M, e.ldc, s.nh, s.nb, s.c_sh, s.c_sb);
+    if (STORE == 1 && e.act == kActGelu)
+      p.tmAux = make_out_map(e.aux, false, s.N, s.M, e.ldaux, s.nh, s.nb, s.c_sh, s.c_sb);
+  }
   p.M = s.M;
   p.N = s.N;
   p.K = s.K;
@@ -530,16 +627,31 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   HZP_LAUNCH_CHECK();
 }
 
-template <int BN>
+template <int BN, int STORE>
 void dispatch_major(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                     cudaStream_t st) {
   if (s.a_mn) {
-    if (s.b_mn) launch_tc<BN, 1, 1>(A, B, C, s, e, st);
-    else launch_tc<BN, 1, 0>(A, B, C, s, e, st);
+    if (s.b_mn) launch_tc<BN, 1, 1, STORE>(A, B, C, s, e, st);
+    else launch_tc<BN, 1, 0, STORE>(A, B, C, s, e, st);
   } else {
-    if (s.b_mn) launch_tc<BN, 0, 1>(A, B, C, s, e, st);
-    else launch_tc<BN, 0, 0>(A, B, C, s, e, st);
+    if (s.b_mn) launch_tc<BN, 0, 1, STORE>(A, B, C, s, e, st);
+    else launch_tc<BN, 0, 0, STORE>(A, B, C, s, e, st);
   }
+}
+
+template <int BN>
+void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
+                    cudaStream_t st) {
+  // TMA-store epilogue whenever the output (and GELU aux) layouts are
+  // 16-byte describable; kEpiAccum into bf16 has no TMA reduce here.
+  const int es = e.out_bf16 ? 2 : 4;
+  bool tma = aligned16(C, e.ldc, s.nh > 1 ? s.c_sh : 0, s.nb > 1 ? s.c_sb : 0, es) &&
+             !(e.out_bf16 && e.mode == kEpiAccum);
+  if (e.act == kActGelu)
+    tma = tma && e.out_bf16 && aligned16(e.aux, e.ldaux, s.nh > 1 ? s.c_sh : 0, s.nb > 1 ? s.c_sb : 0, 2);
+  if (!tma) dispatch_major<BN, 0>(A, B, C, s, e, st);
+  else if (e.out_bf16) dispatch_major<BN, 1>(A, B, C, s, e, st);
+  else dispatch_major<BN, 2>(A, B, C, s, e, st);
 }
 
 }  // namespace
@@ -577,8 +689,8 @@ void gemm_tc_bf16(const void* A, const void* B, void* C, const GemmShape& s, con
     HZP_CUDA(cudaEventCreate(&e1));
     HZP_CUDA(cudaEventRecord(e0, stream));
   }
-  if (s.N > 128) dispatch_major<256>(A, B, C, s, e, stream);
-  else dispatch_major<128>(A, B, C, s, e, stream);
+  if (s.N > 128) dispatch_store<256>(A, B, C, s, e, stream);
+  else dispatch_store<128>(A, B, C, s, e, stream);
   if (prof.on) {
     HZP_CUDA(cudaEventRecord(e1, stream));
     // algorithmic FLOPs: 2MNK per batch; the causal attention products do half

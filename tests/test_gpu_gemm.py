@@ -80,3 +80,60 @@ def test_ordered_f32_gemm_is_sequential_fp32(gpu, a_mn, b_mn):
              N if b_mn else K, N, a_mn, b_mn, 1)
     torch.cuda.synchronize()
     assert torch.equal(C.cpu(), ref)
+
+
+def _ex(A, B, C, M, N, K, lda, ldb, ldc, a_mn, b_mn, mode=0, out_bf16=1, act=0, bias=None, aux=None,
+        ldaux=0, resid=None, ldres=0, rowvec=None, alpha=1.0):
+    import ctypes as C_
+    from paper_2510_20111_b200 import _native as Nn
+    p = lambda t: C_.c_void_p(t.data_ptr() if t is not None else 0)  # noqa: E731
+    Nn.check(Nn.lib.hzp_gemm_bf16_ex(p(A), p(B), p(C), M, N, K, lda, ldb, ldc, a_mn, b_mn, mode,
+                                     out_bf16, act, p(bias), p(aux), ldaux, p(resid), ldres, p(rowvec),
+                                     alpha, None))
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (200, 328, 136), (96, 96, 64)])
+def test_epilogues_match_torch(gpu, M, N, K):
+    A, B, As, Bs, lda, ldb = _mk(M, N, K, 0, 0, gpu)
+    acc = A.float() @ B.float().t()
+    bias = torch.randn(N, device=gpu).to(torch.bfloat16)
+    resid = torch.randn(M, N, device=gpu).to(torch.bfloat16)
+    aux_in = (torch.rand(M, N, device=gpu) * 2 - 1).to(torch.bfloat16)
+    rowvec = torch.randn(M, device=gpu)
+    k = 0.7978845608028654
+    gelu = lambda u: 0.5 * u * (1 + torch.tanh(k * (u + 0.044715 * u ** 3)))  # noqa: E731
+
+    def dgelu(x):
+        t = torch.tanh(k * (x + 0.044715 * x ** 3))
+        return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * k * (1 + 3 * 0.044715 * x * x)
+    cases = [
+        (dict(act=0, bias=bias, resid=resid, ldres=N, alpha=0.5), 0.5 * acc + bias.float() + resid.float(), None),
+        (dict(act=1, bias=bias), torch.tanh(acc + bias.float()), None),
+        (dict(act=2, bias=bias), gelu(acc + bias.float()), acc + bias.float()),
+        (dict(act=3, aux=aux_in, ldaux=N), acc * (1 - aux_in.float() ** 2), None),
+        (dict(act=4, aux=aux_in, ldaux=N), acc * dgelu(aux_in.float()), None),
+        (dict(act=5, aux=aux_in, ldaux=N, rowvec=rowvec, alpha=0.25),
+         aux_in.float() * (0.25 * acc - 0.25 * rowvec[:, None]), None),
+    ]
+    for kw, want, want_aux in cases:
+        C = torch.zeros(M, N, device=gpu, dtype=torch.bfloat16)
+        aux_out = None
+        if kw["act"] == 2:
+            aux_out = torch.zeros(M, N, device=gpu, dtype=torch.bfloat16)
+            kw = dict(kw, aux=aux_out, ldaux=N)
+        _ex(As, Bs, C, M, N, K, lda, ldb, N, 0, 0, **kw)
+        torch.cuda.synchronize()
+        err = (C.float() - want).abs().max().item() / max(want.abs().max().item(), 1e-6)
+        assert err < 2e-2, (kw["act"], err)
+        if want_aux is not None:
+            e2 = (aux_out.float() - want_aux).abs().max().item() / want_aux.abs().max().item()
+            assert e2 < 1e-2, e2
+    # fp32 assign / accumulate through the TMA reduce-add path
+    C = torch.randn(M, N, device=gpu)
+    base = C.clone()
+    _ex(As, Bs, C, M, N, K, lda, ldb, N, 0, 0, mode=1, out_bf16=0)
+    torch.cuda.synchronize()
+    assert (C - (base + acc)).abs().max().item() < 1e-3
+    _ex(As, Bs, C, M, N, K, lda, ldb, N, 0, 0, mode=2, out_bf16=0)
+    torch.cuda.synchronize()
+    assert (C - acc).abs().max().item() < 1e-3
