@@ -136,7 +136,7 @@ SIGNATURES = [
     ("hzp_zero_grads", C.c_int, [_vp]),
     ("hzp_barrier", C.c_int, [_vp]),
     ("hzp_gemm_bf16", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 9 + [_vp]),
-    ("hzp_gemm_bf16_ex", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 12 + [_vp, _vp, C.c_int, _vp, C.c_int,
+    ("hzp_gemm_bf16_ex", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 11 + [_vp, _vp, C.c_int, _vp, C.c_int,
                                                                     _vp, C.c_float, _vp]),
     ("hzp_gemm_f32", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 9 + [_vp]),
 ]

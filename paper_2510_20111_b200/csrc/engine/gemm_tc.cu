@@ -28,7 +28,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
-constexpr int kThreadsTC = 192;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, each owning half the columns
+constexpr int kThreadsTC = 64 + 32 * kEpiWarps;
 
 int g_sm_budget = kNumSMs;
 
@@ -153,14 +154,19 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn, int b_
          (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
+__device__ __forceinline__ float tanh_fast(float x) {  // MUFU.TANH, rel. err ~2^-11 (bf16 outputs)
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k = 0.7978845608028654f;
-  return 0.5f * x * (1.f + tanhf(k * (x + 0.044715f * x * x * x)));
+  return 0.5f * x * (1.f + tanh_fast(k * (x + 0.044715f * x * x * x)));
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k = 0.7978845608028654f;
   const float u = k * (x + 0.044715f * x * x * x);
-  const float t = tanhf(u);
+  const float t = tanh_fast(u);
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k * (1.f + 3.f * 0.044715f * x * x);
 }
 
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -313,8 +319,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // TMA bulk tensor store (reduce-add for fp32 accumulation), so global
     // writes are full-line and coalesced whatever the row pitch.
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;  // 0 | 1: which interleaved 32-column chunks
     const Epilogue& e = p.e;
-    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + (quarter * 2) * 4096;
+    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + ((warp - 2) * 2) * 4096;
     int acc = 0, nchunk = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (e.act == kActSoftmaxGrad && row_ok)
         rv = e.rowvec[int64_t(tc.zh) * e.rv_sh + int64_t(tc.zb) * e.rv_sb + m];
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + acc * BN + c * 32, r);
         const int nb = n0 + c * 32;
@@ -590,8 +597,8 @@ bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
 template <int BN, int A_MN, int B_MN, int STORE>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
-  constexpr int STAGES = BN == 256 ? 4 : 6;
-  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 + 8 * 4096;
+  constexpr int STAGES = BN == 256 ? 3 : 5;
+  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 + kEpiWarps * 2 * 4096;
   static_assert(SMEM <= 232448, "smem budget");
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE>;
   static bool attr_set = false;  // per instantiation

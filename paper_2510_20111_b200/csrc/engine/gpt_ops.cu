@@ -330,6 +330,191 @@ __global__ void __launch_bounds__(kT) cross_entropy_kernel(uint16_t* __restrict_
   if (threadIdx.x == 0) atomicAdd(loss, (lse - xt) * inv_T);
 }
 
+
+// ---- warp-per-row variants (h <= 4096): no block-wide barriers per row ----
+constexpr int kWV = 16;  // max 8-element vectors per lane -> h <= 32*8*16 = 4096
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256) layernorm_fwd_warp_kernel(
+    const uint16_t* __restrict__ x, const uint16_t* __restrict__ g, const uint16_t* __restrict__ be,
+    uint16_t* __restrict__ y, float* __restrict__ mu, float* __restrict__ rs, int rows, int h) {
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int nv = h / 8;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+  float v[kWV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < kWV; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      unpack8(xr[i], v[k]);
+      for (int j = 0; j < 8; ++j) s += v[k][j];
+    }
+  }
+  const float mean = warp_sum(s) / h;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < kWV; ++k)
+    if (lane + 32 * k < nv)
+      for (int j = 0; j < 8; ++j) {
+        const float d = v[k][j] - mean;
+        q += d * d;
+      }
+  const float rstd = rsqrtf(warp_sum(q) / h + 1e-5f);
+  if (lane == 0) {
+    mu[r] = mean;
+    rs[r] = rstd;
+  }
+  uint4* yr = reinterpret_cast<uint4*>(y + int64_t(r) * h);
+#pragma unroll
+  for (int k = 0; k < kWV; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      float gg[8], bb[8], o[8];
+      unpack8(reinterpret_cast<const uint4*>(g)[i], gg);
+      unpack8(reinterpret_cast<const uint4*>(be)[i], bb);
+      for (int j = 0; j < 8; ++j) o[j] = (v[k][j] - mean) * rstd * gg[j] + bb[j];
+      yr[i] = pack8(o);
+    }
+  }
+}
+
+// dg / dbeta partial column sums accumulate in shared memory (red.shared.add)
+// and are flushed once per CTA into part[2][gridDim.x][h].
+constexpr int kWVB = 8;  // bwd keeps x-hat and dy*g live: h <= 2048
+
+__global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
+    const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
+    const float* __restrict__ mu, const float* __restrict__ rs, const uint16_t* __restrict__ resid,
+    uint16_t* __restrict__ dx, float* __restrict__ part, int rows, int h) {
+  extern __shared__ float acc[];  // [2][h]
+  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) acc[i] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  const int nv = h / 8;
+  for (int r = blockIdx.x * 8 + w; r < rows; r += gridDim.x * 8) {
+    const float m = mu[r], rstd = rs[r];
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+    float xh[kWVB][8], dg[kWVB][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < kWVB; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nv) {
+        float d[8], gg[8];
+        unpack8(dyr[i], d);
+        unpack8(xr[i], xh[k]);
+        unpack8(reinterpret_cast<const uint4*>(g)[i], gg);
+        for (int j = 0; j < 8; ++j) {
+          xh[k][j] = (xh[k][j] - m) * rstd;
+          dg[k][j] = d[j] * gg[j];
+          s1 += dg[k][j];
+          s2 += dg[k][j] * xh[k][j];
+          atomicAdd(&acc[8 * i + j], d[j] * xh[k][j]);
+          atomicAdd(&acc[h + 8 * i + j], d[j]);
+        }
+      }
+    }
+    const float a1 = warp_sum(s1) / h, a2 = warp_sum(s2) / h;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
+    const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + int64_t(r) * h) : nullptr;
+#pragma unroll
+    for (int k = 0; k < kWVB; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nv) {
+        float o[8], rv[8];
+        if (rr) unpack8(rr[i], rv);
+        for (int j = 0; j < 8; ++j) {
+          o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
+          if (rr) o[j] += rv[j];
+        }
+        dxr[i] = pack8(o);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    part[int64_t(blockIdx.x) * h + i] = acc[i];
+    part[int64_t(gridDim.x + blockIdx.x) * h + i] = acc[h + i];
+  }
+}
+
+// 32 columns per CTA, 8 warps split the chunk range, smem tree at the end.
+__global__ void __launch_bounds__(256) colsum_finalize_par_kernel(const float* __restrict__ part,
+                                                                 int chunks, int cols, void* out,
+                                                                 int out_bf16, int mode) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  const int c = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (c < cols)
+    for (int k = w; k < chunks; k += 8) s += part[int64_t(k) * cols + c];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = 0.f;
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+    write_mode(out, c, t, out_bf16, mode);
+  }
+}
+
+// Causal softmax, one warp per row, the whole (<= 2048-long) valid prefix
+// held in registers: one read of S, one write of P.
+__global__ void softmax_causal_reg_kernel(const float* __restrict__ S, uint16_t* __restrict__ P,
+                                          int Z, int Sq) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= Z * Sq) return;
+  const int q = row % Sq;
+  const float4* s4 = reinterpret_cast<const float4*>(S + int64_t(row) * Sq);
+  uint2* p4 = reinterpret_cast<uint2*>(P + int64_t(row) * Sq);
+  const int n = q + 1;
+  const int nchunk = (n + 127) / 128;  // 128 elements per warp pass (float4 per lane)
+  const float kL2E = 1.4426950408889634f;
+  float v[16][4];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    if (c < nchunk) {
+      const int k0 = c * 128 + lane * 4;
+      const float4 t = s4[c * 32 + lane];
+      v[c][0] = k0 + 0 < n ? t.x : -INFINITY;
+      v[c][1] = k0 + 1 < n ? t.y : -INFINITY;
+      v[c][2] = k0 + 2 < n ? t.z : -INFINITY;
+      v[c][3] = k0 + 3 < n ? t.w : -INFINITY;
+      mx = fmaxf(mx, fmaxf(fmaxf(v[c][0], v[c][1]), fmaxf(v[c][2], v[c][3])));
+    }
+  }
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (c < nchunk)
+      for (int j = 0; j < 4; ++j) {
+        v[c][j] = exp2f((v[c][j] - mx) * kL2E);  // exp2(-inf) = 0 for masked
+        sum += v[c][j];
+      }
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  const int zend = min(Sq, (q / 128 + 1) * 128);  // zero-fill to the 128-row tile edge
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    if (c * 128 < zend) {
+      float o[4];
+      for (int j = 0; j < 4; ++j) o[j] = c < nchunk ? v[c][j] * inv : 0.f;
+      uint2 w;
+      w.x = uint32_t(f32_to_bf16_bits(o[0])) | (uint32_t(f32_to_bf16_bits(o[1])) << 16);
+      w.y = uint32_t(f32_to_bf16_bits(o[2])) | (uint32_t(f32_to_bf16_bits(o[3])) << 16);
+      p4[c * 32 + lane] = w;
+    }
+  }
+}
 }  // namespace
 
 void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int b, int S,
@@ -345,13 +530,24 @@ void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, 
 void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
                    float* mu, float* rstd, int rows, int h, cudaStream_t s) {
   if (h % 8 || h > 8 * kT * kMaxVec) throw std::invalid_argument("layernorm: h % 8 != 0 or > 8192");
-  layernorm_fwd_kernel<<<rows, kT, 0, s>>>(x, g, beta, y, mu, rstd, h);
+  if (h <= 32 * 8 * kWV) layernorm_fwd_warp_kernel<<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h);
+  else layernorm_fwd_kernel<<<rows, kT, 0, s>>>(x, g, beta, y, mu, rstd, h);
   HZP_LAUNCH_CHECK();
 }
 void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
                    const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
                    int rows, int h, cudaStream_t s) {
-  layernorm_bwd_kernel<<<chunks, kT, 0, s>>>(dy, x, g, mu, rstd, resid, dx, part, chunks, rows, h);
+  if (h <= 32 * 8 * kWVB) {
+    const size_t smem = size_t(2) * h * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      HZP_CUDA(cudaFuncSetAttribute(layernorm_bwd_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+      attr = true;
+    }
+    layernorm_bwd_warp_kernel<<<chunks, 256, smem, s>>>(dy, x, g, mu, rstd, resid, dx, part, rows, h);
+  } else {
+    layernorm_bwd_kernel<<<chunks, kT, 0, s>>>(dy, x, g, mu, rstd, resid, dx, part, chunks, rows, h);
+  }
   HZP_LAUNCH_CHECK();
 }
 void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s) {
@@ -361,7 +557,7 @@ void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chun
 }
 void colsum_finalize(const float* part, int chunks, int cols, void* out, int out_bf16, int mode,
                      cudaStream_t s) {
-  colsum_finalize_kernel<<<(cols + 255) / 256, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
+  colsum_finalize_par_kernel<<<(cols + 31) / 32, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
   HZP_LAUNCH_CHECK();
 }
 void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s) {
@@ -370,7 +566,8 @@ void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, 
 }
 void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s) {
   const int rows = Z * Sq;
-  softmax_causal_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
+  if (Sq <= 2048 && Sq % 128 == 0) softmax_causal_reg_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
+  else softmax_causal_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
   HZP_LAUNCH_CHECK();
 }
 void attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int b, int nh, int S, int hd,
