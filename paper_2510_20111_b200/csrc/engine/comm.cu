@@ -17,7 +17,7 @@
 namespace hzp {
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;  // small enough to co-reside with a tcgen05 GEMM CTA (regs)
 constexpr int kUnroll = 4;
 
 __device__ __forceinline__ void fadd4(float4& a, const float4& b) {

@@ -72,7 +72,7 @@ struct Engine {
   uint64_t rs_seq = 0, barrier_epoch = 0;
   std::vector<hzp_launch_rec> log;
   int64_t launches = 0;
-  int comm_ctas = 32;
+  int comm_ctas = kNumSMs;  // one 256-thread CTA per SM, beside the persistent GEMM
   bool peers_open = false;
   bool debug_sync = false;
 

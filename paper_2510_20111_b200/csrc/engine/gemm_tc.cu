@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;  // 0 | 1: which interleaved 32-column chunks
     const Epilogue& e = p.e;
-    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + ((warp - 2) * 2) * 4096;
+    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + (warp - 2) * 4096;
     int acc = 0, nchunk = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -426,8 +426,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         if (STORE != 0) {
           // ---- stage in smem (swizzled) and TMA-store the 32x32 chunk ----
-          uint8_t* buf = stage_base + (nchunk & 1) * 4096;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          // one staging buffer per warp: the previous chunk's TMA store must
+          // have finished reading it (8 warps interleave, hiding the wait)
+          uint8_t* buf = stage_base;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
           if (STORE == 1) {  // bf16: 32 rows x 64 B, SWIZZLE_64B; GELU aux in the 2nd half
 #pragma unroll
@@ -597,8 +599,8 @@ bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
 template <int BN, int A_MN, int B_MN, int STORE>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
-  constexpr int STAGES = BN == 256 ? 3 : 5;
-  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 + kEpiWarps * 2 * 4096;
+  constexpr int STAGES = BN == 256 ? 4 : 6;
+  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 + kEpiWarps * 4096;
   static_assert(SMEM <= 232448, "smem budget");
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE>;
   static bool attr_set = false;  // per instantiation
