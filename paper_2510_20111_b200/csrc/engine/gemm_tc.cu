@@ -173,6 +173,7 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
 struct TcParams {
   CUtensorMap tmC;    // output (STORE != 0)
   CUtensorMap tmAux;  // GELU pre-activation output (STORE == 1, act == Gelu)
+  CUtensorMap tmSide; // side input (SIDE): aux for the *-grad epilogues, else resid
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
   int nh, causal;
@@ -200,7 +201,7 @@ __device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int&
   else if (p.causal == 3) kb0 = min(nkb, m0 / BK);
 }
 
-template <int BN, int A_MN, int B_MN, int STAGES, int STORE>
+template <int BN, int A_MN, int B_MN, int STAGES, int STORE, int SIDE>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ TcParams p) {
@@ -228,6 +229,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps);
     }
+    if (SIDE)
+      for (int i = 0; i < 2 * kEpiWarps; ++i)
+        mbar_init(reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512) + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -322,6 +326,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int half = (warp - 2) >> 2;  // 0 | 1: which interleaved 32-column chunks
     const Epilogue& e = p.e;
     uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + (warp - 2) * 4096;
+    // SIDE: the side input (P / pre-activation / residual) of each 32x32
+    // chunk is TMA-loaded into one of two 2 KB SW64 buffers per warp, the next
+    // chunk's load issued before the current one is consumed.
+    uint8_t* side_base = smem + STAGES * STAGE_BYTES + 1024 + kEpiWarps * 4096 + (warp - 2) * 4096;
+    uint64_t* side_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512) + (warp - 2) * 2;
+    uint32_t side_phase = 0;  // bit b = parity of buffer b's next completion
+    int side_buf = 0;
     int acc = 0, nchunk = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -331,6 +342,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (kb1 <= kb0) continue;
       const int m0 = tc.m0, n0 = tc.n0;
       const int64_t zoff = int64_t(tc.zh) * p.c_sh + int64_t(tc.zb) * p.c_sb;
+      if (SIDE && lane == 0 && n0 + half * 32 < p.N) {  // first chunk's side input
+        mbar_expect_tx(&side_bar[side_buf], 2048);
+        tma_load_4d(side_base + side_buf * 2048, &p.tmSide, &side_bar[side_buf], n0 + half * 32,
+                    m0 + quarter * 32, tc.zh, tc.zb);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int m = m0 + quarter * 32 + lane;
@@ -345,6 +361,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const int nb = n0 + c * 32;
         if (nb >= p.N) continue;                 // warp-uniform
         if (STORE == 0 && !row_ok) continue;
+        float sd[32];  // side input row (SIDE)
+        if (SIDE) {
+          const int nx = nb + 64;  // this warp's next chunk
+          if (lane == 0 && c + 2 < BN / 32 && nx < p.N) {
+            mbar_expect_tx(&side_bar[side_buf ^ 1], 2048);
+            tma_load_4d(side_base + (side_buf ^ 1) * 2048, &p.tmSide, &side_bar[side_buf ^ 1], nx,
+                        m0 + quarter * 32, tc.zh, tc.zb);
+          }
+          mbar_wait(&side_bar[side_buf], (side_phase >> side_buf) & 1);
+          side_phase ^= 1u << side_buf;
+          const uint8_t* sb = side_base + side_buf * 2048 + lane * 64;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            unpack8f(*reinterpret_cast<const uint4*>(sb + ((q ^ ((lane >> 1) & 3)) * 16)), sd + 8 * q);
+          side_buf ^= 1;
+        }
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * e.alpha;
@@ -382,7 +414,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         } else if (e.act == kActTanhGrad || e.act == kActGeluGrad || e.act == kActSoftmaxGrad) {
           float a[32];
-          if (row_ok) {
+          if (SIDE) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = sd[j];
+          } else if (row_ok) {
             const int64_t ab = zoff + int64_t(m) * e.ldaux + nb;
             if (e.aux_bf16 && full_chunk) {
               const uint4* ap = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(e.aux) + ab);
@@ -412,7 +447,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             for (int j = 0; j < 32; ++j) v[j] = a[j] * (v[j] - e.alpha * rv);
           }
         }
-        if (e.resid && row_ok) {
+        if (SIDE && e.resid) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += sd[j];
+        } else if (e.resid && row_ok) {
           const uint16_t* rp = static_cast<const uint16_t*>(e.resid) + zoff + int64_t(m) * e.ldres + nb;
           if (full_chunk) {
             float rr[32];
@@ -596,13 +634,15 @@ bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
          (sb * es) % 16 == 0;
 }
 
-template <int BN, int A_MN, int B_MN, int STORE>
+template <int BN, int A_MN, int B_MN, int STORE, int SIDE>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
-  constexpr int STAGES = BN == 256 ? 4 : 6;
-  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 + kEpiWarps * 4096;
+  // a side-input epilogue trades one mainloop stage for its smem buffers
+  constexpr int STAGES = (BN == 256 ? 4 : 6) - (SIDE ? 1 : 0);
+  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 +
+                          kEpiWarps * 4096 * (SIDE ? 2 : 1);
   static_assert(SMEM <= 232448, "smem budget");
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE, SIDE>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     HZP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
@@ -617,6 +657,10 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
     p.tmC = make_out_map(C, STORE == 2, s.N, s.M, e.ldc, s.nh, s.nb, s.c_sh, s.c_sb);
     if (STORE == 1 && e.act == kActGelu)
       p.tmAux = make_out_map(e.aux, false, s.N, s.M, e.ldaux, s.nh, s.nb, s.c_sh, s.c_sb);
+  }
+  if (SIDE) {
+    if (e.resid) p.tmSide = make_out_map(e.resid, false, s.N, s.M, e.ldres, s.nh, s.nb, s.c_sh, s.c_sb);
+    else p.tmSide = make_out_map(e.aux, false, s.N, s.M, e.ldaux, s.nh, s.nb, s.c_sh, s.c_sb);
   }
   p.M = s.M;
   p.N = s.N;
@@ -636,15 +680,15 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   HZP_LAUNCH_CHECK();
 }
 
-template <int BN, int STORE>
+template <int BN, int STORE, int SIDE>
 void dispatch_major(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                     cudaStream_t st) {
   if (s.a_mn) {
-    if (s.b_mn) launch_tc<BN, 1, 1, STORE>(A, B, C, s, e, st);
-    else launch_tc<BN, 1, 0, STORE>(A, B, C, s, e, st);
+    if (s.b_mn) launch_tc<BN, 1, 1, STORE, SIDE>(A, B, C, s, e, st);
+    else launch_tc<BN, 1, 0, STORE, SIDE>(A, B, C, s, e, st);
   } else {
-    if (s.b_mn) launch_tc<BN, 0, 1, STORE>(A, B, C, s, e, st);
-    else launch_tc<BN, 0, 0, STORE>(A, B, C, s, e, st);
+    if (s.b_mn) launch_tc<BN, 0, 1, STORE, SIDE>(A, B, C, s, e, st);
+    else launch_tc<BN, 0, 0, STORE, SIDE>(A, B, C, s, e, st);
   }
 }
 
@@ -658,9 +702,16 @@ void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, c
              !(e.out_bf16 && e.mode == kEpiAccum);
   if (e.act == kActGelu)
     tma = tma && e.out_bf16 && aligned16(e.aux, e.ldaux, s.nh > 1 ? s.c_sh : 0, s.nb > 1 ? s.c_sb : 0, 2);
-  if (!tma) dispatch_major<BN, 0>(A, B, C, s, e, st);
-  else if (e.out_bf16) dispatch_major<BN, 1>(A, B, C, s, e, st);
-  else dispatch_major<BN, 2>(A, B, C, s, e, st);
+  // side input through TMA: bf16 grads' aux or the residual, 16-byte layout
+  const bool aux_in = e.act == kActTanhGrad || e.act == kActGeluGrad || e.act == kActSoftmaxGrad;
+  const int64_t zsh = s.nh > 1 ? s.c_sh : 0, zsb = s.nb > 1 ? s.c_sb : 0;
+  const bool side = tma && e.out_bf16 && !(aux_in && e.resid) &&
+                    ((aux_in && e.aux_bf16 && aligned16(e.aux, e.ldaux, zsh, zsb, 2)) ||
+                     (!aux_in && e.resid && aligned16(e.resid, e.ldres, zsh, zsb, 2)));
+  if (!tma) dispatch_major<BN, 0, 0>(A, B, C, s, e, st);
+  else if (!e.out_bf16) dispatch_major<BN, 2, 0>(A, B, C, s, e, st);
+  else if (side) dispatch_major<BN, 1, 1>(A, B, C, s, e, st);
+  else dispatch_major<BN, 1, 0>(A, B, C, s, e, st);
 }
 
 }  // namespace
