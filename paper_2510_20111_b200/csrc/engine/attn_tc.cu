@@ -1,0 +1,281 @@
+// Fused causal attention forward on tcgen05 (sm_100a), head dim 128.
+//
+// One CTA per (128-query tile, head, sequence); 6 warps:
+//   warp 0    TMA producer: Q once, then K_j / V_j tiles (128 keys) into a
+//             2-deep smem ring (128B swizzle; V as MN-major 64x64 boxes)
+//   warp 1    TMEM owner + MMA issuer (one thread):
+//               S_j = Q K_j^T     -> TMEM S[j%2]   (M=128, N=128, K=128)
+//               O  += P_j V_j     -> TMEM O        (M=128, N=128, K=128)
+//             S_{j+1} is issued before O += P_j V_j so the softmax of the
+//             next tile overlaps the PV product of this one
+//   warps 2-5 softmax, one thread per query row (its TMEM lane): online
+//             max / sum in the exp2 domain, causal mask on the diagonal tile,
+//             P (bf16) written to smem as the K-major A operand of the PV MMA
+//             (and to global memory for the GEMM-based backward), O rescaled
+//             in TMEM when the running max moves, final O / l and lse out.
+// The S tile never leaves the SM: no fp32 score matrix in HBM.
+#include <cmath>
+
+#include "engine/gemm.cuh"
+#include "engine/tc_ptx.cuh"
+
+namespace hzp {
+namespace {
+
+using namespace tc;
+
+constexpr int kHd = 128;    // head dim
+constexpr int kBQ = 128;    // query rows per CTA
+constexpr int kBK = 128;    // keys per iteration
+constexpr int kTileBytes = 128 * kHd * 2;  // 32 KB (Q, K_j, V_j, P_j)
+constexpr int kThreads = 192;
+
+struct AttnParams {
+  CUtensorMap tmQ, tmK, tmV;  // 4-D views of qkv: {d, s, head, seq}
+  uint16_t* O;                // [b, S, h]
+  uint16_t* P;                // [b*nh, S, S] or null
+  float* lse;                 // [b*nh, S] or null
+  int S, h, nh, nq;
+  float scale_log2;           // log2(e) / sqrt(d)
+};
+
+// smem map
+constexpr int kOffQ = 0;
+constexpr int kOffK = kTileBytes;              // 2 stages
+constexpr int kOffV = 3 * kTileBytes;          // 2 stages
+constexpr int kOffP = 5 * kTileBytes;          // 2 buffers
+constexpr int kOffBar = 7 * kTileBytes;
+constexpr size_t kSmem = 7 * kTileBytes + 1024 + 1024;
+
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;     // [2]
+  uint64_t* v_full = bar + 3;     // [2]
+  uint64_t* kv_empty = bar + 5;   // [2]
+  uint64_t* s_full = bar + 7;     // [2]
+  uint64_t* s_free = bar + 9;     // [2]
+  uint64_t* p_full = bar + 11;    // [2]
+  uint64_t* p_empty = bar + 13;   // [2]
+  uint64_t* o_ready = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int qt = p.nq - 1 - blockIdx.x;  // heavy (late) query tiles first
+  const int head = blockIdx.y, seq = blockIdx.z;
+  const int q0 = qt * kBQ;
+  const int nkv = qt + 1;  // causal: key tiles 0..qt
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+    }
+    mbar_init(o_ready, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S0: cols [0,128), S1: [128,256), O: [256,384)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, kTileBytes);
+      for (int c = 0; c < 2; ++c)
+        tma_load_4d(smem + kOffQ + c * 16384, &p.tmQ, q_full, c * 64, q0, head, seq);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&kv_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_4d(smem + kOffK + st * kTileBytes + c * 16384, &p.tmK, &k_full[st], c * 64, j * kBK,
+                      head, seq);
+        mbar_expect_tx(&v_full[st], kTileBytes);
+        for (int kc = 0; kc < 2; ++kc)
+          for (int db = 0; db < 2; ++db)
+            tma_load_4d(smem + kOffV + st * kTileBytes + kc * 16384 + db * 8192, &p.tmV, &v_full[st],
+                        db * 64, j * kBK + kc * 64, head, seq);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = make_idesc(128, 128, 0, 0);   // Q K-major, K K-major
+      constexpr uint32_t kIdPV = make_idesc(128, 128, 0, 1);  // P K-major, V MN-major
+      const uint32_t sq = smem_u32(smem + kOffQ);
+      auto issue_pv = [&](int i) {
+        const int st = i & 1;
+        const uint32_t ph = (i >> 1) & 1;
+        mbar_wait(&p_full[st], ph);
+        mbar_wait(&v_full[st], ph);
+        tc_fence_after();
+        const uint32_t sp = smem_u32(smem + kOffP + st * kTileBytes);
+        const uint32_t sv = smem_u32(smem + kOffV + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = smem_desc(sp + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc(sv + (kk >> 2) * 16384 + (kk & 3) * 2048, 8192, 1024);
+          tc_mma(tmem + 256, ad, bd, kIdPV, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&p_empty[st]);
+        tc_commit(&kv_empty[st]);
+        tc_commit(o_ready);
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_full[st], ph);
+        mbar_wait(&s_free[st], ph ^ 1);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(smem + kOffK + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = smem_desc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          tc_mma(tmem + st * 128, ad, bd, kIdS, kk > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[st]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      issue_pv(nkv - 1);
+    }
+  } else {
+    // ---- softmax warps: row = TMEM lane ----
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int q = q0 + row;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const int z = seq * p.nh + head;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(&s_full[st], ph);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + st * 128 + c * 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * p.scale_log2;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[st]);
+      if (j == nkv - 1) {  // diagonal tile: keys j*128 + c > q are masked
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > row) s[c] = -INFINITY;
+      }
+      float mx = m;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      const float corr = exp2f(m - mx);  // 0 on the first tile (m = -inf)
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        s[c] = exp2f(s[c] - mx);
+        sum += s[c];
+      }
+      l = l * corr + sum;
+      m = mx;
+      // P_j -> smem (K-major SW128 A operand) and global (backward)
+      mbar_wait(&p_empty[st], ph ^ 1);
+      uint8_t* pb = smem + kOffP + st * kTileBytes;
+      uint4* pg = p.P ? reinterpret_cast<uint4*>(p.P + (int64_t(z) * p.S + q) * p.S + int64_t(j) * kBK) : nullptr;
+#pragma unroll
+      for (int c8 = 0; c8 < 16; ++c8) {
+        const uint4 w = pack8f(s + 8 * c8);
+        const int kc = c8 >> 3, j8 = c8 & 7;
+        *reinterpret_cast<uint4*>(pb + kc * 16384 + row * 128 + ((j8 ^ (row & 7)) * 16)) = w;
+        if (pg) pg[c8] = w;
+      }
+      if (j >= 1) {  // O holds P_{<j} V; rescale once PV_{j-1} has landed
+        mbar_wait(o_ready, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tmem_st32(tmem + lane_off + 256 + c * 32, r);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[st]);
+    }
+    mbar_wait(o_ready, (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    uint4* og = reinterpret_cast<uint4*>(p.O + (int64_t(seq) * p.S + q) * p.h + int64_t(head) * kHd);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+      float o[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) og[c * 4 + i] = pack8f(o + 8 * i);
+    }
+    if (p.lse) p.lse[int64_t(z) * p.S + q] = (m + log2f(l)) * 0.6931471805599453f;
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+}  // namespace
+
+// qkv [b, S, 3h] (q | k | v, heads contiguous in each), O [b, S, h].
+void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse, int b, int nh,
+                      int S, int h, cudaStream_t stream) {
+  if (h != nh * kHd || S % kBQ) throw std::invalid_argument("fused attention needs head dim 128, S % 128 == 0");
+  static bool attr = false;
+  if (!attr) {
+    HZP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem)));
+    attr = true;
+  }
+  AttnParams p;
+  const int64_t h3 = 3 * int64_t(h);
+  p.tmQ = make_tma_map_bf16(qkv, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmK = make_tma_map_bf16(qkv + h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmV = make_tma_map_bf16(qkv + 2 * h, kHd, S, h3, 64, nh, b, kHd, int64_t(S) * h3);
+  p.O = O;
+  p.P = P;
+  p.lse = lse;
+  p.S = S;
+  p.h = h;
+  p.nh = nh;
+  p.nq = S / kBQ;
+  p.scale_log2 = 1.4426950408889634f / std::sqrt(float(kHd));
+  dim3 grid(S / kBQ, nh, b);
+  attn_fwd_kernel<<<grid, kThreads, kSmem, stream>>>(p);
+  HZP_LAUNCH_CHECK();
+}
+
+}  // namespace hzp

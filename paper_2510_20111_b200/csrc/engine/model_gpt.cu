@@ -16,6 +16,7 @@
 
 #include "engine/gemm.cuh"
 #include "engine/gpt_ops.cuh"
+#include "engine/attn.cuh"
 #include "engine/model.hpp"
 
 namespace hzp {
@@ -62,8 +63,8 @@ class GptModel final : public Model {
     b_ = c.batch;
     T_ = int64_t(b_) * S_;
     L_ = c.layers;
-    if (h_ % 64 || f_ % 64 || V_ % 64 || S_ % 128 || hd_ % 64 || h_ % nh_)
-      throw std::invalid_argument("GPT dims must be multiples of 64 (seq of 128, head dim of 64)");
+    if (h_ % 64 || f_ % 64 || V_ % 64 || S_ % 128 || hd_ != 128 || h_ % nh_)
+      throw std::invalid_argument("GPT dims must be multiples of 64, seq of 128, head dim 128");
     int64_t o = 0;
     auto take = [&](int64_t n) {
       const int64_t r = o;
@@ -145,7 +146,7 @@ class GptModel final : public Model {
     B->muf = f32(T_);
     B->rsf = f32(T_);
     B->logits = bf(T_ * V_);
-    B->S = f32(SS);
+    B->S = nullptr;  // scores stay in TMEM (fused attention)
     B->dS = bf(SS);
     B->D = f32(Z * S_);
     B->dx[0] = bf(T_ * h_);
@@ -263,24 +264,8 @@ class GptModel final : public Model {
       e.bias_any = W + o.b_qkv;
       linear_fwd(a.ln1, W + o.w_qkv, a.qkv, int(h3), h_, e, s);
     }
-    const int64_t SS = int64_t(S_) * S_;
-    {  // S = Q K^T / sqrt(d)  (fp32, causal tile skip)
-      GemmShape sh = attn_shape(S_, S_, hd_, int(h3), int(h3), 0, 0, hd_, S_ * h3, hd_, S_ * h3, SS,
-                                SS * nh_, 1);
-      Epilogue e;
-      e.out_bf16 = 0;
-      e.ldc = S_;
-      e.alpha = 1.f / std::sqrt(float(hd_));
-      gemm_tc_bf16(a.qkv, a.qkv + h_, B->S, sh, e, s);
-    }
-    softmax_causal(B->S, a.P, b_ * nh_, S_, s);
-    {  // O = P V  -> attn [T, h] head slices
-      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 0, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
-                                int64_t(S_) * h_, 2);
-      Epilogue e;
-      e.ldc = h_;
-      gemm_tc_bf16(a.P, a.qkv + 2 * h_, a.attn, sh, e, s);
-    }
+    // fused tcgen05 flash attention: S stays in TMEM; P (bf16) kept for the backward
+    attention_fwd_tc(a.qkv, a.attn, a.P, nullptr, b_, nh_, S_, h_, s);
     {
       Epilogue e;
       e.bias_any = W + o.b_o;
