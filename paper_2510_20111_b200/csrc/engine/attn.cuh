@@ -13,4 +13,11 @@ namespace hzp {
 void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse, int b, int nh,
                       int S, int h, cudaStream_t stream);
 
+// Backward for dK, dV (written into the k / v thirds of dqkv [b, S, 3h]) from
+// qkv, dO [b, S, h], lse and D = rowsum(dO * O) [b*nh, S]; also writes
+// dS^T [b*nh, S(key), S(query)] bf16 (zero where key > query inside the
+// diagonal tile) so dQ = dS K runs as a causal batched GEMM.
+void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse, const float* D,
+                      uint16_t* dqkv, uint16_t* dsT, int b, int nh, int S, int h, cudaStream_t stream);
+
 }  // namespace hzp

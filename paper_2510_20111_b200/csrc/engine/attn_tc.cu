@@ -249,6 +249,219 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused causal attention backward for dK, dV (and dS^T for the dQ GEMM).
+//
+// One CTA per (128-key tile, head, sequence), iterating query tiles q >= key
+// tile.  Rows of every TMEM accumulator are KEYS:
+//   S^T  = K Q_i^T          TMEM [0,128)     (P^T = exp2(S^T*c - lse2_q))
+//   dP^T = V dO_i^T         TMEM [128,256)   (dS^T = P^T (dP^T - D_q) / sqrt(d))
+//   dV  += P^T dO_i         TMEM [256,384)   (P^T from smem, dO_i as MN-major B)
+//   dK  += dS^T Q_i         TMEM [384,512)   (dS^T from smem, Q_i as MN-major B)
+// The same K-major SW128 smem tile of Q_i / dO_i serves as the K-major B of
+// the first products and the MN-major B of the accumulations (64-wide d
+// chunks at LBO = 16 KB, 8-row query groups at SBO = 1 KB).
+struct AttnBwdParams {
+  CUtensorMap tmQ, tmK, tmV, tmdO;
+  const float* lse;  // [z, S] natural log
+  const float* D;    // [z, S] rowsum(dO * O)
+  uint16_t* dqkv;    // [b, S, 3h]: dK, dV written into the k / v thirds
+  uint16_t* dsT;     // [z, S(key), S(q)] bf16, for dQ = dS K
+  int S, h, nh, nq;
+  float scale_log2, scale;
+};
+
+constexpr int kBOffK = 0;
+constexpr int kBOffV = kTileBytes;
+constexpr int kBOffQ = 2 * kTileBytes;
+constexpr int kBOffdO = 3 * kTileBytes;
+constexpr int kBOffPT = 4 * kTileBytes;
+constexpr int kBOffDS = 5 * kTileBytes;
+constexpr int kBOffVec = 6 * kTileBytes;            // lse2[128], D[128]
+constexpr int kBOffBar = 6 * kTileBytes + 1024;
+constexpr size_t kBSmem = 6 * kTileBytes + 2048 + 1024;
+
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnBwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kBOffBar);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qd_full = bar + 1;
+  uint64_t* qd_empty = bar + 2;
+  uint64_t* s_full = bar + 3;
+  uint64_t* s_free = bar + 4;
+  uint64_t* p_full = bar + 5;
+  uint64_t* p_empty = bar + 6;
+  uint64_t* acc_done = bar + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+  float* vec_lse = reinterpret_cast<float*>(smem + kBOffVec);
+  float* vec_D = vec_lse + 128;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x;  // key tile; small kt = most query tiles (launched first)
+  const int head = blockIdx.y, seq = blockIdx.z;
+  const int k0 = kt * kBK;
+  const int nit = p.nq - kt;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    mbar_init(qd_full, 1);
+    mbar_init(qd_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_full, 4);
+    mbar_init(p_empty, 1);
+    mbar_init(acc_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * kTileBytes);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_4d(smem + kBOffK + c * 16384, &p.tmK, kv_full, c * 64, k0, head, seq);
+        tma_load_4d(smem + kBOffV + c * 16384, &p.tmV, kv_full, c * 64, k0, head, seq);
+      }
+      for (int it = 0; it < nit; ++it) {
+        const int q0 = (kt + it) * kBQ;
+        mbar_wait(qd_empty, (it & 1) ^ 1);
+        mbar_expect_tx(qd_full, 2 * kTileBytes);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_4d(smem + kBOffQ + c * 16384, &p.tmQ, qd_full, c * 64, q0, head, seq);
+          tma_load_4d(smem + kBOffdO + c * 16384, &p.tmdO, qd_full, c * 64, q0, head, seq);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdKK = make_idesc(128, 128, 0, 0);  // A, B K-major
+      constexpr uint32_t kIdKM = make_idesc(128, 128, 0, 1);  // A K-major, B MN-major
+      const uint32_t sk = smem_u32(smem + kBOffK), sv = smem_u32(smem + kBOffV);
+      const uint32_t sq = smem_u32(smem + kBOffQ), sdo = smem_u32(smem + kBOffdO);
+      const uint32_t spt = smem_u32(smem + kBOffPT), sds = smem_u32(smem + kBOffDS);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < nit; ++it) {
+        mbar_wait(qd_full, it & 1);
+        mbar_wait(s_free, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma(tmem + 0, smem_desc(sk + o, 16, 1024), smem_desc(sq + o, 16, 1024), kIdKK, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc_mma(tmem + 128, smem_desc(sv + o, 16, 1024), smem_desc(sdo + o, 16, 1024), kIdKK, kk > 0);
+        }
+        tc_commit(s_full);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries
+          const uint32_t a = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t b = kk * 2048;
+          tc_mma(tmem + 256, smem_desc(spt + a, 16, 1024), smem_desc(sdo + b, 16384, 1024), kIdKM,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+          tc_mma(tmem + 384, smem_desc(sds + a, 16, 1024), smem_desc(sq + b, 16384, 1024), kIdKM,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(p_empty);
+        tc_commit(qd_empty);
+      }
+      tc_commit(acc_done);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // key k0 + row
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const int z = seq * p.nh + head;
+    const int tid = threadIdx.x - 64;  // 0..127
+    for (int it = 0; it < nit; ++it) {
+      const int qi = kt + it;
+      const int q0 = qi * kBQ;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile done with vec_*
+      vec_lse[tid] = p.lse[int64_t(z) * p.S + q0 + tid] * 1.4426950408889634f;
+      vec_D[tid] = p.D[int64_t(z) * p.S + q0 + tid];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      mbar_wait(p_empty, (it & 1) ^ 1);  // PT / dS^T smem free (MMAs of it-1 retired)
+      uint8_t* pt = smem + kBOffPT;
+      uint8_t* ds = smem + kBOffDS;
+      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0);
+      const bool diag = qi == kt;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rd[32];
+        tmem_ld32(tmem + lane_off + c * 32, rs);
+        tmem_ld32(tmem + lane_off + 128 + c * 32, rd);
+        float pv[32], dv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int qc = c * 32 + i;
+          const float e = exp2f(__uint_as_float(rs[i]) * p.scale_log2 - vec_lse[qc]);
+          const float pp = (diag && qc < row) ? 0.f : e;  // key > query masked
+          pv[i] = pp;
+          dv[i] = pp * (__uint_as_float(rd[i]) - vec_D[qc]) * p.scale;
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int c8 = c * 4 + g;  // 8-query group index 0..15
+          const int kc = c8 >> 3, j8 = c8 & 7;
+          const int off = kc * 16384 + row * 128 + ((j8 ^ (row & 7)) * 16);
+          *reinterpret_cast<uint4*>(pt + off) = pack8f(pv + 8 * g);
+          const uint4 w = pack8f(dv + 8 * g);
+          *reinterpret_cast<uint4*>(ds + off) = w;
+          dsg[c8] = w;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    const int64_t rowbase = (int64_t(seq) * p.S + k0 + row) * (3 * int64_t(p.h)) + int64_t(head) * kHd;
+    uint4* dkg = reinterpret_cast<uint4*>(p.dqkv + rowbase + p.h);
+    uint4* dvg = reinterpret_cast<uint4*>(p.dqkv + rowbase + 2 * p.h);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      float o[32];
+      tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dvg[c * 4 + i] = pack8f(o + 8 * i);
+      tmem_ld32(tmem + lane_off + 384 + c * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dkg[c * 4 + i] = pack8f(o + 8 * i);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 }  // namespace
 
 // qkv [b, S, 3h] (q | k | v, heads contiguous in each), O [b, S, h].
@@ -275,6 +488,35 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
   p.scale_log2 = 1.4426950408889634f / std::sqrt(float(kHd));
   dim3 grid(S / kBQ, nh, b);
   attn_fwd_kernel<<<grid, kThreads, kSmem, stream>>>(p);
+  HZP_LAUNCH_CHECK();
+}
+
+void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse, const float* D,
+                      uint16_t* dqkv, uint16_t* dsT, int b, int nh, int S, int h, cudaStream_t stream) {
+  if (h != nh * kHd || S % kBQ) throw std::invalid_argument("fused attention needs head dim 128, S % 128 == 0");
+  static bool attr = false;
+  if (!attr) {
+    HZP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBSmem)));
+    attr = true;
+  }
+  AttnBwdParams p;
+  const int64_t h3 = 3 * int64_t(h);
+  p.tmQ = make_tma_map_bf16(qkv, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmK = make_tma_map_bf16(qkv + h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmV = make_tma_map_bf16(qkv + 2 * h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmdO = make_tma_map_bf16(dO, kHd, S, h, 128, nh, b, kHd, int64_t(S) * h);
+  p.lse = lse;
+  p.D = D;
+  p.dqkv = dqkv;
+  p.dsT = dsT;
+  p.S = S;
+  p.h = h;
+  p.nh = nh;
+  p.nq = S / kBQ;
+  p.scale = 1.f / std::sqrt(float(kHd));
+  p.scale_log2 = 1.4426950408889634f * p.scale;
+  dim3 grid(S / kBK, nh, b);
+  attn_bwd_kernel<<<grid, kThreads, kBSmem, stream>>>(p);
   HZP_LAUNCH_CHECK();
 }
 

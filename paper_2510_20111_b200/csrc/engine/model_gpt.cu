@@ -8,9 +8,10 @@
 //   layer L+1      head: lnf_g lnf_b [h] | w_head [V, h]  (untied)
 // Every matrix is row-major [out, in] like the reference's W (train.cpp:42-53),
 // so all three products of each linear layer map onto the tcgen05 GEMM
-// without transposes (gemm.cuh).  Attention runs as batched causal tcgen05
-// GEMMs over (sequence, head): S = QK^T * d^-1/2 (fp32, upper tiles skipped),
-// causal softmax, O = PV; backward dS = P * (dP - rowdot(dO, O)), dQ, dK, dV.
+// without transposes (gemm.cuh).  Attention is fused on tcgen05 (attn_tc.cu):
+// forward keeps S in TMEM (online softmax, lse saved); backward recomputes P
+// per key tile, accumulates dK / dV in TMEM and emits dS^T for dQ = dS K
+// (a causal batched GEMM).
 #include <cmath>
 #include <vector>
 
@@ -27,8 +28,8 @@ struct BlockOff {  // element offsets inside a block's parameter range
 };
 
 struct LayerActs {  // saved activations of one block (one microbatch)
-  uint16_t *ln1, *qkv, *P, *attn, *xm, *ln2, *fpre, *fact;
-  float *mu1, *rs1, *mu2, *rs2;
+  uint16_t *ln1, *qkv, *attn, *xm, *ln2, *fpre, *fact;
+  float *mu1, *rs1, *mu2, *rs2, *lse;  // lse [Z, S]: softmax stats for the backward
 };
 
 struct GptBuffers {
@@ -131,7 +132,7 @@ class GptModel final : public Model {
       LayerActs& a = B->acts[l];
       a.ln1 = bf(T_ * h_);
       a.qkv = bf(T_ * 3 * h_);
-      a.P = bf(SS);
+      a.lse = f32(int64_t(b_) * nh_ * S_);
       a.attn = bf(T_ * h_);
       a.xm = bf(T_ * h_);
       a.ln2 = bf(T_ * h_);
@@ -166,7 +167,7 @@ class GptModel final : public Model {
     auto* B = static_cast<GptBuffers*>(p);
     for (auto* x : B->x) cudaFree(x);
     for (auto& a : B->acts) {
-      for (void* q : {(void*)a.ln1, (void*)a.qkv, (void*)a.P, (void*)a.attn, (void*)a.xm,
+      for (void* q : {(void*)a.ln1, (void*)a.qkv, (void*)a.lse, (void*)a.attn, (void*)a.xm,
                       (void*)a.ln2, (void*)a.fpre, (void*)a.fact, (void*)a.mu1, (void*)a.rs1,
                       (void*)a.mu2, (void*)a.rs2})
         cudaFree(q);
@@ -265,7 +266,7 @@ class GptModel final : public Model {
       linear_fwd(a.ln1, W + o.w_qkv, a.qkv, int(h3), h_, e, s);
     }
     // fused tcgen05 flash attention: S stays in TMEM; P (bf16) kept for the backward
-    attention_fwd_tc(a.qkv, a.attn, a.P, nullptr, b_, nh_, S_, h_, s);
+    attention_fwd_tc(a.qkv, a.attn, nullptr, a.lse, b_, nh_, S_, h_, s);
     {
       Epilogue e;
       e.bias_any = W + o.b_o;
@@ -340,44 +341,17 @@ class GptModel final : public Model {
       Epilogue e;
       linear_dgrad(B->dxm, W + o.w_o, B->dattn, h_, h_, e, s);
     }
-    // attention core
+    // attention core: fused tcgen05 backward for dK, dV (P recomputed from
+    // lse, dS^T emitted), then dQ = dS K as a causal batched GEMM
     const int64_t SS = int64_t(S_) * S_;
-    const float scale = 1.f / std::sqrt(float(hd_));
     attn_rowdot(B->dattn, a.attn, B->D, b_, nh_, S_, hd_, s);
-    {  // dS = scale * P * (dO V^T - D)
-      GemmShape sh = attn_shape(S_, S_, hd_, h_, int(h3), 0, 0, hd_, int64_t(S_) * h_, hd_, S_ * h3,
-                                SS, SS * nh_, 1);
-      Epilogue e;
-      e.ldc = S_;
-      e.act = kActSoftmaxGrad;
-      e.aux = a.P;
-      e.ldaux = S_;
-      e.alpha = scale;
-      e.rowvec = B->D;
-      e.rv_sh = S_;
-      e.rv_sb = int64_t(S_) * nh_;
-      gemm_tc_bf16(B->dattn, a.qkv + 2 * h_, B->dS, sh, e, s);
-    }
-    {  // dQ = dS K
-      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 0, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
+    attention_bwd_tc(a.qkv, B->dattn, a.lse, B->D, B->dqkv, B->dS, b_, nh_, S_, h_, s);
+    {  // dQ[q, d] = sum_key dS^T[key, q] K[key, d]
+      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 1, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
                                 S_ * h3, 2);
       Epilogue e;
       e.ldc = int(h3);
       gemm_tc_bf16(B->dS, a.qkv + h_, B->dqkv, sh, e, s);
-    }
-    {  // dK = dS^T Q
-      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 1, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
-                                S_ * h3, 3);
-      Epilogue e;
-      e.ldc = int(h3);
-      gemm_tc_bf16(B->dS, a.qkv, B->dqkv + h_, sh, e, s);
-    }
-    {  // dV = P^T dO
-      GemmShape sh = attn_shape(S_, hd_, S_, S_, h_, 1, 1, SS, SS * nh_, hd_, int64_t(S_) * h_, hd_,
-                                S_ * h3, 3);
-      Epilogue e;
-      e.ldc = int(h3);
-      gemm_tc_bf16(a.P, B->dattn, B->dqkv + 2 * h_, sh, e, s);
     }
     linear_wgrad(B->dqkv, a.ln1, int(h3), h_, g, o.w_qkv, o.b_qkv, B, s);
     {
