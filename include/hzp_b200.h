@@ -289,6 +289,13 @@ int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K,
                      int ldc, int a_mn, int b_mn, int mode, int out_bf16, int act,
                      const void* bias_bf16, void* aux, int ldaux, const void* resid, int ldres,
                      const float* rowvec, float alpha, void* stream);
+/* Fused causal attention (head dim 128) on bf16 device buffers: qkv [b,S,3h],
+ * O [b,S,h], lse [b*nh,S] fp32; backward from dO [b,S,h] and
+ * D = rowsum(dO*O) [b*nh,S] writes dK, dV into dqkv [b,S,3h] and dS^T
+ * [b*nh,S,S] (bf16) — dQ is then one causal GEMM (done here too). */
+int hzp_attention_fwd(const void* qkv, void* O, float* lse, int b, int nh, int S, int h, void* stream);
+int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const float* lse, float* D,
+                      void* dqkv, void* dsT, int b, int nh, int S, int h, void* stream);
 /* Same contract, fp32 operands on the CUDA cores (fp32 parity tier). */
 int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                  int ldb, int ldc, int a_mn, int b_mn, int epi, void* stream);

@@ -138,6 +138,8 @@ SIGNATURES = [
     ("hzp_gemm_bf16", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 9 + [_vp]),
     ("hzp_gemm_bf16_ex", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 11 + [_vp, _vp, C.c_int, _vp, C.c_int,
                                                                     _vp, C.c_float, _vp]),
+    ("hzp_attention_fwd", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 4 + [_vp]),
+    ("hzp_attention_bwd", C.c_int, [_vp] * 7 + [C.c_int] * 4 + [_vp]),
     ("hzp_gemm_f32", C.c_int, [_vp, _vp, _vp] + [C.c_int] * 9 + [_vp]),
 ]
 

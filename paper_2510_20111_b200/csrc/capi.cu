@@ -9,7 +9,9 @@
 #include <cstring>
 #include <string>
 
+#include "engine/attn.cuh"
 #include "engine/engine.hpp"
+#include "engine/gpt_ops.cuh"
 #include "engine/gemm.cuh"
 #include "hzp_b200.h"
 
@@ -664,6 +666,39 @@ int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K,
     e.rowvec = rowvec;
     e.alpha = alpha;
     gemm_tc_bf16(A, B, C, s, e, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hzp_attention_fwd(const void* qkv, void* O, float* lse, int b, int nh, int S, int h, void* stream) {
+  return guarded([&] {
+    attention_fwd_tc(static_cast<const uint16_t*>(qkv), static_cast<uint16_t*>(O), nullptr, lse, b, nh, S, h,
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const float* lse, float* D,
+                      void* dqkv, void* dsT, int b, int nh, int S, int h, void* stream) {
+  return guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    const auto* q = static_cast<const uint16_t*>(qkv);
+    auto* dq = static_cast<uint16_t*>(dqkv);
+    auto* ds = static_cast<uint16_t*>(dsT);
+    attn_rowdot(static_cast<const uint16_t*>(dO), static_cast<const uint16_t*>(O), D, b, nh, S, 128, st);
+    attention_bwd_tc(q, static_cast<const uint16_t*>(dO), lse, D, dq, ds, b, nh, S, h, st);
+    const int64_t h3 = 3 * int64_t(h), SS = int64_t(S) * S;
+    GemmShape sh{S, 128, S, S, int(h3), 1, 1};
+    sh.nh = nh;
+    sh.nb = b;
+    sh.a_sh = SS;
+    sh.a_sb = SS * nh;
+    sh.b_sh = 128;
+    sh.b_sb = S * h3;
+    sh.c_sh = 128;
+    sh.c_sb = S * h3;
+    sh.causal = 2;
+    Epilogue e;
+    e.ldc = int(h3);
+    gemm_tc_bf16(ds, q + h, dq, sh, e, st);
   });
 }
 
