@@ -186,15 +186,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       float mx = m;
 #pragma unroll
       for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
-      const float corr = exp2f(m - mx);  // 0 on the first tile (m = -inf)
+      // lazy rescaling (FA4): keep the stale max unless it grew by > 8 (log2
+      // units); P <= 2^8 stays well inside fp32 / bf16 range and O, l use the
+      // same reference max, so the result is exact up to rounding
+      const bool bump = mx > m + 8.f;
+      const float mref = bump ? mx : m;
+      const float corr = bump ? exp2_fast(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
       float sum = 0.f;
 #pragma unroll
       for (int c = 0; c < 128; ++c) {
-        s[c] = exp2f(s[c] - mx);
+        s[c] = exp2_fast(s[c] - mref);
         sum += s[c];
       }
       l = l * corr + sum;
-      m = mx;
+      m = mref;
       // P_j -> smem (K-major SW128 A operand) and global (backward)
       mbar_wait(&p_empty[st], ph ^ 1);
       uint8_t* pb = smem + kOffP + st * kTileBytes;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int qc = c * 32 + i;
-          const float e = exp2f(__uint_as_float(rs[i]) * p.scale_log2 - vec_lse[qc]);
+          const float e = exp2_fast(__uint_as_float(rs[i]) * p.scale_log2 - vec_lse[qc]);
           const float pp = (diag && qc < row) ? 0.f : e;  // key > query masked
           pv[i] = pp;
           dv[i] = pp * (__uint_as_float(rd[i]) - vec_D[qc]) * p.scale;

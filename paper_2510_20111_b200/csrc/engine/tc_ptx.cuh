@@ -136,6 +136,11 @@ __device__ __forceinline__ float tanh_fast(float x) {  // MUFU.TANH, rel. err ~2
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float exp2_fast(float x) {  // MUFU.EX2, ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k = 0.7978845608028654f;
   return 0.5f * x * (1.f + tanh_fast(k * (x + 0.044715f * x * x * x)));

@@ -71,6 +71,35 @@ def bench_comm():
             eng.close()
 
 
+def bench_attn():
+    import ctypes as C
+    from paper_2510_20111_b200 import _native as N
+    dev = torch.device("cuda:0")
+    b, nh, S, hd = 4, 16, 2048, 128
+    h = nh * hd
+    qkv = (torch.randn(b, S, 3 * h, device=dev) * 0.5).to(torch.bfloat16)
+    do = (torch.randn(b, S, h, device=dev) * 0.1).to(torch.bfloat16)
+    O = torch.zeros(b, S, h, device=dev, dtype=torch.bfloat16)
+    lse = torch.zeros(b * nh, S, device=dev)
+    D = torch.zeros(b * nh, S, device=dev)
+    dqkv = torch.zeros(b, S, 3 * h, device=dev, dtype=torch.bfloat16)
+    dsT = torch.zeros(b * nh, S, S, device=dev, dtype=torch.bfloat16)
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    fwd = lambda: N.check(N.lib.hzp_attention_fwd(p(qkv), p(O), p(lse), b, nh, S, h, st))  # noqa: E731
+    bwd = lambda: N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv), p(dsT), b, nh, S, h, st))  # noqa: E731
+    flops_fwd = 4.0 * b * nh * S * S * hd / 2  # causal QK^T + PV
+    for name, fn, fl in (("attn_fwd", fwd, flops_fwd), ("attn_bwd(+rowdot+dQ gemm)", bwd, 2.5 * flops_fwd)):
+        ms = timeit(fn)
+        print(json.dumps({"kernel": name, "b": b, "nh": nh, "S": S, "ms": round(ms, 4),
+                          "tflops_causal": round(fl / ms / 1e9, 1)}), flush=True)
+    ms = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(
+        qkv[..., :h].view(b, S, nh, hd).transpose(1, 2), qkv[..., h:2 * h].view(b, S, nh, hd).transpose(1, 2),
+        qkv[..., 2 * h:].view(b, S, nh, hd).transpose(1, 2), is_causal=True))
+    print(json.dumps({"kernel": "torch_sdpa_fwd (comparator)", "ms": round(ms, 4),
+                      "tflops_causal": round(flops_fwd / ms / 1e9, 1)}), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "gemm"
-    {"gemm": bench_gemm, "comm": bench_comm}[what]()
+    {"gemm": bench_gemm, "comm": bench_comm, "attn": bench_attn}[what]()
