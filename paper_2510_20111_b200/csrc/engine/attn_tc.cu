@@ -211,18 +211,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         *reinterpret_cast<uint4*>(pb + kc * 16384 + row * 128 + ((j8 ^ (row & 7)) * 16)) = w;
         if (pg) pg[c8] = w;
       }
-      if (j >= 1) {  // O holds P_{<j} V; rescale once PV_{j-1} has landed
+      // O holds P_{<j} V; only a row whose reference max moved needs PV_{j-1}
+      // to land before rescaling.  Skipping the wait otherwise is safe: PV_j
+      // cannot complete before this warp arrives on p_full[j], so o_ready is
+      // never more than one phase ahead of the one waited for.
+      if (j >= 1 && __any_sync(0xffffffffu, bump)) {
         mbar_wait(o_ready, (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_off + 256 + c * 32, r);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
-            tmem_st32(tmem + lane_off + 256 + c * 32, r);
-          }
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+          tmem_st32(tmem + lane_off + 256 + c * 32, r);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -258,15 +260,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 // ---------------------------------------------------------------------------
 // Fused causal attention backward for dK, dV (and dS^T for the dQ GEMM).
 //
-// One CTA per (128-key tile, head, sequence), iterating query tiles q >= key
-// tile.  Rows of every TMEM accumulator are KEYS:
-//   S^T  = K Q_i^T          TMEM [0,128)     (P^T = exp2(S^T*c - lse2_q))
-//   dP^T = V dO_i^T         TMEM [128,256)   (dS^T = P^T (dP^T - D_q) / sqrt(d))
-//   dV  += P^T dO_i         TMEM [256,384)   (P^T from smem, dO_i as MN-major B)
-//   dK  += dS^T Q_i         TMEM [384,512)   (dS^T from smem, Q_i as MN-major B)
-// The same K-major SW128 smem tile of Q_i / dO_i serves as the K-major B of
-// the first products and the MN-major B of the accumulations (64-wide d
-// chunks at LBO = 16 KB, 8-row query groups at SBO = 1 KB).
+// One CTA per (128-key tile, head, sequence), iterating 64-query sub-tiles
+// q >= key tile.  Rows of every TMEM accumulator are KEYS:
+//   S^T  = K Q_i^T          TMEM S[b]  (64 cols)  P^T  = exp2(S^T*c - lse2_q)
+//   dP^T = V dO_i^T         TMEM dP[b] (64 cols)  dS^T = P^T (dP^T - D_q) / sqrt(d)
+//   dV  += P^T dO_i         TMEM [256,384)        (P^T from smem, dO_i as MN-major B)
+//   dK  += dS^T Q_i         TMEM [384,512)        (dS^T from smem, Q_i as MN-major B)
+// Q_i / dO_i (+ their lse / D slices, bulk-copied on the same barrier),
+// S^T / dP^T and P^T / dS^T are all double-buffered, so the MMAs of sub-tile
+// i+1 run while the softmax warps process sub-tile i.  The same K-major SW128
+// smem tile of Q_i / dO_i serves as the K-major B of the first products and
+// the MN-major B of the accumulations (64-wide d chunks at LBO = 8 KB, 8-row
+// query groups at SBO = 1 KB).
+constexpr int kBQ2 = 64;  // query rows per backward sub-tile
 struct AttnBwdParams {
   CUtensorMap tmQ, tmK, tmV, tmdO;
   const float* lse;  // [z, S] natural log
@@ -277,46 +283,48 @@ struct AttnBwdParams {
   float scale_log2, scale;
 };
 
-constexpr int kBOffK = 0;
-constexpr int kBOffV = kTileBytes;
-constexpr int kBOffQ = 2 * kTileBytes;
-constexpr int kBOffdO = 3 * kTileBytes;
-constexpr int kBOffPT = 4 * kTileBytes;
-constexpr int kBOffDS = 5 * kTileBytes;
-constexpr int kBOffVec = 6 * kTileBytes;            // lse2[128], D[128]
-constexpr int kBOffBar = 6 * kTileBytes + 1024;
-constexpr size_t kBSmem = 6 * kTileBytes + 2048 + 1024;
+constexpr int kQTile = kBQ2 * kHd * 2;                 // 16 KB
+constexpr int kBOffK = 0;                              // 32 KB
+constexpr int kBOffV = kTileBytes;                     // 32 KB
+constexpr int kBOffQ = 2 * kTileBytes;                 // 2 x 16 KB
+constexpr int kBOffdO = kBOffQ + 2 * kQTile;           // 2 x 16 KB
+constexpr int kBOffPT = kBOffdO + 2 * kQTile;          // 2 x 16 KB (128 keys x 64 q)
+constexpr int kBOffDS = kBOffPT + 2 * kQTile;          // 2 x 16 KB
+constexpr int kBOffVec = kBOffDS + 2 * kQTile;         // 2 x (lse[64] + D[64])
+constexpr int kBOffBar = kBOffVec + 1024;
+constexpr size_t kBSmem = size_t(kBOffBar) + 1024 + 1024;
 
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kBOffBar);
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;
-  uint64_t* qd_empty = bar + 2;
-  uint64_t* s_full = bar + 3;
-  uint64_t* s_free = bar + 4;
-  uint64_t* p_full = bar + 5;
-  uint64_t* p_empty = bar + 6;
-  uint64_t* acc_done = bar + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
-  float* vec_lse = reinterpret_cast<float*>(smem + kBOffVec);
-  float* vec_D = vec_lse + 128;
+  uint64_t* qd_full = bar + 1;   // [2]
+  uint64_t* qd_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* s_free = bar + 7;    // [2]
+  uint64_t* p_full = bar + 9;    // [2]
+  uint64_t* p_empty = bar + 11;  // [2]
+  uint64_t* acc_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int kt = blockIdx.x;  // key tile; small kt = most query tiles (launched first)
   const int head = blockIdx.y, seq = blockIdx.z;
   const int k0 = kt * kBK;
-  const int nit = p.nq - kt;
+  const int nit = (p.S - k0) / kBQ2;
+  const int z = seq * p.nh + head;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    mbar_init(qd_full, 1);
-    mbar_init(qd_empty, 1);
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 4);
-    mbar_init(p_full, 4);
-    mbar_init(p_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qd_full[i], 1);
+      mbar_init(&qd_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+    }
     mbar_init(acc_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -328,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot;  // S^T[b] = b*128, dP^T[b] = b*128 + 64, dV 256, dK 384
 
   if (warp == 0) {
     if (lane == 0) {
@@ -338,105 +346,123 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         tma_load_4d(smem + kBOffV + c * 16384, &p.tmV, kv_full, c * 64, k0, head, seq);
       }
       for (int it = 0; it < nit; ++it) {
-        const int q0 = (kt + it) * kBQ;
-        mbar_wait(qd_empty, (it & 1) ^ 1);
-        mbar_expect_tx(qd_full, 2 * kTileBytes);
+        const int b = it & 1;
+        const uint32_t ph = (it >> 1) & 1;
+        const int q0 = k0 + it * kBQ2;
+        mbar_wait(&qd_empty[b], ph ^ 1);
+        mbar_expect_tx(&qd_full[b], 2 * kQTile + 2 * kBQ2 * 4);
         for (int c = 0; c < 2; ++c) {
-          tma_load_4d(smem + kBOffQ + c * 16384, &p.tmQ, qd_full, c * 64, q0, head, seq);
-          tma_load_4d(smem + kBOffdO + c * 16384, &p.tmdO, qd_full, c * 64, q0, head, seq);
+          tma_load_4d(smem + kBOffQ + b * kQTile + c * 8192, &p.tmQ, &qd_full[b], c * 64, q0, head, seq);
+          tma_load_4d(smem + kBOffdO + b * kQTile + c * 8192, &p.tmdO, &qd_full[b], c * 64, q0, head, seq);
         }
+        float* vec = reinterpret_cast<float*>(smem + kBOffVec + b * 512);
+        bulk_load(vec, p.lse + int64_t(z) * p.S + q0, kBQ2 * 4, &qd_full[b]);
+        bulk_load(vec + kBQ2, p.D + int64_t(z) * p.S + q0, kBQ2 * 4, &qd_full[b]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t kIdKK = make_idesc(128, 128, 0, 0);  // A, B K-major
-      constexpr uint32_t kIdKM = make_idesc(128, 128, 0, 1);  // A K-major, B MN-major
+      constexpr uint32_t kIdS = make_idesc(128, 64, 0, 0);    // K/V K-major, Q/dO K-major (N = 64 q)
+      constexpr uint32_t kIdAcc = make_idesc(128, 128, 0, 1); // P^T/dS^T K-major, dO/Q MN-major
       const uint32_t sk = smem_u32(smem + kBOffK), sv = smem_u32(smem + kBOffV);
-      const uint32_t sq = smem_u32(smem + kBOffQ), sdo = smem_u32(smem + kBOffdO);
-      const uint32_t spt = smem_u32(smem + kBOffPT), sds = smem_u32(smem + kBOffDS);
+      auto accumulate = [&](int i) {
+        const int b = i & 1;
+        const uint32_t ph = (i >> 1) & 1;
+        mbar_wait(&p_full[b], ph);
+        tc_fence_after();
+        const uint32_t spt = smem_u32(smem + kBOffPT + b * kQTile);
+        const uint32_t sds = smem_u32(smem + kBOffDS + b * kQTile);
+        const uint32_t sq = smem_u32(smem + kBOffQ + b * kQTile);
+        const uint32_t sdo = smem_u32(smem + kBOffdO + b * kQTile);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
+          tc_mma(tmem + 256, smem_desc(spt + kk * 32, 16, 1024), smem_desc(sdo + kk * 2048, 8192, 1024),
+                 kIdAcc, (i > 0 || kk > 0) ? 1u : 0u);
+          tc_mma(tmem + 384, smem_desc(sds + kk * 32, 16, 1024), smem_desc(sq + kk * 2048, 8192, 1024),
+                 kIdAcc, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&p_empty[b]);
+        tc_commit(&qd_empty[b]);
+      };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < nit; ++it) {
-        mbar_wait(qd_full, it & 1);
-        mbar_wait(s_free, (it & 1) ^ 1);
+        const int b = it & 1;
+        const uint32_t ph = (it >> 1) & 1;
+        mbar_wait(&qd_full[b], ph);
+        mbar_wait(&s_free[b], ph ^ 1);
         tc_fence_after();
+        const uint32_t sq = smem_u32(smem + kBOffQ + b * kQTile);
+        const uint32_t sdo = smem_u32(smem + kBOffdO + b * kQTile);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-          tc_mma(tmem + 0, smem_desc(sk + o, 16, 1024), smem_desc(sq + o, 16, 1024), kIdKK, kk > 0);
+        for (int kk = 0; kk < 8; ++kk) {  // K = 128 head dims
+          const uint32_t ok = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t oq = (kk >> 2) * 8192 + (kk & 3) * 32;
+          tc_mma(tmem + b * 128, smem_desc(sk + ok, 16, 1024), smem_desc(sq + oq, 16, 1024), kIdS, kk > 0);
+          tc_mma(tmem + b * 128 + 64, smem_desc(sv + ok, 16, 1024), smem_desc(sdo + oq, 16, 1024), kIdS,
+                 kk > 0);
         }
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-          tc_mma(tmem + 128, smem_desc(sv + o, 16, 1024), smem_desc(sdo + o, 16, 1024), kIdKK, kk > 0);
-        }
-        tc_commit(s_full);
-        mbar_wait(p_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries
-          const uint32_t a = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t b = kk * 2048;
-          tc_mma(tmem + 256, smem_desc(spt + a, 16, 1024), smem_desc(sdo + b, 16384, 1024), kIdKM,
-                 (it > 0 || kk > 0) ? 1u : 0u);
-          tc_mma(tmem + 384, smem_desc(sds + a, 16, 1024), smem_desc(sq + b, 16384, 1024), kIdKM,
-                 (it > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc_commit(p_empty);
-        tc_commit(qd_empty);
+        tc_commit(&s_full[b]);
+        if (it >= 1) accumulate(it - 1);
       }
+      accumulate(nit - 1);
       tc_commit(acc_done);
     }
   } else {
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // key k0 + row
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const int z = seq * p.nh + head;
-    const int tid = threadIdx.x - 64;  // 0..127
     for (int it = 0; it < nit; ++it) {
-      const int qi = kt + it;
-      const int q0 = qi * kBQ;
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile done with vec_*
-      vec_lse[tid] = p.lse[int64_t(z) * p.S + q0 + tid] * 1.4426950408889634f;
-      vec_D[tid] = p.D[int64_t(z) * p.S + q0 + tid];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(s_full, it & 1);
+      const int b = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      const int q0 = k0 + it * kBQ2;
+      mbar_wait(&qd_full[b], ph);  // lse / D slices
+      mbar_wait(&s_full[b], ph);
       tc_fence_after();
-      mbar_wait(p_empty, (it & 1) ^ 1);  // PT / dS^T smem free (MMAs of it-1 retired)
-      uint8_t* pt = smem + kBOffPT;
-      uint8_t* ds = smem + kBOffDS;
-      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0);
-      const bool diag = qi == kt;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rs[32], rd[32];
-        tmem_ld32(tmem + lane_off + c * 32, rs);
-        tmem_ld32(tmem + lane_off + 128 + c * 32, rd);
-        float pv[32], dv[32];
+      uint32_t rs[64], rd[64];
+      {
+        uint32_t t[32];
+        tmem_ld32(tmem + lane_off + b * 128, t);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int qc = c * 32 + i;
-          const float e = exp2_fast(__uint_as_float(rs[i]) * p.scale_log2 - vec_lse[qc]);
-          const float pp = (diag && qc < row) ? 0.f : e;  // key > query masked
-          pv[i] = pp;
-          dv[i] = pp * (__uint_as_float(rd[i]) - vec_D[qc]) * p.scale;
-        }
+        for (int i = 0; i < 32; ++i) rs[i] = t[i];
+        tmem_ld32(tmem + lane_off + b * 128 + 32, t);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int c8 = c * 4 + g;  // 8-query group index 0..15
-          const int kc = c8 >> 3, j8 = c8 & 7;
-          const int off = kc * 16384 + row * 128 + ((j8 ^ (row & 7)) * 16);
-          *reinterpret_cast<uint4*>(pt + off) = pack8f(pv + 8 * g);
-          const uint4 w = pack8f(dv + 8 * g);
-          *reinterpret_cast<uint4*>(ds + off) = w;
-          dsg[c8] = w;
-        }
+        for (int i = 0; i < 32; ++i) rs[32 + i] = t[i];
+        tmem_ld32(tmem + lane_off + b * 128 + 64, t);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) rd[i] = t[i];
+        tmem_ld32(tmem + lane_off + b * 128 + 96, t);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) rd[32 + i] = t[i];
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(s_free);
+      if (lane == 0) mbar_arrive(&s_free[b]);
+      const float* vl = reinterpret_cast<const float*>(smem + kBOffVec + b * 512);
+      const float* vd = vl + kBQ2;
+      const int lim = q0 - k0 - row;  // query index qc masked (key > query) iff qc < -lim
+      float pv[64], dv[64];
+#pragma unroll
+      for (int qc = 0; qc < 64; ++qc) {
+        const float e = exp2_fast(__uint_as_float(rs[qc]) * p.scale_log2 - vl[qc] * 1.4426950408889634f);
+        const float pp = (qc + lim < 0) ? 0.f : e;
+        pv[qc] = pp;
+        dv[qc] = pp * (__uint_as_float(rd[qc]) - vd[qc]) * p.scale;
+      }
+      mbar_wait(&p_empty[b], ph ^ 1);  // P^T / dS^T buffer b free (MMAs of it-2 retired)
+      uint8_t* pt = smem + kBOffPT + b * kQTile;
+      uint8_t* ds = smem + kBOffDS + b * kQTile;
+      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0);
+#pragma unroll
+      for (int j8 = 0; j8 < 8; ++j8) {
+        const int off = row * 128 + ((j8 ^ (row & 7)) * 16);
+        *reinterpret_cast<uint4*>(pt + off) = pack8f(pv + 8 * j8);
+        const uint4 w = pack8f(dv + 8 * j8);
+        *reinterpret_cast<uint4*>(ds + off) = w;
+        dsg[j8] = w;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[b]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
@@ -506,10 +532,10 @@ void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse,
   }
   AttnBwdParams p;
   const int64_t h3 = 3 * int64_t(h);
-  p.tmQ = make_tma_map_bf16(qkv, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmQ = make_tma_map_bf16(qkv, kHd, S, h3, kBQ2, nh, b, kHd, int64_t(S) * h3);
   p.tmK = make_tma_map_bf16(qkv + h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
   p.tmV = make_tma_map_bf16(qkv + 2 * h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
-  p.tmdO = make_tma_map_bf16(dO, kHd, S, h, 128, nh, b, kHd, int64_t(S) * h);
+  p.tmdO = make_tma_map_bf16(dO, kHd, S, h, kBQ2, nh, b, kHd, int64_t(S) * h);
   p.lse = lse;
   p.D = D;
   p.dqkv = dqkv;

@@ -80,6 +80,14 @@ __device__ __forceinline__ void unpack8f(uint4 w, float* a) {
   a[4] = __uint_as_float(w.z << 16); a[5] = __uint_as_float(w.z & 0xFFFF0000u);
   a[6] = __uint_as_float(w.w << 16); a[7] = __uint_as_float(w.w & 0xFFFF0000u);
 }
+// 1-D bulk copy global -> shared (TMA engine), completes on `bar` (tx bytes).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
