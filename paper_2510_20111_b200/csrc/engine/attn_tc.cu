@@ -257,6 +257,227 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 }
 
 
+
+// ---------------------------------------------------------------------------
+// Forward, two 128-row query tiles per CTA (qt0 = 2i, qt1 = 2i+1) sharing the
+// K / V stream; 10 warps: TMA, MMA, and two softmax warpgroups (WG g owns Q
+// tile g, TMEM S_g = [g*128, +128), O_g = [256 + g*128, +128)).  The tensor
+// core alternates S0_j, S1_j, PV0_{j-1}, PV1_{j-1} so each warpgroup's
+// softmax overlaps the other's MMAs.  Q0 skips the last key tile (fully
+// masked).  K is double-buffered, V single-buffered.
+constexpr int kThreads2 = 320;
+constexpr int k2OffQ = 0;                  // 2 x 32 KB
+constexpr int k2OffK = 2 * kTileBytes;     // 2 x 32 KB
+constexpr int k2OffV = 4 * kTileBytes;     // 32 KB
+constexpr int k2OffP = 5 * kTileBytes;     // 2 x 32 KB
+constexpr int k2OffBar = 7 * kTileBytes;
+constexpr size_t k2Smem = 7 * kTileBytes + 1024 + 1024;
+
+__global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + k2OffBar);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;
+  uint64_t* v_empty = bar + 6;
+  uint64_t* s_full = bar + 7;   // [g]
+  uint64_t* s_free = bar + 9;   // [g]
+  uint64_t* p_full = bar + 11;  // [g]
+  uint64_t* p_empty = bar + 13; // [g]
+  uint64_t* o_ready = bar + 15; // [g]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int pair = (p.nq / 2) - 1 - blockIdx.x;  // heavy pairs first
+  const int head = blockIdx.y, seq = blockIdx.z;
+  const int qt0 = 2 * pair;
+  const int nkv = qt0 + 2;  // key tiles 0..qt1
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_ready[i], 1);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * kTileBytes);
+      for (int g = 0; g < 2; ++g)
+        for (int c = 0; c < 2; ++c)
+          tma_load_4d(smem + k2OffQ + g * kTileBytes + c * 16384, &p.tmQ, q_full, c * 64,
+                      (qt0 + g) * kBQ, head, seq);
+      for (int j = 0; j < nkv; ++j) {
+        const int kb = j & 1;
+        mbar_wait(&k_empty[kb], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[kb], kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_4d(smem + k2OffK + kb * kTileBytes + c * 16384, &p.tmK, &k_full[kb], c * 64, j * kBK,
+                      head, seq);
+        mbar_wait(v_empty, (j & 1) ^ 1);
+        mbar_expect_tx(v_full, kTileBytes);
+        for (int kc = 0; kc < 2; ++kc)
+          for (int db = 0; db < 2; ++db)
+            tma_load_4d(smem + k2OffV + kc * 16384 + db * 8192, &p.tmV, v_full, db * 64, j * kBK + kc * 64,
+                        head, seq);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = make_idesc(128, 128, 0, 0);
+      constexpr uint32_t kIdPV = make_idesc(128, 128, 0, 1);
+      auto issue_pv = [&](int i) {  // both query tiles' O += P V_i
+        mbar_wait(v_full, i & 1);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + k2OffV);
+        for (int g = 0; g < 2; ++g) {
+          if (g == 0 && i == nkv - 1) continue;  // Q0 fully masked on the last key tile
+          mbar_wait(&p_full[g], i & 1);
+          tc_fence_after();
+          const uint32_t sp = smem_u32(smem + k2OffP + g * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            tc_mma(tmem + 256 + g * 128, smem_desc(sp + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   smem_desc(sv + (kk >> 2) * 16384 + (kk & 3) * 2048, 8192, 1024), kIdPV,
+                   (i > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&p_empty[g]);
+          tc_commit(&o_ready[g]);
+        }
+        tc_commit(v_empty);
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int kb = j & 1;
+        mbar_wait(&k_full[kb], (j >> 1) & 1);
+        const uint32_t sk = smem_u32(smem + k2OffK + kb * kTileBytes);
+        for (int g = 0; g < 2; ++g) {
+          if (g == 0 && j == nkv - 1) continue;
+          mbar_wait(&s_free[g], (j & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t sq = smem_u32(smem + k2OffQ + g * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            tc_mma(tmem + g * 128, smem_desc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   smem_desc(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
+          tc_commit(&s_full[g]);
+        }
+        tc_commit(&k_empty[kb]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      issue_pv(nkv - 1);
+    }
+  } else {
+    const int g = (warp - 2) >> 2;  // softmax warpgroup = query tile
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int qt = qt0 + g;
+    const int q = qt * kBQ + row;
+    const int nj = qt + 1;  // this tile's key tiles
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const uint32_t s_col = g * 128, o_col = 256 + g * 128;
+    const int z = seq * p.nh + head;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nj; ++j) {
+      mbar_wait(&s_full[g], j & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * p.scale_log2;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[g]);
+      if (j == nj - 1) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > row) s[c] = -INFINITY;
+      }
+      float mx = m;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      const bool bump = mx > m + 8.f;
+      const float mref = bump ? mx : m;
+      const float corr = bump ? exp2_fast(m - mx) : 1.f;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        s[c] = exp2_fast(s[c] - mref);
+        sum += s[c];
+      }
+      l = l * corr + sum;
+      m = mref;
+      mbar_wait(&p_empty[g], (j & 1) ^ 1);
+      uint8_t* pb = smem + k2OffP + g * kTileBytes;
+#pragma unroll
+      for (int c8 = 0; c8 < 16; ++c8) {
+        const int kc = c8 >> 3, j8 = c8 & 7;
+        *reinterpret_cast<uint4*>(pb + kc * 16384 + row * 128 + ((j8 ^ (row & 7)) * 16)) = pack8f(s + 8 * c8);
+      }
+      if (j >= 1 && __any_sync(0xffffffffu, bump)) {
+        mbar_wait(&o_ready[g], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_off + o_col + c * 32, r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+          tmem_st32(tmem + lane_off + o_col + c * 32, r);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[g]);
+    }
+    mbar_wait(&o_ready[g], (nj - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    uint4* og = reinterpret_cast<uint4*>(p.O + (int64_t(seq) * p.S + q) * p.h + int64_t(head) * kHd);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_off + o_col + c * 32, r);
+      float o[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) og[c * 4 + i] = pack8f(o + 8 * i);
+    }
+    if (p.lse) p.lse[int64_t(z) * p.S + q] = (m + log2f(l)) * 0.6931471805599453f;
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Fused causal attention backward for dK, dV (and dS^T for the dQ GEMM).
 //
@@ -517,6 +738,17 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
   p.nh = nh;
   p.nq = S / kBQ;
   p.scale_log2 = 1.4426950408889634f / std::sqrt(float(kHd));
+  if (P == nullptr && (S / kBQ) % 2 == 0) {  // two query tiles per CTA
+    static bool attr2 = false;
+    if (!attr2) {
+      HZP_CUDA(cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(k2Smem)));
+      attr2 = true;
+    }
+    dim3 grid(S / kBQ / 2, nh, b);
+    attn_fwd2_kernel<<<grid, kThreads2, k2Smem, stream>>>(p);
+    HZP_LAUNCH_CHECK();
+    return;
+  }
   dim3 grid(S / kBQ, nh, b);
   attn_fwd_kernel<<<grid, kThreads, kSmem, stream>>>(p);
   HZP_LAUNCH_CHECK();

@@ -250,7 +250,7 @@ void Engine::z1_adam(cudaStream_t s) {
   a.bc1 = one - static_cast<float>(std::pow(static_cast<double>(a.b1), step));
   a.bc2 = one - static_cast<float>(std::pow(static_cast<double>(a.b2), step));
   launch_z1_adam(dtable, dtiles + z1_off, z1_n, geom.z2, geom.replicas(), &a, 1, bf16,
-                 l0.dbg != nullptr, std::max(comm_ctas, 2 * kNumSMs), s);
+                 l0.dbg != nullptr, 8 * kNumSMs, s);  // HBM-bound, never beside a GEMM
   ++launches;
 }
 

@@ -19,6 +19,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "engine/gemm.cuh"
@@ -33,6 +35,7 @@ constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, each owning half the
 constexpr int kThreadsTC = 64 + 32 * kEpiWarps;
 
 int g_sm_budget = kNumSMs;
+bool g_cluster = std::getenv("HZP_GEMM_NO_CLUSTER") == nullptr;
 
 using namespace tc;
 
@@ -40,8 +43,10 @@ struct TcParams {
   CUtensorMap tmC;    // output (STORE != 0)
   CUtensorMap tmAux;  // GELU pre-activation output (STORE == 1, act == Gelu)
   CUtensorMap tmSide; // side input (SIDE): aux for the *-grad epilogues, else resid
+  CUtensorMap tmBh;   // CL == 2, K-major B: half-height boxes (each CTA loads one half)
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
+  int pairs_m;        // CL == 2: ceil(tiles_m / 2); tile index space = pairs
   int nh, causal;
   int64_t c_sh, c_sb;
   Epilogue e;
@@ -57,6 +62,11 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int t, int bn
   const int r = t - z * p.tiles_mn;
   return {(r % p.tiles_m) * BM, (r / p.tiles_m) * bn, z % p.nh, z / p.nh};
 }
+// Cluster of 2 along M: unit t is a pair of M tiles sharing one B tile;
+// CTA `rank` owns M tile 2*(t % pairs_m) + rank (possibly past M: zero fill).
+__device__ __forceinline__ TileCoord pair_coord(const TcParams& p, int t, int bn, int rank) {
+  return {(2 * (t % p.pairs_m) + rank) * BM, (t / p.pairs_m) * bn, 0, 0};
+}
 // K-block range of a tile under the causal mode (see GemmShape::causal).
 __device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int& kb0, int& kb1) {
   const int nkb = (p.K + BK - 1) / BK;
@@ -67,7 +77,7 @@ __device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int&
   else if (p.causal == 3) kb0 = min(nkb, m0 / BK);
 }
 
-template <int BN, int A_MN, int B_MN, int STAGES, int STORE, int SIDE>
+template <int BN, int A_MN, int B_MN, int STAGES, int STORE, int SIDE, int CL>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ TcParams p) {
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // released by the MMA commit of every CTA sharing the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -112,13 +122,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  // CL == 2: both CTAs of a cluster walk the same pair sequence
+  const int rank = CL == 2 ? int(cluster_rank()) : 0;
+  const int unit0 = CL == 2 ? int(blockIdx.x) / 2 : int(blockIdx.x);
+  const int ustep = CL == 2 ? int(gridDim.x) / 2 : int(gridDim.x);
+  const int nunits = CL == 2 ? p.pairs_m * p.tiles_n : p.num_tiles;
+  if (CL == 2) cluster_sync_all();  // peers' barriers initialised before any multicast
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const TileCoord tc = tile_coord(p, t, BN);
+      for (int t = unit0; t < nunits; t += ustep) {
+        const TileCoord tc = CL == 2 ? pair_coord(p, t, BN, rank) : tile_coord(p, t, BN);
         int kb0, kb1;
         kb_range(p, tc.m0, tc.n0, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -134,7 +150,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           } else {
             tma_load_4d(sa, &tmA, &full[stage], k0, tc.m0, tc.zh, tc.zb);
           }
-          if (B_MN) {
+          if (CL == 2) {  // this CTA's half of the shared B tile, multicast to both
+            if (B_MN) {
+#pragma unroll
+              for (int j = rank; j < BN / 64; j += 2)
+                tma_load_4d_mc(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, 0, 0, 0x3);
+            } else {
+              tma_load_4d_mc(sb + rank * (BN / 2) * 128, &p.tmBh, &full[stage], k0,
+                             tc.n0 + rank * (BN / 2), 0, 0, 0x3);
+            }
+          } else if (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_4d(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, tc.zh, tc.zb);
@@ -151,8 +176,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const TileCoord tc = tile_coord(p, t, BN);
+      for (int t = unit0; t < nunits; t += ustep) {
+        const TileCoord tc = CL == 2 ? pair_coord(p, t, BN, rank) : tile_coord(p, t, BN);
         int kb0, kb1;
         kb_range(p, tc.m0, tc.n0, kb0, kb1);
         if (kb1 <= kb0) continue;  // skipped tile: the epilogue skips it too
@@ -174,7 +199,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                      : smem_desc(sb + k * 32, 16, 1024);
             tc_mma(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);  // frees this smem stage when the MMAs retire
+          if (CL == 2) tc_commit_mc(&empty[stage], 0x3);  // both CTAs' copies of the stage
+          else tc_commit(&empty[stage]);  // frees this smem stage when the MMAs retire
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
@@ -201,8 +227,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int side_buf = 0;
     int acc = 0, nchunk = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const TileCoord tc = tile_coord(p, t, BN);
+    for (int t = unit0; t < nunits; t += ustep) {
+      const TileCoord tc = CL == 2 ? pair_coord(p, t, BN, rank) : tile_coord(p, t, BN);
       int kb0, kb1;
       kb_range(p, tc.m0, tc.n0, kb0, kb1);
       if (kb1 <= kb0) continue;
@@ -397,6 +423,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (STORE != 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
+  if (CL == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -486,7 +513,7 @@ bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
          (sb * es) % 16 == 0;
 }
 
-template <int BN, int A_MN, int B_MN, int STORE, int SIDE>
+template <int BN, int A_MN, int B_MN, int STORE, int SIDE, int CL>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
   // a side-input epilogue trades one mainloop stage for its smem buffers
@@ -494,7 +521,7 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 +
                           kEpiWarps * 4096 * (SIDE ? 2 : 1);
   static_assert(SMEM <= 232448, "smem budget");
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE, SIDE>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE, SIDE, CL>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     HZP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
@@ -527,20 +554,41 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   p.c_sb = s.c_sb;
   p.e = e;
   p.C = C;
+  if (CL == 2) {
+    if (!B_MN) p.tmBh = make_map(B, s.K, s.N, s.ldb, BN / 2, 1, 1, 0, 0);
+    p.pairs_m = (p.tiles_m + 1) / 2;
+    const int units = p.pairs_m * p.tiles_n;
+    const int clusters = std::min(units, g_sm_budget / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kThreadsTC);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HZP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+    ++launch_counter();
+    return;
+  }
   const int grid = p.num_tiles < g_sm_budget ? p.num_tiles : g_sm_budget;
   kern<<<grid, kThreadsTC, SMEM, stream>>>(ta, tb, p);
   HZP_LAUNCH_CHECK();
 }
 
-template <int BN, int STORE, int SIDE>
+template <int BN, int STORE, int SIDE, int CL>
 void dispatch_major(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                     cudaStream_t st) {
   if (s.a_mn) {
-    if (s.b_mn) launch_tc<BN, 1, 1, STORE, SIDE>(A, B, C, s, e, st);
-    else launch_tc<BN, 1, 0, STORE, SIDE>(A, B, C, s, e, st);
+    if (s.b_mn) launch_tc<BN, 1, 1, STORE, SIDE, CL>(A, B, C, s, e, st);
+    else throw std::invalid_argument("A MN-major with B K-major is not instantiated");
   } else {
-    if (s.b_mn) launch_tc<BN, 0, 1, STORE, SIDE>(A, B, C, s, e, st);
-    else launch_tc<BN, 0, 0, STORE, SIDE>(A, B, C, s, e, st);
+    if (s.b_mn) launch_tc<BN, 0, 1, STORE, SIDE, CL>(A, B, C, s, e, st);
+    else launch_tc<BN, 0, 0, STORE, SIDE, CL>(A, B, C, s, e, st);
   }
 }
 
@@ -560,10 +608,19 @@ void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, c
   const bool side = tma && e.out_bf16 && !(aux_in && e.resid) &&
                     ((aux_in && e.aux_bf16 && aligned16(e.aux, e.ldaux, zsh, zsb, 2)) ||
                      (!aux_in && e.resid && aligned16(e.resid, e.ldres, zsh, zsb, 2)));
-  if (!tma) dispatch_major<BN, 0, 0>(A, B, C, s, e, st);
-  else if (!e.out_bf16) dispatch_major<BN, 2, 0>(A, B, C, s, e, st);
-  else if (side) dispatch_major<BN, 1, 1>(A, B, C, s, e, st);
-  else dispatch_major<BN, 1, 0>(A, B, C, s, e, st);
+  // 2-CTA clusters (B tile multicast) for the plain linear-layer products
+  const bool pair = g_cluster && s.nh * s.nb == 1 && !s.causal && (s.M + BM - 1) / BM >= 2;
+  if (!tma) dispatch_major<BN, 0, 0, 1>(A, B, C, s, e, st);
+  else if (!e.out_bf16) {
+    if (pair) dispatch_major<BN, 2, 0, 2>(A, B, C, s, e, st);
+    else dispatch_major<BN, 2, 0, 1>(A, B, C, s, e, st);
+  } else if (side) {
+    if (pair) dispatch_major<BN, 1, 1, 2>(A, B, C, s, e, st);
+    else dispatch_major<BN, 1, 1, 1>(A, B, C, s, e, st);
+  } else {
+    if (pair) dispatch_major<BN, 1, 0, 2>(A, B, C, s, e, st);
+    else dispatch_major<BN, 1, 0, 1>(A, B, C, s, e, st);
+  }
 }
 
 }  // namespace

@@ -384,19 +384,26 @@ __global__ void __launch_bounds__(256) layernorm_fwd_warp_kernel(
   }
 }
 
-// dg / dbeta partial column sums accumulate in shared memory (red.shared.add)
-// and are flushed once per CTA into part[2][gridDim.x][h].
-constexpr int kWVB = 8;  // bwd keeps x-hat and dy*g live: h <= 2048
+// dg / dbeta partial column sums: each warp accumulates its rows into a
+// private smem slab (plain read-modify-write, no atomics), reduced across the
+// 8 warps once per CTA into part[2][gridDim.x][h].
+constexpr int kWVB = 8;  // h <= 2048
 
 __global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
     const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
     const float* __restrict__ mu, const float* __restrict__ rs, const uint16_t* __restrict__ resid,
     uint16_t* __restrict__ dx, float* __restrict__ part, int rows, int h) {
-  extern __shared__ float acc[];  // [2][h]
-  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) acc[i] = 0.f;
-  __syncthreads();
+  extern __shared__ float acc[];  // [8 warps][2][h]
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
   const int nv = h / 8;
+  float* ag = acc + size_t(w) * 2 * h;
+  float* ab = ag + h;
+  for (int i = lane; i < 2 * h; i += 32) ag[i] = 0.f;
+  __syncwarp();
+  float gg[kWVB][8];
+#pragma unroll
+  for (int k = 0; k < kWVB; ++k)
+    if (lane + 32 * k < nv) unpack8(reinterpret_cast<const uint4*>(g)[lane + 32 * k], gg[k]);
   for (int r = blockIdx.x * 8 + w; r < rows; r += gridDim.x * 8) {
     const float m = mu[r], rstd = rs[r];
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
@@ -407,18 +414,23 @@ __global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
     for (int k = 0; k < kWVB; ++k) {
       const int i = lane + 32 * k;
       if (i < nv) {
-        float d[8], gg[8];
+        float d[8];
         unpack8(dyr[i], d);
         unpack8(xr[i], xh[k]);
-        unpack8(reinterpret_cast<const uint4*>(g)[i], gg);
+        float4* pg = reinterpret_cast<float4*>(ag + 8 * i);
+        float4* pb = reinterpret_cast<float4*>(ab + 8 * i);
+        float4 g0 = pg[0], g1 = pg[1], b0 = pb[0], b1 = pb[1];
         for (int j = 0; j < 8; ++j) {
           xh[k][j] = (xh[k][j] - m) * rstd;
-          dg[k][j] = d[j] * gg[j];
+          dg[k][j] = d[j] * gg[k][j];
           s1 += dg[k][j];
           s2 += dg[k][j] * xh[k][j];
-          atomicAdd(&acc[8 * i + j], d[j] * xh[k][j]);
-          atomicAdd(&acc[h + 8 * i + j], d[j]);
         }
+        g0.x += d[0] * xh[k][0]; g0.y += d[1] * xh[k][1]; g0.z += d[2] * xh[k][2]; g0.w += d[3] * xh[k][3];
+        g1.x += d[4] * xh[k][4]; g1.y += d[5] * xh[k][5]; g1.z += d[6] * xh[k][6]; g1.w += d[7] * xh[k][7];
+        b0.x += d[0]; b0.y += d[1]; b0.z += d[2]; b0.w += d[3];
+        b1.x += d[4]; b1.y += d[5]; b1.z += d[6]; b1.w += d[7];
+        pg[0] = g0; pg[1] = g1; pb[0] = b0; pb[1] = b1;
       }
     }
     const float a1 = warp_sum(s1) / h, a2 = warp_sum(s2) / h;
@@ -439,9 +451,11 @@ __global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < h; i += blockDim.x) {
-    part[int64_t(blockIdx.x) * h + i] = acc[i];
-    part[int64_t(gridDim.x + blockIdx.x) * h + i] = acc[h + i];
+  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) {
+    float t = 0.f;
+    for (int ww = 0; ww < 8; ++ww) t += acc[size_t(ww) * 2 * h + i];
+    if (i < h) part[int64_t(blockIdx.x) * h + i] = t;
+    else part[int64_t(gridDim.x + blockIdx.x) * h + (i - h)] = t;
   }
 }
 
@@ -538,10 +552,10 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
                    const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
                    int rows, int h, cudaStream_t s) {
   if (h <= 32 * 8 * kWVB) {
-    const size_t smem = size_t(2) * h * sizeof(float);
+    const size_t smem = size_t(16) * h * sizeof(float);  // 8 warps x (dg, dbeta)
     static bool attr = false;
     if (!attr) {
-      HZP_CUDA(cudaFuncSetAttribute(layernorm_bwd_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+      HZP_CUDA(cudaFuncSetAttribute(layernorm_bwd_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
       attr = true;
     }
     layernorm_bwd_warp_kernel<<<chunks, 256, smem, s>>>(dy, x, g, mu, rstd, resid, dx, part, rows, h);

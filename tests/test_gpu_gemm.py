@@ -33,6 +33,8 @@ def _mk(M, N, K, a_mn, b_mn, dev):
 def test_tcgen05_gemm_matches_torch(gpu, shape, a_mn, b_mn):
     from paper_2510_20111_b200.engine import gemm_bf16
     M, N, K = shape
+    if a_mn and not b_mn:
+        pytest.skip("A MN-major x B K-major is not used by any layer product (not instantiated)")
     if (a_mn and M % 8) or (b_mn and N % 8):
         pytest.skip("MN-major leading dim must be a multiple of 8 for TMA")
     A, B, As, Bs, lda, ldb = _mk(M, N, K, a_mn, b_mn, gpu)
