@@ -63,8 +63,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int qt = p.nq - 1 - blockIdx.x;  // heavy (late) query tiles first
-  const int head = blockIdx.y, seq = blockIdx.z;
+  // grid (heads, seqs, tiles): the tile index varies slowest, so every head's
+  // heavy (late) query tiles are dispatched before any light one (LPT order)
+  const int qt = p.nq - 1 - blockIdx.z;
+  const int head = blockIdx.x, seq = blockIdx.y;
   const int q0 = qt * kBQ;
   const int nkv = qt + 1;  // causal: key tiles 0..qt
 
@@ -290,8 +292,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int pair = (p.nq / 2) - 1 - blockIdx.x;  // heavy pairs first
-  const int head = blockIdx.y, seq = blockIdx.z;
+  const int pair = (p.nq / 2) - 1 - blockIdx.z;  // heavy pairs first (LPT order)
+  const int head = blockIdx.x, seq = blockIdx.y;
   const int qt0 = 2 * pair;
   const int nkv = qt0 + 2;  // key tiles 0..qt1
 
@@ -530,8 +532,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x;  // key tile; small kt = most query tiles (launched first)
-  const int head = blockIdx.y, seq = blockIdx.z;
+  const int kt = blockIdx.z;  // key tile; small kt = most query tiles (launched first)
+  const int head = blockIdx.x, seq = blockIdx.y;
   const int k0 = kt * kBK;
   const int nit = (p.S - k0) / kBQ2;
   const int z = seq * p.nh + head;
@@ -744,12 +746,12 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
       HZP_CUDA(cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(k2Smem)));
       attr2 = true;
     }
-    dim3 grid(S / kBQ / 2, nh, b);
+    dim3 grid(nh, b, S / kBQ / 2);
     attn_fwd2_kernel<<<grid, kThreads2, k2Smem, stream>>>(p);
     HZP_LAUNCH_CHECK();
     return;
   }
-  dim3 grid(S / kBQ, nh, b);
+  dim3 grid(nh, b, S / kBQ);
   attn_fwd_kernel<<<grid, kThreads, kSmem, stream>>>(p);
   HZP_LAUNCH_CHECK();
 }
@@ -778,7 +780,7 @@ void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse,
   p.nq = S / kBQ;
   p.scale = 1.f / std::sqrt(float(kHd));
   p.scale_log2 = 1.4426950408889634f * p.scale;
-  dim3 grid(S / kBK, nh, b);
+  dim3 grid(nh, b, S / kBK);
   attn_bwd_kernel<<<grid, kThreads, kBSmem, stream>>>(p);
   HZP_LAUNCH_CHECK();
 }

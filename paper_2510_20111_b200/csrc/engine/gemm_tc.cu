@@ -47,7 +47,7 @@ struct TcParams {
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
   int pairs_m;        // CL == 2: ceil(tiles_m / 2); tile index space = pairs
-  int nh, causal;
+  int nh, nz, causal;
   int64_t c_sh, c_sb;
   Epilogue e;
   void* C;
@@ -62,10 +62,13 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int t, int bn
   const int r = t - z * p.tiles_mn;
   return {(r % p.tiles_m) * BM, (r / p.tiles_m) * bn, z % p.nh, z / p.nh};
 }
-// Cluster of 2 along M: unit t is a pair of M tiles sharing one B tile;
-// CTA `rank` owns M tile 2*(t % pairs_m) + rank (possibly past M: zero fill).
+// CTA pair along M: unit t is a 256 x bn tile; CTA `rank` owns M rows
+// [m0 + 128 rank, +128) (possibly past M: zero fill) and B half `rank`.
 __device__ __forceinline__ TileCoord pair_coord(const TcParams& p, int t, int bn, int rank) {
-  return {(2 * (t % p.pairs_m) + rank) * BM, (t / p.pairs_m) * bn, 0, 0};
+  const int per_z = p.pairs_m * p.tiles_n;
+  const int z = t / per_z;
+  const int r = t - z * per_z;
+  return {(2 * (r % p.pairs_m) + rank) * BM, (r / p.pairs_m) * bn, z % p.nh, z / p.nh};
 }
 // K-block range of a tile under the causal mode (see GemmShape::causal).
 __device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int& kb0, int& kb1) {
@@ -82,10 +85,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ TcParams p) {
   constexpr uint32_t A_BYTES = BM * BK * 2;
-  constexpr uint32_t B_BYTES = BN * BK * 2;
+  // CL == 2 (CTA pair, cta_group::2): each CTA holds its own 128 A rows and
+  // one half of the BN-wide B tile; the leader's MMA (M = 256) reads both.
+  constexpr uint32_t B_BYTES = (CL == 2 ? BN / 2 : BN) * BK * 2;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  constexpr uint32_t IDESC = make_idesc(BM, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC = make_idesc(BM * CL, BN, A_MN, B_MN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -99,11 +104,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // released by the MMA commit of every CTA sharing the stage
+      mbar_init(&empty[s], 1);  // released by the (leader's) MMA commit
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], kEpiWarps * CL);  // CL == 2: both CTAs' epilogues, on the leader
     }
     if (SIDE)
       for (int i = 0; i < 2 * kEpiWarps; ++i)
@@ -112,11 +117,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
+  if (CL == 2) cluster_sync_all();  // peers' barriers initialised before any cross-CTA signal
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_base_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CL == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_base_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_base_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -126,8 +139,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int rank = CL == 2 ? int(cluster_rank()) : 0;
   const int unit0 = CL == 2 ? int(blockIdx.x) / 2 : int(blockIdx.x);
   const int ustep = CL == 2 ? int(gridDim.x) / 2 : int(gridDim.x);
-  const int nunits = CL == 2 ? p.pairs_m * p.tiles_n : p.num_tiles;
-  if (CL == 2) cluster_sync_all();  // peers' barriers initialised before any multicast
+  const int nunits = CL == 2 ? p.pairs_m * p.tiles_n * p.nz : p.num_tiles;
+  if (CL == 2) cluster_sync_all();  // both TMEM allocations done
 
   if (warp == 0) {
     if (lane == 0) {
@@ -141,8 +154,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
           const int k0 = kb * BK;
+          if (CL == 2) {  // both CTAs' loads complete on the leader's full barrier
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            if (A_MN) {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_4d_pair(sa + j * (BK * 128), &tmA, fb, tc.m0 + 64 * j, k0, tc.zh, tc.zb);
+            } else {
+              tma_load_4d_pair(sa, &tmA, fb, k0, tc.m0, tc.zh, tc.zb);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 128; ++j)
+                tma_load_4d_pair(sb + j * (BK * 128), &tmB, fb, tc.n0 + rank * (BN / 2) + 64 * j, k0, tc.zh,
+                                 tc.zb);
+            } else {
+              tma_load_4d_pair(sb, &p.tmBh, fb, k0, tc.n0 + rank * (BN / 2), tc.zh, tc.zb);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
           if (A_MN) {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
@@ -150,16 +184,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           } else {
             tma_load_4d(sa, &tmA, &full[stage], k0, tc.m0, tc.zh, tc.zb);
           }
-          if (CL == 2) {  // this CTA's half of the shared B tile, multicast to both
-            if (B_MN) {
-#pragma unroll
-              for (int j = rank; j < BN / 64; j += 2)
-                tma_load_4d_mc(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, 0, 0, 0x3);
-            } else {
-              tma_load_4d_mc(sb + rank * (BN / 2) * 128, &p.tmBh, &full[stage], k0,
-                             tc.n0 + rank * (BN / 2), 0, 0, 0x3);
-            }
-          } else if (B_MN) {
+          if (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_4d(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, tc.zh, tc.zb);
@@ -171,7 +196,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {  // CL == 2: the leader issues the pair's MMAs
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -197,13 +222,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                      : smem_desc(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc(sb + k * 2048, BK * 128, 1024)
                                      : smem_desc(sb + k * 32, 16, 1024);
-            tc_mma(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
+            if (CL == 2) tc_mma_pair(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
+            else tc_mma(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
           }
-          if (CL == 2) tc_commit_mc(&empty[stage], 0x3);  // both CTAs' copies of the stage
-          else tc_commit(&empty[stage]);  // frees this smem stage when the MMAs retire
+          // frees this smem stage (in both CTAs of a pair) when the MMAs retire
+          if (CL == 2) tc_commit_pair_mc(&empty[stage], 0x3);
+          else tc_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue(s)
+        if (CL == 2) tc_commit_pair_mc(&tfull[acc], 0x3);
+        else tc_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -417,7 +446,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CL == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (STORE != 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -426,8 +458,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (CL == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+    if (CL == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
 }
 
@@ -516,10 +550,12 @@ bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
 template <int BN, int A_MN, int B_MN, int STORE, int SIDE, int CL>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
-  // a side-input epilogue trades one mainloop stage for its smem buffers
-  constexpr int STAGES = (BN == 256 ? 4 : 6) - (SIDE ? 1 : 0);
-  constexpr size_t SMEM = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024 + 1024 +
-                          kEpiWarps * 4096 * (SIDE ? 2 : 1);
+  // as many mainloop stages as fit beside the epilogue staging (a side-input
+  // epilogue doubles that); a CTA pair holds half a B tile per stage
+  constexpr size_t STAGE_B = size_t(BM * BK * 2) + size_t(CL == 2 ? BN / 2 : BN) * BK * 2;
+  constexpr size_t FIXED = 1024 + 1024 + size_t(kEpiWarps) * 4096 * (SIDE ? 2 : 1);
+  constexpr int STAGES = int((232448 - FIXED) / STAGE_B) > 8 ? 8 : int((232448 - FIXED) / STAGE_B);
+  constexpr size_t SMEM = size_t(STAGES) * STAGE_B + FIXED;
   static_assert(SMEM <= 232448, "smem budget");
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, STAGES, STORE, SIDE, CL>;
   static bool attr_set = false;  // per instantiation
@@ -549,15 +585,16 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   p.tiles_mn = p.tiles_m * p.tiles_n;
   p.num_tiles = p.tiles_mn * s.nh * s.nb;
   p.nh = s.nh;
+  p.nz = s.nh * s.nb;
   p.causal = s.causal;
   p.c_sh = s.c_sh;
   p.c_sb = s.c_sb;
   p.e = e;
   p.C = C;
   if (CL == 2) {
-    if (!B_MN) p.tmBh = make_map(B, s.K, s.N, s.ldb, BN / 2, 1, 1, 0, 0);
+    if (!B_MN) p.tmBh = make_map(B, s.K, s.N, s.ldb, BN / 2, s.nh, s.nb, s.b_sh, s.b_sb);
     p.pairs_m = (p.tiles_m + 1) / 2;
-    const int units = p.pairs_m * p.tiles_n;
+    const int units = p.pairs_m * p.tiles_n * p.nz;
     const int clusters = std::min(units, g_sm_budget / 2);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * clusters);
@@ -608,8 +645,10 @@ void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, c
   const bool side = tma && e.out_bf16 && !(aux_in && e.resid) &&
                     ((aux_in && e.aux_bf16 && aligned16(e.aux, e.ldaux, zsh, zsb, 2)) ||
                      (!aux_in && e.resid && aligned16(e.resid, e.ldres, zsh, zsb, 2)));
-  // 2-CTA clusters (B tile multicast) for the plain linear-layer products
-  const bool pair = g_cluster && s.nh * s.nb == 1 && !s.causal && (s.M + BM - 1) / BM >= 2;
+  // CTA pairs (cta_group::2, M = 256 per MMA) for every non-causal product
+  // with at least two M tiles: each CTA stages half the B tile, halving the
+  // per-SM operand traffic and smem per stage (deeper pipeline)
+  const bool pair = g_cluster && !s.causal && (s.M + BM - 1) / BM >= 2;
   if (!tma) dispatch_major<BN, 0, 0, 1>(A, B, C, s, e, st);
   else if (!e.out_bf16) {
     if (pair) dispatch_major<BN, 2, 0, 2>(A, B, C, s, e, st);
