@@ -291,8 +291,10 @@ int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K,
                      const float* rowvec, float alpha, void* stream);
 /* Fused causal attention (head dim 128) on bf16 device buffers: qkv [b,S,3h],
  * O [b,S,h], lse [b*nh,S] fp32; backward from dO [b,S,h] and
- * D = rowsum(dO*O) [b*nh,S] writes dK, dV into dqkv [b,S,3h] and dS^T
- * [b*nh,S,S] (bf16) — dQ is then one causal GEMM (done here too). */
+ * workspace D [2,b*nh,S] fp32 (filled here with -rowsum(dO*O)/sqrt(128) and
+ * -lse*log2(e), the backward's per-query vectors) writes dK, dV into dqkv
+ * [b,S,3h] and dS^T [b*nh,S,S] (bf16) — dQ is then one causal GEMM (done
+ * here too). */
 int hzp_attention_fwd(const void* qkv, void* O, float* lse, int b, int nh, int S, int h, void* stream);
 int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const float* lse, float* D,
                       void* dqkv, void* dsT, int b, int nh, int S, int h, void* stream);

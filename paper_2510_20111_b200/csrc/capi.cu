@@ -683,7 +683,7 @@ int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const floa
     const auto* q = static_cast<const uint16_t*>(qkv);
     auto* dq = static_cast<uint16_t*>(dqkv);
     auto* ds = static_cast<uint16_t*>(dsT);
-    attn_rowdot(static_cast<const uint16_t*>(dO), static_cast<const uint16_t*>(O), D, b, nh, S, 128, st);
+    attn_rowdot(static_cast<const uint16_t*>(dO), static_cast<const uint16_t*>(O), lse, D, b, nh, S, 128, st);
     attention_bwd_tc(q, static_cast<const uint16_t*>(dO), lse, D, dq, ds, b, nh, S, h, st);
     const int64_t h3 = 3 * int64_t(h), SS = int64_t(S) * S;
     GemmShape sh{S, 128, S, S, int(h3), 1, 1};

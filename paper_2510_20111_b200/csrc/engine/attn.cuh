@@ -14,7 +14,8 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
                       int S, int h, cudaStream_t stream);
 
 // Backward for dK, dV (written into the k / v thirds of dqkv [b, S, 3h]) from
-// qkv, dO [b, S, h], lse and D = rowsum(dO * O) [b*nh, S]; also writes
+// qkv, dO [b, S, h] and the per-query vectors V [2][b*nh][S] of attn_rowdot
+// (-D/sqrt(d), -lse log2 e), passed as `D`; also writes
 // dS^T [b*nh, S(key), S(query)] bf16 (zero where key > query inside the
 // diagonal tile) so dQ = dS K runs as a causal batched GEMM.
 void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse, const float* D,

@@ -15,6 +15,7 @@
 //             in TMEM when the running max moves, final O / l and lse out.
 // The S tile never leaves the SM: no fp32 score matrix in HBM.
 #include <cmath>
+#include <type_traits>
 
 #include "engine/gemm.cuh"
 #include "engine/tc_ptx.cuh"
@@ -267,28 +268,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 // core alternates S0_j, S1_j, PV0_{j-1}, PV1_{j-1} so each warpgroup's
 // softmax overlaps the other's MMAs.  Q0 skips the last key tile (fully
 // masked).  K is double-buffered, V single-buffered.
-constexpr int kThreads2 = 320;
-constexpr int k2OffQ = 0;                  // 2 x 32 KB
-constexpr int k2OffK = 2 * kTileBytes;     // 2 x 32 KB
-constexpr int k2OffV = 4 * kTileBytes;     // 32 KB
-constexpr int k2OffP = 5 * kTileBytes;     // 2 x 32 KB
-constexpr int k2OffBar = 7 * kTileBytes;
-constexpr size_t k2Smem = 7 * kTileBytes + 1024 + 1024;
+constexpr int kThreads2 = 320;  // producer, MMA, 2 softmax warpgroups
+constexpr int kKSt = 3;  // K_j stages
+constexpr int kVSt = 2;  // V_j stages
+constexpr int k2OffQ = 0;                               // 2 x 32 KB (both query tiles)
+constexpr int k2OffK = 2 * kTileBytes;                  // 3 x 32 KB
+constexpr int k2OffV = k2OffK + kKSt * kTileBytes;      // 2 x 32 KB
+constexpr int k2OffBar = k2OffV + kVSt * kTileBytes;
+constexpr size_t k2Smem = size_t(k2OffBar) + 256 + 1024;
+static_assert(k2Smem <= 232448, "attention forward smem budget");
 
+// P_j never touches shared memory: each softmax warpgroup writes it as bf16
+// into the first 64 TMEM columns of its own S region, and O += P V_j reads A
+// from TMEM.  That frees the smem for a 3-deep K ring and a 2-deep V ring.
 __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + k2OffBar);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;   // [2]
-  uint64_t* k_empty = bar + 3;  // [2]
-  uint64_t* v_full = bar + 5;
-  uint64_t* v_empty = bar + 6;
-  uint64_t* s_full = bar + 7;   // [g]
-  uint64_t* s_free = bar + 9;   // [g]
-  uint64_t* p_full = bar + 11;  // [g]
-  uint64_t* p_empty = bar + 13; // [g]
-  uint64_t* o_ready = bar + 15; // [g]
+  uint64_t* k_full = bar + 1;    // [kKSt]
+  uint64_t* k_empty = bar + 4;   // [kKSt]
+  uint64_t* v_full = bar + 7;    // [kVSt]
+  uint64_t* v_empty = bar + 9;   // [kVSt]
+  uint64_t* s_full = bar + 11;   // [g]
+  uint64_t* p_full = bar + 13;   // [g]
+  uint64_t* o_ready = bar + 15;  // [g]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -299,17 +303,19 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKSt; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < kVSt; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
       mbar_init(&p_full[i], 4);
-      mbar_init(&p_empty[i], 1);
       mbar_init(&o_ready[i], 1);
     }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot;  // S/P [g*128, +128), O [256 + g*128, +128)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -330,63 +336,67 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
           tma_load_4d(smem + k2OffQ + g * kTileBytes + c * 16384, &p.tmQ, q_full, c * 64,
                       (qt0 + g) * kBQ, head, seq);
       for (int j = 0; j < nkv; ++j) {
-        const int kb = j & 1;
-        mbar_wait(&k_empty[kb], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[kb], kTileBytes);
+        const int ks = j % kKSt, vs = j % kVSt;
+        mbar_wait(&k_empty[ks], ((j / kKSt) & 1) ^ 1);
+        mbar_expect_tx(&k_full[ks], kTileBytes);
         for (int c = 0; c < 2; ++c)
-          tma_load_4d(smem + k2OffK + kb * kTileBytes + c * 16384, &p.tmK, &k_full[kb], c * 64, j * kBK,
+          tma_load_4d(smem + k2OffK + ks * kTileBytes + c * 16384, &p.tmK, &k_full[ks], c * 64, j * kBK,
                       head, seq);
-        mbar_wait(v_empty, (j & 1) ^ 1);
-        mbar_expect_tx(v_full, kTileBytes);
+        mbar_wait(&v_empty[vs], ((j / kVSt) & 1) ^ 1);
+        mbar_expect_tx(&v_full[vs], kTileBytes);
         for (int kc = 0; kc < 2; ++kc)
           for (int db = 0; db < 2; ++db)
-            tma_load_4d(smem + k2OffV + kc * 16384 + db * 8192, &p.tmV, v_full, db * 64, j * kBK + kc * 64,
-                        head, seq);
+            tma_load_4d(smem + k2OffV + vs * kTileBytes + kc * 16384 + db * 8192, &p.tmV, &v_full[vs],
+                        db * 64, j * kBK + kc * 64, head, seq);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t kIdS = make_idesc(128, 128, 0, 0);
       constexpr uint32_t kIdPV = make_idesc(128, 128, 0, 1);
-      auto issue_pv = [&](int i) {  // both query tiles' O += P V_i
-        mbar_wait(v_full, i & 1);
-        tc_fence_after();
-        const uint32_t sv = smem_u32(smem + k2OffV);
-        for (int g = 0; g < 2; ++g) {
-          if (g == 0 && i == nkv - 1) continue;  // Q0 fully masked on the last key tile
-          mbar_wait(&p_full[g], i & 1);
-          tc_fence_after();
-          const uint32_t sp = smem_u32(smem + k2OffP + g * kTileBytes);
+      // Ping-pong order: as soon as tile g's P_j is in TMEM, O_g += P_j V_j and
+      // S_g = Q_g K_{j+1} are issued back to back (the latter overwrites P_j's
+      // columns after the former has read them: same-thread MMAs run in
+      // order), so each softmax warpgroup's next scores are computed while
+      // the other warpgroup runs its softmax.  (Q0 is fully masked on the last
+      // key tile: neither product is issued for it.)
+      auto issue_s = [&](int g, int j) {
+        const uint32_t sq = smem_u32(smem + k2OffQ + g * kTileBytes);
+        const uint32_t sk = smem_u32(smem + k2OffK + (j % kKSt) * kTileBytes);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            tc_mma(tmem + 256 + g * 128, smem_desc(sp + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                   smem_desc(sv + (kk >> 2) * 16384 + (kk & 3) * 2048, 8192, 1024), kIdPV,
-                   (i > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&p_empty[g]);
-          tc_commit(&o_ready[g]);
-        }
-        tc_commit(v_empty);
+        for (int kk = 0; kk < 8; ++kk)
+          tc_mma(tmem + g * 128, smem_desc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                 smem_desc(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
+        tc_commit(&s_full[g]);
       };
       mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      for (int g = 0; g < 2; ++g)
+        if (!(g == 0 && nkv == 1)) issue_s(g, 0);
+      tc_commit(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
-        const int kb = j & 1;
-        mbar_wait(&k_full[kb], (j >> 1) & 1);
-        const uint32_t sk = smem_u32(smem + k2OffK + kb * kTileBytes);
+        const bool knext = j + 1 < nkv;
+        mbar_wait(&v_full[j % kVSt], (j / kVSt) & 1);
+        if (knext) mbar_wait(&k_full[(j + 1) % kKSt], ((j + 1) / kKSt) & 1);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + k2OffV + (j % kVSt) * kTileBytes);
         for (int g = 0; g < 2; ++g) {
-          if (g == 0 && j == nkv - 1) continue;
-          mbar_wait(&s_free[g], (j & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t sq = smem_u32(smem + k2OffQ + g * kTileBytes);
+          if (!(g == 0 && j == nkv - 1)) {
+            mbar_wait(&p_full[g], j & 1);
+            tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            tc_mma(tmem + g * 128, smem_desc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                   smem_desc(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
-          tc_commit(&s_full[g]);
+            for (int kk = 0; kk < 8; ++kk)  // A = P_j (bf16 pairs, 8 columns per K = 16)
+              tc_mma_ts(tmem + 256 + g * 128, tmem + g * 128 + kk * 8,
+                        smem_desc(sv + (kk >> 2) * 16384 + (kk & 3) * 2048, 8192, 1024), kIdPV,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+            tc_commit(&o_ready[g]);
+          }
+          if (knext && !(g == 0 && j + 1 == nkv - 1)) issue_s(g, j + 1);
         }
-        tc_commit(&k_empty[kb]);
-        if (j >= 1) issue_pv(j - 1);
+        tc_commit(&v_empty[j % kVSt]);
+        if (knext) tc_commit(&k_empty[(j + 1) % kKSt]);
       }
-      issue_pv(nkv - 1);
     }
   } else {
     const int g = (warp - 2) >> 2;  // softmax warpgroup = query tile
@@ -398,47 +408,79 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     const uint32_t s_col = g * 128, o_col = 256 + g * 128;
     const int z = seq * p.nh + head;
+    // m: running row max in log2 units (scores x scale log2 e)
     float m = -INFINITY, l = 0.f;
+    const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
     for (int j = 0; j < nj; ++j) {
       mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
-      float s[128];
+      // Two passes over S_j in TMEM (32 columns at a time keeps the register
+      // footprint small): the row max, then P = 2^(s c - mref) packed to bf16
+      // and stored over S_j's first 64 columns — chunk c's P lands on columns
+      // [16c, 16c+16), already consumed.
+      const bool diag = j == nj - 1;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+        if (diag) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * p.scale_log2;
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i > row) r[i] = 0xff800000u;  // -inf
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mx4[k] = fmaxf(mx4[k], fmaxf(__uint_as_float(r[i + 2 * k]), __uint_as_float(r[i + 2 * k + 1])));
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[g]);
-      if (j == nj - 1) {
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > row) s[c] = -INFINITY;
-      }
-      float mx = m;
-#pragma unroll
-      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      const float mx = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2);
       const bool bump = mx > m + 8.f;
       const float mref = bump ? mx : m;
-      const float corr = bump ? exp2_fast(m - mx) : 1.f;
+      const float corr = bump ? exp2_fast(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
+      // FFMA2 per pair; 3 of every 8 pairs' exp2 on the FMA pipe so MUFU
+      // (16/clk/SM) stops bounding the tile
+      const uint64_t nm2 = f2_pack(-mref, -mref);
+      uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32], pw[16];
+        tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i > row) r[i] = 0xff800000u;
+        }
+#pragma unroll
+        for (int ii = 0; ii < 16; ++ii) {
+          const int i = c * 16 + ii;
+          const uint64_t x = f2_fma(f2_pack(__uint_as_float(r[2 * ii]), __uint_as_float(r[2 * ii + 1])), sc2, nm2);
+          uint64_t e;
+          if ((i & 7) >= 5) {
+            e = exp2_poly2(x);
+          } else {
+            float a0, a1;
+            f2_unpack(x, a0, a1);
+            e = f2_pack(exp2_fast(a0), exp2_fast(a1));
+          }
+          acc[i & 3] = f2_add(acc[i & 3], e);
+          float e0, e1;
+          f2_unpack(e, e0, e1);
+          pw[ii] = bf16x2(e0, e1);
+        }
+        tmem_st16_nw(tmem + lane_off + s_col + c * 16, pw);
+      }
       float sum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        s[c] = exp2_fast(s[c] - mref);
-        sum += s[c];
+      for (int k = 0; k < 4; ++k) {
+        float a0, a1;
+        f2_unpack(acc[k], a0, a1);
+        sum += a0 + a1;
       }
       l = l * corr + sum;
       m = mref;
-      mbar_wait(&p_empty[g], (j & 1) ^ 1);
-      uint8_t* pb = smem + k2OffP + g * kTileBytes;
-#pragma unroll
-      for (int c8 = 0; c8 < 16; ++c8) {
-        const int kc = c8 >> 3, j8 = c8 & 7;
-        *reinterpret_cast<uint4*>(pb + kc * 16384 + row * 128 + ((j8 ^ (row & 7)) * 16)) = pack8f(s + 8 * c8);
-      }
+      tmem_wait_st();
       if (j >= 1 && __any_sync(0xffffffffu, bump)) {
         mbar_wait(&o_ready[g], (j - 1) & 1);
         tc_fence_after();
@@ -451,7 +493,6 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
           tmem_st32(tmem + lane_off + o_col + c * 32, r);
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[g]);
@@ -496,10 +537,11 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
 // the MN-major B of the accumulations (64-wide d chunks at LBO = 8 KB, 8-row
 // query groups at SBO = 1 KB).
 constexpr int kBQ2 = 64;  // query rows per backward sub-tile
+constexpr int kThreadsB = 320;  // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 struct AttnBwdParams {
   CUtensorMap tmQ, tmK, tmV, tmdO;
-  const float* lse;  // [z, S] natural log
-  const float* D;    // [z, S] rowsum(dO * O)
+  const float* V;    // [2][z][S]: -rowsum(dO * O) / sqrt(d) | -lse log2(e)
+  int64_t zS;        // z * S (offset of the second vector)
   uint16_t* dqkv;    // [b, S, 3h]: dK, dV written into the k / v thirds
   uint16_t* dsT;     // [z, S(key), S(q)] bf16, for dQ = dS K
   int S, h, nh, nq;
@@ -509,27 +551,32 @@ struct AttnBwdParams {
 constexpr int kQTile = kBQ2 * kHd * 2;                 // 16 KB
 constexpr int kBOffK = 0;                              // 32 KB
 constexpr int kBOffV = kTileBytes;                     // 32 KB
-constexpr int kBOffQ = 2 * kTileBytes;                 // 2 x 16 KB
-constexpr int kBOffdO = kBOffQ + 2 * kQTile;           // 2 x 16 KB
-constexpr int kBOffPT = kBOffdO + 2 * kQTile;          // 2 x 16 KB (128 keys x 64 q)
+// Q_i / dO_i (and their vector slices) are released only when sub-tile i's
+// accumulation MMAs retire, i.e. after its softmax; three stages keep the
+// next two sub-tiles' loads in flight across that.
+constexpr int kQStages = 3;
+constexpr int kBOffQ = 2 * kTileBytes;                 // 3 x 16 KB
+constexpr int kBOffdO = kBOffQ + kQStages * kQTile;    // 3 x 16 KB
+constexpr int kBOffPT = kBOffdO + kQStages * kQTile;   // 2 x 16 KB (128 keys x 64 q)
 constexpr int kBOffDS = kBOffPT + 2 * kQTile;          // 2 x 16 KB
-constexpr int kBOffVec = kBOffDS + 2 * kQTile;         // 2 x (lse[64] + D[64])
-constexpr int kBOffBar = kBOffVec + 1024;
-constexpr size_t kBSmem = size_t(kBOffBar) + 1024 + 1024;
+constexpr int kBOffVec = kBOffDS + 2 * kQTile;         // 3 x (-lse log2 e [64] | -D/sqrt(d) [64])
+constexpr int kBOffBar = kBOffVec + kQStages * 512;
+constexpr size_t kBSmem = size_t(kBOffBar) + 256 + 1024;
+static_assert(kBSmem <= 232448, "attention backward smem budget");
 
-__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnBwdParams p) {
+__global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_constant__ AttnBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kBOffBar);
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;   // [2]
-  uint64_t* qd_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_free = bar + 7;    // [2]
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* p_empty = bar + 11;  // [2]
-  uint64_t* acc_done = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* qd_full = bar + 1;   // [kQStages]
+  uint64_t* qd_empty = bar + 4;  // [kQStages]
+  uint64_t* s_full = bar + 7;    // [2]
+  uint64_t* s_free = bar + 9;    // [2]
+  uint64_t* p_full = bar + 11;   // [2]
+  uint64_t* p_empty = bar + 13;  // [2]
+  uint64_t* acc_done = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int kt = blockIdx.z;  // key tile; small kt = most query tiles (launched first)
@@ -540,12 +587,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kQStages; ++i) {
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&p_empty[i], 1);
     }
     mbar_init(acc_done, 1);
@@ -569,18 +618,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         tma_load_4d(smem + kBOffV + c * 16384, &p.tmV, kv_full, c * 64, k0, head, seq);
       }
       for (int it = 0; it < nit; ++it) {
-        const int b = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
+        const int qs = it % kQStages;
+        const uint32_t qph = (it / kQStages) & 1;
         const int q0 = k0 + it * kBQ2;
-        mbar_wait(&qd_empty[b], ph ^ 1);
-        mbar_expect_tx(&qd_full[b], 2 * kQTile + 2 * kBQ2 * 4);
+        mbar_wait(&qd_empty[qs], qph ^ 1);
+        mbar_expect_tx(&qd_full[qs], 2 * kQTile + 2 * kBQ2 * 4);
         for (int c = 0; c < 2; ++c) {
-          tma_load_4d(smem + kBOffQ + b * kQTile + c * 8192, &p.tmQ, &qd_full[b], c * 64, q0, head, seq);
-          tma_load_4d(smem + kBOffdO + b * kQTile + c * 8192, &p.tmdO, &qd_full[b], c * 64, q0, head, seq);
+          tma_load_4d(smem + kBOffQ + qs * kQTile + c * 8192, &p.tmQ, &qd_full[qs], c * 64, q0, head, seq);
+          tma_load_4d(smem + kBOffdO + qs * kQTile + c * 8192, &p.tmdO, &qd_full[qs], c * 64, q0, head, seq);
         }
-        float* vec = reinterpret_cast<float*>(smem + kBOffVec + b * 512);
-        bulk_load(vec, p.lse + int64_t(z) * p.S + q0, kBQ2 * 4, &qd_full[b]);
-        bulk_load(vec + kBQ2, p.D + int64_t(z) * p.S + q0, kBQ2 * 4, &qd_full[b]);
+        float* vec = reinterpret_cast<float*>(smem + kBOffVec + qs * 512);
+        bulk_load(vec, p.V + p.zS + int64_t(z) * p.S + q0, kBQ2 * 4, &qd_full[qs]);  // -lse log2 e
+        bulk_load(vec + kBQ2, p.V + int64_t(z) * p.S + q0, kBQ2 * 4, &qd_full[qs]);  // -D / sqrt(d)
       }
     }
   } else if (warp == 1) {
@@ -591,12 +640,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       auto accumulate = [&](int i) {
         const int b = i & 1;
         const uint32_t ph = (i >> 1) & 1;
+        const int qs = i % kQStages;
         mbar_wait(&p_full[b], ph);
         tc_fence_after();
         const uint32_t spt = smem_u32(smem + kBOffPT + b * kQTile);
         const uint32_t sds = smem_u32(smem + kBOffDS + b * kQTile);
-        const uint32_t sq = smem_u32(smem + kBOffQ + b * kQTile);
-        const uint32_t sdo = smem_u32(smem + kBOffdO + b * kQTile);
+        const uint32_t sq = smem_u32(smem + kBOffQ + qs * kQTile);
+        const uint32_t sdo = smem_u32(smem + kBOffdO + qs * kQTile);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
           tc_mma(tmem + 256, smem_desc(spt + kk * 32, 16, 1024), smem_desc(sdo + kk * 2048, 8192, 1024),
@@ -605,17 +655,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                  kIdAcc, (i > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(&p_empty[b]);
-        tc_commit(&qd_empty[b]);
+        tc_commit(&qd_empty[qs]);
       };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < nit; ++it) {
         const int b = it & 1;
         const uint32_t ph = (it >> 1) & 1;
-        mbar_wait(&qd_full[b], ph);
+        const int qs = it % kQStages;
+        mbar_wait(&qd_full[qs], (it / kQStages) & 1);
         mbar_wait(&s_free[b], ph ^ 1);
         tc_fence_after();
-        const uint32_t sq = smem_u32(smem + kBOffQ + b * kQTile);
-        const uint32_t sdo = smem_u32(smem + kBOffdO + b * kQTile);
+        const uint32_t sq = smem_u32(smem + kBOffQ + qs * kQTile);
+        const uint32_t sdo = smem_u32(smem + kBOffdO + qs * kQTile);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 head dims
           const uint32_t ok = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -632,56 +683,82 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;     // which 32 of the sub-tile's 64 queries
     const int row = quarter * 32 + lane;  // key k0 + row
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), dsc2 = f2_pack(p.scale, p.scale);
     for (int it = 0; it < nit; ++it) {
       const int b = it & 1;
       const uint32_t ph = (it >> 1) & 1;
       const int q0 = k0 + it * kBQ2;
-      mbar_wait(&qd_full[b], ph);  // lse / D slices
+      const int qs = it % kQStages;
+      mbar_wait(&qd_full[qs], (it / kQStages) & 1);  // -lse log2 e / -D / sqrt(d) slices
       mbar_wait(&s_full[b], ph);
       tc_fence_after();
-      uint32_t rs[64], rd[64];
-      {
-        uint32_t t[32];
-        tmem_ld32(tmem + lane_off + b * 128, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rs[i] = t[i];
-        tmem_ld32(tmem + lane_off + b * 128 + 32, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rs[32 + i] = t[i];
-        tmem_ld32(tmem + lane_off + b * 128 + 64, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rd[i] = t[i];
-        tmem_ld32(tmem + lane_off + b * 128 + 96, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rd[32 + i] = t[i];
-      }
+      uint32_t rs[32], rd[32];
+      tmem_ld32_nw(tmem + lane_off + b * 128 + half * 32, rs);
+      tmem_ld32_nw(tmem + lane_off + b * 128 + 64 + half * 32, rd);
+      tmem_wait_ld32(rs);
+      tmem_pin32(rd);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[b]);
-      const float* vl = reinterpret_cast<const float*>(smem + kBOffVec + b * 512);
-      const float* vd = vl + kBQ2;
-      const int lim = q0 - k0 - row;  // query index qc masked (key > query) iff qc < -lim
-      float pv[64], dv[64];
+      // P^T = 2^(S^T c - lse log2 e), dS^T = P^T (dP^T / sqrt(d) - D / sqrt(d)):
+      // two queries per FFMA2/FMUL2; every 4th pair's exp2 on the FMA pipe
+      const uint32_t vs = smem_u32(smem + kBOffVec + qs * 512) + half * 128;
+      float nl[32], nd[32];
 #pragma unroll
-      for (int qc = 0; qc < 64; ++qc) {
-        const float e = exp2_fast(__uint_as_float(rs[qc]) * p.scale_log2 - vl[qc] * 1.4426950408889634f);
-        const float pp = (qc + lim < 0) ? 0.f : e;
-        pv[qc] = pp;
-        dv[qc] = pp * (__uint_as_float(rd[qc]) - vd[qc]) * p.scale;
+      for (int i = 0; i < 8; ++i) {
+        lds128(vs + 16 * i, nl + 4 * i);
+        lds128(vs + kBQ2 * 4 + 16 * i, nd + 4 * i);
       }
-      mbar_wait(&p_empty[b], ph ^ 1);  // P^T / dS^T buffer b free (MMAs of it-2 retired)
-      uint8_t* pt = smem + kBOffPT + b * kQTile;
-      uint8_t* ds = smem + kBOffDS + b * kQTile;
-      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0);
+      // queries q0 + half*32 + qc with qc < -lim are masked (key > query);
+      // only the diagonal sub-tiles have any, warp-uniformly known
+      const int lim = q0 + half * 32 - k0 - row;
+      const bool masked = __any_sync(0xffffffffu, lim < 0);
+      uint32_t ptw[16], dsw[16];
+      auto body = [&](auto mask_tag) {
 #pragma unroll
-      for (int j8 = 0; j8 < 8; ++j8) {
-        const int off = row * 128 + ((j8 ^ (row & 7)) * 16);
-        *reinterpret_cast<uint4*>(pt + off) = pack8f(pv + 8 * j8);
-        const uint4 w = pack8f(dv + 8 * j8);
-        *reinterpret_cast<uint4*>(ds + off) = w;
-        dsg[j8] = w;
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t x = f2_fma(f2_pack(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), sc2,
+                                    f2_pack(nl[2 * i], nl[2 * i + 1]));
+          uint64_t e;
+          if ((i & 3) == 3) {
+            e = exp2_poly2(x);
+          } else {
+            float a0, a1;
+            f2_unpack(x, a0, a1);
+            e = f2_pack(exp2_fast(a0), exp2_fast(a1));
+          }
+          if (decltype(mask_tag)::value) {
+            float e0, e1;
+            f2_unpack(e, e0, e1);
+            e = f2_pack(2 * i + lim < 0 ? 0.f : e0, 2 * i + 1 + lim < 0 ? 0.f : e1);
+          }
+          const uint64_t dsv =
+              f2_mul(e, f2_fma(f2_pack(__uint_as_float(rd[2 * i]), __uint_as_float(rd[2 * i + 1])), dsc2,
+                               f2_pack(nd[2 * i], nd[2 * i + 1])));
+          float e0, e1, d0, d1;
+          f2_unpack(e, e0, e1);
+          f2_unpack(dsv, d0, d1);
+          ptw[i] = bf16x2(e0, e1);
+          dsw[i] = bf16x2(d0, d1);
+        }
+      };
+      if (masked) body(std::true_type{});
+      else body(std::false_type{});
+      mbar_wait(&p_empty[b], ph ^ 1);  // P^T / dS^T buffer b free (MMAs of it-2 retired)
+      const uint32_t pt = smem_u32(smem + kBOffPT + b * kQTile);
+      const uint32_t ds = smem_u32(smem + kBOffDS + b * kQTile);
+      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0 + half * 32);
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const int j8 = half * 4 + j4;
+        const uint32_t off = row * 128 + ((j8 ^ (row & 7)) * 16);
+        sts128(pt + off, make_uint4(ptw[4 * j4], ptw[4 * j4 + 1], ptw[4 * j4 + 2], ptw[4 * j4 + 3]));
+        const uint4 w = make_uint4(dsw[4 * j4], dsw[4 * j4 + 1], dsw[4 * j4 + 2], dsw[4 * j4 + 3]);
+        sts128(ds + off, w);
+        dsg[j4] = w;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -693,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     uint4* dkg = reinterpret_cast<uint4*>(p.dqkv + rowbase + p.h);
     uint4* dvg = reinterpret_cast<uint4*>(p.dqkv + rowbase + 2 * p.h);
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = half * 2; c < half * 2 + 2; ++c) {  // each half writes 64 of the 128 dims
       uint32_t r[32];
       float o[32];
       tmem_ld32(tmem + lane_off + 256 + c * 32, r);
@@ -770,8 +847,9 @@ void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse,
   p.tmK = make_tma_map_bf16(qkv + h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
   p.tmV = make_tma_map_bf16(qkv + 2 * h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
   p.tmdO = make_tma_map_bf16(dO, kHd, S, h, kBQ2, nh, b, kHd, int64_t(S) * h);
-  p.lse = lse;
-  p.D = D;
+  (void)lse;  // consumed through D (attn_rowdot's -lse log2 e vector)
+  p.V = D;
+  p.zS = int64_t(b) * nh * S;
   p.dqkv = dqkv;
   p.dsT = dsT;
   p.S = S;
@@ -781,7 +859,7 @@ void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse,
   p.scale = 1.f / std::sqrt(float(kHd));
   p.scale_log2 = 1.4426950408889634f * p.scale;
   dim3 grid(nh, b, S / kBK);
-  attn_bwd_kernel<<<grid, kThreads, kBSmem, stream>>>(p);
+  attn_bwd_kernel<<<grid, kThreadsB, kBSmem, stream>>>(p);
   HZP_LAUNCH_CHECK();
 }
 

@@ -64,19 +64,32 @@ __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int t, int bn
 }
 // CTA pair along M: unit t is a 256 x bn tile; CTA `rank` owns M rows
 // [m0 + 128 rank, +128) (possibly past M: zero fill) and B half `rank`.
+// Causal (mode 2) products walk the M pairs heaviest-first (LPT order).
 __device__ __forceinline__ TileCoord pair_coord(const TcParams& p, int t, int bn, int rank) {
+  if (p.causal) {
+    const int per_m = p.tiles_n * p.nz;
+    const int mp = p.pairs_m - 1 - t / per_m;
+    const int r = t - (t / per_m) * per_m;
+    const int z = r / p.tiles_n;
+    return {(2 * mp + rank) * BM, (r - z * p.tiles_n) * bn, z % p.nh, z / p.nh};
+  }
   const int per_z = p.pairs_m * p.tiles_n;
   const int z = t / per_z;
   const int r = t - z * per_z;
   return {(2 * (r % p.pairs_m) + rank) * BM, (r / p.pairs_m) * bn, z % p.nh, z / p.nh};
 }
-// K-block range of a tile under the causal mode (see GemmShape::causal).
+// K-block range of a tile under the causal mode (see GemmShape::causal).  A
+// CTA pair shares one range: the union over its 256 rows (mode 2 only; the
+// lower CTA then reads A past its diagonal, which the caller keeps zero).
+template <int CL>
 __device__ __forceinline__ void kb_range(const TcParams& p, int m0, int n0, int& kb0, int& kb1) {
   const int nkb = (p.K + BK - 1) / BK;
+  const int span = CL == 2 ? 2 * BM : BM;
+  if (CL == 2) m0 &= ~(2 * BM - 1);  // pair base (pairs start at multiples of 256)
   kb0 = 0;
   kb1 = nkb;
-  if (p.causal == 1 && n0 >= m0 + BM) kb1 = 0;  // fully masked tile: no work
-  else if (p.causal == 2) kb1 = min(nkb, (m0 + BM + BK - 1) / BK);
+  if (p.causal == 1 && n0 >= m0 + span) kb1 = 0;  // fully masked tile: no work
+  else if (p.causal == 2) kb1 = min(nkb, (m0 + span + BK - 1) / BK);
   else if (p.causal == 3) kb0 = min(nkb, m0 / BK);
 }
 
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int t = unit0; t < nunits; t += ustep) {
         const TileCoord tc = CL == 2 ? pair_coord(p, t, BN, rank) : tile_coord(p, t, BN);
         int kb0, kb1;
-        kb_range(p, tc.m0, tc.n0, kb0, kb1);
+        kb_range<CL>(p, tc.m0, tc.n0, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -204,7 +217,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int t = unit0; t < nunits; t += ustep) {
         const TileCoord tc = CL == 2 ? pair_coord(p, t, BN, rank) : tile_coord(p, t, BN);
         int kb0, kb1;
-        kb_range(p, tc.m0, tc.n0, kb0, kb1);
+        kb_range<CL>(p, tc.m0, tc.n0, kb0, kb1);
         if (kb1 <= kb0) continue;  // skipped tile: the epilogue skips it too
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -259,7 +272,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     for (int t = unit0; t < nunits; t += ustep) {
       const TileCoord tc = CL == 2 ? pair_coord(p, t, BN, rank) : tile_coord(p, t, BN);
       int kb0, kb1;
-      kb_range(p, tc.m0, tc.n0, kb0, kb1);
+      kb_range<CL>(p, tc.m0, tc.n0, kb0, kb1);
       if (kb1 <= kb0) continue;
       const int m0 = tc.m0, n0 = tc.n0;
       const int64_t zoff = int64_t(tc.zh) * p.c_sh + int64_t(tc.zb) * p.c_sb;
@@ -647,7 +660,9 @@ void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, c
                      (!aux_in && e.resid && aligned16(e.resid, e.ldres, zsh, zsb, 2)));
   // CTA pairs (cta_group::2, M = 256 per MMA) for every non-causal product
   // with at least two M tiles: each CTA stages half the B tile, halving the
-  // per-SM operand traffic and smem per stage (deeper pipeline)
+  // per-SM operand traffic and smem per stage (deeper pipeline).  (Pairing
+  // the causal dQ product measured slower: 79 vs 67 us — the pair's union K
+  // range outweighs the halved B traffic at N = 128.)
   const bool pair = g_cluster && !s.causal && (s.M + BM - 1) / BM >= 2;
   if (!tma) dispatch_major<BN, 0, 0, 1>(A, B, C, s, e, st);
   else if (!e.out_bf16) {

@@ -3,6 +3,7 @@
 
 #include "engine/gemm.cuh"
 #include "engine/gpt_ops.cuh"
+#include "engine/tc_ptx.cuh"
 
 namespace hzp {
 namespace {
@@ -270,23 +271,31 @@ __global__ void softmax_causal_kernel(const float* __restrict__ S, uint16_t* __r
 }
 
 // one warp per (token, head)
+// Half a warp per (token, head) row: 16 lanes x 8 bf16 (one uint4 each of dO
+// and O) cover head dim 128; hd must be 128.
 __global__ void attn_rowdot_kernel(const uint16_t* __restrict__ dO, const uint16_t* __restrict__ O,
-                                   float* __restrict__ D, int b, int nh, int S, int hd) {
-  const int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (w >= b * S * nh) return;
-  const int hh = w % nh, t = w / nh;
+                                   const float* __restrict__ lse, float* __restrict__ V, int b, int nh,
+                                   int S, int hd, float scale) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 16;  // (token, head) row
+  const int sub = threadIdx.x & 15;
+  if (r >= b * S * nh) return;
+  const int hh = r % nh, t = r / nh;
   const int bi = t / S, s = t % S;
-  const int64_t base = int64_t(t) * nh * hd + int64_t(hh) * hd;
+  const int64_t base = int64_t(t) * nh * hd + int64_t(hh) * hd + sub * 8;
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(dO + base));
+  const uint4 c = __ldg(reinterpret_cast<const uint4*>(O + base));
+  float fa[8], fc[8];
+  tc::unpack8f(a, fa);
+  tc::unpack8f(c, fc);
   float acc = 0.f;
-  for (int d = lane * 2; d < hd; d += 64) {
-    const uint32_t a = *reinterpret_cast<const uint32_t*>(dO + base + d);
-    const uint32_t c = *reinterpret_cast<const uint32_t*>(O + base + d);
-    acc += __uint_as_float(a << 16) * __uint_as_float(c << 16) +
-           __uint_as_float(a & 0xFFFF0000u) * __uint_as_float(c & 0xFFFF0000u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += fa[i] * fc[i];
+  for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (sub == 0) {
+    const int64_t zq = (int64_t(bi) * nh + hh) * S + s;
+    V[zq] = -scale * acc;
+    V[int64_t(b) * nh * S + zq] = -1.4426950408889634f * lse[zq];
   }
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) D[(int64_t(bi) * nh + hh) * S + s] = acc;
 }
 
 // one CTA per token row of the logits
@@ -584,10 +593,12 @@ void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s) 
   else softmax_causal_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
   HZP_LAUNCH_CHECK();
 }
-void attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int b, int nh, int S, int hd,
-                 cudaStream_t s) {
-  const int warps = b * S * nh;
-  attn_rowdot_kernel<<<(warps + 7) / 8, 256, 0, s>>>(dO, O, D, b, nh, S, hd);
+void attn_rowdot(const uint16_t* dO, const uint16_t* O, const float* lse, float* V, int b, int nh, int S,
+                 int hd, cudaStream_t s) {
+  if (hd != 128) throw std::invalid_argument("attn_rowdot needs head dim 128");
+  const int64_t threads = int64_t(b) * S * nh * 16;
+  attn_rowdot_kernel<<<unsigned((threads + 255) / 256), 256, 0, s>>>(dO, O, lse, V, b, nh, S, hd,
+                                                                      1.f / sqrtf(float(hd)));
   HZP_LAUNCH_CHECK();
 }
 void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* loss,

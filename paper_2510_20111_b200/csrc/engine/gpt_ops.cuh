@@ -36,9 +36,11 @@ void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, 
 // Causal softmax of fp32 scores S[z][q][k] (already scaled): P = exp(S - lse)
 // for k <= q, 0 for q < k < 128*ceil((q+1)/128); P bf16, same layout.
 void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s);
-// D[z][q] = sum_d dO[b, q, head, d] * O[b, q, head, d]  (rows of [T, h] head slices)
-void attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int b, int nh, int S, int hd,
-                 cudaStream_t s);
+// Per-query vectors of the attention backward, V [2][z][q]:
+//   V[0] = -scale * sum_d dO[b, q, head, d] * O[b, q, head, d]   (-D / sqrt(d))
+//   V[1] = -log2(e) * lse[z][q]
+void attn_rowdot(const uint16_t* dO, const uint16_t* O, const float* lse, float* V, int b, int nh, int S,
+                 int hd, cudaStream_t s);
 
 // Fused softmax cross-entropy over rows of bf16 logits [T, V]: loss +=
 // sum_t (lse - logit[target]) / T; logits <- (softmax - onehot) / T in place.

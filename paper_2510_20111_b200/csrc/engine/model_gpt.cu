@@ -40,7 +40,7 @@ struct GptBuffers {
   uint16_t* logits = nullptr;  // [T, V]; dlogits in place after the fused CE
   float* S = nullptr;          // [Z, S, S] fp32 scores
   uint16_t* dS = nullptr;      // [Z, S, S]
-  float* D = nullptr;          // [Z, S]
+  float* D = nullptr;          // [2, Z, S]: attn_rowdot's per-query vectors
   uint16_t* dx[2] = {nullptr, nullptr};
   int cur = 0;
   uint16_t *dln = nullptr, *dqkv = nullptr, *dattn = nullptr, *dfc1 = nullptr, *dxm = nullptr;
@@ -149,7 +149,7 @@ class GptModel final : public Model {
     B->logits = bf(T_ * V_);
     B->S = nullptr;  // scores stay in TMEM (fused attention)
     B->dS = bf(SS);
-    B->D = f32(Z * S_);
+    B->D = f32(2 * Z * S_);
     B->dx[0] = bf(T_ * h_);
     B->dx[1] = bf(T_ * h_);
     B->dln = bf(T_ * h_);
@@ -344,7 +344,7 @@ class GptModel final : public Model {
     // attention core: fused tcgen05 backward for dK, dV (P recomputed from
     // lse, dS^T emitted), then dQ = dS K as a causal batched GEMM
     const int64_t SS = int64_t(S_) * S_;
-    attn_rowdot(B->dattn, a.attn, B->D, b_, nh_, S_, hd_, s);
+    attn_rowdot(B->dattn, a.attn, a.lse, B->D, b_, nh_, S_, hd_, s);
     attention_bwd_tc(a.qkv, B->dattn, a.lse, B->D, B->dqkv, B->dS, b_, nh_, S_, h_, s);
     {  // dQ[q, d] = sum_key dS^T[key, q] K[key, d]
       GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 1, 1, SS, SS * nh_, hd_, S_ * h3, hd_,

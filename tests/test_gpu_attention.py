@@ -32,7 +32,7 @@ def test_fused_attention_fwd_bwd(gpu, b, nh, S):
     lse = torch.zeros(b * nh, S, device=gpu)
     p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     N.check(N.lib.hzp_attention_fwd(p(qkv), p(O), p(lse), b, nh, S, h, None))
-    D = torch.zeros(b * nh, S, device=gpu)
+    D = torch.zeros(2, b * nh, S, device=gpu)  # backward workspace (per-query vectors)
     dqkv = torch.zeros(b, S, 3 * h, device=gpu, dtype=torch.bfloat16)
     dsT = torch.zeros(b * nh, S, S, device=gpu, dtype=torch.bfloat16)
     N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv), p(dsT), b, nh, S, h, None))

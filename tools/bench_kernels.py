@@ -92,7 +92,7 @@ def bench_attn():
     do = (torch.randn(b, S, h, device=dev) * 0.1).to(torch.bfloat16)
     O = torch.zeros(b, S, h, device=dev, dtype=torch.bfloat16)
     lse = torch.zeros(b * nh, S, device=dev)
-    D = torch.zeros(b * nh, S, device=dev)
+    D = torch.zeros(2, b * nh, S, device=dev)
     dqkv = torch.zeros(b, S, 3 * h, device=dev, dtype=torch.bfloat16)
     dsT = torch.zeros(b * nh, S, S, device=dev, dtype=torch.bfloat16)
     p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
