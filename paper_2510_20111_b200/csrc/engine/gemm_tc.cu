@@ -259,11 +259,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;  // 0 | 1: which interleaved 32-column chunks
     const Epilogue& e = p.e;
-    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + (warp - 2) * 4096;
+    // two 4 KB staging buffers per warp (chunk parity), so packing chunk i+1
+    // never waits for chunk i's TMA store to drain
+    uint8_t* stage_base = smem + STAGES * STAGE_BYTES + 1024 + (warp - 2) * 8192;
     // SIDE: the side input (P / pre-activation / residual) of each 32x32
     // chunk is TMA-loaded into one of two 2 KB SW64 buffers per warp, the next
     // chunk's load issued before the current one is consumed.
-    uint8_t* side_base = smem + STAGES * STAGE_BYTES + 1024 + kEpiWarps * 4096 + (warp - 2) * 4096;
+    uint8_t* side_base = smem + STAGES * STAGE_BYTES + 1024 + kEpiWarps * 8192 + (warp - 2) * 4096;
     uint64_t* side_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512) + (warp - 2) * 2;
     uint32_t side_phase = 0;  // bit b = parity of buffer b's next completion
     int side_buf = 0;
@@ -292,6 +294,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + acc * BN + c * 32, r);
+        if (c + 2 >= BN / 32) {  // last read of this accumulator: hand it back to the MMA warp now
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CL == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            else mbar_arrive(&tempty[acc]);
+          }
+        }
         const int nb = n0 + c * 32;
         if (nb >= p.N) continue;                 // warp-uniform
         if (STORE == 0 && !row_ok) continue;
@@ -312,19 +322,43 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           side_buf ^= 1;
         }
         float v[32];
+        if (e.alpha != 1.f) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * e.alpha;
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * e.alpha;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        }
         const bool full_chunk = nb + 32 <= p.N;
         if (row_ok) {
-          if (e.bias_any) {
+          if (e.bias_any) {  // same 32 bias values for every lane: 4 broadcast 16-byte loads
             const uint16_t* bp = static_cast<const uint16_t*>(e.bias_any) + nb;
+            if (full_chunk && (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
+              float bb[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (full_chunk || nb + j < p.N) v[j] += bf16_bits_to_f32(bp[j]);
+              for (int q = 0; q < 4; ++q) unpack8f(__ldg(reinterpret_cast<const uint4*>(bp) + q), bb + 8 * q);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += bb[j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < p.N) v[j] += bf16_bits_to_f32(bp[j]);
+            }
           } else if (e.bias) {
+            if (full_chunk && (reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (full_chunk || nb + j < p.N) v[j] += e.bias[nb + j];
+              for (int q = 0; q < 8; ++q) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + nb) + q);
+                v[4 * q] += b4.x;
+                v[4 * q + 1] += b4.y;
+                v[4 * q + 2] += b4.z;
+                v[4 * q + 3] += b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < p.N) v[j] += e.bias[nb + j];
+            }
           }
         }
         float pre[32];  // GELU pre-activation (aux output)
@@ -343,7 +377,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
               for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(aux)[q] = pack8f(pre + 8 * q);
             } else {
-              for (int j = 0; j < 32 && nb + j < p.N; ++j) aux[j] = f32_to_bf16_bits(pre[j]);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < p.N) aux[j] = f32_to_bf16_bits(pre[j]);
             }
           }
         } else if (e.act == kActTanhGrad || e.act == kActGeluGrad || e.act == kActSoftmaxGrad) {
@@ -393,15 +429,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += rr[j];
           } else {
-            for (int j = 0; j < 32 && nb + j < p.N; ++j) v[j] += bf16_bits_to_f32(rp[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < p.N) v[j] += bf16_bits_to_f32(rp[j]);
           }
         }
         if (STORE != 0) {
           // ---- stage in smem (swizzled) and TMA-store the 32x32 chunk ----
-          // one staging buffer per warp: the previous chunk's TMA store must
-          // have finished reading it (8 warps interleave, hiding the wait)
-          uint8_t* buf = stage_base;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          // buffer nchunk & 1: the store issued two chunks ago must have
+          // finished reading it
+          uint8_t* buf = stage_base + (nchunk & 1) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
           if (STORE == 1) {  // bf16: 32 rows x 64 B, SWIZZLE_64B; GELU aux in the 2nd half
 #pragma unroll
@@ -445,23 +483,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(out)[q] = pack8f(v + 8 * q);
           } else {
-            for (int j = 0; j < 32 && nb + j < p.N; ++j) out[j] = f32_to_bf16_bits(v[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < p.N) out[j] = f32_to_bf16_bits(v[j]);
           }
         } else {
           float* out = static_cast<float*>(p.C) + ci;
-          for (int j = 0; j < 32 && nb + j < p.N; ++j) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (nb + j >= p.N) continue;
             float w = v[j];
             if (e.mode == kEpiAccum) w += out[j];
             else if (e.mode == kEpiAssign0) w = __fadd_rn(0.f, w);
             out[j] = w;
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CL == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-        else mbar_arrive(&tempty[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -566,7 +602,7 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   // as many mainloop stages as fit beside the epilogue staging (a side-input
   // epilogue doubles that); a CTA pair holds half a B tile per stage
   constexpr size_t STAGE_B = size_t(BM * BK * 2) + size_t(CL == 2 ? BN / 2 : BN) * BK * 2;
-  constexpr size_t FIXED = 1024 + 1024 + size_t(kEpiWarps) * 4096 * (SIDE ? 2 : 1);
+  constexpr size_t FIXED = 1024 + 1024 + size_t(kEpiWarps) * (8192 + (SIDE ? 4096 : 0));
   constexpr int STAGES = int((232448 - FIXED) / STAGE_B) > 8 ? 8 : int((232448 - FIXED) / STAGE_B);
   constexpr size_t SMEM = size_t(STAGES) * STAGE_B + FIXED;
   static_assert(SMEM <= 232448, "smem budget");

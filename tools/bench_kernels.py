@@ -82,6 +82,33 @@ def bench_comm():
             eng.close()
 
 
+def bench_epi():
+    """The step's epilogue variants on their real shapes (8 warps, TMA store)."""
+    import ctypes as C
+    from paper_2510_20111_b200 import _native as N
+    dev = torch.device("cuda:0")
+    p = lambda t: C.c_void_p(t.data_ptr() if t is not None else 0)  # noqa: E731
+
+    def ex(A, B, Cm, M, N_, K, act=0, bias=None, aux=None, resid=None, out_bf16=1, mode=0, b_mn=0):
+        N.check(N.lib.hzp_gemm_bf16_ex(p(A), p(B), p(Cm), M, N_, K, K, N_ if b_mn else K, N_, 0, b_mn, mode,
+                                       out_bf16, act, p(bias), p(aux), N_ if aux is not None else 0, p(resid),
+                                       N_ if resid is not None else 0, None, 1.0,
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    for (M, N_, K, what) in ((8192, 8192, 2048, "plain"), (8192, 8192, 2048, "bias"), (8192, 8192, 2048, "gelu"),
+                             (8192, 8192, 2048, "gelugrad"), (8192, 6144, 2048, "bias"),
+                             (8192, 2048, 2048, "bias+resid"), (8192, 2048, 8192, "bias+resid")):
+        A = torch.randn(M, K, device=dev).to(torch.bfloat16)
+        B = torch.randn(N_, K, device=dev).to(torch.bfloat16)
+        Cm = torch.empty(M, N_, device=dev, dtype=torch.bfloat16)
+        bias = torch.randn(N_, device=dev).to(torch.bfloat16)
+        aux = torch.randn(M, N_, device=dev).to(torch.bfloat16)
+        kw = {"plain": {}, "bias": dict(bias=bias), "gelu": dict(act=2, bias=bias, aux=aux),
+              "gelugrad": dict(act=4, aux=aux), "bias+resid": dict(bias=bias, resid=aux)}[what]
+        ms = timeit(lambda: ex(A, B, Cm, M, N_, K, **kw))
+        print(json.dumps({"kernel": "gemm_epi", "M": M, "N": N_, "K": K, "epilogue": what, "ms": round(ms, 4),
+                          "tflops": round(2 * M * N_ * K / ms / 1e9, 1)}), flush=True)
+
+
 def bench_attn():
     import ctypes as C
     from paper_2510_20111_b200 import _native as N
@@ -113,4 +140,4 @@ def bench_attn():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "gemm"
-    {"gemm": bench_gemm, "comm": bench_comm, "attn": bench_attn}[what]()
+    {"gemm": bench_gemm, "comm": bench_comm, "attn": bench_attn, "epi": bench_epi}[what]()
