@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "engine/gemm.cuh"
 #include "engine/tc_ptx.cuh"
@@ -44,9 +45,12 @@ struct TcParams {
   CUtensorMap tmAux;  // GELU pre-activation output (STORE == 1, act == Gelu)
   CUtensorMap tmSide; // side input (SIDE): aux for the *-grad epilogues, else resid
   CUtensorMap tmBh;   // CL == 2, K-major B: half-height boxes (each CTA loads one half)
+  CUtensorMap tmBq;   // CL == 2, K-major B: quarter-height boxes (split tail units)
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
   int pairs_m;        // CL == 2: ceil(tiles_m / 2); tile index space = pairs
+  int nfull;          // CL == 2: units [0, nfull) are 256 x BN; the rest are the
+                      // last units split into two 256 x BN/2 halves (tail wave)
   int nh, nz, causal;
   int64_t c_sh, c_sb;
   Epilogue e;
@@ -56,27 +60,42 @@ struct TcParams {
 // Tile t -> (m0, n0, zh, zb); z slowest so concurrent CTAs share operands.
 struct TileCoord {
   int m0, n0, zh, zb;
+  int w;  // tile width (BN, or BN/2 for a split tail unit)
 };
 __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int t, int bn) {
   const int z = t / p.tiles_mn;
   const int r = t - z * p.tiles_mn;
-  return {(r % p.tiles_m) * BM, (r / p.tiles_m) * bn, z % p.nh, z / p.nh};
+  return {(r % p.tiles_m) * BM, (r / p.tiles_m) * bn, z % p.nh, z / p.nh, bn};
 }
 // CTA pair along M: unit t is a 256 x bn tile; CTA `rank` owns M rows
 // [m0 + 128 rank, +128) (possibly past M: zero fill) and B half `rank`.
 // Causal (mode 2) products walk the M pairs heaviest-first (LPT order).
+// Units past nfull are halves (alternating left / right) of the last units.
 __device__ __forceinline__ TileCoord pair_coord(const TcParams& p, int t, int bn, int rank) {
+  int half = -1;
+  if (t >= p.nfull) {
+    const int h = t - p.nfull;
+    t = p.nfull + (h >> 1);
+    half = h & 1;
+  }
+  TileCoord c;
   if (p.causal) {
     const int per_m = p.tiles_n * p.nz;
     const int mp = p.pairs_m - 1 - t / per_m;
     const int r = t - (t / per_m) * per_m;
     const int z = r / p.tiles_n;
-    return {(2 * mp + rank) * BM, (r - z * p.tiles_n) * bn, z % p.nh, z / p.nh};
+    c = {(2 * mp + rank) * BM, (r - z * p.tiles_n) * bn, z % p.nh, z / p.nh, bn};
+  } else {
+    const int per_z = p.pairs_m * p.tiles_n;
+    const int z = t / per_z;
+    const int r = t - z * per_z;
+    c = {(2 * (r % p.pairs_m) + rank) * BM, (r / p.pairs_m) * bn, z % p.nh, z / p.nh, bn};
   }
-  const int per_z = p.pairs_m * p.tiles_n;
-  const int z = t / per_z;
-  const int r = t - z * per_z;
-  return {(2 * (r % p.pairs_m) + rank) * BM, (r / p.pairs_m) * bn, z % p.nh, z / p.nh};
+  if (half >= 0) {
+    c.n0 += half * (bn / 2);
+    c.w = bn / 2;
+  }
+  return c;
 }
 // K-block range of a tile under the causal mode (see GemmShape::causal).  A
 // CTA pair shares one range: the union over its 256 rows (mode 2 only; the
@@ -104,6 +123,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   constexpr uint32_t IDESC = make_idesc(BM * CL, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC_H = make_idesc(BM * CL, BN / 2, A_MN, B_MN);  // split tail units
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -152,7 +172,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int rank = CL == 2 ? int(cluster_rank()) : 0;
   const int unit0 = CL == 2 ? int(blockIdx.x) / 2 : int(blockIdx.x);
   const int ustep = CL == 2 ? int(gridDim.x) / 2 : int(gridDim.x);
-  const int nunits = CL == 2 ? p.pairs_m * p.tiles_n * p.nz : p.num_tiles;
+  const int nunits = CL == 2 ? 2 * p.pairs_m * p.tiles_n * p.nz - p.nfull : p.num_tiles;
   if (CL == 2) cluster_sync_all();  // both TMEM allocations done
 
   if (warp == 0) {
@@ -170,7 +190,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const int k0 = kb * BK;
           if (CL == 2) {  // both CTAs' loads complete on the leader's full barrier
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-            if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            const bool split = tc.w != BN;  // tail half-unit: each CTA stages a quarter of B
+            if (rank == 0)
+              mbar_expect_tx(&full[stage], 2 * (A_BYTES + uint32_t(tc.w / 2) * BK * 2));
             if (A_MN) {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
@@ -179,12 +201,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               tma_load_4d_pair(sa, &tmA, fb, k0, tc.m0, tc.zh, tc.zb);
             }
             if (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 128; ++j)
-                tma_load_4d_pair(sb + j * (BK * 128), &tmB, fb, tc.n0 + rank * (BN / 2) + 64 * j, k0, tc.zh,
+              for (int j = 0; j < tc.w / 128; ++j)
+                tma_load_4d_pair(sb + j * (BK * 128), &tmB, fb, tc.n0 + rank * (tc.w / 2) + 64 * j, k0, tc.zh,
                                  tc.zb);
             } else {
-              tma_load_4d_pair(sb, &p.tmBh, fb, k0, tc.n0 + rank * (BN / 2), tc.zh, tc.zb);
+              tma_load_4d_pair(sb, split ? &p.tmBq : &p.tmBh, fb, k0, tc.n0 + rank * (tc.w / 2), tc.zh, tc.zb);
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
@@ -235,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                      : smem_desc(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc(sb + k * 2048, BK * 128, 1024)
                                      : smem_desc(sb + k * 32, 16, 1024);
-            if (CL == 2) tc_mma_pair(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
+            if (CL == 2) tc_mma_pair(d_tmem, ad, bd, tc.w == BN ? IDESC : IDESC_H, (kb > kb0 || k) ? 1u : 0u);
             else tc_mma(d_tmem, ad, bd, IDESC, (kb > kb0 || k) ? 1u : 0u);
           }
           // frees this smem stage (in both CTAs of a pair) when the MMAs retire
@@ -291,10 +312,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (e.act == kActSoftmaxGrad && row_ok)
         rv = e.rowvec[int64_t(tc.zh) * e.rv_sh + int64_t(tc.zb) * e.rv_sb + m];
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      const int nch = tc.w / 32;
+      for (int c = half; c < nch; c += 2) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + acc * BN + c * 32, r);
-        if (c + 2 >= BN / 32) {  // last read of this accumulator: hand it back to the MMA warp now
+        if (c + 2 >= nch) {  // last read of this accumulator: hand it back to the MMA warp now
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -308,7 +330,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         float sd[32];  // side input row (SIDE)
         if (SIDE) {
           const int nx = nb + 64;  // this warp's next chunk
-          if (lane == 0 && c + 2 < BN / 32 && nx < p.N) {
+          if (lane == 0 && c + 2 < nch && nx < p.N) {
             mbar_expect_tx(&side_bar[side_buf ^ 1], 2048);
             tma_load_4d(side_base + (side_buf ^ 1) * 2048, &p.tmSide, &side_bar[side_buf ^ 1], nx,
                         m0 + quarter * 32, tc.zh, tc.zb);
@@ -596,6 +618,30 @@ bool aligned16(const void* p, int64_t ld, int64_t sh, int64_t sb, int es) {
          (sb * es) % 16 == 0;
 }
 
+// Tail-wave balancing for the persistent CTA-pair kernel: units are dealt
+// round-robin to `clusters`; converting the last x units into two half-width
+// units each (2x BN/2 work items) shortens the final wave.  Returns the
+// number of full units (units - x) minimising the most-loaded cluster's work
+// (in half-unit weights, +1 per extra item for its pipeline fill), keeping
+// all units whole unless that saves >= 4%.
+int split_tail(int units, int clusters, bool allowed) {
+  if (!allowed || clusters <= 1 || units % clusters == 0) return units;
+  auto makespan = [&](int nfull) {
+    std::vector<int> load(clusters, 0);
+    const int items = nfull + 2 * (units - nfull);
+    for (int i = 0; i < items; ++i) load[i % clusters] += (i < nfull ? 8 : 4) + 1;
+    return *std::max_element(load.begin(), load.end());
+  };
+  int best_n = units, best = makespan(units);
+  const int waves = (units + clusters - 1) / clusters;
+  for (int w = 0; w < waves; ++w) {  // halves start on a wave boundary
+    const int nfull = w * clusters;
+    const int m = makespan(nfull);
+    if (m < best) { best = m; best_n = nfull; }
+  }
+  return best * 100 <= makespan(units) * 96 ? best_n : units;
+}
+
 template <int BN, int A_MN, int B_MN, int STORE, int SIDE, int CL>
 void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const Epilogue& e,
                cudaStream_t stream) {
@@ -641,10 +687,14 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   p.e = e;
   p.C = C;
   if (CL == 2) {
-    if (!B_MN) p.tmBh = make_map(B, s.K, s.N, s.ldb, BN / 2, s.nh, s.nb, s.b_sh, s.b_sb);
+    if (!B_MN) {
+      p.tmBh = make_map(B, s.K, s.N, s.ldb, BN / 2, s.nh, s.nb, s.b_sh, s.b_sb);
+      p.tmBq = make_map(B, s.K, s.N, s.ldb, BN / 4, s.nh, s.nb, s.b_sh, s.b_sb);
+    }
     p.pairs_m = (p.tiles_m + 1) / 2;
     const int units = p.pairs_m * p.tiles_n * p.nz;
     const int clusters = std::min(units, g_sm_budget / 2);
+    p.nfull = split_tail(units, clusters, BN == 256 && s.N % BN == 0);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * clusters);
     cfg.blockDim = dim3(kThreadsTC);
@@ -661,6 +711,7 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
     ++launch_counter();
     return;
   }
+  p.nfull = p.num_tiles;
   const int grid = p.num_tiles < g_sm_budget ? p.num_tiles : g_sm_budget;
   kern<<<grid, kThreadsTC, SMEM, stream>>>(ta, tb, p);
   HZP_LAUNCH_CHECK();

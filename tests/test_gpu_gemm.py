@@ -13,6 +13,8 @@ SHAPES = [
     (200, 136, 72),     # M/N/K tails (TMA zero-fill, masked stores)
     (8, 64, 128),       # tiny M
     (1024, 1024, 2048),
+    (8192, 2048, 128),  # CTA pairs with the tail wave split into half-width units
+    (6144, 2048, 192),
 ]
 
 
