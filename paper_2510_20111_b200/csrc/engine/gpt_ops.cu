@@ -538,6 +538,180 @@ __global__ void softmax_causal_reg_kernel(const float* __restrict__ S, uint16_t*
     }
   }
 }
+
+// ---- LayerNorm / column reductions for h a multiple of 256 -------------------
+// NVL = h / 256: 16-byte vectors per lane, so every array below is sized at
+// compile time and lives in registers.
+template <int NVL>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const uint16_t* __restrict__ x,
+                                                     const uint16_t* __restrict__ g,
+                                                     const uint16_t* __restrict__ be, uint16_t* __restrict__ y,
+                                                     float* __restrict__ mu, float* __restrict__ rs, int rows,
+                                                     int h) {
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+  float v[NVL][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NVL; ++k) {
+    unpack8(__ldg(xr + lane + 32 * k), v[k]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[k][j];
+  }
+  const float mean = warp_sum(s) / h;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NVL; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float d = v[k][j] - mean;
+      q += d * d;
+    }
+  const float rstd = rsqrtf(warp_sum(q) / h + 1e-5f);
+  if (lane == 0) {
+    mu[r] = mean;
+    rs[r] = rstd;
+  }
+  uint4* yr = reinterpret_cast<uint4*>(y + int64_t(r) * h);
+#pragma unroll
+  for (int k = 0; k < NVL; ++k) {
+    const int i = lane + 32 * k;
+    float gg[8], bb[8], o[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i), gg);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(be) + i), bb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (v[k][j] - mean) * rstd * gg[j] + bb[j];
+    yr[i] = pack8(o);
+  }
+}
+
+// dx = rstd (dy g - mean(dy g) - xhat mean(dy g xhat)) (+ resid); warp per row.
+template <int NVL>
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint16_t* __restrict__ dy,
+                                                        const uint16_t* __restrict__ x,
+                                                        const uint16_t* __restrict__ g,
+                                                        const float* __restrict__ mu, const float* __restrict__ rs,
+                                                        const uint16_t* __restrict__ resid,
+                                                        uint16_t* __restrict__ dx, int rows, int h) {
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float m = mu[r], rstd = rs[r];
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+  float xh[NVL][8], dg[NVL][8];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < NVL; ++k) {
+    const int i = lane + 32 * k;
+    float d[8], gg[8];
+    unpack8(__ldg(dyr + i), d);
+    unpack8(__ldg(xr + i), xh[k]);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i), gg);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      xh[k][j] = (xh[k][j] - m) * rstd;
+      dg[k][j] = d[j] * gg[j];
+      s1 += dg[k][j];
+      s2 += dg[k][j] * xh[k][j];
+    }
+  }
+  const float a1 = warp_sum(s1) / h, a2 = warp_sum(s2) / h;
+  uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
+#pragma unroll
+  for (int k = 0; k < NVL; ++k) {
+    const int i = lane + 32 * k;
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
+    if (resid) {
+      float rv[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(resid + int64_t(r) * h) + i), rv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += rv[j];
+    }
+    dxr[i] = pack8(o);
+  }
+}
+
+// Column partial sums over a chunk of rows: part[chunk][c] = sum_r d[r][c]
+// and, with LN, part2[chunk][c] = sum_r d[r][c] * xhat[r][c] (dgamma; part
+// then holds dbeta).  CTA = 8 warps x 256 columns (8 per lane), the warps
+// interleaving the chunk's rows; registers, then one smem fold.
+template <bool LN>
+__global__ void __launch_bounds__(256) colred_kernel(const uint16_t* __restrict__ d,
+                                                     const uint16_t* __restrict__ x,
+                                                     const float* __restrict__ mu, const float* __restrict__ rs,
+                                                     int rows, int cols, float* __restrict__ part,
+                                                     float* __restrict__ part2, int chunks) {
+  __shared__ float red[LN ? 2 : 1][8][257];
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  const int c0 = blockIdx.x * 256 + lane * 8;
+  const int per = (rows + chunks - 1) / chunks;
+  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c0 < cols) {
+#pragma unroll 2
+    for (int r = r0 + w; r < r1; r += 8) {
+      float f[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(d + int64_t(r) * cols + c0)), f);
+      if (LN) {
+        float xv[8];
+        unpack8(__ldg(reinterpret_cast<const uint4*>(x + int64_t(r) * cols + c0)), xv);
+        const float m = mu[r], rstd = rs[r];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] += f[j] * ((xv[j] - m) * rstd);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += f[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    red[0][w][lane * 8 + j] = a[j];
+    if (LN) red[LN ? 1 : 0][w][lane * 8 + j] = b[j];
+  }
+  __syncthreads();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < cols) {
+    float t = 0.f, u = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      t += red[0][i][threadIdx.x];
+      if (LN) u += red[LN ? 1 : 0][i][threadIdx.x];
+    }
+    part[int64_t(blockIdx.y) * cols + c] = t;
+    if (LN) part2[int64_t(blockIdx.y) * cols + c] = u;
+  }
+}
+
+// out[c] (mode) = sum_k part[k][c]; 4 threads per column, 64 columns per CTA.
+__global__ void __launch_bounds__(256) colsum_finalize4_kernel(const float* __restrict__ part, int chunks,
+                                                               int cols, void* out, int out_bf16, int mode) {
+  __shared__ float red[4][64];
+  const int cl = threadIdx.x & 63, sub = threadIdx.x >> 6;
+  const int c = blockIdx.x * 64 + cl;
+  float s = 0.f;
+  if (c < cols)
+    for (int k = sub; k < chunks; k += 4) s += part[int64_t(k) * cols + c];
+  red[sub][cl] = s;
+  __syncthreads();
+  if (sub == 0 && c < cols) write_mode(out, c, ((red[0][cl] + red[1][cl]) + red[2][cl]) + red[3][cl], out_bf16, mode);
+}
+
+#define HZP_NVL_SWITCH(nvl, ...)                      \
+  switch (nvl) {                                      \
+    case 1: { constexpr int NVL = 1; __VA_ARGS__; } break;   \
+    case 2: { constexpr int NVL = 2; __VA_ARGS__; } break;   \
+    case 3: { constexpr int NVL = 3; __VA_ARGS__; } break;   \
+    case 4: { constexpr int NVL = 4; __VA_ARGS__; } break;   \
+    case 6: { constexpr int NVL = 6; __VA_ARGS__; } break;   \
+    case 8: { constexpr int NVL = 8; __VA_ARGS__; } break;   \
+    case 12: { constexpr int NVL = 12; __VA_ARGS__; } break; \
+    case 16: { constexpr int NVL = 16; __VA_ARGS__; } break; \
+    default: handled = false;                         \
+  }
+
 }  // namespace
 
 void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int b, int S,
@@ -553,13 +727,31 @@ void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, 
 void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
                    float* mu, float* rstd, int rows, int h, cudaStream_t s) {
   if (h % 8 || h > 8 * kT * kMaxVec) throw std::invalid_argument("layernorm: h % 8 != 0 or > 8192");
-  if (h <= 32 * 8 * kWV) layernorm_fwd_warp_kernel<<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h);
-  else layernorm_fwd_kernel<<<rows, kT, 0, s>>>(x, g, beta, y, mu, rstd, h);
+  bool handled = h % 256 == 0;
+  if (handled) {
+    HZP_NVL_SWITCH(h / 256, (ln_fwd_kernel<NVL><<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h)));
+  }
+  if (!handled) {
+    if (h <= 32 * 8 * kWV) layernorm_fwd_warp_kernel<<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h);
+    else layernorm_fwd_kernel<<<rows, kT, 0, s>>>(x, g, beta, y, mu, rstd, h);
+  }
   HZP_LAUNCH_CHECK();
 }
 void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
                    const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
                    int rows, int h, cudaStream_t s) {
+  bool handled = h % 256 == 0;
+  if (handled) {  // dx pass (warp per row) + column pass for dgamma / dbeta
+    HZP_NVL_SWITCH(h / 256, (ln_bwd_dx_kernel<NVL><<<(rows + 7) / 8, 256, 0, s>>>(dy, x, g, mu, rstd, resid, dx,
+                                                                                   rows, h)));
+  }
+  if (handled) {
+    HZP_LAUNCH_CHECK();
+    colred_kernel<true><<<dim3(h / 256, chunks), 256, 0, s>>>(dy, x, mu, rstd, rows, h,
+                                                              part + int64_t(chunks) * h, part, chunks);
+    HZP_LAUNCH_CHECK();
+    return;
+  }
   if (h <= 32 * 8 * kWVB) {
     const size_t smem = size_t(16) * h * sizeof(float);  // 8 warps x (dg, dbeta)
     static bool attr = false;
@@ -574,13 +766,14 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
   HZP_LAUNCH_CHECK();
 }
 void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s) {
-  dim3 grid((cols / 8 + 127) / 128, chunks);
-  colsum_partial_kernel<<<grid, 128, 0, s>>>(d, rows, cols, part, chunks);
+  if (cols % 8) throw std::invalid_argument("colsum: cols % 8 != 0");
+  colred_kernel<false><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(d, nullptr, nullptr, nullptr, rows, cols,
+                                                                        part, nullptr, chunks);
   HZP_LAUNCH_CHECK();
 }
 void colsum_finalize(const float* part, int chunks, int cols, void* out, int out_bf16, int mode,
                      cudaStream_t s) {
-  colsum_finalize_par_kernel<<<(cols + 31) / 32, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
+  colsum_finalize4_kernel<<<(cols + 63) / 64, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
   HZP_LAUNCH_CHECK();
 }
 void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s) {

@@ -50,7 +50,7 @@ struct GptBuffers {
   const int* tokens = nullptr;  // current microbatch
 };
 
-constexpr int kChunks = 2 * kNumSMs;
+constexpr int kChunks = 64;  // row chunks of the column reductions (bias / LN parameter grads)
 
 class GptModel final : public Model {
  public:
