@@ -330,6 +330,7 @@ int hzp_ctx_open_peers(hzp_ctx* ctx, const void* handles, size_t handle_len, int
       e.table.flags[r] = a.flags;
     }
     HZP_CUDA(cudaMemcpy(e.dtable, &e.table, sizeof(RankTable), cudaMemcpyHostToDevice));
+    e.setup_rs_staging();
     e.peers_open = true;
   });
 }

@@ -17,8 +17,14 @@
 namespace hzp {
 namespace {
 
-constexpr int kThreads = 256;  // small enough to co-reside with a tcgen05 GEMM CTA (regs)
-constexpr int kUnroll = 4;
+constexpr int kThreads = 256;  // Z1 / optimizer kernels (run alone)
+// AG / RS run beside a persistent tcgen05 GEMM CTA on every SM: 128 threads
+// capped at 80 registers (10 K) fit next to the GEMM's 320 x 168 (53.7 K) in
+// the 64 K register file, so neither kernel waits for the other to drain.
+constexpr int kCommThreads = 128;
+constexpr int kCommRegs = 80;
+constexpr int kUnroll = 8;    // AG: 16-byte vectors in flight per thread
+constexpr int kUnrollRS = 4;  // RS: per source
 
 __device__ __forceinline__ void fadd4(float4& a, const float4& b) {
   a.x = __fadd_rn(a.x, b.x);
@@ -46,7 +52,7 @@ __device__ __forceinline__ void bf8_to_f8(uint4 v, float4& lo, float4& hi) {
 // AG: copy tile from owner shard to local slot.  Elements are moved as raw
 // bits (bit-exact by construction).
 template <int kElemBytes>
-__global__ void __launch_bounds__(kThreads) ag_pull_kernel(const RankTable* __restrict__ T,
+__global__ void __maxnreg__(kCommRegs) ag_pull_kernel(const RankTable* __restrict__ T,
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int slot,
                                                            int64_t slot_elems) {
@@ -61,16 +67,16 @@ __global__ void __launch_bounds__(kThreads) ag_pull_kernel(const RankTable* __re
       const uint4* s4 = reinterpret_cast<const uint4*>(src);
       uint4* d4 = reinterpret_cast<uint4*>(dst);
       int64_t i = threadIdx.x;
-      for (; i + (kUnroll - 1) * kThreads < nv; i += kUnroll * kThreads) {
+      for (; i + (kUnroll - 1) * kCommThreads < nv; i += kUnroll * kCommThreads) {
         uint4 v[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = ld_nc_v4(s4 + i + u * kThreads);
+        for (int u = 0; u < kUnroll; ++u) v[u] = ld_nc_v4(s4 + i + u * kCommThreads);
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) st_v4(d4 + i + u * kThreads, v[u]);
+        for (int u = 0; u < kUnroll; ++u) st_v4(d4 + i + u * kCommThreads, v[u]);
       }
-      for (; i < nv; i += kThreads) st_v4(d4 + i, ld_nc_v4(s4 + i));
+      for (; i < nv; i += kCommThreads) st_v4(d4 + i, ld_nc_v4(s4 + i));
     } else {
-      for (int64_t i = threadIdx.x; i < t.len; i += kThreads) {
+      for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
         if (kElemBytes == 2)
           reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(src)[i];
         else
@@ -83,7 +89,7 @@ __global__ void __launch_bounds__(kThreads) ag_pull_kernel(const RankTable* __re
 // ---------------------------------------------------------------------------
 // RS: grad[local][a_off + i] (+)= sum_{q=0..z2-1} wire(wgrad[base+q][slot][b_off + i])
 template <bool kBf16Wire>
-__global__ void __launch_bounds__(kThreads) rs_pull_kernel(const RankTable* __restrict__ T,
+__global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restrict__ T,
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int wslot,
                                                            int64_t wslot_elems, int z2,
@@ -95,47 +101,70 @@ __global__ void __launch_bounds__(kThreads) rs_pull_kernel(const RankTable* __re
     float* g = T->grad[T->global_rank[t.local]] + t.a_off;  // local index -> global rank
     const int64_t woff = (int64_t(wslot) * wslot_elems + t.b_off) * kEB;
     if (t.vec) {
+      // kUnrollRS 16-byte vectors per thread and source in flight before any
+      // use (peer loads are ~2 us away); sources summed in ascending order.
       constexpr int kPer = kBf16Wire ? 8 : 4;  // elements per 16-byte load
       const int64_t nv = t.len / kPer;
-      for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-        float4 lo, hi;
+      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += int64_t(kUnrollRS) * kCommThreads) {
+        float4 lo[kUnrollRS], hi[kUnrollRS];
+        uint4 v[kUnrollRS];
         {
-          const char* p = static_cast<const char*>(T->wgrad[t.src]) + woff + i * 16;
-          const uint4 v = ld_nc_v4(p);
-          if (kBf16Wire) bf8_to_f8(v, lo, hi); else lo = as_f4(v);
+          const char* p = static_cast<const char*>(T->wgrad[t.src]) + woff;
+#pragma unroll
+          for (int u = 0; u < kUnrollRS; ++u) {
+            const int64_t i = i0 + int64_t(u) * kCommThreads;
+            v[u] = i < nv ? ld_nc_v4(p + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnrollRS; ++u) {
+            if (kBf16Wire) bf8_to_f8(v[u], lo[u], hi[u]);
+            else lo[u] = as_f4(v[u]);
+          }
         }
         for (int q = 1; q < z2; ++q) {
-          const char* p = static_cast<const char*>(T->wgrad[t.src + q]) + woff + i * 16;
-          const uint4 v = ld_nc_v4(p);
-          if (kBf16Wire) {
-            float4 a, b;
-            bf8_to_f8(v, a, b);
-            fadd4(lo, a);
-            fadd4(hi, b);
-          } else {
-            fadd4(lo, as_f4(v));
+          const char* p = static_cast<const char*>(T->wgrad[t.src + q]) + woff;
+#pragma unroll
+          for (int u = 0; u < kUnrollRS; ++u) {
+            const int64_t i = i0 + int64_t(u) * kCommThreads;
+            v[u] = i < nv ? ld_nc_v4(p + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnrollRS; ++u) {
+            if (kBf16Wire) {
+              float4 a, b;
+              bf8_to_f8(v[u], a, b);
+              fadd4(lo[u], a);
+              fadd4(hi[u], b);
+            } else {
+              fadd4(lo[u], as_f4(v[u]));
+            }
           }
         }
-        if (do_scale) {
-          lo.x = __fmul_rn(lo.x, scale); lo.y = __fmul_rn(lo.y, scale);
-          lo.z = __fmul_rn(lo.z, scale); lo.w = __fmul_rn(lo.w, scale);
-          if (kBf16Wire) {
-            hi.x = __fmul_rn(hi.x, scale); hi.y = __fmul_rn(hi.y, scale);
-            hi.z = __fmul_rn(hi.z, scale); hi.w = __fmul_rn(hi.w, scale);
+#pragma unroll
+        for (int u = 0; u < kUnrollRS; ++u) {
+          const int64_t i = i0 + int64_t(u) * kCommThreads;
+          if (i >= nv) continue;
+          if (do_scale) {
+            lo[u].x = __fmul_rn(lo[u].x, scale); lo[u].y = __fmul_rn(lo[u].y, scale);
+            lo[u].z = __fmul_rn(lo[u].z, scale); lo[u].w = __fmul_rn(lo[u].w, scale);
+            if (kBf16Wire) {
+              hi[u].x = __fmul_rn(hi[u].x, scale); hi[u].y = __fmul_rn(hi[u].y, scale);
+              hi[u].z = __fmul_rn(hi[u].z, scale); hi[u].w = __fmul_rn(hi[u].w, scale);
+            }
           }
-        }
-        float4* g4 = reinterpret_cast<float4*>(g) + i * (kPer / 4);
-        float4 acc = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[0];
-        fadd4(acc, lo);
-        g4[0] = acc;
-        if (kBf16Wire) {
-          float4 acc2 = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[1];
-          fadd4(acc2, hi);
-          g4[1] = acc2;
+          float4* g4 = reinterpret_cast<float4*>(g) + i * (kPer / 4);
+          float4 acc = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[0];
+          fadd4(acc, lo[u]);
+          g4[0] = acc;
+          if (kBf16Wire) {
+            float4 acc2 = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[1];
+            fadd4(acc2, hi[u]);
+            g4[1] = acc2;
+          }
         }
       }
     } else {
-      for (int64_t i = threadIdx.x; i < t.len; i += kThreads) {
+      for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
         float s = 0.f;
         for (int q = 0; q < z2; ++q) {
           const char* p = static_cast<const char*>(T->wgrad[t.src + q]) + woff;
@@ -270,9 +299,9 @@ void launch_ag_pull(const RankTable* T, const CommTile* tiles, int ntiles, int s
                     int64_t slot_elems, bool bf16, int ctas, cudaStream_t s) {
   if (ntiles <= 0) return;
   if (bf16)
-    ag_pull_kernel<2><<<grid_for(ntiles, ctas), kThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems);
+    ag_pull_kernel<2><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems);
   else
-    ag_pull_kernel<4><<<grid_for(ntiles, ctas), kThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems);
+    ag_pull_kernel<4><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems);
   HZP_LAUNCH_CHECK();
 }
 
@@ -281,10 +310,10 @@ void launch_rs_pull(const RankTable* T, const CommTile* tiles, int ntiles, int w
                     int ctas, cudaStream_t s) {
   if (ntiles <= 0) return;
   if (bf16_wire)
-    rs_pull_kernel<true><<<grid_for(ntiles, ctas), kThreads, 0, s>>>(T, tiles, ntiles, wslot,
+    rs_pull_kernel<true><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, wslot,
                                                                      wslot_elems, z2, assign, scale);
   else
-    rs_pull_kernel<false><<<grid_for(ntiles, ctas), kThreads, 0, s>>>(T, tiles, ntiles, wslot,
+    rs_pull_kernel<false><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, wslot,
                                                                       wslot_elems, z2, assign, scale);
   HZP_LAUNCH_CHECK();
 }

@@ -169,6 +169,9 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   HZP_CUDA(cudaMemcpy(dtable, &table, sizeof(RankTable), cudaMemcpyHostToDevice));
   peers_open = emulate || c.par.dp == 1;
   debug_sync = std::getenv("HZP_DEBUG_SYNC") != nullptr;
+  if (const char* c = std::getenv("HZP_COMM_CTAS")) comm_ctas = std::max(1, std::atoi(c));  // tuning knob
+  if (const char* c = std::getenv("HZP_AG_CE")) ag_ce = std::atoi(c) != 0;
+  if (const char* c = std::getenv("HZP_RS_CE")) rs_ce = std::atoi(c) != 0;
   build_tiles();
 }
 
@@ -187,6 +190,8 @@ Engine::~Engine() {
     else if (a.base) cudaIpcCloseMemHandle(a.base);
   }
   cudaFree(dtable);
+  for (auto d : dtable_staged) cudaFree(d);
+  for (auto p : rs_stage) cudaFree(p);
   cudaFree(dtiles);
   cudaFree(dinputs);
   cudaFreeHost(hloss);
@@ -213,8 +218,40 @@ void Engine::build_tiles() {
   TileTables T = build_comm_tiles(geom, lr, ranks, bf16 ? 2 : 4, direct_grad);
   ag_off = T.ag_off;
   rs_off = T.rs_off;
+  ag_runs.assign(ag_off.size() > 0 ? ag_off.size() - 1 : 0, {});
+  for (size_t l = 0; l + 1 < ag_off.size(); ++l)
+    for (int i = ag_off[l]; i < ag_off[l + 1]; ++i) {
+      const CommTile& t = T.tiles[i];
+      auto& runs = ag_runs[l];
+      if (!runs.empty()) {
+        CopyRun& r = runs.back();
+        if (r.local == t.local && r.src == t.src && r.dst_off + r.len == t.a_off && r.src_off + r.len == t.b_off) {
+          r.len += t.len;
+          continue;
+        }
+      }
+      runs.push_back({t.local, t.src, t.a_off, t.b_off, t.len});
+    }
   z1_off = T.z1_off;
   z1_n = T.z1_n;
+  rs_runs.assign(rs_off.size() > 0 ? rs_off.size() - 1 : 0, {});
+  for (size_t l = 0; l + 1 < rs_off.size(); ++l)
+    for (int i = rs_off[l]; i < rs_off[l + 1]; ++i) {
+      const CommTile& t = T.tiles[i];
+      for (int q = 0; q < geom.z2; ++q) {
+        const int g = t.src + q;
+        if (local_index(g) >= 0) continue;  // driven here: read in place
+        auto& runs = rs_runs[l];
+        bool merged = false;
+        for (auto& r : runs)
+          if (r.src == g && r.src_off + r.len == t.b_off) {
+            r.len += t.len;
+            merged = true;
+            break;
+          }
+        if (!merged) runs.push_back({0, g, 0, t.b_off, t.len});
+      }
+    }
   if (dtiles) cudaFree(dtiles);
   HZP_CUDA(cudaMalloc(&dtiles, std::max<size_t>(1, T.tiles.size()) * sizeof(CommTile)));
   if (!T.tiles.empty())
@@ -222,12 +259,50 @@ void Engine::build_tiles() {
 }
 
 void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
+  if (ag_ce) {
+    const int es = bf16 ? 2 : 4;
+    for (const CopyRun& r : ag_runs[layer])
+      HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(table.ag_slots[r.local]) + (slot * slot_elems + r.dst_off) * es,
+                               static_cast<const char*>(table.param[r.src]) + r.src_off * es, r.len * es,
+                               cudaMemcpyDeviceToDevice, s));
+    ++launches;
+    return;
+  }
   launch_ag_pull(dtable, dtiles + ag_off[layer], ag_off[layer + 1] - ag_off[layer], slot,
                  slot_elems, bf16, comm_ctas, s);
   ++launches;
 }
 
+void Engine::setup_rs_staging() {
+  if (emulate || direct_grad || geom.z2 <= 1 || !rs_ce) return;
+  const int es = bf16 ? 2 : 4;
+  const int base = geom.z2_base(cfg.my_rank);
+  rs_stage.assign(cfg.par.dp, nullptr);
+  for (int q = 0; q < geom.z2; ++q)
+    if (base + q != cfg.my_rank) HZP_CUDA(cudaMalloc(&rs_stage[base + q], size_t(slot_elems) * es));
+  for (int w = 0; w < int(wslots); ++w) {
+    RankTable t = table;
+    for (int r = 0; r < cfg.par.dp; ++r)
+      if (rs_stage[r]) t.wgrad[r] = static_cast<char*>(rs_stage[r]) - int64_t(w) * slot_elems * es;
+    RankTable* d = nullptr;
+    HZP_CUDA(cudaMalloc(&d, sizeof(RankTable)));
+    HZP_CUDA(cudaMemcpy(d, &t, sizeof(RankTable), cudaMemcpyHostToDevice));
+    dtable_staged.push_back(d);
+  }
+}
+
 void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
+  if (!dtable_staged.empty()) {
+    const int es = bf16 ? 2 : 4;
+    for (const CopyRun& r : rs_runs[layer])
+      HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(rs_stage[r.src]) + r.src_off * es,
+                               static_cast<const char*>(table.wgrad[r.src]) + (wslot * slot_elems + r.src_off) * es,
+                               r.len * es, cudaMemcpyDeviceToDevice, s));
+    launch_rs_pull(dtable_staged[wslot], dtiles + rs_off[layer], rs_off[layer + 1] - rs_off[layer], wslot,
+                   slot_elems, geom.z2, bf16, assign, static_cast<float>(cfg.grad_scale), comm_ctas, s);
+    ++launches;
+    return;
+  }
   launch_rs_pull(dtable, dtiles + rs_off[layer], rs_off[layer + 1] - rs_off[layer], wslot,
                  slot_elems, geom.z2, bf16, assign, static_cast<float>(cfg.grad_scale), comm_ctas, s);
   ++launches;

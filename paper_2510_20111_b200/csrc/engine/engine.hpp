@@ -63,6 +63,23 @@ struct Engine {
 
   CommTile* dtiles = nullptr;
   std::vector<int> ag_off, rs_off;  // [nlocal_layers + 1] per layer tile ranges
+  // AG through the copy engines (no SMs taken from the concurrent GEMMs): the
+  // layer's tiles merged into contiguous (owner -> slot) runs
+  struct CopyRun {
+    int local, src;
+    int64_t dst_off, src_off, len;
+  };
+  std::vector<std::vector<CopyRun>> ag_runs;
+  bool ag_ce = false;  // HZP_AG_CE=1
+  // RS with the NVLink leg on the copy engines: each remote Z2 member's
+  // gradient-buffer segment is copied into a local staging slot, then the
+  // (now HBM-local) reduction kernel runs on a table whose remote wgrad
+  // entries point at the staging slots (one table per ring slot).
+  std::vector<std::vector<CopyRun>> rs_runs;  // CopyRun.src = global rank
+  std::vector<void*> rs_stage;                // [dp] staging slot per remote member (or null)
+  std::vector<RankTable*> dtable_staged;      // [wslots]
+  bool rs_ce = false;  // HZP_RS_CE=1: measured no faster than the SM pull at dp=2
+  void setup_rs_staging();
   int z1_off = 0, z1_n = 0;
 
   void* dinputs = nullptr;
