@@ -686,20 +686,7 @@ int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const floa
     auto* ds = static_cast<uint16_t*>(dsT);
     attn_rowdot(static_cast<const uint16_t*>(dO), static_cast<const uint16_t*>(O), lse, D, b, nh, S, 128, st);
     attention_bwd_tc(q, static_cast<const uint16_t*>(dO), lse, D, dq, ds, b, nh, S, h, st);
-    const int64_t h3 = 3 * int64_t(h), SS = int64_t(S) * S;
-    GemmShape sh{S, 128, S, S, int(h3), 1, 1};
-    sh.nh = nh;
-    sh.nb = b;
-    sh.a_sh = SS;
-    sh.a_sb = SS * nh;
-    sh.b_sh = 128;
-    sh.b_sb = S * h3;
-    sh.c_sh = 128;
-    sh.c_sb = S * h3;
-    sh.causal = 2;
-    Epilogue e;
-    e.ldc = int(h3);
-    gemm_tc_bf16(ds, q + h, dq, sh, e, st);
+    attention_dq(q, ds, dq, b, nh, S, h, st);
   });
 }
 

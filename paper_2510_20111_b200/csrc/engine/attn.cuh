@@ -21,4 +21,9 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
 void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse, const float* D,
                       uint16_t* dqkv, uint16_t* dsT, int b, int nh, int S, int h, cudaStream_t stream);
 
+// dQ = dS K into the q third of dqkv: one batched causal tcgen05 product
+// over (sequence, head), K range [0, end of the 128-query tile).
+void attention_dq(const uint16_t* qkv, const uint16_t* dsT, uint16_t* dqkv, int b, int nh, int S, int h,
+                  cudaStream_t stream);
+
 }  // namespace hzp

@@ -795,6 +795,28 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
 
 }  // namespace
 
+void attention_dq(const uint16_t* qkv, const uint16_t* dsT, uint16_t* dqkv, int b, int nh, int S, int h,
+                  cudaStream_t stream) {
+  const int64_t h3 = 3 * int64_t(h), SS = int64_t(S) * S;
+  // dQ[q, d] = sum_key dS[q, key] K[key, d]: A = dS stored as dSᵀ [key][q]
+  // (MN-major), B = K [key][d] (MN-major), K range [0, q tile end).  The
+  // product is HBM-bound on dSᵀ (b·nh·S² bf16 read once); the transposed
+  // formulation (N = 256 query tiles) measured slower (77 vs 67 us).
+  GemmShape sh{S, kHd, S, S, int(h3), 1, 1};
+  sh.nh = nh;
+  sh.nb = b;
+  sh.a_sh = SS;
+  sh.a_sb = SS * nh;
+  sh.b_sh = kHd;
+  sh.b_sb = S * h3;
+  sh.c_sh = kHd;
+  sh.c_sb = S * h3;
+  sh.causal = 2;
+  Epilogue e;
+  e.ldc = int(h3);
+  gemm_tc_bf16(dsT, qkv + h, dqkv, sh, e, stream);
+}
+
 // qkv [b, S, 3h] (q | k | v, heads contiguous in each), O [b, S, h].
 void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse, int b, int nh,
                       int S, int h, cudaStream_t stream) {

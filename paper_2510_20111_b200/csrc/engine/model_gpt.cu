@@ -342,17 +342,10 @@ class GptModel final : public Model {
       linear_dgrad(B->dxm, W + o.w_o, B->dattn, h_, h_, e, s);
     }
     // attention core: fused tcgen05 backward for dK, dV (P recomputed from
-    // lse, dS^T emitted), then dQ = dS K as a causal batched GEMM
-    const int64_t SS = int64_t(S_) * S_;
+    // lse, dS^T emitted), then dQ = dS K as one transposed causal product
     attn_rowdot(B->dattn, a.attn, a.lse, B->D, b_, nh_, S_, hd_, s);
     attention_bwd_tc(a.qkv, B->dattn, a.lse, B->D, B->dqkv, B->dS, b_, nh_, S_, h_, s);
-    {  // dQ[q, d] = sum_key dS^T[key, q] K[key, d]
-      GemmShape sh = attn_shape(S_, hd_, S_, S_, int(h3), 1, 1, SS, SS * nh_, hd_, S_ * h3, hd_,
-                                S_ * h3, 2);
-      Epilogue e;
-      e.ldc = int(h3);
-      gemm_tc_bf16(B->dS, a.qkv + h_, B->dqkv, sh, e, s);
-    }
+    attention_dq(a.qkv, B->dS, B->dqkv, b_, nh_, S_, h_, s);  // dQ = dS K (transposed product)
     linear_wgrad(B->dqkv, a.ln1, int(h3), h_, g, o.w_qkv, o.b_qkv, B, s);
     {
       Epilogue e;
