@@ -203,37 +203,52 @@ __global__ void __launch_bounds__(kThreads) z1_adam_kernel(const RankTable* __re
     float* mv = T->var[t.local] + t.a_off;
     float* gd = dbg ? T->z1_grad_dbg[t.local] + t.a_off : nullptr;
     if (t.vec) {
+      // two float4 per thread per pass: all ten 16-byte loads issued before
+      // the (IEEE div / sqrt heavy) Adam math
       const int64_t nv = t.len / 4;
-      for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-        float4 g = as_f4(ld_v4(T->grad[t.src] + t.b_off + 4 * i));
-        for (int b = 1; b < replicas; ++b)
-          fadd4(g, as_f4(ld_v4(T->grad[t.src + b * z2] + t.b_off + 4 * i)));
-        if (gd) reinterpret_cast<float4*>(gd)[i] = g;
-        float4 m = reinterpret_cast<float4*>(mm)[i];
-        float4 v = reinterpret_cast<float4*>(mv)[i];
-        float4 w = reinterpret_cast<float4*>(mw)[i];
-        adam_one(g.x, m.x, v.x, w.x, a);
-        adam_one(g.y, m.y, v.y, w.y, a);
-        adam_one(g.z, m.z, v.z, w.z, a);
-        adam_one(g.w, m.w, v.w, w.w, a);
-        reinterpret_cast<float4*>(mm)[i] = m;
-        reinterpret_cast<float4*>(mv)[i] = v;
-        reinterpret_cast<float4*>(mw)[i] = w;
-        uint64_t targets = t.mask;
-        if (kBf16Param) {
-          const uint32_t lo = uint32_t(f32_to_bf16_bits(w.x)) | (uint32_t(f32_to_bf16_bits(w.y)) << 16);
-          const uint32_t hi = uint32_t(f32_to_bf16_bits(w.z)) | (uint32_t(f32_to_bf16_bits(w.w)) << 16);
-          while (targets) {
-            const int q = __ffsll(targets) - 1;
-            targets &= targets - 1;
-            uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(T->param[q]) + t.c_off) + i;
-            *p = make_uint2(lo, hi);
-          }
-        } else {
-          while (targets) {
-            const int q = __ffsll(targets) - 1;
-            targets &= targets - 1;
-            reinterpret_cast<float4*>(static_cast<float*>(T->param[q]) + t.c_off)[i] = w;
+      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += 2 * kThreads) {
+        float4 g[2], m[2], v[2], w[2];
+        bool ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t i = i0 + int64_t(u) * kThreads;
+          ok[u] = i < nv;
+          if (!ok[u]) continue;
+          g[u] = as_f4(ld_v4(T->grad[t.src] + t.b_off + 4 * i));
+          for (int b = 1; b < replicas; ++b)
+            fadd4(g[u], as_f4(ld_v4(T->grad[t.src + b * z2] + t.b_off + 4 * i)));
+          m[u] = reinterpret_cast<const float4*>(mm)[i];
+          v[u] = reinterpret_cast<const float4*>(mv)[i];
+          w[u] = reinterpret_cast<const float4*>(mw)[i];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!ok[u]) continue;
+          const int64_t i = i0 + int64_t(u) * kThreads;
+          if (gd) reinterpret_cast<float4*>(gd)[i] = g[u];
+          adam_one(g[u].x, m[u].x, v[u].x, w[u].x, a);
+          adam_one(g[u].y, m[u].y, v[u].y, w[u].y, a);
+          adam_one(g[u].z, m[u].z, v[u].z, w[u].z, a);
+          adam_one(g[u].w, m[u].w, v[u].w, w[u].w, a);
+          reinterpret_cast<float4*>(mm)[i] = m[u];
+          reinterpret_cast<float4*>(mv)[i] = v[u];
+          reinterpret_cast<float4*>(mw)[i] = w[u];
+          uint64_t targets = t.mask;
+          if (kBf16Param) {
+            const uint32_t lo = uint32_t(f32_to_bf16_bits(w[u].x)) | (uint32_t(f32_to_bf16_bits(w[u].y)) << 16);
+            const uint32_t hi = uint32_t(f32_to_bf16_bits(w[u].z)) | (uint32_t(f32_to_bf16_bits(w[u].w)) << 16);
+            while (targets) {
+              const int q = __ffsll(targets) - 1;
+              targets &= targets - 1;
+              uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(T->param[q]) + t.c_off) + i;
+              *p = make_uint2(lo, hi);
+            }
+          } else {
+            while (targets) {
+              const int q = __ffsll(targets) - 1;
+              targets &= targets - 1;
+              reinterpret_cast<float4*>(static_cast<float*>(T->param[q]) + t.c_off)[i] = w[u];
+            }
           }
         }
       }
