@@ -259,7 +259,7 @@ void Engine::build_tiles() {
 }
 
 void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
-  if (ag_ce) {
+  if (ag_ce && !emulate) {  // multi-process: NVLink leg on the copy engines
     const int es = bf16 ? 2 : 4;
     for (const CopyRun& r : ag_runs[layer])
       HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(table.ag_slots[r.local]) + (slot * slot_elems + r.dst_off) * es,
