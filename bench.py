@@ -172,6 +172,59 @@ def run_reference(args):
     return 0
 
 
+NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU
+
+
+def collectives(eng, N, local, max_over_ranks, barrier, iters=5):
+    """AG / RS bus bandwidth of one 1.3B transformer layer (the step's own
+    collective, through the ctx: copy-engine NVLink leg by default) and an NCCL
+    comparator on the same bytes.  busbw = (N-1)/N x layer bytes / time
+    (nccl-tests convention)."""
+    import torch
+    import torch.distributed as dist
+    off, n = eng.layers[1]
+    nbytes = n * 2  # bf16 working copy / bf16 gradient wire
+    out = {"layer_elems": int(n), "layer_bytes": int(nbytes), "nvlink_peak_GBps": NVLINK_GBPS}
+
+    def timed(fn, stream_ptr):
+        st = torch.cuda.ExternalStream(stream_ptr, device=f"cuda:{local}") if stream_ptr else None
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if st is not None:
+            e0.record(st)
+        else:
+            e0.record()
+        for _ in range(iters):
+            fn()
+        if st is not None:
+            e1.record(st)
+        else:
+            e1.record()
+        e1.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / iters)
+
+    for name, fn, sid in (("ag", lambda: eng.ag_layer(1, 0), 1), ("rs", lambda: eng.rs_layer(1, 0), 2)):
+        ms = timed(fn, eng.stream(sid))
+        bw = (N - 1) / N * nbytes / (ms / 1e3) / 1e9
+        out[name] = {"ms": round(ms, 4), "busbw_GBps": round(bw, 1), "frac": round(bw / NVLINK_GBPS, 3)}
+    try:  # NCCL comparator (setup only; never on the step's data path)
+        g = dist.new_group(backend="nccl")
+        full = torch.empty(n - n % N, dtype=torch.bfloat16, device=f"cuda:{local}")
+        part = torch.empty(full.numel() // N, dtype=torch.bfloat16, device=f"cuda:{local}")
+        for name, fn in (("nccl_all_gather", lambda: dist.all_gather_into_tensor(full, part, group=g)),
+                         ("nccl_reduce_scatter", lambda: dist.reduce_scatter_tensor(part, full, group=g))):
+            ms = timed(fn, None)
+            bw = (N - 1) / N * full.numel() * 2 / (ms / 1e3) / 1e9
+            out[name] = {"ms": round(ms, 4), "busbw_GBps": round(bw, 1)}
+        dist.destroy_process_group(g)
+    except Exception as exc:  # noqa: BLE001
+        out["nccl"] = f"unavailable: {exc}"[:200]
+    return out
+
+
 def run_hzp(args):
     import numpy as np
     import torch
@@ -261,6 +314,19 @@ def run_hzp(args):
             "kernel": "gemm_tc_kernel (tcgen05 bf16)", "launches_per_step": gn,
             "share_of_step": round(gms / ms, 3) if ms else None,
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
+    # ---- exposed comm: compute-stream idle of one recorded step (sched.cpp:341-350) ----
+    eng.set_timeline(True)
+    eng.step_async(dev.data_ptr(), True)
+    eng.sync()
+    tl = eng.timeline()
+    eng.set_timeline(False)
+    idle = max_over_ranks(tl["compute_idle_ms"])
+    mk = max_over_ranks(tl["makespan_ms"])
+    exposed = {"compute_idle_ms": round(idle, 3), "makespan_ms": round(mk, 3),
+               "frac": round(idle / mk, 4) if mk else None,
+               "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
+                             "CUDA-event timeline of one extra step, max over ranks"}
+    colls = collectives(eng, N, local, max_over_ranks, barrier) if N > 1 else None
     line = None
     if rank == 0:
         cb = cpu_reference(2, 0, "cpu_baseline") if not args.no_cpu_baseline else None
@@ -277,7 +343,7 @@ def run_hzp(args):
                            "parallelism": f"dp{N} (z1=z2=z3={N})", "prelaunch_depth": 2,
                            "rs_slots": 1, "l2": "activation working set >> 126 MB L2 (no flush needed)"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
-                "roofline": roof,
+                "roofline": roof, "exposed_comm": exposed, "collectives": colls,
                 "cpu_baseline": ({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
                                  if cb else None)}
         print(json.dumps(line), flush=True)

@@ -236,6 +236,10 @@ int hzp_launch_log(const hzp_ctx* ctx, hzp_launch_rec* out, int cap, int* n);
  * (= last compute end - sum compute busy, sched.cpp:341-350). */
 int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, int* n,
                  double* compute_idle_ms, double* compute_busy_ms, double* makespan_ms);
+/* Turn per-task event recording on/off for the following steps (events are
+ * created on first use), so a timed run can be measured untouched and one
+ * extra step recorded for hzp_timeline. */
+int hzp_set_timeline(hzp_ctx* ctx, int on);
 
 /* Extra device work counters (kernels launched by the last step). */
 int hzp_ctx_launch_count(const hzp_ctx* ctx, int64_t* kernels);

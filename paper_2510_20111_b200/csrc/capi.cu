@@ -454,6 +454,25 @@ int hzp_launch_log(const hzp_ctx* ctx, hzp_launch_rec* out, int cap, int* n) {
   return HZP_OK;
 }
 
+int hzp_set_timeline(hzp_ctx* ctx, int on) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    HZP_CUDA(cudaDeviceSynchronize());
+    const int n = static_cast<int>(e.plan.entries.size());
+    if (on && static_cast<int>(e.tev0.size()) != n) {
+      e.tev0.resize(n);
+      e.tev1.resize(n);
+      for (int i = 0; i < n; ++i) {
+        HZP_CUDA(cudaEventCreate(&e.tev0[i]));
+        HZP_CUDA(cudaEventCreate(&e.tev1[i]));
+      }
+    }
+    e.cfg.timeline = on ? 1 : 0;
+  });
+}
+
 int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, int* n,
                  double* compute_idle_ms, double* compute_busy_ms, double* makespan_ms) {
   if (!ctx || !n) return HZP_ERR_ARG;

@@ -93,10 +93,14 @@ __global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restric
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int wslot,
                                                            int64_t wslot_elems, int z2,
-                                                           int assign, float scale) {
+                                                           int assign, float scale, int split) {
+  // `split` CTAs share a tile (part = blockIdx % split takes every split-th
+  // group of kUnrollRS x kCommThreads vectors): HBM-local reduces want more
+  // CTAs in flight than NVLink pulls do.
   constexpr int kEB = kBf16Wire ? 2 : 4;
   const bool do_scale = scale != 1.0f;
-  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+  const int part = int(blockIdx.x) % split;
+  for (int ti = int(blockIdx.x) / split; ti < ntiles; ti += int(gridDim.x) / split) {
     const CommTile t = tiles[ti];
     float* g = T->grad[T->global_rank[t.local]] + t.a_off;  // local index -> global rank
     const int64_t woff = (int64_t(wslot) * wslot_elems + t.b_off) * kEB;
@@ -105,7 +109,8 @@ __global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restric
       // use (peer loads are ~2 us away); sources summed in ascending order.
       constexpr int kPer = kBf16Wire ? 8 : 4;  // elements per 16-byte load
       const int64_t nv = t.len / kPer;
-      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += int64_t(kUnrollRS) * kCommThreads) {
+      for (int64_t i0 = threadIdx.x + int64_t(part) * kUnrollRS * kCommThreads; i0 < nv;
+           i0 += int64_t(kUnrollRS) * kCommThreads * split) {
         float4 lo[kUnrollRS], hi[kUnrollRS];
         uint4 v[kUnrollRS];
         {
@@ -164,6 +169,7 @@ __global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restric
         }
       }
     } else {
+      if (part != 0) continue;
       for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
         float s = 0.f;
         for (int q = 0; q < z2; ++q) {
@@ -322,14 +328,16 @@ void launch_ag_pull(const RankTable* T, const CommTile* tiles, int ntiles, int s
 
 void launch_rs_pull(const RankTable* T, const CommTile* tiles, int ntiles, int wslot,
                     int64_t wslot_elems, int z2, bool bf16_wire, bool assign, float scale,
-                    int ctas, cudaStream_t s) {
+                    int ctas, cudaStream_t s, int split) {
   if (ntiles <= 0) return;
+  split = split < 1 ? 1 : split;
+  const int grid = grid_for(ntiles, ctas) * split;
   if (bf16_wire)
-    rs_pull_kernel<true><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, wslot,
-                                                                     wslot_elems, z2, assign, scale);
+    rs_pull_kernel<true><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2, assign,
+                                                       scale, split);
   else
-    rs_pull_kernel<false><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, wslot,
-                                                                      wslot_elems, z2, assign, scale);
+    rs_pull_kernel<false><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2, assign,
+                                                        scale, split);
   HZP_LAUNCH_CHECK();
 }
 

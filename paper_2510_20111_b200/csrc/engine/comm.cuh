@@ -53,9 +53,10 @@ enum FlagKind { kFlagBarrier = 0, kFlagRsReady = 1, kFlagRsDone = 2, kNumFlagKin
 // Launch wrappers (stream-ordered; grid sized by `ctas`).
 void launch_ag_pull(const RankTable* dev_table, const CommTile* tiles, int ntiles, int slot,
                     int64_t slot_elems, bool bf16, int ctas, cudaStream_t s);
+// split: CTAs per tile (HBM-local reduces of staged gradients use > 1).
 void launch_rs_pull(const RankTable* dev_table, const CommTile* tiles, int ntiles, int wslot,
                     int64_t wslot_elems, int z2, bool bf16_wire, bool assign, float scale,
-                    int ctas, cudaStream_t s);
+                    int ctas, cudaStream_t s, int split = 1);
 void launch_z1_adam(const RankTable* dev_table, const CommTile* tiles, int ntiles, int z2,
                     int replicas, const AdamArgs* per_local, int nlocal, bool bf16_param,
                     bool dbg, int ctas, cudaStream_t s);

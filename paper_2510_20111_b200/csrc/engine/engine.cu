@@ -191,6 +191,8 @@ Engine::~Engine() {
   }
   cudaFree(dtable);
   for (auto d : dtable_staged) cudaFree(d);
+  for (auto e : rs_ev) cudaEventDestroy(e);
+  if (rs_red_stream) cudaStreamDestroy(rs_red_stream);
   for (auto p : rs_stage) cudaFree(p);
   cudaFree(dtiles);
   cudaFree(dinputs);
@@ -218,6 +220,7 @@ void Engine::build_tiles() {
   TileTables T = build_comm_tiles(geom, lr, ranks, bf16 ? 2 : 4, direct_grad);
   ag_off = T.ag_off;
   rs_off = T.rs_off;
+  tiles_host = T.tiles;
   ag_runs.assign(ag_off.size() > 0 ? ag_off.size() - 1 : 0, {});
   for (size_t l = 0; l + 1 < ag_off.size(); ++l)
     for (int i = ag_off[l]; i < ag_off[l + 1]; ++i) {
@@ -234,24 +237,6 @@ void Engine::build_tiles() {
     }
   z1_off = T.z1_off;
   z1_n = T.z1_n;
-  rs_runs.assign(rs_off.size() > 0 ? rs_off.size() - 1 : 0, {});
-  for (size_t l = 0; l + 1 < rs_off.size(); ++l)
-    for (int i = rs_off[l]; i < rs_off[l + 1]; ++i) {
-      const CommTile& t = T.tiles[i];
-      for (int q = 0; q < geom.z2; ++q) {
-        const int g = t.src + q;
-        if (local_index(g) >= 0) continue;  // driven here: read in place
-        auto& runs = rs_runs[l];
-        bool merged = false;
-        for (auto& r : runs)
-          if (r.src == g && r.src_off + r.len == t.b_off) {
-            r.len += t.len;
-            merged = true;
-            break;
-          }
-        if (!merged) runs.push_back({0, g, 0, t.b_off, t.len});
-      }
-    }
   if (dtiles) cudaFree(dtiles);
   HZP_CUDA(cudaMalloc(&dtiles, std::max<size_t>(1, T.tiles.size()) * sizeof(CommTile)));
   if (!T.tiles.empty())
@@ -280,6 +265,11 @@ void Engine::setup_rs_staging() {
   rs_stage.assign(cfg.par.dp, nullptr);
   for (int q = 0; q < geom.z2; ++q)
     if (base + q != cfg.my_rank) HZP_CUDA(cudaMalloc(&rs_stage[base + q], size_t(slot_elems) * es));
+  int lo = 0, hi = 0;
+  HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  HZP_CUDA(cudaStreamCreateWithPriority(&rs_red_stream, cudaStreamNonBlocking, hi));
+  rs_ev.resize(64);
+  for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int w = 0; w < int(wslots); ++w) {
     RankTable t = table;
     for (int r = 0; r < cfg.par.dp; ++r)
@@ -294,12 +284,29 @@ void Engine::setup_rs_staging() {
 void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
   if (!dtable_staged.empty()) {
     const int es = bf16 ? 2 : 4;
-    for (const CopyRun& r : rs_runs[layer])
-      HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(rs_stage[r.src]) + r.src_off * es,
-                               static_cast<const char*>(table.wgrad[r.src]) + (wslot * slot_elems + r.src_off) * es,
-                               r.len * es, cudaMemcpyDeviceToDevice, s));
-    launch_rs_pull(dtable_staged[wslot], dtiles + rs_off[layer], rs_off[layer + 1] - rs_off[layer], wslot,
-                   slot_elems, geom.z2, bf16, assign, static_cast<float>(cfg.grad_scale), comm_ctas, s);
+    const int t0 = rs_off[layer], t1 = rs_off[layer + 1];
+    const int base = geom.z2_base(cfg.my_rank);
+    int ev = 0;
+    for (int c0 = t0; c0 < t1; c0 += kRsChunkTiles, ++ev) {
+      const int c1 = std::min(t1, c0 + kRsChunkTiles);
+      const int64_t b0 = tiles_host[c0].b_off;
+      const int64_t b1 = tiles_host[c1 - 1].b_off + tiles_host[c1 - 1].len;
+      for (int q = 0; q < geom.z2; ++q) {
+        const int g = base + q;
+        if (!rs_stage[g]) continue;  // this rank's own buffer is read in place
+        HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(rs_stage[g]) + b0 * es,
+                                 static_cast<const char*>(table.wgrad[g]) + (wslot * slot_elems + b0) * es,
+                                 (b1 - b0) * es, cudaMemcpyDeviceToDevice, s));
+      }
+      cudaEvent_t e = rs_ev[ev % rs_ev.size()];
+      HZP_CUDA(cudaEventRecord(e, s));
+      HZP_CUDA(cudaStreamWaitEvent(rs_red_stream, e, 0));
+      launch_rs_pull(dtable_staged[wslot], dtiles + c0, c1 - c0, wslot, slot_elems, geom.z2, bf16, assign,
+                     static_cast<float>(cfg.grad_scale), comm_ctas, rs_red_stream, 4);
+    }
+    cudaEvent_t e = rs_ev[ev % rs_ev.size()];
+    HZP_CUDA(cudaEventRecord(e, rs_red_stream));
+    HZP_CUDA(cudaStreamWaitEvent(s, e, 0));  // the RS task ends when its last reduce does
     ++launches;
     return;
   }

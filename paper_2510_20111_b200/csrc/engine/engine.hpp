@@ -75,9 +75,14 @@ struct Engine {
   // gradient-buffer segment is copied into a local staging slot, then the
   // (now HBM-local) reduction kernel runs on a table whose remote wgrad
   // entries point at the staging slots (one table per ring slot).
-  std::vector<std::vector<CopyRun>> rs_runs;  // CopyRun.src = global rank
   std::vector<void*> rs_stage;                // [dp] staging slot per remote member (or null)
   std::vector<RankTable*> dtable_staged;      // [wslots]
+  // The copy of chunk c+1 overlaps the HBM-local reduce of chunk c: copies
+  // on the RS stream, reduces on rs_red_stream, chained by rs_ev.
+  std::vector<CommTile> tiles_host;
+  cudaStream_t rs_red_stream = nullptr;
+  std::vector<cudaEvent_t> rs_ev;
+  static constexpr int kRsChunkTiles = 128;  // 4 M elements per pipelined chunk
   bool rs_ce = true;   // HZP_RS_CE=0 to use the SM pull (dp=4: 184.5 -> 160.1 ms with both CE legs)
   void setup_rs_staging();
   int z1_off = 0, z1_n = 0;

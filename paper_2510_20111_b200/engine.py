@@ -195,6 +195,9 @@ class HzpEngine:
                 "compute_idle_ms": idle.value, "compute_busy_ms": busy.value,
                 "makespan_ms": mk.value}
 
+    def set_timeline(self, on: bool) -> None:
+        N.check(N.lib.hzp_set_timeline(self._h, 1 if on else 0))
+
     def stream(self, which: int = 0) -> int:
         p = C.c_void_p()
         N.check(N.lib.hzp_ctx_stream(self._h, which, C.byref(p)))
