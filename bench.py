@@ -309,8 +309,17 @@ def run_hzp(args):
     gf, gms, gn = gemm_profile_read()
     burst, sustained, hbm, src = peaks()
     achieved = gf / (gms / 1e3) / 1e12
+    traffic, traffic_src = None, None
+    tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gemm_dram_traffic.json")
+    if os.path.exists(tf):  # committed ncu capture of this kernel (DRAM bytes per launch, one step)
+        with open(tf) as fh:
+            tj = json.load(fh)
+        traffic = int(tj["dram_bytes_per_launch"])
+        traffic_src = (f"profiles/r01_gemm_dram_traffic.json: ncu dram__bytes_read+write per launch over "
+                       f"{tj['launches']} launches; algorithmic {int(tj['algorithmic_bytes_per_launch'])} B "
+                       f"(ratio {tj['ratio']:.2f})")
     roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": sustained, "unit": "TFLOP/s",
-            "frac": round(achieved / sustained, 3), "traffic": None,
+            "frac": round(achieved / sustained, 3), "traffic": traffic, "traffic_source": traffic_src,
             "kernel": "gemm_tc_kernel (tcgen05 bf16)", "launches_per_step": gn,
             "share_of_step": round(gms / ms, 3) if ms else None,
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}

@@ -55,6 +55,7 @@ struct TcParams {
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
   int pairs_m;        // CL == 2: ceil(tiles_m / 2); tile index space = pairs
+  int n_fast;         // raster: 1 = N tiles vary fastest (A streamed once, B kept in L2)
   int nfull;          // CL == 2: units [0, nfull) are 256 x BN; the rest are the
                       // last units split into two 256 x BN/2 halves (tail wave)
   int nh, nz, causal;
@@ -71,6 +72,7 @@ struct TileCoord {
 __device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int t, int bn) {
   const int z = t / p.tiles_mn;
   const int r = t - z * p.tiles_mn;
+  if (p.n_fast) return {(r / p.tiles_n) * BM, (r % p.tiles_n) * bn, z % p.nh, z / p.nh, bn};
   return {(r % p.tiles_m) * BM, (r / p.tiles_m) * bn, z % p.nh, z / p.nh, bn};
 }
 // CTA pair along M: unit t is a 256 x bn tile; CTA `rank` owns M rows
@@ -95,7 +97,10 @@ __device__ __forceinline__ TileCoord pair_coord(const TcParams& p, int t, int bn
     const int per_z = p.pairs_m * p.tiles_n;
     const int z = t / per_z;
     const int r = t - z * per_z;
-    c = {(2 * (r % p.pairs_m) + rank) * BM, (r / p.pairs_m) * bn, z % p.nh, z / p.nh, bn};
+    if (p.n_fast)
+      c = {(2 * (r / p.tiles_n) + rank) * BM, (r % p.tiles_n) * bn, z % p.nh, z / p.nh, bn};
+    else
+      c = {(2 * (r % p.pairs_m) + rank) * BM, (r / p.pairs_m) * bn, z % p.nh, z / p.nh, bn};
   }
   if (half >= 0) {
     c.n0 += half * (bn / 2);
@@ -689,6 +694,10 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   p.num_tiles = p.tiles_mn * s.nh * s.nb;
   p.nh = s.nh;
   p.nz = s.nh * s.nb;
+  // Raster order: the units in flight at once cover a band of the faster
+  // dimension; vary N fastest when A (M x K) is the larger operand so every
+  // A row block is read from HBM once while B stays L2-resident, else M.
+  p.n_fast = (int64_t(s.M) * s.K > int64_t(s.N) * s.K) ? 1 : 0;
   p.causal = s.causal;
   p.c_sh = s.c_sh;
   p.c_sb = s.c_sb;
