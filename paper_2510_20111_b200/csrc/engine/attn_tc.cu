@@ -528,14 +528,17 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
 // q >= key tile.  Rows of every TMEM accumulator are KEYS:
 //   S^T  = K Q_i^T          TMEM S[b]  (64 cols)  P^T  = exp2(S^T*c - lse2_q)
 //   dP^T = V dO_i^T         TMEM dP[b] (64 cols)  dS^T = P^T (dP^T - D_q) / sqrt(d)
-//   dV  += P^T dO_i         TMEM [256,384)        (P^T from smem, dO_i as MN-major B)
-//   dK  += dS^T Q_i         TMEM [384,512)        (dS^T from smem, Q_i as MN-major B)
-// Q_i / dO_i (+ their lse / D slices, bulk-copied on the same barrier),
-// S^T / dP^T and P^T / dS^T are all double-buffered, so the MMAs of sub-tile
-// i+1 run while the softmax warps process sub-tile i.  The same K-major SW128
-// smem tile of Q_i / dO_i serves as the K-major B of the first products and
-// the MN-major B of the accumulations (64-wide d chunks at LBO = 8 KB, 8-row
-// query groups at SBO = 1 KB).
+//   dV  += P^T dO_i         TMEM [256,384)        (A = P^T from TMEM, dO_i as MN-major B)
+//   dK  += dS^T Q_i         TMEM [384,512)        (A = dS^T from TMEM, Q_i as MN-major B)
+// The softmax warps write P^T / dS^T as bf16 pairs back over the S^T / dP^T
+// columns they read (each warp only over its own), so they never touch
+// shared memory.  Q_i / dO_i (+ their lse / D slices, bulk-copied on the same
+// barrier) are a 4-deep ring and S / dP double-buffered in TMEM, so the MMAs
+// of sub-tile i+1 run while the softmax warps process sub-tile i.  The same
+// K-major SW128 smem tile of Q_i / dO_i serves as the K-major B of the first
+// products and the MN-major B of the accumulations (64-wide d chunks at LBO =
+// 8 KB, 8-row query groups at SBO = 1 KB).  A 128-query variant (M = N = 128
+// everywhere, single-buffered S / dP) measured slower: 232 vs 206 us.
 constexpr int kBQ2 = 64;  // query rows per backward sub-tile
 constexpr int kThreadsB = 320;  // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 struct AttnBwdParams {
@@ -552,14 +555,13 @@ constexpr int kQTile = kBQ2 * kHd * 2;                 // 16 KB
 constexpr int kBOffK = 0;                              // 32 KB
 constexpr int kBOffV = kTileBytes;                     // 32 KB
 // Q_i / dO_i (and their vector slices) are released only when sub-tile i's
-// accumulation MMAs retire, i.e. after its softmax; three stages keep the
-// next two sub-tiles' loads in flight across that.
-constexpr int kQStages = 3;
-constexpr int kBOffQ = 2 * kTileBytes;                 // 3 x 16 KB
-constexpr int kBOffdO = kBOffQ + kQStages * kQTile;    // 3 x 16 KB
-constexpr int kBOffPT = kBOffdO + kQStages * kQTile;   // 2 x 16 KB (128 keys x 64 q)
-constexpr int kBOffDS = kBOffPT + 2 * kQTile;          // 2 x 16 KB
-constexpr int kBOffVec = kBOffDS + 2 * kQTile;         // 3 x (-lse log2 e [64] | -D/sqrt(d) [64])
+// accumulation MMAs retire, i.e. after its softmax; four stages keep the
+// next sub-tiles' loads in flight across that (P^T / dS^T live in TMEM, so
+// the smem they used to take holds the extra stages).
+constexpr int kQStages = 4;
+constexpr int kBOffQ = 2 * kTileBytes;                 // 4 x 16 KB
+constexpr int kBOffdO = kBOffQ + kQStages * kQTile;    // 4 x 16 KB
+constexpr int kBOffVec = kBOffdO + kQStages * kQTile;  // 4 x (-lse log2 e [64] | -D/sqrt(d) [64])
 constexpr int kBOffBar = kBOffVec + kQStages * 512;
 constexpr size_t kBSmem = size_t(kBOffBar) + 256 + 1024;
 static_assert(kBSmem <= 232448, "attention backward smem budget");
@@ -570,13 +572,11 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kBOffBar);
   uint64_t* kv_full = bar + 0;
   uint64_t* qd_full = bar + 1;   // [kQStages]
-  uint64_t* qd_empty = bar + 4;  // [kQStages]
-  uint64_t* s_full = bar + 7;    // [2]
-  uint64_t* s_free = bar + 9;    // [2]
+  uint64_t* qd_empty = bar + 5;  // [kQStages]
+  uint64_t* s_full = bar + 9;    // [2]
   uint64_t* p_full = bar + 11;   // [2]
-  uint64_t* p_empty = bar + 13;  // [2]
-  uint64_t* acc_done = bar + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* acc_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int kt = blockIdx.z;  // key tile; small kt = most query tiles (launched first)
@@ -593,9 +593,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 8);
       mbar_init(&p_full[i], 8);
-      mbar_init(&p_empty[i], 1);
     }
     mbar_init(acc_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -635,7 +633,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t kIdS = make_idesc(128, 64, 0, 0);    // K/V K-major, Q/dO K-major (N = 64 q)
-      constexpr uint32_t kIdAcc = make_idesc(128, 128, 0, 1); // P^T/dS^T K-major, dO/Q MN-major
+      constexpr uint32_t kIdAcc = make_idesc(128, 128, 0, 1); // A = P^T / dS^T in TMEM, dO/Q MN-major
       const uint32_t sk = smem_u32(smem + kBOffK), sv = smem_u32(smem + kBOffV);
       auto accumulate = [&](int i) {
         const int b = i & 1;
@@ -643,18 +641,16 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
         const int qs = i % kQStages;
         mbar_wait(&p_full[b], ph);
         tc_fence_after();
-        const uint32_t spt = smem_u32(smem + kBOffPT + b * kQTile);
-        const uint32_t sds = smem_u32(smem + kBOffDS + b * kQTile);
         const uint32_t sq = smem_u32(smem + kBOffQ + qs * kQTile);
         const uint32_t sdo = smem_u32(smem + kBOffdO + qs * kQTile);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
-          tc_mma(tmem + 256, smem_desc(spt + kk * 32, 16, 1024), smem_desc(sdo + kk * 2048, 8192, 1024),
-                 kIdAcc, (i > 0 || kk > 0) ? 1u : 0u);
-          tc_mma(tmem + 384, smem_desc(sds + kk * 32, 16, 1024), smem_desc(sq + kk * 2048, 8192, 1024),
-                 kIdAcc, (i > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries (16 per step: 8 packed columns)
+          const uint32_t ac = b * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
+          tc_mma_ts(tmem + 256, tmem + ac, smem_desc(sdo + kk * 2048, 8192, 1024), kIdAcc,
+                    (i > 0 || kk > 0) ? 1u : 0u);
+          tc_mma_ts(tmem + 384, tmem + 64 + ac, smem_desc(sq + kk * 2048, 8192, 1024), kIdAcc,
+                    (i > 0 || kk > 0) ? 1u : 0u);
         }
-        tc_commit(&p_empty[b]);
         tc_commit(&qd_empty[qs]);
       };
       mbar_wait(kv_full, 0);
@@ -663,8 +659,10 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
         const uint32_t ph = (it >> 1) & 1;
         const int qs = it % kQStages;
         mbar_wait(&qd_full[qs], (it / kQStages) & 1);
-        mbar_wait(&s_free[b], ph ^ 1);
+        // region b (S^T / P^T, dP^T / dS^T of it-2) is free: accumulate(it-2)
+        // read it and was issued earlier by this thread (in-order MMAs)
         tc_fence_after();
+        (void)ph;
         const uint32_t sq = smem_u32(smem + kBOffQ + qs * kQTile);
         const uint32_t sdo = smem_u32(smem + kBOffdO + qs * kQTile);
 #pragma unroll
@@ -700,9 +698,6 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
       tmem_ld32_nw(tmem + lane_off + b * 128 + 64 + half * 32, rd);
       tmem_wait_ld32(rs);
       tmem_pin32(rd);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);
       // P^T = 2^(S^T c - lse log2 e), dS^T = P^T (dP^T / sqrt(d) - D / sqrt(d)):
       // two queries per FFMA2/FMUL2; every 4th pair's exp2 on the FMA pipe
       const uint32_t vs = smem_u32(smem + kBOffVec + qs * 512) + half * 128;
@@ -747,22 +742,18 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
       };
       if (masked) body(std::true_type{});
       else body(std::false_type{});
-      mbar_wait(&p_empty[b], ph ^ 1);  // P^T / dS^T buffer b free (MMAs of it-2 retired)
-      const uint32_t pt = smem_u32(smem + kBOffPT + b * kQTile);
-      const uint32_t ds = smem_u32(smem + kBOffDS + b * kQTile);
-      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0 + half * 32);
-#pragma unroll
-      for (int j4 = 0; j4 < 4; ++j4) {
-        const int j8 = half * 4 + j4;
-        const uint32_t off = row * 128 + ((j8 ^ (row & 7)) * 16);
-        sts128(pt + off, make_uint4(ptw[4 * j4], ptw[4 * j4 + 1], ptw[4 * j4 + 2], ptw[4 * j4 + 3]));
-        const uint4 w = make_uint4(dsw[4 * j4], dsw[4 * j4 + 1], dsw[4 * j4 + 2], dsw[4 * j4 + 3]);
-        sts128(ds + off, w);
-        dsg[j4] = w;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // P^T / dS^T (bf16 pairs) over the consumed S^T / dP^T columns this
+      // warp read: the A operands of dV / dK
+      tmem_st16_nw(tmem + lane_off + b * 128 + half * 32, ptw);
+      tmem_st16_nw(tmem + lane_off + b * 128 + 64 + half * 32, dsw);
+      tmem_wait_st();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
+      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0 + half * 32);
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4)
+        dsg[j4] = make_uint4(dsw[4 * j4], dsw[4 * j4 + 1], dsw[4 * j4 + 2], dsw[4 * j4 + 3]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
@@ -792,6 +783,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
+
 
 }  // namespace
 
