@@ -205,22 +205,6 @@ __global__ void __launch_bounds__(kT) layernorm_bwd_kernel(
   }
 }
 
-__global__ void colsum_partial_kernel(const uint16_t* __restrict__ d, int rows, int cols,
-                                      float* __restrict__ part, int chunks) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column vector index
-  if (v * 8 >= cols) return;
-  const int per = (rows + chunks - 1) / chunks;
-  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0; r < r1; ++r) {
-    float f[8];
-    unpack8(reinterpret_cast<const uint4*>(d + int64_t(r) * cols)[v], f);
-    for (int j = 0; j < 8; ++j) acc[j] += f[j];
-  }
-  float4* o = reinterpret_cast<float4*>(part + int64_t(blockIdx.y) * cols + 8 * v);
-  o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-}
 
 __device__ __forceinline__ void write_mode(void* out, int64_t i, float v, int out_bf16, int mode) {
   if (out_bf16) {
@@ -231,14 +215,6 @@ __device__ __forceinline__ void write_mode(void* out, int64_t i, float v, int ou
   }
 }
 
-__global__ void colsum_finalize_kernel(const float* __restrict__ part, int chunks, int cols,
-                                       void* out, int out_bf16, int mode) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float s = 0.f;
-  for (int k = 0; k < chunks; ++k) s += part[int64_t(k) * cols + c];
-  write_mode(out, c, s, out_bf16, mode);
-}
 
 __global__ void grad_write_kernel(const float* __restrict__ src, int64_t n, void* out, int out_bf16,
                                   int mode) {
@@ -247,28 +223,6 @@ __global__ void grad_write_kernel(const float* __restrict__ src, int64_t n, void
     write_mode(out, i, src[i], out_bf16, mode);
 }
 
-// one warp per (z, q) row
-__global__ void softmax_causal_kernel(const float* __restrict__ S, uint16_t* __restrict__ P, int Z,
-                                      int Sq) {
-  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row >= Z * Sq) return;
-  const int q = row % Sq;
-  const float* s = S + int64_t(row) * Sq;
-  uint16_t* p = P + int64_t(row) * Sq;
-  const int n = q + 1;
-  const float kL2E = 1.4426950408889634f;
-  float mx = -INFINITY;
-  for (int k = lane; k < n; k += 32) mx = fmaxf(mx, s[k]);
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.f;
-  for (int k = lane; k < n; k += 32) sum += exp2f((s[k] - mx) * kL2E);
-  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const float inv = 1.f / sum;
-  const int zend = min(Sq, (q / 128 + 1) * 128);
-  for (int k = lane; k < zend; k += 32)
-    p[k] = f32_to_bf16_bits(k < n ? exp2f((s[k] - mx) * kL2E) * inv : 0.f);
-}
 
 // one warp per (token, head)
 // Half a warp per (token, head) row: 16 lanes x 8 bf16 (one uint4 each of dO
@@ -468,76 +422,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
   }
 }
 
-// 32 columns per CTA, 8 warps split the chunk range, smem tree at the end.
-__global__ void __launch_bounds__(256) colsum_finalize_par_kernel(const float* __restrict__ part,
-                                                                 int chunks, int cols, void* out,
-                                                                 int out_bf16, int mode) {
-  __shared__ float red[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
-  const int c = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (c < cols)
-    for (int k = w; k < chunks; k += 8) s += part[int64_t(k) * cols + c];
-  red[w][lane] = s;
-  __syncthreads();
-  if (w == 0 && c < cols) {
-    float t = 0.f;
-    for (int i = 0; i < 8; ++i) t += red[i][lane];
-    write_mode(out, c, t, out_bf16, mode);
-  }
-}
 
-// Causal softmax, one warp per row, the whole (<= 2048-long) valid prefix
-// held in registers: one read of S, one write of P.
-__global__ void softmax_causal_reg_kernel(const float* __restrict__ S, uint16_t* __restrict__ P,
-                                          int Z, int Sq) {
-  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row >= Z * Sq) return;
-  const int q = row % Sq;
-  const float4* s4 = reinterpret_cast<const float4*>(S + int64_t(row) * Sq);
-  uint2* p4 = reinterpret_cast<uint2*>(P + int64_t(row) * Sq);
-  const int n = q + 1;
-  const int nchunk = (n + 127) / 128;  // 128 elements per warp pass (float4 per lane)
-  const float kL2E = 1.4426950408889634f;
-  float v[16][4];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    if (c < nchunk) {
-      const int k0 = c * 128 + lane * 4;
-      const float4 t = s4[c * 32 + lane];
-      v[c][0] = k0 + 0 < n ? t.x : -INFINITY;
-      v[c][1] = k0 + 1 < n ? t.y : -INFINITY;
-      v[c][2] = k0 + 2 < n ? t.z : -INFINITY;
-      v[c][3] = k0 + 3 < n ? t.w : -INFINITY;
-      mx = fmaxf(mx, fmaxf(fmaxf(v[c][0], v[c][1]), fmaxf(v[c][2], v[c][3])));
-    }
-  }
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.f;
-#pragma unroll
-  for (int c = 0; c < 16; ++c)
-    if (c < nchunk)
-      for (int j = 0; j < 4; ++j) {
-        v[c][j] = exp2f((v[c][j] - mx) * kL2E);  // exp2(-inf) = 0 for masked
-        sum += v[c][j];
-      }
-  sum = warp_sum(sum);
-  const float inv = 1.f / sum;
-  const int zend = min(Sq, (q / 128 + 1) * 128);  // zero-fill to the 128-row tile edge
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    if (c * 128 < zend) {
-      float o[4];
-      for (int j = 0; j < 4; ++j) o[j] = c < nchunk ? v[c][j] * inv : 0.f;
-      uint2 w;
-      w.x = uint32_t(f32_to_bf16_bits(o[0])) | (uint32_t(f32_to_bf16_bits(o[1])) << 16);
-      w.y = uint32_t(f32_to_bf16_bits(o[2])) | (uint32_t(f32_to_bf16_bits(o[3])) << 16);
-      p4[c * 32 + lane] = w;
-    }
-  }
-}
 
 // ---- LayerNorm / column reductions for h a multiple of 256 -------------------
 // NVL = h / 256: 16-byte vectors per lane, so every array below is sized at
@@ -778,12 +663,6 @@ void colsum_finalize(const float* part, int chunks, int cols, void* out, int out
 }
 void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s) {
   grad_write_kernel<<<4 * kNumSMs, 256, 0, s>>>(src, n, out, out_bf16, mode);
-  HZP_LAUNCH_CHECK();
-}
-void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s) {
-  const int rows = Z * Sq;
-  if (Sq <= 2048 && Sq % 128 == 0) softmax_causal_reg_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
-  else softmax_causal_kernel<<<(rows + 7) / 8, 256, 0, s>>>(S, P, Z, Sq);
   HZP_LAUNCH_CHECK();
 }
 void attn_rowdot(const uint16_t* dO, const uint16_t* O, const float* lse, float* V, int b, int nh, int S,

@@ -33,9 +33,6 @@ void colsum_finalize(const float* part, int chunks, int cols, void* out, int out
 // out[i] (mode, dtype) <- src[i] (fp32 scratch -> gradient target)
 void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s);
 
-// Causal softmax of fp32 scores S[z][q][k] (already scaled): P = exp(S - lse)
-// for k <= q, 0 for q < k < 128*ceil((q+1)/128); P bf16, same layout.
-void softmax_causal(const float* S, uint16_t* P, int Z, int Sq, cudaStream_t s);
 // Per-query vectors of the attention backward, V [2][z][q]:
 //   V[0] = -scale * sum_d dO[b, q, head, d] * O[b, q, head, d]   (-D / sqrt(d))
 //   V[1] = -log2(e) * lse[z][q]
