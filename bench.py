@@ -225,6 +225,32 @@ def collectives(eng, N, local, max_over_ranks, barrier, iters=5):
     return out
 
 
+def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, iters=3):
+    """Fused Z1 stage (replica pull-reduce + Adam + bf16 push) timed through
+    hzp_z1_adam_step on the step's own state (after the timed region), vs
+    max(remote / NVLink, local / HBM) with SURVEY §8(d)'s bytes per element
+    of the rank's Z1 chunk: 4R grad (R = dp/z2 replicas; remote R-1 or R)
+    + 12 read + 12 write (master, m, v) + 2k bf16 pushes (k = z1/z3 owners).
+    Flat ZeRO-3 (z1 = z2 = z3 = dp): R = 1, k = 1 -> 30 B/elem, all local."""
+    import torch
+    st = torch.cuda.ExternalStream(eng.stream(0), device=f"cuda:{local}")
+    eng.z1_adam_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(iters):
+        eng.z1_adam_step()
+    e1.record(st)
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / iters)
+    nbytes = 30 * eng.s1
+    gbps = nbytes / (ms / 1e3) / 1e9
+    return {"ms": round(ms, 3), "elems": int(eng.s1), "bytes_per_elem": 30, "GBps": round(gbps, 1),
+            "bound": "hbm", "peak_GBps": hbm_gbps, "frac": round(gbps / hbm_gbps, 3),
+            "note": "includes the two device-wide barriers around the kernel (no-op at N=1)"}
+
+
 def run_hzp(args):
     import numpy as np
     import torch
@@ -336,6 +362,7 @@ def run_hzp(args):
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}
     colls = collectives(eng, N, local, max_over_ranks, barrier) if N > 1 else None
+    z1 = z1_roofline(eng, N, local, max_over_ranks, barrier, hbm)
     line = None
     if rank == 0:
         cb = cpu_reference(2, 0, "cpu_baseline") if not args.no_cpu_baseline else None
@@ -352,7 +379,7 @@ def run_hzp(args):
                            "parallelism": f"dp{N} (z1=z2=z3={N})", "prelaunch_depth": 2,
                            "rs_slots": 1, "l2": "activation working set >> 126 MB L2 (no flush needed)"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
-                "roofline": roof, "exposed_comm": exposed, "collectives": colls,
+                "roofline": roof, "exposed_comm": exposed, "collectives": colls, "z1_adam": z1,
                 "cpu_baseline": ({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
                                  if cb else None)}
         print(json.dumps(line), flush=True)
