@@ -45,6 +45,12 @@ struct GptBuffers {
   int cur = 0;
   uint16_t *dln = nullptr, *dqkv = nullptr, *dattn = nullptr, *dfc1 = nullptr, *dxm = nullptr;
   float* part = nullptr;       // column-sum partials
+  // weight gradients of a block run on a side stream (they are leaves of the
+  // backward DAG), so they fill the SMs the dgrad chain's tail waves leave
+  // idle; own column-sum partials, fork/join by events.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[8] = {};
+  float* part_side = nullptr;
   float* emb = nullptr;        // fp32 scratch for the embedding gradient [V*h + S*h]
   float* loss = nullptr;
   const int* tokens = nullptr;  // current microbatch
@@ -158,6 +164,9 @@ class GptModel final : public Model {
     B->dfc1 = bf(T_ * f_);
     B->dxm = bf(T_ * h_);
     B->part = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
+    B->part_side = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
+    HZP_CUDA(cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking));
+    for (auto& e : B->ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     B->emb = f32(int64_t(V_) * h_ + int64_t(S_) * h_);
     B->loss = f32(1);
     HZP_CUDA(cudaMemset(B->loss, 0, 4));
@@ -175,8 +184,11 @@ class GptModel final : public Model {
     for (void* q : {(void*)B->lnf, (void*)B->muf, (void*)B->rsf, (void*)B->logits, (void*)B->S,
                     (void*)B->dS, (void*)B->D, (void*)B->dx[0], (void*)B->dx[1], (void*)B->dln,
                     (void*)B->dqkv, (void*)B->dattn, (void*)B->dfc1, (void*)B->dxm, (void*)B->part,
+                    (void*)B->part_side,
                     (void*)B->emb, (void*)B->loss})
       cudaFree(q);
+    for (auto e : B->ev) cudaEventDestroy(e);
+    if (B->side) cudaStreamDestroy(B->side);
     delete B;
   }
   void begin_step(void* p, cudaStream_t s) override {
@@ -195,6 +207,7 @@ class GptModel final : public Model {
   // dW[N, K] = dy[T, N]^T x[T, K] -> grad target (+ bias grad colsum(dy) if db_off >= 0)
   void linear_wgrad(const uint16_t* dy, const uint16_t* x, int N, int K, const GradTarget& g,
                     int64_t w_off, int64_t b_off, GptBuffers* B, cudaStream_t s) const {
+    float* part = s == B->side ? B->part_side : B->part;
     GemmShape sh{N, K, int(T_), N, K, 1, 1};
     Epilogue e;
     e.mode = g.mode;
@@ -202,8 +215,8 @@ class GptModel final : public Model {
     e.ldc = K;
     gemm_tc_bf16(dy, x, gptr(g, w_off), sh, e, s);
     if (b_off >= 0) {
-      colsum_partial(dy, int(T_), N, B->part, kChunks, s);
-      colsum_finalize(B->part, kChunks, N, gptr(g, b_off), g.bf16, g.mode, s);
+      colsum_partial(dy, int(T_), N, part, kChunks, s);
+      colsum_finalize(part, kChunks, N, gptr(g, b_off), g.bf16, g.mode, s);
     }
   }
   // dx[T, K] = dy[T, N] W[N, K]   (+ epilogue)
@@ -318,8 +331,16 @@ class GptModel final : public Model {
     const int64_t h3 = 3 * int64_t(h_);
     uint16_t* dout = B->dx[B->cur];
     uint16_t* din = B->dx[B->cur ^ 1];
+    int nev = 0;
+    auto to_side = [&] {  // everything issued on s so far is visible to the side stream
+      HZP_CUDA(cudaEventRecord(B->ev[nev], s));
+      HZP_CUDA(cudaStreamWaitEvent(B->side, B->ev[nev], 0));
+      ++nev;
+    };
+    cudaStream_t ws = B->side;
     // MLP
-    linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, o.b_fc2, B, s);
+    to_side();
+    linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, o.b_fc2, B, ws);
     {
       Epilogue e;
       e.act = kActGeluGrad;
@@ -327,7 +348,8 @@ class GptModel final : public Model {
       e.ldaux = f_;
       linear_dgrad(dout, W + o.w_fc2, B->dfc1, h_, f_, e, s);
     }
-    linear_wgrad(B->dfc1, a.ln2, f_, h_, g, o.w_fc1, o.b_fc1, B, s);
+    to_side();
+    linear_wgrad(B->dfc1, a.ln2, f_, h_, g, o.w_fc1, o.b_fc1, B, ws);
     {
       Epilogue e;
       linear_dgrad(B->dfc1, W + o.w_fc1, B->dln, f_, h_, e, s);
@@ -336,7 +358,8 @@ class GptModel final : public Model {
                   h_, s);
     ln_param_grads(B, g, o.ln2_g, o.ln2_b, s);
     // attention output projection
-    linear_wgrad(B->dxm, a.attn, h_, h_, g, o.w_o, o.b_o, B, s);
+    to_side();
+    linear_wgrad(B->dxm, a.attn, h_, h_, g, o.w_o, o.b_o, B, ws);
     {
       Epilogue e;
       linear_dgrad(B->dxm, W + o.w_o, B->dattn, h_, h_, e, s);
@@ -345,8 +368,9 @@ class GptModel final : public Model {
     // lse, dS^T emitted), then dQ = dS K as one transposed causal product
     attn_rowdot(B->dattn, a.attn, a.lse, B->D, b_, nh_, S_, hd_, s);
     attention_bwd_tc(a.qkv, B->dattn, a.lse, B->D, B->dqkv, B->dS, b_, nh_, S_, h_, s);
-    attention_dq(a.qkv, B->dS, B->dqkv, b_, nh_, S_, h_, s);  // dQ = dS K (transposed product)
-    linear_wgrad(B->dqkv, a.ln1, int(h3), h_, g, o.w_qkv, o.b_qkv, B, s);
+    attention_dq(a.qkv, B->dS, B->dqkv, b_, nh_, S_, h_, s);  // dQ = dS K
+    to_side();
+    linear_wgrad(B->dqkv, a.ln1, int(h3), h_, g, o.w_qkv, o.b_qkv, B, ws);
     {
       Epilogue e;
       linear_dgrad(B->dqkv, W + o.w_qkv, B->dln, int(h3), h_, e, s);
@@ -354,6 +378,10 @@ class GptModel final : public Model {
     layernorm_bwd(B->dln, B->x[l], W + o.ln1_g, a.mu1, a.rs1, B->dxm, din, B->part, kChunks,
                   int(T_), h_, s);
     ln_param_grads(B, g, o.ln1_g, o.ln1_b, s);
+    // join: the block's task ends when its weight gradients are written (the
+    // RS / next block reuse the buffers they read)
+    HZP_CUDA(cudaEventRecord(B->ev[nev], ws));
+    HZP_CUDA(cudaStreamWaitEvent(s, B->ev[nev], 0));
     B->cur ^= 1;
   }
 
