@@ -309,14 +309,18 @@ class GptModel final : public Model {
   void bwd(void* p, int l, const void* params, const GradTarget& g, cudaStream_t s) override {
     auto* B = static_cast<GptBuffers*>(p);
     const auto* W = static_cast<const uint16_t*>(params);
-    if (l == L_ + 1) {  // head: dlogits already in B->logits
-      linear_wgrad(B->logits, B->lnf, V_, h_, g, 2 * h_, -1, B, s);
+    if (l == L_ + 1) {  // head: dlogits already in B->logits; dW_head on the side stream
+      HZP_CUDA(cudaEventRecord(B->ev[0], s));
+      HZP_CUDA(cudaStreamWaitEvent(B->side, B->ev[0], 0));
+      linear_wgrad(B->logits, B->lnf, V_, h_, g, 2 * h_, -1, B, B->side);
       Epilogue e;
       linear_dgrad(B->logits, W + 2 * h_, B->dln, V_, h_, e, s);
       B->cur = 0;
       layernorm_bwd(B->dln, B->x[l], W, B->muf, B->rsf, nullptr, B->dx[0], B->part, kChunks,
                     int(T_), h_, s);
       ln_param_grads(B, g, 0, h_, s);
+      HZP_CUDA(cudaEventRecord(B->ev[1], B->side));
+      HZP_CUDA(cudaStreamWaitEvent(s, B->ev[1], 0));
       return;
     }
     if (l == 0) {
