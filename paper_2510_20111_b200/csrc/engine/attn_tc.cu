@@ -1,19 +1,19 @@
-// Fused causal attention forward on tcgen05 (sm_100a), head dim 128.
+// Fused causal attention (head dim 128) on tcgen05 (sm_100a).
 //
-// One CTA per (128-query tile, head, sequence); 6 warps:
-//   warp 0    TMA producer: Q once, then K_j / V_j tiles (128 keys) into a
-//             2-deep smem ring (128B swizzle; V as MN-major 64x64 boxes)
-//   warp 1    TMEM owner + MMA issuer (one thread):
-//               S_j = Q K_j^T     -> TMEM S[j%2]   (M=128, N=128, K=128)
-//               O  += P_j V_j     -> TMEM O        (M=128, N=128, K=128)
-//             S_{j+1} is issued before O += P_j V_j so the softmax of the
-//             next tile overlaps the PV product of this one
-//   warps 2-5 softmax, one thread per query row (its TMEM lane): online
-//             max / sum in the exp2 domain, causal mask on the diagonal tile,
-//             P (bf16) written to smem as the K-major A operand of the PV MMA
-//             (and to global memory for the GEMM-based backward), O rescaled
-//             in TMEM when the running max moves, final O / l and lse out.
-// The S tile never leaves the SM: no fp32 score matrix in HBM.
+// Forward, attn_fwd2_kernel (used whenever the query-tile count is even; the
+// single-tile attn_fwd_kernel below covers odd counts and the optional P
+// output): one CTA per (head, sequence, pair of 128-query tiles), 10 warps:
+//   warp 0    TMA producer: both Q tiles once, then K_j (3-deep ring) and V_j
+//             (2-deep, MN-major 64x64 boxes), 128 keys per tile
+//   warp 1    TMEM owner + MMA issuer (one thread), ping-pong per query tile g:
+//               S_g = Q_g K_j^T   -> TMEM [g*128, +128)    (M=N=K=128)
+//               O_g += P_g V_j    -> TMEM [256 + g*128, +128), A = P_g from TMEM
+//   warps 2-9 two softmax warpgroups (one per query tile), one thread per
+//             query row (its TMEM lane): row max over S, P = 2^(s c - m) with
+//             FFMA2 and 3/8 of the exp2 on the FMA pipe, P (bf16) written back
+//             over the consumed S columns, lazy O rescale, final O / l and lse.
+// Neither S nor P ever leaves the SM.  The backward (attn_bwd_kernel, further
+// down) works per 128-key tile with P^T / dS^T kept in TMEM the same way.
 #include <cmath>
 #include <type_traits>
 
@@ -656,13 +656,11 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
       mbar_wait(kv_full, 0);
       for (int it = 0; it < nit; ++it) {
         const int b = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
         const int qs = it % kQStages;
         mbar_wait(&qd_full[qs], (it / kQStages) & 1);
         // region b (S^T / P^T, dP^T / dS^T of it-2) is free: accumulate(it-2)
         // read it and was issued earlier by this thread (in-order MMAs)
         tc_fence_after();
-        (void)ph;
         const uint32_t sq = smem_u32(smem + kBOffQ + qs * kQTile);
         const uint32_t sdo = smem_u32(smem + kBOffdO + qs * kQTile);
 #pragma unroll

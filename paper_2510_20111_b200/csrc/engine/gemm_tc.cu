@@ -1,14 +1,16 @@
 // tcgen05 GEMM for sm_100a: C = epilogue(A · Bᵀ), bf16 operands, fp32
 // accumulation in TMEM.
 //
-// Structure (one persistent CTA per SM, 6 warps, warp-specialised):
-//   warp 0  : TMA producer — one elected lane streams A/B tiles (128B swizzle)
-//             into a `kStages`-deep shared-memory ring (mbarrier full/empty).
-//   warp 1  : TMEM allocator + MMA issuer — one elected lane issues
-//             tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) and
-//             commits completion to the smem ring / accumulator barriers.
-//   warps 2-5: epilogue — tcgen05.ld 32x32b.x32 from TMEM, bias/activation/
-//             accumulate, vectorised global stores.
+// Structure (persistent, one CTA per SM, 10 warps, warp-specialised):
+//   warp 0   : TMA producer — one lane streams A/B k-blocks (128B swizzle)
+//              into a STAGES-deep shared-memory ring (mbarrier full/empty).
+//   warp 1   : TMEM allocator + MMA issuer — one lane issues tcgen05.mma.
+//              Products with >= 2 M tiles run on CTA pairs (cluster of 2,
+//              cta_group::2, M = 256 per MMA, each CTA staging its A rows and
+//              half of B); the rest on single CTAs (cta_group::1, M = 128).
+//   warps 2-9: epilogue — two warps per TMEM lane quarter, alternating 32-column
+//              chunks: tcgen05.ld, bias / activation / residual / accumulate,
+//              swizzled smem staging, TMA bulk tensor store (or reduce-add).
 // Two TMEM accumulators (2 x BN fp32 columns) let the epilogue of tile i
 // overlap the MMAs of tile i+1.
 //
