@@ -420,17 +420,21 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
       // [16c, 16c+16), already consumed.
       const bool diag = j == nj - 1;
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      {  // pass 1: all 128 scores in flight at once, one wait
+        uint32_t r[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+        for (int c = 0; c < 4; ++c) tmem_ld32_nw(tmem + lane_off + s_col + c * 32, r + 32 * c);
+        tmem_wait_ld32(r);
+        tmem_pin32(r + 32);
+        tmem_pin32(r + 64);
+        tmem_pin32(r + 96);
         if (diag) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i > row) r[i] = 0xff800000u;  // -inf
+          for (int i = 0; i < 128; ++i)
+            if (i > row) r[i] = 0xff800000u;  // -inf
         }
 #pragma unroll
-        for (int i = 0; i < 32; i += 8)
+        for (int i = 0; i < 128; i += 8)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             mx4[k] = fmaxf(mx4[k], fmaxf(__uint_as_float(r[i + 2 * k]), __uint_as_float(r[i + 2 * k + 1])));
@@ -439,14 +443,19 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
       const bool bump = mx > m + 8.f;
       const float mref = bump ? mx : m;
       const float corr = bump ? exp2_fast(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
-      // FFMA2 per pair; 3 of every 8 pairs' exp2 on the FMA pipe so MUFU
-      // (16/clk/SM) stops bounding the tile
+      // pass 2: P = 2^(s c - mref), FFMA2 per pair; 3 of every 8 pairs' exp2
+      // on the FMA pipe so MUFU (16/clk/SM) stops bounding the tile.  Chunk
+      // c+1's scores are loaded while chunk c is exponentiated.
       const uint64_t nm2 = f2_pack(-mref, -mref);
       uint64_t acc[4] = {0, 0, 0, 0};
+      uint32_t rb[2][32];
+      tmem_ld32_nw(tmem + lane_off + s_col, rb[0]);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t r[32], pw[16];
-        tmem_ld32(tmem + lane_off + s_col + c * 32, r);
+        uint32_t* r = rb[c & 1];
+        tmem_wait_ld32(r);
+        if (c + 1 < 4) tmem_ld32_nw(tmem + lane_off + s_col + (c + 1) * 32, rb[(c + 1) & 1]);
+        uint32_t pw[16];
         if (diag) {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
