@@ -33,6 +33,18 @@ UNIT = "tokens/s"
 
 # BASELINE.json configs[1] dims (SURVEY App. A-5 proposal; untied LM head)
 GPT13B = dict(layers=24, hidden=2048, heads=16, ffn=8192, vocab=50304, seq=2048)
+# BASELINE configs[2]: 7B dense decoder, hierarchical ZeRO-3 group 4 x ZeRO-1 group 2
+GPT7B = dict(layers=32, hidden=4096, heads=32, ffn=16384, vocab=50304, seq=2048)
+
+
+def layout_for(model: str, N: int):
+    """(z1, z2, z3) per BASELINE config: 1.3B flat ZeRO-3 over all ranks; 7B
+    hierarchical with the ZeRO-1 group twice the ZeRO-3 group (4 x 2 at 8 GPUs,
+    N/2 x 2 below, flat at N = 1)."""
+    if model == "7b" and N > 1:
+        z3 = min(4, N // 2) if N >= 2 else 1
+        return N, z3, z3
+    return N, N, N
 
 
 def peaks():
@@ -106,7 +118,7 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_reference(steps: int, warmup: int, label: str):
+def cpu_reference(steps: int, warmup: int, label: str, c=None):
     """The reference's train_step_hzp<float> (mixed) on the host, 1 thread.
 
     The reference has no transformer; the bounded sample is its own MLP shaped
@@ -140,7 +152,7 @@ def cpu_reference(steps: int, warmup: int, label: str):
         sec = wall / max(1, steps)
     sample_tok = mbs * rows
     sample_flops_tok = 6.0 * (dims[0] * dims[1] + dims[1] * dims[2])
-    c = GPT13B
+    c = c or GPT13B
     model_flops_tok = 6.0 * (c["layers"] * (4 * c["hidden"] ** 2 + 2 * c["hidden"] * c["ffn"]) +
                              c["vocab"] * c["hidden"])
     raw = sample_tok / sec
@@ -148,16 +160,16 @@ def cpu_reference(steps: int, warmup: int, label: str):
     return {"value": equiv, "unit": UNIT, "cores": 1, "kind": kind,
             "sample": (f"{label}: train_step_hzp<float> mixed, MLP{dims} dp=1, {mbs}x{rows} rows/step, "
                        f"{sec:.3f} s/step = {raw:.2f} sample tokens/s; scaled by dense FLOPs/token "
-                       f"{sample_flops_tok/1e6:.0f}M -> {model_flops_tok/1e9:.2f}G to 1.3B-model tokens/s; "
+                       f"{sample_flops_tok/1e6:.0f}M -> {model_flops_tok/1e9:.2f}G to model tokens/s; "
                        f"{wall:.1f} s wall, 1 thread (the reference is single-threaded)")}
 
 
 def _ref_worker(a):
-    steps, warmup = a
-    return cpu_reference(steps, warmup, "reference arm worker")
+    steps, warmup, c = a
+    return cpu_reference(steps, warmup, "reference arm worker", c)
 
 
-def cpu_reference_parallel(steps: int, warmup: int):
+def cpu_reference_parallel(steps: int, warmup: int, c=None):
     """The reference arm on all the host cores it can use: the reference is
     single-threaded, so P independent processes each run the same bounded
     sample concurrently (data-parallel replicas on the host) and the
@@ -171,9 +183,9 @@ def cpu_reference_parallel(steps: int, warmup: int):
         pass
     cores = max(1, min(cores, 64))
     if cores == 1:
-        return cpu_reference(steps, warmup, "reference arm")
+        return cpu_reference(steps, warmup, "reference arm", c)
     with mp.get_context("fork").Pool(cores) as pool:
-        res = pool.map(_ref_worker, [(steps, warmup)] * cores)
+        res = pool.map(_ref_worker, [(steps, warmup, c)] * cores)
     total = sum(r["value"] for r in res)
     r0 = res[0]
     return {"value": total, "unit": r0["unit"], "cores": cores, "kind": r0["kind"],
@@ -186,14 +198,14 @@ def run_reference(args):
     if rank != 0:
         return 0
     steps = max(1, min(args.steps, 10))
-    cb = cpu_reference_parallel(steps, min(args.warmup, 1))
-    c = GPT13B
+    c = GPT7B if args.model == "7b" else GPT13B
+    cb = cpu_reference_parallel(steps, min(args.warmup, 1), c)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "reference CPU train_step_hzp (MLP sample, 1.3B-equivalent tokens)",
-                       "model": "gpt-1.3b-class", "seq_len": c["seq"], "parallelism": f"dp{args.gpus}"},
+            "config": {"workload": f"reference CPU train_step_hzp (MLP sample, {args.model}-equivalent tokens)",
+                       "model": f"gpt-{args.model}-class", "seq_len": c["seq"], "parallelism": f"dp{args.gpus}"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -204,7 +216,7 @@ def run_reference(args):
 NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU
 
 
-def collectives(eng, N, local, max_over_ranks, barrier, iters=5):
+def collectives(eng, N, local, max_over_ranks, barrier, z2, z3, iters=5):
     """AG / RS bus bandwidth of one 1.3B transformer layer (the step's own
     collective, through the ctx: copy-engine NVLink leg by default) and an NCCL
     comparator on the same bytes.  busbw = (N-1)/N x layer bytes / time
@@ -235,10 +247,13 @@ def collectives(eng, N, local, max_over_ranks, barrier, iters=5):
         e1.synchronize()
         return max_over_ranks(e0.elapsed_time(e1) / iters)
 
-    for name, fn, sid in (("ag", lambda: eng.ag_layer(1, 0), 1), ("rs", lambda: eng.rs_layer(1, 0), 2)):
+    for name, fn, sid, g in (("ag", lambda: eng.ag_layer(1, 0), 1, z3), ("rs", lambda: eng.rs_layer(1, 0), 2, z2)):
+        if g <= 1:  # z3 = 1: layers read the shard in place; z2 = 1: RS fused into wgrad
+            out[name] = None
+            continue
         ms = timed(fn, eng.stream(sid))
-        bw = (N - 1) / N * nbytes / (ms / 1e3) / 1e9
-        out[name] = {"ms": round(ms, 4), "busbw_GBps": round(bw, 1), "frac": round(bw / NVLINK_GBPS, 3)}
+        bw = (g - 1) / g * nbytes / (ms / 1e3) / 1e9
+        out[name] = {"group": g, "ms": round(ms, 4), "busbw_GBps": round(bw, 1), "frac": round(bw / NVLINK_GBPS, 3)}
     try:  # NCCL comparator (setup only; never on the step's data path)
         g = dist.new_group(backend="nccl")
         full = torch.empty(n - n % N, dtype=torch.bfloat16, device=f"cuda:{local}")
@@ -254,7 +269,7 @@ def collectives(eng, N, local, max_over_ranks, barrier, iters=5):
     return out
 
 
-def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, iters=3):
+def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, z1=1, z2=1, z3=1, iters=3):
     """Fused Z1 stage (replica pull-reduce + Adam + bf16 push) timed through
     hzp_z1_adam_step on the step's own state (after the timed region), vs
     max(remote / NVLink, local / HBM) with SURVEY §8(d)'s bytes per element
@@ -273,10 +288,17 @@ def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, iters=3):
     e1.record(st)
     e1.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / iters)
-    nbytes = 30 * eng.s1
-    gbps = nbytes / (ms / 1e3) / 1e9
-    return {"ms": round(ms, 3), "elems": int(eng.s1), "bytes_per_elem": 30, "GBps": round(gbps, 1),
-            "bound": "hbm", "peak_GBps": hbm_gbps, "frac": round(gbps / hbm_gbps, 3),
+    R, k = max(1, N // z2), max(1, z1 // z3)
+    per = 4 * R + 24 + 2 * k
+    remote = 4 * (R - 1) + 2 * (k - 1)  # at least R-1 replica reads and k-1 owner pushes cross NVLink
+    t_hbm = per * eng.s1 / (hbm_gbps * 1e9)
+    t_nvl = remote * eng.s1 / (NVLINK_GBPS * 1e9)
+    bound = "nvlink" if t_nvl > t_hbm else "hbm"
+    floor_ms = max(t_hbm, t_nvl) * 1e3
+    return {"ms": round(ms, 3), "elems": int(eng.s1), "replicas": R, "owners": k, "bytes_per_elem": per,
+            "remote_bytes_per_elem": remote, "GBps": round(per * eng.s1 / (ms / 1e3) / 1e9, 1),
+            "bound": bound, "roofline_ms": round(floor_ms, 3), "frac": round(floor_ms / ms, 3),
+            "peak_GBps": {"hbm": hbm_gbps, "nvlink": NVLINK_GBPS},
             "note": "includes the two device-wide barriers around the kernel (no-op at N=1)"}
 
 
@@ -293,12 +315,13 @@ def run_hzp(args):
         dist.init_process_group("gloo", init_method="env://")
     torch.cuda.set_device(local)
     N = world
-    c = GPT13B
+    c = GPT7B if args.model == "7b" else GPT13B
+    z1, z2, z3 = layout_for(args.model, N)
     mb, nmb = args.batch, args.microbatches
     cfg = EngineConfig(model=1, precision=1, gpt_layers=c["layers"], gpt_hidden=c["hidden"],
                        gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
                        gpt_seq=c["seq"], batch=mb, num_microbatches=nmb,
-                       par=ParallelConfig(dp=N, z1=N, z2=N, z3=N), prelaunch_depth=2, rs_slots=1,
+                       par=ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3), prelaunch_depth=2, rs_slots=1,
                        device=local, my_rank=rank if N > 1 else 0)
     eng = HzpEngine(cfg)
     if N > 1:
@@ -390,25 +413,28 @@ def run_hzp(args):
                "frac": round(idle / mk, 4) if mk else None,
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}
-    colls = collectives(eng, N, local, max_over_ranks, barrier) if N > 1 else None
-    z1 = z1_roofline(eng, N, local, max_over_ranks, barrier, hbm)
+    colls = collectives(eng, N, local, max_over_ranks, barrier, z2, z3) if N > 1 else None
+    z1r = z1_roofline(eng, N, local, max_over_ranks, barrier, hbm, z1, z2, z3)
     line = None
     if rank == 0:
-        cb = cpu_reference(2, 0, "cpu_baseline") if (N == 1 and not args.no_cpu_baseline) else None
+        cb = cpu_reference(2, 0, "cpu_baseline", c) if (N == 1 and not args.no_cpu_baseline) else None
         clocks = clk.summary()
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": N,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (uniform random token ids; hash-uniform init weights)",
-                "config": {"workload": "BASELINE configs[1]: 1.3B-class GPT decoder, flat ZeRO-3",
-                           "model": "gpt-1.3b-class (L24 h2048 16 heads ffn8192 vocab50304 untied head)",
+                "config": {"workload": ("BASELINE configs[2]: 7B-class GPT decoder, hierarchical ZeRO"
+                                        if args.model == "7b" else
+                                        "BASELINE configs[1]: 1.3B-class GPT decoder, flat ZeRO-3"),
+                           "model": (f"gpt-{args.model}-class (L{c['layers']} h{c['hidden']} {c['heads']} heads "
+                                     f"ffn{c['ffn']} vocab{c['vocab']} untied head)"),
                            "params": eng.P, "global_batch": N * mb * nmb, "seq_len": c["seq"],
                            "micro_batch": mb, "num_microbatches": nmb,
                            "tokens_per_step": N * tokens_per_step,
-                           "parallelism": f"dp{N} (z1=z2=z3={N})", "prelaunch_depth": 2,
+                           "parallelism": f"dp{N} (z1={z1}, z2={z2}, z3={z3})", "prelaunch_depth": 2,
                            "rs_slots": 1, "l2": "activation working set >> 126 MB L2 (no flush needed)"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
-                "roofline": roof, "exposed_comm": exposed, "collectives": colls, "z1_adam": z1,
+                "roofline": roof, "exposed_comm": exposed, "collectives": colls, "z1_adam": z1r,
                 "cpu_baseline": ({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
                                  if cb else None)}
         print(json.dumps(line), flush=True)
@@ -427,6 +453,8 @@ def main():
     ap.add_argument("--impl", default="hzp", choices=["hzp", "reference"])
     ap.add_argument("--batch", type=int, default=4, help="sequences per microbatch per GPU")
     ap.add_argument("--microbatches", type=int, default=2)
+    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b"],
+                    help="BASELINE configs[1] (default, the headline) or configs[2]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
