@@ -12,6 +12,9 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 CFG = dict(layers=2, hidden=256, heads=2, ffn=1024, vocab=512, seq=256, batch=2)
+# the 1.3B block width: CTA-pair GEMMs (incl. split tail waves), the h = 2048
+# register-resident LayerNorm kernels, two-tile attention, bias column sums
+CFG_WIDE = dict(layers=1, hidden=2048, heads=16, ffn=8192, vocab=1024, seq=512, batch=2)
 
 
 def layout(c):
@@ -87,8 +90,8 @@ def _bf16_bits(x):
             ((np.ascontiguousarray(x, np.float32).view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
 
 
-def test_gpt_gradient_matches_torch(gpu):
-    c = CFG
+@pytest.mark.parametrize("c", [CFG, CFG_WIDE], ids=["small", "wide"])
+def test_gpt_gradient_matches_torch(gpu, c):
     eng = _engine(c)
     master = init_params(c)
     work = _bf16_bits(master)
