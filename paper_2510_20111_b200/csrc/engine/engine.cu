@@ -172,6 +172,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   if (const char* c = std::getenv("HZP_COMM_CTAS")) comm_ctas = std::max(1, std::atoi(c));  // tuning knob
   if (const char* c = std::getenv("HZP_AG_CE")) ag_ce = std::atoi(c) != 0;
   if (const char* c = std::getenv("HZP_RS_CE")) rs_ce = std::atoi(c) != 0;
+  if (const char* c = std::getenv("HZP_Z1_CE")) z1_ce = std::atoi(c) != 0;
   build_tiles();
 }
 
@@ -192,6 +193,9 @@ Engine::~Engine() {
   cudaFree(dtable);
   for (auto d : dtable_staged) cudaFree(d);
   for (auto e : rs_ev) cudaEventDestroy(e);
+  for (auto& ch : z1_chunks) cudaFree(ch.table);
+  for (auto p : z1_stage) cudaFree(p);
+  if (z1_copy_stream) cudaStreamDestroy(z1_copy_stream);
   if (rs_red_stream) cudaStreamDestroy(rs_red_stream);
   for (auto p : rs_stage) cudaFree(p);
   cudaFree(dtiles);
@@ -258,7 +262,65 @@ void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
   ++launches;
 }
 
+void Engine::setup_z1_staging() {
+  if (emulate || !z1_ce || geom.replicas() <= 1) return;
+  const int t_end = z1_off + z1_n;
+  // chunk boundaries: whole tiles, <= kZ1ChunkElems elements
+  std::vector<std::pair<int, int>> ranges;
+  for (int t = z1_off; t < t_end;) {
+    int64_t n = 0;
+    int u = t;
+    while (u < t_end && (u == t || n + tiles_host[u].len <= kZ1ChunkElems)) n += tiles_host[u++].len;
+    ranges.push_back({t, u});
+    t = u;
+  }
+  z1_stage.assign(cfg.par.dp, nullptr);
+  for (int r = 0; r < cfg.par.dp; ++r)
+    if (local_index(r) < 0) {
+      // a rank is a remote replica source if some chunk tile reads from it
+      bool used = false;
+      for (int t = z1_off; t < t_end && !used; ++t)
+        for (int b = 1; b < geom.replicas() && !used; ++b) used = tiles_host[t].src + b * geom.z2 == r;
+      for (int t = z1_off; t < t_end && !used; ++t) used = tiles_host[t].src == r;
+      if (used) HZP_CUDA(cudaMalloc(&z1_stage[r], size_t(2 * kZ1ChunkElems) * 4));
+    }
+  for (size_t c = 0; c < ranges.size(); ++c) {
+    Z1Chunk ch;
+    ch.t0 = ranges[c].first;
+    ch.t1 = ranges[c].second;
+    RankTable t = table;
+    for (int r = 0; r < cfg.par.dp; ++r) {
+      if (!z1_stage[r]) continue;
+      // rank r's grad offsets read by this chunk form one contiguous range
+      int64_t lo = INT64_MAX, hi = -1;
+      for (int u = ch.t0; u < ch.t1; ++u) {
+        const CommTile& x = tiles_host[u];
+        bool reads = false;
+        for (int b = 0; b < geom.replicas(); ++b) reads = reads || x.src + b * geom.z2 == r;
+        if (!reads) continue;
+        lo = std::min<int64_t>(lo, x.b_off);
+        hi = std::max<int64_t>(hi, x.b_off + x.len);
+      }
+      if (hi < 0) continue;
+      float* buf = static_cast<float*>(z1_stage[r]) + (c & 1) * kZ1ChunkElems;
+      t.grad[r] = buf - lo;  // the kernel indexes grad[r] + b_off
+      ch.copies.push_back({0, r, 0, lo, hi - lo});
+    }
+    HZP_CUDA(cudaMalloc(&ch.table, sizeof(RankTable)));
+    HZP_CUDA(cudaMemcpy(ch.table, &t, sizeof(RankTable), cudaMemcpyHostToDevice));
+    z1_chunks.push_back(ch);
+  }
+  int lo = 0, hi = 0;
+  HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  HZP_CUDA(cudaStreamCreateWithPriority(&z1_copy_stream, cudaStreamNonBlocking, hi));
+  if (rs_ev.empty()) {
+    rs_ev.resize(64);
+    for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+}
+
 void Engine::setup_rs_staging() {
+  setup_z1_staging();
   if (emulate || direct_grad || geom.z2 <= 1 || !rs_ce) return;
   const int es = bf16 ? 2 : 4;
   const int base = geom.z2_base(cfg.my_rank);
@@ -268,8 +330,10 @@ void Engine::setup_rs_staging() {
   int lo = 0, hi = 0;
   HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   HZP_CUDA(cudaStreamCreateWithPriority(&rs_red_stream, cudaStreamNonBlocking, hi));
-  rs_ev.resize(64);
-  for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (rs_ev.empty()) {
+    rs_ev.resize(64);
+    for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   for (int w = 0; w < int(wslots); ++w) {
     RankTable t = table;
     for (int r = 0; r < cfg.par.dp; ++r)
@@ -331,6 +395,32 @@ void Engine::z1_adam(cudaStream_t s) {
   a.omb2 = one - a.b2;
   a.bc1 = one - static_cast<float>(std::pow(static_cast<double>(a.b1), step));
   a.bc2 = one - static_cast<float>(std::pow(static_cast<double>(a.b2), step));
+  if (!z1_chunks.empty()) {
+    // chunk c's copy (copy engines, z1_copy_stream) overlaps chunk c-1's
+    // kernel (s); buffer c & 1 is reused by chunk c+2 only after chunk c's
+    // kernel retired
+    std::vector<cudaEvent_t> done_k(z1_chunks.size());
+    cudaEvent_t e0 = rs_ev[0];
+    HZP_CUDA(cudaEventRecord(e0, s));  // grads complete (the caller's barrier)
+    HZP_CUDA(cudaStreamWaitEvent(z1_copy_stream, e0, 0));
+    for (size_t c = 0; c < z1_chunks.size(); ++c) {
+      const Z1Chunk& ch = z1_chunks[c];
+      if (c >= 2) HZP_CUDA(cudaStreamWaitEvent(z1_copy_stream, done_k[c - 2], 0));
+      for (const CopyRun& r : ch.copies)
+        HZP_CUDA(cudaMemcpyAsync(static_cast<float*>(z1_stage[r.src]) + (c & 1) * kZ1ChunkElems,
+                                 table.grad[r.src] + r.src_off, size_t(r.len) * 4, cudaMemcpyDeviceToDevice,
+                                 z1_copy_stream));
+      cudaEvent_t ec = rs_ev[1 + (2 * c) % (rs_ev.size() - 1)];
+      HZP_CUDA(cudaEventRecord(ec, z1_copy_stream));
+      HZP_CUDA(cudaStreamWaitEvent(s, ec, 0));
+      launch_z1_adam(ch.table, dtiles + ch.t0, ch.t1 - ch.t0, geom.z2, geom.replicas(), &a, 1, bf16,
+                     l0.dbg != nullptr, 8 * kNumSMs, s);
+      done_k[c] = rs_ev[1 + (2 * c + 1) % (rs_ev.size() - 1)];
+      HZP_CUDA(cudaEventRecord(done_k[c], s));
+    }
+    ++launches;
+    return;
+  }
   launch_z1_adam(dtable, dtiles + z1_off, z1_n, geom.z2, geom.replicas(), &a, 1, bf16,
                  l0.dbg != nullptr, 8 * kNumSMs, s);  // HBM-bound, never beside a GEMM
   ++launches;

@@ -83,7 +83,22 @@ struct Engine {
   cudaStream_t rs_red_stream = nullptr;
   std::vector<cudaEvent_t> rs_ev;
   static constexpr int kRsChunkTiles = 128;  // 4 M elements per pipelined chunk
-  bool rs_ce = true;   // HZP_RS_CE=0 to use the SM pull (dp=4: 184.5 -> 160.1 ms with both CE legs)
+  bool rs_ce = true;
+  // Z1 with DZP replicas (R > 1): the remote replicas' gradient segments of
+  // this rank's chunk are copied (copy engines) into double-buffered local
+  // staging, chunk by chunk, while the fused Z1 kernel consumes the previous
+  // chunk through a table whose remote grad entries point at the staging.
+  bool z1_ce = false;  // HZP_Z1_CE=1 (7B dp=4: 36.6 vs 31.3 ms SM pull, so off)
+  struct Z1Chunk {
+    int t0, t1;                       // tile range (within the Z1 tiles)
+    RankTable* table;                 // device table for this chunk
+    std::vector<CopyRun> copies;      // CopyRun.src = global rank; dst_off into its staging buffer
+  };
+  std::vector<Z1Chunk> z1_chunks;
+  std::vector<void*> z1_stage;        // [dp]: 2 x kZ1ChunkElems fp32 per remote replica rank
+  cudaStream_t z1_copy_stream = nullptr;
+  static constexpr int64_t kZ1ChunkElems = int64_t(16) << 20;
+  void setup_z1_staging();   // HZP_RS_CE=0 to use the SM pull (dp=4: 184.5 -> 160.1 ms with both CE legs)
   void setup_rs_staging();
   int z1_off = 0, z1_n = 0;
 
