@@ -183,6 +183,11 @@ typedef struct {
   int my_rank;         /* global rank driven by this process, or -1 = emulate all
                           dp ranks on `device` (single-process parity mode) */
   int timeline;        /* record per-task CUDA events (measured timeline) */
+  /* GPT only: mixture-of-experts feed-forward (0 = dense).  Each block's FFN
+   * becomes gpt_experts GELU experts of width gpt_ffn with a top-gpt_topk
+   * router; gpt_capacity = slots per expert per microbatch (0 = 1.25 x
+   * topk x tokens / experts, rounded up to 128). */
+  int gpt_experts, gpt_topk, gpt_capacity;
 } hzp_engine_config;
 
 typedef struct hzp_ctx hzp_ctx;

@@ -48,6 +48,9 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     mcfg.ffn = c.gpt_ffn;
     mcfg.vocab = c.gpt_vocab;
     mcfg.seq = c.gpt_seq;
+    mcfg.experts = c.gpt_experts;
+    mcfg.topk = c.gpt_topk;
+    mcfg.capacity = c.gpt_capacity;
     if (!bf16) throw std::invalid_argument("the GPT model runs in bf16 only");
     model = make_gpt_model(mcfg);
   }

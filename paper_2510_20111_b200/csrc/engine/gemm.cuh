@@ -45,6 +45,7 @@ struct Epilogue {
   int ldres = 0;
   const float* rowvec = nullptr;  // fp32 per-row vector (softmax-grad D), batch strides below
   int64_t rv_sh = 0, rv_sb = 0;
+  int64_t bias_sh = 0;  // batched products: bias_any of head-batch zh starts at + zh * bias_sh (experts)
 };
 
 struct GemmShape {

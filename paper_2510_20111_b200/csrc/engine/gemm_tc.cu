@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const bool full_chunk = nb + 32 <= p.N;
         if (row_ok) {
           if (e.bias_any) {  // same 32 bias values for every lane: 4 broadcast 16-byte loads
-            const uint16_t* bp = static_cast<const uint16_t*>(e.bias_any) + nb;
+            const uint16_t* bp = static_cast<const uint16_t*>(e.bias_any) + int64_t(tc.zh) * e.bias_sh + nb;
             if (full_chunk && (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
               float bb[32];
 #pragma unroll

@@ -57,6 +57,7 @@ struct ModelConfig {
   std::vector<int> dims;  // MLP widths
   int batch = 1;       // MLP rows / GPT sequences per microbatch
   int layers = 0, hidden = 0, heads = 0, ffn = 0, vocab = 0, seq = 0;
+  int experts = 0, topk = 2, capacity = 0;  // GPT MoE feed-forward (experts = 0: dense)
 };
 
 std::unique_ptr<Model> make_mlp_model(const ModelConfig& c);

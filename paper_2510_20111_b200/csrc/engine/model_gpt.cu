@@ -6,6 +6,12 @@
 //                  ln1_g ln1_b [h] | w_qkv [3h, h] | b_qkv [3h] | w_o [h, h] | b_o [h] |
 //                  ln2_g ln2_b [h] | w_fc1 [f, h] | b_fc1 [f] | w_fc2 [h, f] | b_fc2 [h]
 //   layer L+1      head: lnf_g lnf_b [h] | w_head [V, h]  (untied)
+// MoE variant (experts E > 0, BASELINE configs[3]): the FFN part of a block is
+//                  ln2_g ln2_b [h] | w_router [E, h] | E x (w_fc1 [f, h] | b_fc1 [f] |
+//                  w_fc2 [h, f] | b_fc2 [h])
+// with top-K routing (renormalised gates), capacity-bounded deterministic
+// dispatch (moe_ops.cuh) and the E expert products as single batched
+// tcgen05 GEMMs over [E, C] slots (per-expert weights via the batch stride).
 // Every matrix is row-major [out, in] like the reference's W (train.cpp:42-53),
 // so all three products of each linear layer map onto the tcgen05 GEMM
 // without transposes (gemm.cuh).  Attention is fused on tcgen05 (attn_tc.cu):
@@ -19,17 +25,23 @@
 #include "engine/gpt_ops.cuh"
 #include "engine/attn.cuh"
 #include "engine/model.hpp"
+#include "engine/moe_ops.cuh"
 
 namespace hzp {
 namespace {
 
 struct BlockOff {  // element offsets inside a block's parameter range
   int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2, size;
+  int64_t w_router = 0, ex_stride = 0;  // MoE: router, and expert e's tensors at + e * ex_stride
 };
 
 struct LayerActs {  // saved activations of one block (one microbatch)
   uint16_t *ln1, *qkv, *attn, *xm, *ln2, *fpre, *fact;
   float *mu1, *rs1, *mu2, *rs2, *lse;  // lse [Z, S]: softmax stats for the backward
+  // MoE: router stats and the expert-major slot buffers ([E*C, .] rows)
+  float *logits = nullptr, *probs = nullptr, *gate = nullptr;
+  int *sel = nullptr, *pos = nullptr, *slot_tok = nullptr, *slot_k = nullptr;
+  uint16_t *xp = nullptr, *y = nullptr;
 };
 
 struct GptBuffers {
@@ -51,6 +63,9 @@ struct GptBuffers {
   cudaStream_t side = nullptr;
   cudaEvent_t ev[8] = {};
   float* part_side = nullptr;
+  // MoE backward scratch
+  uint16_t *moe_dy = nullptr, *moe_dh = nullptr, *moe_dxp = nullptr, *moe_dlogits = nullptr;
+  float* moe_dgate = nullptr;
   float* emb = nullptr;        // fp32 scratch for the embedding gradient [V*h + S*h]
   float* loss = nullptr;
   const int* tokens = nullptr;  // current microbatch
@@ -70,6 +85,14 @@ class GptModel final : public Model {
     b_ = c.batch;
     T_ = int64_t(b_) * S_;
     L_ = c.layers;
+    E_ = c.experts;
+    K_ = c.topk > 0 ? c.topk : 2;
+    if (E_ > 0) {
+      if (E_ > 64 || K_ > 4 || K_ > E_ || E_ % 8) throw std::invalid_argument("MoE: experts % 8 == 0, <= 64, topk <= 4");
+      const int64_t autoc = (int64_t(K_) * T_ * 5 / 4 + E_ - 1) / E_;
+      C_ = c.capacity > 0 ? c.capacity : int(autoc);
+      C_ = (C_ + 127) / 128 * 128;
+    }
     if (h_ % 64 || f_ % 64 || V_ % 64 || S_ % 128 || hd_ != 128 || h_ % nh_)
       throw std::invalid_argument("GPT dims must be multiples of 64, seq of 128, head dim 128");
     int64_t o = 0;
@@ -86,10 +109,16 @@ class GptModel final : public Model {
     bo_.b_o = take(h_);
     bo_.ln2_g = take(h_);
     bo_.ln2_b = take(h_);
+    if (E_ > 0) bo_.w_router = take(int64_t(E_) * h_);
+    const int64_t ex0 = o;
     bo_.w_fc1 = take(int64_t(f_) * h_);
     bo_.b_fc1 = take(f_);
     bo_.w_fc2 = take(int64_t(h_) * f_);
     bo_.b_fc2 = take(h_);
+    if (E_ > 0) {
+      bo_.ex_stride = o - ex0;
+      o = ex0 + int64_t(E_) * bo_.ex_stride;
+    }
     bo_.size = o;
     int64_t off = 0;
     ranges_.push_back({off, int64_t(V_) * h_ + int64_t(S_) * h_});
@@ -112,7 +141,9 @@ class GptModel final : public Model {
   double flops_per_mb() const override {
     // 6 * dense params * tokens + causal attention (QK^T and PV, fwd + bwd = 3x):
     // 3 * 2 * 2 * S^2/2 * h * b * L
-    const double dense = double(L_) * (4.0 * h_ * h_ + 2.0 * h_ * f_) + double(V_) * h_;
+    // MoE: the active parameters per token (K experts + router)
+    const double ffn = E_ > 0 ? double(K_) * 2.0 * h_ * f_ + double(E_) * h_ : 2.0 * h_ * f_;
+    const double dense = double(L_) * (4.0 * h_ * h_ + ffn) + double(V_) * h_;
     return 6.0 * dense * double(T_) + 6.0 * double(S_) * S_ * h_ * b_ * L_;
   }
   int64_t launches_per_fwd() const override { return 9; }
@@ -129,6 +160,11 @@ class GptModel final : public Model {
       HZP_CUDA(cudaMalloc(&p, size_t(n) * 4));
       return p;
     };
+    auto i32 = [](int64_t n) {
+      int* p = nullptr;
+      HZP_CUDA(cudaMalloc(&p, size_t(n) * 4));
+      return p;
+    };
     const int64_t Z = int64_t(b_) * nh_;
     const int64_t SS = Z * S_ * S_;
     B->x.assign(L_ + 2, nullptr);
@@ -142,8 +178,20 @@ class GptModel final : public Model {
       a.attn = bf(T_ * h_);
       a.xm = bf(T_ * h_);
       a.ln2 = bf(T_ * h_);
-      a.fpre = bf(T_ * f_);
-      a.fact = bf(T_ * f_);
+      const int64_t frows = E_ > 0 ? int64_t(E_) * C_ : T_;
+      a.fpre = bf(frows * f_);
+      a.fact = bf(frows * f_);
+      if (E_ > 0) {
+        a.logits = f32(T_ * E_);
+        a.probs = f32(T_ * E_);
+        a.gate = f32(T_ * K_);
+        a.sel = i32(T_ * K_);
+        a.pos = i32(T_ * K_);
+        a.slot_tok = i32(int64_t(E_) * C_);
+        a.slot_k = i32(int64_t(E_) * C_);
+        a.xp = bf(int64_t(E_) * C_ * h_);
+        a.y = bf(int64_t(E_) * C_ * h_);
+      }
       a.mu1 = f32(T_);
       a.rs1 = f32(T_);
       a.mu2 = f32(T_);
@@ -162,6 +210,13 @@ class GptModel final : public Model {
     B->dqkv = bf(T_ * 3 * h_);
     B->dattn = bf(T_ * h_);
     B->dfc1 = bf(T_ * f_);
+    if (E_ > 0) {
+      B->moe_dy = bf(int64_t(E_) * C_ * h_);
+      B->moe_dh = bf(int64_t(E_) * C_ * f_);
+      B->moe_dxp = bf(int64_t(E_) * C_ * h_);
+      B->moe_dlogits = bf(T_ * E_);
+      B->moe_dgate = f32(T_ * K_);
+    }
     B->dxm = bf(T_ * h_);
     B->part = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
     B->part_side = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
@@ -178,13 +233,16 @@ class GptModel final : public Model {
     for (auto& a : B->acts) {
       for (void* q : {(void*)a.ln1, (void*)a.qkv, (void*)a.lse, (void*)a.attn, (void*)a.xm,
                       (void*)a.ln2, (void*)a.fpre, (void*)a.fact, (void*)a.mu1, (void*)a.rs1,
-                      (void*)a.mu2, (void*)a.rs2})
+                      (void*)a.mu2, (void*)a.rs2, (void*)a.logits, (void*)a.probs, (void*)a.gate,
+                      (void*)a.sel, (void*)a.pos, (void*)a.slot_tok, (void*)a.slot_k, (void*)a.xp,
+                      (void*)a.y})
         cudaFree(q);
     }
     for (void* q : {(void*)B->lnf, (void*)B->muf, (void*)B->rsf, (void*)B->logits, (void*)B->S,
                     (void*)B->dS, (void*)B->D, (void*)B->dx[0], (void*)B->dx[1], (void*)B->dln,
                     (void*)B->dqkv, (void*)B->dattn, (void*)B->dfc1, (void*)B->dxm, (void*)B->part,
-                    (void*)B->part_side,
+                    (void*)B->part_side, (void*)B->moe_dy, (void*)B->moe_dh, (void*)B->moe_dxp,
+                    (void*)B->moe_dlogits, (void*)B->moe_dgate,
                     (void*)B->emb, (void*)B->loss})
       cudaFree(q);
     for (auto e : B->ev) cudaEventDestroy(e);
@@ -252,6 +310,125 @@ class GptModel final : public Model {
     return sh;
   }
 
+  // ---- MoE feed-forward ---------------------------------------------------------
+  // E experts batched in one GEMM: batch index = expert, per-expert slot rows
+  // at stride C, per-expert weights at stride ex_stride.
+  GemmShape expert_shape(int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int64_t a_sh,
+                         int64_t b_sh, int64_t c_sh) const {
+    GemmShape sh{M, N, K, lda, ldb, a_mn, b_mn};
+    sh.nh = E_;
+    sh.nb = 1;
+    sh.a_sh = a_sh;
+    sh.b_sh = b_sh;
+    sh.c_sh = c_sh;
+    return sh;
+  }
+  void moe_fwd(const LayerActs& a, const uint16_t* W, uint16_t* out, cudaStream_t s) const {
+    const BlockOff& o = bo_;
+    const int64_t EC = int64_t(E_) * C_;
+    {  // router logits [T, E] fp32
+      GemmShape sh{int(T_), E_, h_, h_, h_, 0, 0};
+      Epilogue e;
+      e.out_bf16 = 0;
+      e.ldc = E_;
+      gemm_tc_bf16(a.ln2, W + o.w_router, a.logits, sh, e, s);
+    }
+    moe_route(a.logits, int(T_), E_, K_, a.probs, a.sel, a.gate, s);
+    moe_dispatch(a.sel, int(T_), E_, K_, C_, a.pos, a.slot_tok, a.slot_k, s);
+    moe_gather(a.ln2, a.slot_tok, int(EC), h_, a.xp, s);
+    {  // H_e = GELU(Xp_e W1_e^T + b1_e)  (pre-activation kept for the backward)
+      GemmShape sh = expert_shape(C_, f_, h_, h_, h_, 0, 0, int64_t(C_) * h_, o.ex_stride, int64_t(C_) * f_);
+      Epilogue e;
+      e.bias_any = W + o.b_fc1;
+      e.bias_sh = o.ex_stride;
+      e.act = kActGelu;
+      e.aux = a.fpre;
+      e.ldaux = f_;
+      e.ldc = f_;
+      gemm_tc_bf16(a.xp, W + o.w_fc1, a.fact, sh, e, s);
+    }
+    {  // Y_e = H_e W2_e^T + b2_e
+      GemmShape sh = expert_shape(C_, h_, f_, f_, f_, 0, 0, int64_t(C_) * f_, o.ex_stride, int64_t(C_) * h_);
+      Epilogue e;
+      e.bias_any = W + o.b_fc2;
+      e.bias_sh = o.ex_stride;
+      e.ldc = h_;
+      gemm_tc_bf16(a.fact, W + o.w_fc2, a.y, sh, e, s);
+    }
+    moe_combine(a.y, a.pos, a.gate, a.xm, int(T_), K_, h_, out, s);  // + residual
+  }
+  // Backward of the MoE FFN from dout (grad of the block output); leaves the
+  // grad of the ln2 output in B->dattn (scratch here).  Weight gradients run
+  // on ws after to_side().
+  template <class ToSide>
+  void moe_bwd(GptBuffers* B, const LayerActs& a, const uint16_t* W, const GradTarget& g, const uint16_t* dout,
+               cudaStream_t s, cudaStream_t ws, ToSide to_side) const {
+    const BlockOff& o = bo_;
+    const int64_t EC = int64_t(E_) * C_;
+    moe_combine_bwd(dout, a.y, a.pos, a.gate, a.slot_tok, a.slot_k, int(T_), K_, int(EC), h_, B->moe_dy,
+                    B->moe_dgate, s);
+    to_side();
+    {  // dW2_e [h, f] = dY_e^T H_e ; db2_e = colsum dY_e
+      GemmShape sh = expert_shape(h_, f_, C_, h_, f_, 1, 1, int64_t(C_) * h_, int64_t(C_) * f_, o.ex_stride);
+      Epilogue e;
+      e.mode = g.mode;
+      e.out_bf16 = g.bf16;
+      e.ldc = f_;
+      gemm_tc_bf16(B->moe_dy, a.fact, gptr(g, o.w_fc2), sh, e, ws);
+      for (int x = 0; x < E_; ++x) {
+        colsum_partial(B->moe_dy + int64_t(x) * C_ * h_, C_, h_, B->part_side, kChunks, ws);
+        colsum_finalize(B->part_side, kChunks, h_, gptr(g, o.b_fc2 + x * o.ex_stride), g.bf16, g.mode, ws);
+      }
+    }
+    {  // dH_e = GELU'(pre) * (dY_e W2_e)
+      GemmShape sh = expert_shape(C_, f_, h_, h_, f_, 0, 1, int64_t(C_) * h_, o.ex_stride, int64_t(C_) * f_);
+      Epilogue e;
+      e.act = kActGeluGrad;
+      e.aux = a.fpre;
+      e.ldaux = f_;
+      e.ldc = f_;
+      gemm_tc_bf16(B->moe_dy, W + o.w_fc2, B->moe_dh, sh, e, s);
+    }
+    to_side();
+    {  // dW1_e [f, h] = dH_e^T Xp_e ; db1_e = colsum dH_e
+      GemmShape sh = expert_shape(f_, h_, C_, f_, h_, 1, 1, int64_t(C_) * f_, int64_t(C_) * h_, o.ex_stride);
+      Epilogue e;
+      e.mode = g.mode;
+      e.out_bf16 = g.bf16;
+      e.ldc = h_;
+      gemm_tc_bf16(B->moe_dh, a.xp, gptr(g, o.w_fc1), sh, e, ws);
+      for (int x = 0; x < E_; ++x) {
+        colsum_partial(B->moe_dh + int64_t(x) * C_ * f_, C_, f_, B->part_side, kChunks, ws);
+        colsum_finalize(B->part_side, kChunks, f_, gptr(g, o.b_fc1 + x * o.ex_stride), g.bf16, g.mode, ws);
+      }
+    }
+    {  // dXp_e = dH_e W1_e
+      GemmShape sh = expert_shape(C_, h_, f_, f_, h_, 0, 1, int64_t(C_) * f_, o.ex_stride, int64_t(C_) * h_);
+      Epilogue e;
+      e.ldc = h_;
+      gemm_tc_bf16(B->moe_dh, W + o.w_fc1, B->moe_dxp, sh, e, s);
+    }
+    moe_gather_bwd(B->moe_dxp, a.pos, int(T_), K_, h_, B->dln, s);  // expert path of d ln2-out
+    moe_router_bwd(a.probs, a.sel, B->moe_dgate, int(T_), E_, K_, B->moe_dlogits, s);
+    to_side();
+    {  // dW_router [E, h] = dlogits^T ln2
+      GemmShape sh{E_, h_, int(T_), E_, h_, 1, 1};
+      Epilogue e;
+      e.mode = g.mode;
+      e.out_bf16 = g.bf16;
+      e.ldc = h_;
+      gemm_tc_bf16(B->moe_dlogits, a.ln2, gptr(g, o.w_router), sh, e, ws);
+    }
+    {  // d ln2-out = expert path + dlogits W_router
+      GemmShape sh{int(T_), h_, E_, E_, h_, 0, 1};
+      Epilogue e;
+      e.resid = B->dln;
+      e.ldres = h_;
+      e.ldc = h_;
+      gemm_tc_bf16(B->moe_dlogits, W + o.w_router, B->dattn, sh, e, s);
+    }
+  }
+
   // ---- forward ---------------------------------------------------------------
   void fwd(void* p, int l, const void* input_mb, const void* params, cudaStream_t s) override {
     auto* B = static_cast<GptBuffers*>(p);
@@ -288,6 +465,10 @@ class GptModel final : public Model {
       linear_fwd(a.attn, W + o.w_o, a.xm, h_, h_, e, s);
     }
     layernorm_fwd(a.xm, W + o.ln2_g, W + o.ln2_b, a.ln2, a.mu2, a.rs2, int(T_), h_, s);
+    if (E_ > 0) {
+      moe_fwd(a, W, B->x[l + 1], s);
+      return;
+    }
     {
       Epilogue e;
       e.bias_any = W + o.b_fc1;
@@ -342,6 +523,12 @@ class GptModel final : public Model {
       ++nev;
     };
     cudaStream_t ws = B->side;
+    if (E_ > 0) {
+      moe_bwd(B, a, W, g, dout, s, ws, to_side);
+      layernorm_bwd(B->dattn, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_), h_,
+                    s);
+      ln_param_grads(B, g, o.ln2_g, o.ln2_b, s);
+    } else {
     // MLP
     to_side();
     linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, o.b_fc2, B, ws);
@@ -361,6 +548,7 @@ class GptModel final : public Model {
     layernorm_bwd(B->dln, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_),
                   h_, s);
     ln_param_grads(B, g, o.ln2_g, o.ln2_b, s);
+    }
     // attention output projection
     to_side();
     linear_wgrad(B->dxm, a.attn, h_, h_, g, o.w_o, o.b_o, B, ws);
@@ -392,6 +580,7 @@ class GptModel final : public Model {
  private:
   ModelConfig c_;
   int h_, nh_, hd_, f_, V_, S_, b_, L_;
+  int E_ = 0, K_ = 2, C_ = 0;  // MoE experts, top-k, slots per expert (E_ = 0: dense FFN)
   int64_t T_;
   BlockOff bo_;
   std::vector<LayerRange> ranges_;
