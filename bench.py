@@ -35,6 +35,10 @@ UNIT = "tokens/s"
 GPT13B = dict(layers=24, hidden=2048, heads=16, ffn=8192, vocab=50304, seq=2048)
 # BASELINE configs[2]: 7B dense decoder, hierarchical ZeRO-3 group 4 x ZeRO-1 group 2
 GPT7B = dict(layers=32, hidden=4096, heads=32, ffn=16384, vocab=50304, seq=2048)
+# BASELINE configs[3]: MoE 16 experts top-2 (SURVEY App. A-5 dims, GELU experts of
+# width 4864), hierarchical ZeRO-3 group 2 x ZeRO-1 group 4
+MOE = dict(layers=16, hidden=2048, heads=16, ffn=4864, vocab=50304, seq=2048, experts=16, topk=2)
+MODELS = {"1.3b": GPT13B, "7b": GPT7B, "moe": MOE}
 
 
 def layout_for(model: str, N: int):
@@ -43,6 +47,9 @@ def layout_for(model: str, N: int):
     N/2 x 2 below, flat at N = 1)."""
     if model == "7b" and N > 1:
         z3 = min(4, N // 2) if N >= 2 else 1
+        return N, z3, z3
+    if model == "moe" and N > 1:
+        z3 = min(2, N)
         return N, z3, z3
     return N, N, N
 
@@ -153,8 +160,8 @@ def cpu_reference(steps: int, warmup: int, label: str, c=None):
     sample_tok = mbs * rows
     sample_flops_tok = 6.0 * (dims[0] * dims[1] + dims[1] * dims[2])
     c = c or GPT13B
-    model_flops_tok = 6.0 * (c["layers"] * (4 * c["hidden"] ** 2 + 2 * c["hidden"] * c["ffn"]) +
-                             c["vocab"] * c["hidden"])
+    ffn = c.get("topk", 1) * 2 * c["hidden"] * c["ffn"] if c.get("experts") else 2 * c["hidden"] * c["ffn"]
+    model_flops_tok = 6.0 * (c["layers"] * (4 * c["hidden"] ** 2 + ffn) + c["vocab"] * c["hidden"])
     raw = sample_tok / sec
     equiv = raw * sample_flops_tok / model_flops_tok
     return {"value": equiv, "unit": UNIT, "cores": 1, "kind": kind,
@@ -198,7 +205,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     steps = max(1, min(args.steps, 10))
-    c = GPT7B if args.model == "7b" else GPT13B
+    c = MODELS[args.model]
     cb = cpu_reference_parallel(steps, min(args.warmup, 1), c)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": None,
@@ -315,12 +322,13 @@ def run_hzp(args):
         dist.init_process_group("gloo", init_method="env://")
     torch.cuda.set_device(local)
     N = world
-    c = GPT7B if args.model == "7b" else GPT13B
+    c = MODELS[args.model]
     z1, z2, z3 = layout_for(args.model, N)
     mb, nmb = args.batch, args.microbatches
     cfg = EngineConfig(model=1, precision=1, gpt_layers=c["layers"], gpt_hidden=c["hidden"],
                        gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
                        gpt_seq=c["seq"], batch=mb, num_microbatches=nmb,
+                       gpt_experts=c.get("experts", 0), gpt_topk=c.get("topk", 2),
                        par=ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3), prelaunch_depth=2, rs_slots=1,
                        device=local, my_rank=rank if N > 1 else 0)
     eng = HzpEngine(cfg)
@@ -423,11 +431,13 @@ def run_hzp(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (uniform random token ids; hash-uniform init weights)",
-                "config": {"workload": ("BASELINE configs[2]: 7B-class GPT decoder, hierarchical ZeRO"
-                                        if args.model == "7b" else
-                                        "BASELINE configs[1]: 1.3B-class GPT decoder, flat ZeRO-3"),
+                "config": {"workload": {"7b": "BASELINE configs[2]: 7B-class GPT decoder, hierarchical ZeRO",
+                                        "moe": "BASELINE configs[3]: MoE 16 experts top-2, hierarchical ZeRO",
+                                        "1.3b": "BASELINE configs[1]: 1.3B-class GPT decoder, flat ZeRO-3"}[args.model],
                            "model": (f"gpt-{args.model}-class (L{c['layers']} h{c['hidden']} {c['heads']} heads "
-                                     f"ffn{c['ffn']} vocab{c['vocab']} untied head)"),
+                                     f"ffn{c['ffn']}" + (f" x {c['experts']} experts top-{c['topk']}"
+                                                         if c.get("experts") else "") +
+                                     f" vocab{c['vocab']} untied head)"),
                            "params": eng.P, "global_batch": N * mb * nmb, "seq_len": c["seq"],
                            "micro_batch": mb, "num_microbatches": nmb,
                            "tokens_per_step": N * tokens_per_step,
@@ -453,8 +463,8 @@ def main():
     ap.add_argument("--impl", default="hzp", choices=["hzp", "reference"])
     ap.add_argument("--batch", type=int, default=4, help="sequences per microbatch per GPU")
     ap.add_argument("--microbatches", type=int, default=2)
-    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b"],
-                    help="BASELINE configs[1] (default, the headline) or configs[2]")
+    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b", "moe"],
+                    help="BASELINE configs[1] (default, the headline), configs[2] or configs[3]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
