@@ -213,6 +213,8 @@ enum { HZP_F_PARAM = 0, HZP_F_GRAD = 1, HZP_F_MASTER = 2, HZP_F_MOM = 3, HZP_F_V
 int hzp_state_upload(hzp_ctx* ctx, int rank, int field, const void* host, int64_t n);
 int hzp_state_download(hzp_ctx* ctx, int rank, int field, void* host, int64_t n);
 int hzp_state_set_step(hzp_ctx* ctx, int rank, int adam_step);
+/* The Adam step counter of a driven rank (checkpointing). */
+int hzp_state_get_step(const hzp_ctx* ctx, int rank, int* adam_step);
 /* shard_init (train.cpp:224-253) done on the host by the caller and
  * uploaded, or seeded on the device for throughput runs: */
 int hzp_state_init_random(hzp_ctx* ctx, uint64_t seed, double scale);

@@ -117,6 +117,7 @@ SIGNATURES = [
     ("hzp_state_upload", C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64]),
     ("hzp_state_download", C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64]),
     ("hzp_state_set_step", C.c_int, [_vp, C.c_int, C.c_int]),
+    ("hzp_state_get_step", C.c_int, [_vp, C.c_int, _P(C.c_int)]),
     ("hzp_state_init_random", C.c_int, [_vp, C.c_uint64, C.c_double]),
     ("hzp_step", C.c_int, [_vp, _vp, C.c_int, _P(C.c_float)]),
     ("hzp_sync", C.c_int, [_vp]),

@@ -386,6 +386,14 @@ int hzp_state_set_step(hzp_ctx* ctx, int rank, int adam_step) {
   return HZP_OK;
 }
 
+int hzp_state_get_step(const hzp_ctx* ctx, int rank, int* adam_step) {
+  if (!ctx || !adam_step) return HZP_ERR_ARG;
+  const int li = ctx->e->local_index(rank);
+  if (li < 0) return HZP_ERR_ARG;
+  *adam_step = ctx->e->locals[li].adam_step;
+  return HZP_OK;
+}
+
 namespace {
 __device__ __forceinline__ float hash_uniform(uint64_t e, uint64_t seed) {
   uint64_t x = e * 0x9E3779B97F4A7C15ull ^ seed;

@@ -140,6 +140,43 @@ class HzpEngine:
     def set_step(self, rank: int, step: int) -> None:
         N.check(N.lib.hzp_state_set_step(self._h, rank, step))
 
+    def get_step(self, rank: int) -> int:
+        v = C.c_int()
+        N.check(N.lib.hzp_state_get_step(self._h, rank, C.byref(v)))
+        return v.value
+
+    # ---- checkpoint (save / restore ShardedState per rank) ------------
+    def driven_ranks(self) -> List[int]:
+        if self.cfg.my_rank >= 0:
+            return [self.cfg.my_rank]
+        return list(range(self.cfg.par.dp))
+
+    def save_checkpoint(self, path: str) -> None:
+        """One .npz per driven rank: param (working dtype), grad, master, m, v
+        shards and the Adam step — the reference's ShardedState (train.hpp:73-83)."""
+        import os
+        os.makedirs(path, exist_ok=True)
+        for r in self.driven_ranks():
+            np.savez(os.path.join(path, f"rank{r}.npz"), param=self.download(r, F_PARAM),
+                     grad=self.download(r, F_GRAD), master=self.download(r, F_MASTER),
+                     mom=self.download(r, F_MOM), var=self.download(r, F_VAR),
+                     adam_step=np.int64(self.get_step(r)), P=np.int64(self.P),
+                     layout=np.array([self.cfg.par.dp, self.cfg.par.z1, self.cfg.par.z2, self.cfg.par.z3]))
+
+    def load_checkpoint(self, path: str) -> None:
+        import os
+        for r in self.driven_ranks():
+            z = np.load(os.path.join(path, f"rank{r}.npz"))
+            if int(z["P"]) != self.P or list(z["layout"]) != [self.cfg.par.dp, self.cfg.par.z1,
+                                                              self.cfg.par.z2, self.cfg.par.z3]:
+                raise ValueError("checkpoint layout does not match this ctx")
+            self.upload(r, F_PARAM, z["param"])
+            self.upload(r, F_GRAD, z["grad"])
+            self.upload(r, F_MASTER, z["master"])
+            self.upload(r, F_MOM, z["mom"])
+            self.upload(r, F_VAR, z["var"])
+            self.set_step(r, int(z["adam_step"]))
+
     def init_random(self, seed: int = 1234, scale: float = 0.04) -> None:
         N.check(N.lib.hzp_state_init_random(self._h, seed, scale))
 

@@ -164,3 +164,22 @@ def test_async_never_worse_than_vanilla():
         assert a.compute_idle <= v.compute_idle + 1e-12
         assert a.makespan <= v.makespan + 1e-12
         assert a.compute_busy == v.compute_busy
+
+
+def test_chrome_trace_matches_reference_format():
+    """trace.cpp:33-73 layout: process/thread metadata + one X event per task."""
+    from paper_2510_20111_b200 import hzp as H
+    from paper_2510_20111_b200.trace import chrome_trace
+    g = H.build_task_graph(H.ModelSpec(num_layers=2, params_per_layer=100, num_microbatches=2),
+                           H.ParallelConfig(dp=8, z1=8, z2=4, z3=4), H.CostModel())
+    tl = H.simulate(g, 2, 1, H.ASYNC)
+    tr = chrome_trace(g, tl.start, tl.end, "sim")
+    ev = tr["traceEvents"]
+    assert ev[0] == {"name": "process_name", "ph": "M", "pid": 1, "tid": 0, "args": {"name": "sim"}}
+    assert [e["args"]["name"] for e in ev[1:4]] == ["compute", "all-gather", "reduce-scatter"]
+    xs = [e for e in ev if e["ph"] == "X"]
+    assert len(xs) == len(g.tasks)
+    for t, e in zip(g.tasks, xs):
+        assert e["name"] == H.KIND_NAMES[t.kind] and e["args"]["task_id"] == t.id
+        assert abs(e["ts"] - tl.start[t.id] * 1e6) < 1e-6 and e["dur"] >= 0
+    assert tr["displayTimeUnit"] == "ms"
