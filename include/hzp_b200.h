@@ -101,6 +101,21 @@ typedef struct {
  * (sched.hpp:66-76) with the default one-F-one-B-per-microbatch order. */
 int hzp_graph_build(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* cost,
                     int defer_rs, int rank, hzp_graph** out);
+
+/* ReuseReport (pipeline.hpp:57). */
+typedef struct {
+  int r1_eliminated_ag, r2_merged_rs, r3_eliminated_ag;
+  int64_t extra_cached_bytes;
+} hzp_reuse_report;
+
+/* The CLI's graph (hzpsim.cpp:111-127): build_task_graph over `rank`'s slot
+ * order of the pipeline schedule (build_schedule, pipeline.cpp:84-105: 1F1B,
+ * interleaved when par->vpp > 1), then apply_reuse (pipeline.cpp:167-279)
+ * when `reuse`, then recompute_rule (pipeline.cpp:281-318) when `recompute`.
+ * `report` (optional) receives the reuse counters. */
+int hzp_graph_build_pipeline(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* cost,
+                             int defer_rs, int rank, int reuse, int recompute, hzp_reuse_report* report,
+                             hzp_graph** out);
 void hzp_graph_destroy(hzp_graph* g);
 int hzp_graph_size(const hzp_graph* g);
 int hzp_graph_task(const hzp_graph* g, int i, hzp_task* out);
@@ -188,6 +203,12 @@ typedef struct {
    * router; gpt_capacity = slots per expert per microbatch (0 = 1.25 x
    * topk x tokens / experts, rounded up to 128). */
   int gpt_experts, gpt_topk, gpt_capacity;
+  /* 1 = apply the CLI's parameter reuse to the step's graph (apply_reuse,
+   * pipeline.cpp:167-279; hzpsim.cpp:126).  At pp = 1 only R3 fires: every
+   * forward after the first reads microbatch 0's forward all-gather, which
+   * lands in a per-layer side cache (full bf16 layer per layer) instead of a
+   * ring slot; backward all-gathers keep the ring. */
+  int reuse;
 } hzp_engine_config;
 
 typedef struct hzp_ctx hzp_ctx;

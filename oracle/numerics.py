@@ -305,14 +305,17 @@ class RefLib:
 
     def task_graph(self, layers, ppl, seq=1024, mbsize=1, num_mb=1, flops=6e6, dp=8, z1=8, z2=4,
                    z3=4, pp=1, vpp=1, intra_bw=1e10, intra_lat=1e-6, device_flops=1e12,
-                   defer_rs=False, rank=0, with_reuse=False, depth=2, rs_slots=1, vanilla=False):
+                   defer_rs=False, rank=0, with_reuse=False, depth=2, rs_slots=1, vanilla=False,
+                   recompute=False):
         class Sim(C.Structure):
             _fields_ = [("makespan", C.c_double), ("compute_idle", C.c_double),
                         ("compute_busy", C.c_double), ("peak_memory", C.c_longlong),
                         ("fragmentation", C.c_double), ("peak_grad_buffer_bytes", C.c_longlong),
                         ("ag_slot_count", C.c_int), ("rs_slot_count", C.c_int),
-                        ("ag_slot_bytes", C.c_longlong), ("rs_slot_bytes", C.c_longlong)]
-        cap = 5 * layers * num_mb * max(1, vpp) + 4 * layers + 8
+                        ("ag_slot_bytes", C.c_longlong), ("rs_slot_bytes", C.c_longlong),
+                        ("r1_eliminated_ag", C.c_int), ("r2_merged_rs", C.c_int),
+                        ("r3_eliminated_ag", C.c_int), ("extra_cached_bytes", C.c_longlong)]
+        cap = 6 * layers * num_mb * max(1, vpp) + 4 * layers + 8
         ints = lambda: np.zeros(cap, dtype=np.int32)  # noqa: E731
         dbl = lambda: np.zeros(cap, dtype=np.float64)  # noqa: E731
         kind, layer, mb, pas = ints(), ints(), ints(), ints()
@@ -324,11 +327,11 @@ class RefLib:
         sim = Sim()
         L = self.L
         L.ref_task_graph.argtypes = (
-            [C.c_longlong] * 5 + [C.c_double] + [C.c_int] * 6 + [C.c_double] * 3 + [C.c_int] * 7
+            [C.c_longlong] * 5 + [C.c_double] + [C.c_int] * 6 + [C.c_double] * 3 + [C.c_int] * 8
             + [_i32p] * 4 + [_i64p] + [_f64p] * 4 + [_i32p, _i32p, C.c_int, C.POINTER(Sim)])
         n = L.ref_task_graph(layers, ppl, seq, mbsize, num_mb, flops, dp, z1, z2, z3, pp, vpp,
                              intra_bw, intra_lat, device_flops, int(defer_rs), rank,
-                             int(with_reuse), depth, rs_slots, int(vanilla), cap, kind, layer, mb,
+                             int(with_reuse), int(recompute), depth, rs_slots, int(vanilla), cap, kind, layer, mb,
                              pas, nbytes, dur, start, end, rel, dep_off, deps, dep_cap,
                              C.byref(sim))
         if n < 0:

@@ -223,7 +223,10 @@ void ref_all_reduce_f32(const float* ts, int g, long long n, float* out) {
 // Task graph + simulation (src/sched.cpp:75-387).  Outputs per task:
 // kind, layer, microbatch, pass, bytes, start, end, pool_release; deps
 // flattened with dep_off[n+1].  Returns task count (or -1 on error; if
-// cap < count, only the count is returned).
+// cap < count, only the count is returned).  with_reuse: 0 = default
+// one-F-one-B-per-microbatch order; 1 = the CLI's order (build_schedule for
+// `rank`) + apply_reuse (hzpsim.cpp:111-126); 2 = that order without reuse.
+// recompute != 0 then applies recompute_rule (hzpsim.cpp:127).
 struct RefSimOut {
   double makespan, compute_idle, compute_busy;
   long long peak_memory;
@@ -231,12 +234,14 @@ struct RefSimOut {
   long long peak_grad_buffer_bytes;
   int ag_slot_count, rs_slot_count;
   long long ag_slot_bytes, rs_slot_bytes;
+  int r1_eliminated_ag, r2_merged_rs, r3_eliminated_ag;  // ReuseReport (pipeline.hpp:44-49)
+  long long extra_cached_bytes;
 };
 
 int ref_task_graph(long long layers, long long ppl, long long seq, long long mbsize,
                    long long num_mb, double flops_per_tok_layer, int dp, int z1, int z2,
                    int z3, int pp, int vpp, double intra_bw, double intra_lat,
-                   double device_flops, int defer_rs, int rank, int with_reuse, int depth,
+                   double device_flops, int defer_rs, int rank, int with_reuse, int recompute, int depth,
                    int rs_slots, int vanilla, int cap, int* kind, int* layer, int* mb,
                    int* pass, long long* bytes, double* dur, double* start, double* end,
                    double* pool_release, int* dep_off, int* deps, int dep_cap,
@@ -270,7 +275,9 @@ int ref_task_graph(long long layers, long long ppl, long long seq, long long mbs
       pol.order = sched.per_rank[rank];
     }
     auto g = hzp::build_task_graph(spec, cfg, cost, pol);
-    if (with_reuse) hzp::apply_reuse(sched, g);
+    hzp::ReuseReport rep;
+    if (with_reuse == 1) rep = hzp::apply_reuse(sched, g);
+    hzp::recompute_rule(g, recompute != 0);
     const int n = static_cast<int>(g.tasks.size());
     if (n > cap) return n;
     const auto pools = hzp::make_pools(g, depth, rs_slots);
@@ -306,6 +313,10 @@ int ref_task_graph(long long layers, long long ppl, long long seq, long long mbs
     sim->rs_slot_count = pools.rs.slot_count;
     sim->ag_slot_bytes = pools.ag.slot_bytes;
     sim->rs_slot_bytes = pools.rs.slot_bytes;
+    sim->r1_eliminated_ag = rep.r1_eliminated_ag;
+    sim->r2_merged_rs = rep.r2_merged_rs;
+    sim->r3_eliminated_ag = rep.r3_eliminated_ag;
+    sim->extra_cached_bytes = rep.extra_cached_bytes;
     return n;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -42,6 +42,11 @@ class hzp_task(C.Structure):
                 ("bytes", C.c_int64), ("num_deps", C.c_int), ("deps", C.POINTER(C.c_int))]
 
 
+class hzp_reuse_report(C.Structure):
+    _fields_ = [("r1_eliminated_ag", C.c_int), ("r2_merged_rs", C.c_int), ("r3_eliminated_ag", C.c_int),
+                ("extra_cached_bytes", C.c_int64)]
+
+
 class hzp_pool(C.Structure):
     _fields_ = [("capacity", C.c_int64), ("slot_count", C.c_int), ("slot_bytes", C.c_int64)]
 
@@ -73,7 +78,7 @@ class hzp_engine_config(C.Structure):
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("grad_scale", C.c_double), ("device", C.c_int), ("my_rank", C.c_int),
                 ("timeline", C.c_int), ("gpt_experts", C.c_int), ("gpt_topk", C.c_int),
-                ("gpt_capacity", C.c_int)]
+                ("gpt_capacity", C.c_int), ("reuse", C.c_int)]
 
 
 class hzp_launch_rec(C.Structure):
@@ -94,6 +99,8 @@ SIGNATURES = [
     ("hzp_groups", C.c_int, [_P(hzp_parallel), C.c_int, _P(C.c_int), C.c_int, _P(C.c_int), _P(C.c_int)]),
     ("hzp_graph_build", C.c_int, [_P(hzp_model_spec), _P(hzp_parallel), _P(hzp_cost), C.c_int,
                                   C.c_int, _P(_vp)]),
+    ("hzp_graph_build_pipeline", C.c_int, [_P(hzp_model_spec), _P(hzp_parallel), _P(hzp_cost), C.c_int,
+                                           C.c_int, C.c_int, C.c_int, _P(hzp_reuse_report), _P(_vp)]),
     ("hzp_graph_destroy", None, [_vp]),
     ("hzp_graph_size", C.c_int, [_vp]),
     ("hzp_graph_task", C.c_int, [_vp, C.c_int, _P(hzp_task)]),

@@ -149,6 +149,35 @@ int hzp_graph_build(const hzp_model_spec* spec, const hzp_parallel* par, const h
   });
 }
 
+int hzp_graph_build_pipeline(const hzp_model_spec* spec, const hzp_parallel* par, const hzp_cost* cost,
+                             int defer_rs, int rank, int reuse, int recompute, hzp_reuse_report* report,
+                             hzp_graph** out) {
+  if (!spec || !par || !cost || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    CostModel cm;
+    cm.topo = to_topo(cost);
+    cm.device_flops = cost->device_flops;
+    const ModelSpec ms = to_spec(spec);
+    const ParallelConfig pc = to_cfg(par);
+    GraphPolicy pol;
+    pol.defer_rs = defer_rs != 0;
+    pol.rank = rank;
+    pol.order = pipeline_order(pc.pp, pc.vpp, int(ms.num_microbatches), rank);
+    auto* g = new hzp_graph();
+    try {
+      g->g = build_task_graph(ms, pc, cm, pol);
+      ReuseReport rep;
+      if (reuse) rep = apply_reuse(g->g);
+      if (recompute) recompute_rule(g->g);
+      if (report) *report = {rep.r1_eliminated_ag, rep.r2_merged_rs, rep.r3_eliminated_ag, rep.extra_cached_bytes};
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
 void hzp_graph_destroy(hzp_graph* g) { delete g; }
 int hzp_graph_size(const hzp_graph* g) { return g ? static_cast<int>(g->g.tasks.size()) : 0; }
 int64_t hzp_graph_ag_slot_bytes(const hzp_graph* g) { return g ? g->g.ag_slot_bytes : 0; }

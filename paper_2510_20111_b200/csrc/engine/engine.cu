@@ -77,8 +77,29 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   cost.topo.num_nodes = 1;
   cost.topo.ranks_per_node = c.par.dp;
   graph = build_task_graph(spec, ParallelConfig{c.par.dp, c.par.z1, c.par.z2, c.par.z3}, cost, {});
+  if (c.reuse) apply_reuse(graph);
   pools = make_pools(graph, depth, rs_slots);
   plan = build_launch_plan(graph, pools);
+  {
+    const int nt = static_cast<int>(graph.tasks.size());
+    std::vector<int> consumers(nt, 0);
+    for (const Task& t : graph.tasks)
+      if ((t.kind == TaskKind::Fwd || t.kind == TaskKind::Bwd) && !t.deps.empty()) ++consumers[t.deps[0]];
+    ag_slot.assign(nt, -1);
+    param_slot.assign(nt, -1);
+    for (const Task& t : graph.tasks)
+      if (t.kind == TaskKind::AgParam) {
+        const bool cached = consumers[t.id] > 1 && !zero_copy_ag;
+        ag_slot[t.id] = cached ? depth + t.layer : plan.entries[t.id].slot;
+        if (cached) cache_slots = L;
+      }
+    for (const Task& t : graph.tasks)
+      if (t.kind == TaskKind::Fwd || t.kind == TaskKind::Bwd) {
+        if (t.deps.empty() || graph.tasks[t.deps[0]].kind != TaskKind::AgParam)
+          throw std::logic_error("compute task without its all-gather as first dependency");
+        param_slot[t.id] = ag_slot[t.deps[0]];
+      }
+  }
 
   // ---- streams / events ----
   int lo = 0, hi = 0;
@@ -136,7 +157,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   for (int r : mine) {
     LocalRank lr;
     lr.rank = r;
-    HZP_CUDA(cudaMalloc(&lr.ag, size_t(depth) * slot_elems * es));
+    HZP_CUDA(cudaMalloc(&lr.ag, size_t(depth + cache_slots) * slot_elems * es));
     HZP_CUDA(cudaMalloc(&lr.master, size_t(geom.s1) * 4));
     HZP_CUDA(cudaMalloc(&lr.mom, size_t(geom.s1) * 4));
     HZP_CUDA(cudaMalloc(&lr.var, size_t(geom.s1) * 4));
@@ -530,12 +551,12 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
         if (zero_copy_ag) {
           rec_log(e, -1, e.id, e.id);  // identity: layers read the shard in place
         } else {
-          ag_layer(e.layer, e.slot, s);
+          ag_layer(e.layer, ag_slot[e.id], s);
           rec_log(e, int(e.stream), e.id, e.id);
         }
         break;
       case TaskKind::Fwd: {
-        const int slot = plan.entries[e.waits[0]].slot;  // deps[0] = its AG
+        const int slot = param_slot[e.id];
         for (size_t li = 0; li < locals.size(); ++li) {
           const char* in = in_dev + (li * nmb + e.microbatch) * input_bytes_per_mb;
           model->fwd(locals[li].mbuf, e.layer, in, layer_params(int(li), e.layer, slot), s);
@@ -545,7 +566,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
         break;
       }
       case TaskKind::Bwd: {
-        const int slot = plan.entries[e.waits[0]].slot;
+        const int slot = param_slot[e.id];
         const int rs = rs_of_bwd[e.id];
         const int k = rs >= 0 ? rs_index[rs] : 0;
         const int wslot = static_cast<int>((seq0 + k) % wslots);

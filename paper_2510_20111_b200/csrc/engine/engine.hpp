@@ -25,7 +25,7 @@ struct Arena {
 
 struct LocalRank {
   int rank = 0;
-  void* ag = nullptr;  // [depth][slot_elems]
+  void* ag = nullptr;  // [depth + cache_slots][slot_elems]: ring, then the reuse cache
   float* master = nullptr;
   float* mom = nullptr;
   float* var = nullptr;
@@ -50,6 +50,11 @@ struct Engine {
   TaskGraph graph;
   PoolSet pools;
   LaunchPlan plan;
+  // Parameter reuse (cfg.reuse): an AG consumed by more than one FWD/BWD lands
+  // in cache slot depth + layer (it outlives its ring slot); param_slot[task]
+  // = the AG-buffer slot a FWD/BWD reads, ag_slot[task] = where an AG writes.
+  int cache_slots = 0;
+  std::vector<int> param_slot, ag_slot;
 
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> done;

@@ -2,6 +2,7 @@
 // Semantics follow /root/reference/proj/src/sched.cpp:75-387 and are checked
 // bit-exactly (task list, deps, simulated start/end doubles) against
 // tests/golden/sched.json by tests/test_host.py.
+#include <array>
 #include "hzp/sched.hpp"
 
 #include <algorithm>
@@ -79,6 +80,166 @@ class GraphWriter {
 };
 
 }  // namespace
+
+namespace {
+
+struct SlotRun {  // one F or B slot of the graph: its tasks' layers, in order
+  Pass pass;
+  int mb, vstage;
+  std::vector<int> layers;
+};
+
+std::vector<SlotRun> slot_runs(const TaskGraph& g) {
+  std::vector<SlotRun> runs;
+  for (const Task& t : g.tasks) {
+    if (t.kind != TaskKind::Fwd && t.kind != TaskKind::Bwd) continue;
+    if (runs.empty() || runs.back().pass != t.pass || runs.back().mb != t.microbatch ||
+        runs.back().vstage != t.virtual_stage)
+      runs.push_back({t.pass, t.microbatch, t.virtual_stage, {}});
+    runs.back().layers.push_back(t.layer);
+  }
+  return runs;
+}
+
+}  // namespace
+
+ReuseReport apply_reuse(TaskGraph& graph) {
+  const std::vector<SlotRun> runs = slot_runs(graph);
+  // (pass, mb, vstage, layer) -> AG id;  (mb, vstage, layer) -> RS id
+  std::map<std::array<int, 4>, int> ag;
+  std::map<std::array<int, 3>, int> rs;
+  for (const Task& t : graph.tasks) {
+    if (t.kind == TaskKind::AgParam) ag[{int(t.pass), t.microbatch, t.virtual_stage, t.layer}] = t.id;
+    if (t.kind == TaskKind::RsGrad) rs[{t.microbatch, t.virtual_stage, t.layer}] = t.id;
+  }
+  ReuseReport rep;
+  std::vector<int> redirect(graph.tasks.size(), -1);  // dropped task -> keeper
+  auto drop = [&](int victim, int keeper) {
+    if (redirect[victim] >= 0) return false;
+    redirect[victim] = keeper;
+    return true;
+  };
+  auto serve_ags = [&](const SlotRun& from, const SlotRun& to) {
+    int n = 0;
+    for (int layer : to.layers)
+      n += drop(ag.at({int(to.pass), to.mb, to.vstage, layer}), ag.at({int(from.pass), from.mb, from.vstage, layer}));
+    return n;
+  };
+  const size_t n = runs.size();
+  for (size_t i = 0; i + 1 < n; ++i)  // R1
+    if (runs[i].pass == runs[i + 1].pass && runs[i].vstage == runs[i + 1].vstage)
+      rep.r1_eliminated_ag += serve_ags(runs[i], runs[i + 1]);
+  for (size_t i = 0; i + 2 < n; ++i)  // R3
+    if (runs[i].pass == Pass::Forward && runs[i + 1].pass == Pass::Backward &&
+        runs[i + 2].pass == Pass::Forward && runs[i].vstage == runs[i + 2].vstage) {
+      const int k = serve_ags(runs[i], runs[i + 2]);
+      rep.r3_eliminated_ag += k;
+      if (k > 0) rep.extra_cached_bytes += std::int64_t(runs[i + 2].layers.size()) * graph.ag_slot_bytes;
+    }
+  for (size_t i = 0; i < n;) {  // R2
+    if (runs[i].pass != Pass::Backward) {
+      ++i;
+      continue;
+    }
+    size_t j = i;
+    while (j + 1 < n && runs[j + 1].pass == Pass::Backward && runs[j + 1].vstage == runs[i].vstage) ++j;
+    for (int layer : runs[j].layers) {
+      const int keeper = rs.at({runs[j].mb, runs[j].vstage, layer});
+      for (size_t k = i; k < j; ++k) {
+        const int victim = rs.at({runs[k].mb, runs[k].vstage, layer});
+        if (!drop(victim, keeper)) continue;
+        ++rep.r2_merged_rs;
+        std::vector<int>& kd = graph.tasks[keeper].deps;
+        for (int d : graph.tasks[victim].deps)
+          if (std::find(kd.begin(), kd.end(), d) == kd.end()) kd.push_back(d);
+      }
+    }
+    i = j + 1;
+  }
+  // compact: keep order, renumber, route deps through the (transitive) keepers
+  std::vector<int> id_of(graph.tasks.size(), -1);
+  std::vector<Task> out;
+  for (const Task& t : graph.tasks)
+    if (redirect[t.id] < 0) {
+      id_of[t.id] = int(out.size());
+      out.push_back(t);
+    }
+  for (Task& t : out) {
+    std::vector<int> deps;
+    for (int d : t.deps) {
+      while (redirect[d] >= 0) d = redirect[d];
+      const int nd = id_of[d];
+      if (nd >= 0 && std::find(deps.begin(), deps.end(), nd) == deps.end()) deps.push_back(nd);
+    }
+    t.deps = std::move(deps);
+    t.id = id_of[t.id];
+  }
+  graph.tasks = std::move(out);
+  return rep;
+}
+
+void recompute_rule(TaskGraph& graph) {
+  std::map<int, double> fwd_time;  // last FWD of each layer
+  for (const Task& t : graph.tasks)
+    if (t.kind == TaskKind::Fwd) fwd_time[t.layer] = t.duration;
+  std::vector<int> moved(graph.tasks.size());
+  std::vector<Task> out;
+  out.reserve(graph.tasks.size() * 3 / 2);
+  for (const Task& src : graph.tasks) {
+    Task t = src;
+    for (int& d : t.deps) d = moved[d];
+    if (t.kind == TaskKind::Bwd) {
+      Task rc;
+      rc.id = int(out.size());
+      rc.kind = TaskKind::FwdRecompute;
+      rc.layer = t.layer;
+      rc.microbatch = t.microbatch;
+      rc.virtual_stage = t.virtual_stage;
+      rc.pass = Pass::Backward;
+      auto it = fwd_time.find(t.layer);
+      rc.duration = it != fwd_time.end() ? it->second : t.duration / 2.0;
+      rc.deps = t.deps;
+      out.push_back(rc);
+      std::vector<int> deps;
+      for (int d : t.deps)
+        if (out[d].kind == TaskKind::AgParam) deps.push_back(d);
+      deps.push_back(rc.id);
+      t.deps = std::move(deps);
+    }
+    t.id = int(out.size());
+    moved[src.id] = t.id;
+    out.push_back(std::move(t));
+  }
+  graph.tasks = std::move(out);
+}
+
+std::vector<ScheduleSlot> pipeline_order(int pp, int vpp, int microbatches, int rank) {
+  using E = SchedError::Code;
+  if (pp < 1 || vpp < 1 || microbatches < 1) throw SchedError(E::InvalidPolicy, "degrees must be >= 1");
+  if (rank < 0 || rank >= pp) throw SchedError(E::InvalidPolicy, "rank out of range");
+  if (vpp > 1 && microbatches % pp != 0)
+    throw SchedError(E::InvalidPolicy, "interleaved schedule needs microbatches divisible by pp");
+  // unit i of the forward stream -> (microbatch, virtual stage); backward
+  // units walk the virtual stages in reverse.  vpp == 1 reduces to 1F1B.
+  const int units = microbatches * vpp;
+  auto fwd = [&](int i) {
+    return ScheduleSlot{Pass::Forward, (i / (pp * vpp)) * pp + i % pp, (i / pp) % vpp};
+  };
+  auto bwd = [&](int i) {
+    return ScheduleSlot{Pass::Backward, (i / (pp * vpp)) * pp + i % pp, vpp - 1 - (i / pp) % vpp};
+  };
+  const int warm = vpp == 1 ? std::min(pp - rank - 1, microbatches)
+                            : std::min(2 * (pp - rank - 1) + (vpp - 1) * pp, units);
+  std::vector<ScheduleSlot> order;
+  int f = 0, b = 0;
+  while (f < warm) order.push_back(fwd(f++));
+  while (f < units) {
+    order.push_back(fwd(f++));
+    order.push_back(bwd(b++));
+  }
+  while (b < units) order.push_back(bwd(b++));
+  return order;
+}
 
 TaskGraph build_task_graph(const ModelSpec& spec, const ParallelConfig& cfg,
                            const CostModel& cost, const GraphPolicy& policy) {

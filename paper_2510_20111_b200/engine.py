@@ -51,6 +51,7 @@ class EngineConfig:
     gpt_experts: int = 0       # GPT: MoE feed-forward with this many experts (0 = dense)
     gpt_topk: int = 2
     gpt_capacity: int = 0      # slots per expert per microbatch (0 = auto)
+    reuse: int = 0             # CLI parameter reuse (R3 side cache for later forwards)
 
     def c(self) -> N.hzp_engine_config:
         c = N.hzp_engine_config()
@@ -67,6 +68,7 @@ class EngineConfig:
         c.lr, c.beta1, c.beta2, c.eps = self.lr, self.beta1, self.beta2, self.eps
         c.grad_scale, c.device, c.my_rank, c.timeline = self.grad_scale, self.device, self.my_rank, self.timeline
         c.gpt_experts, c.gpt_topk, c.gpt_capacity = self.gpt_experts, self.gpt_topk, self.gpt_capacity
+        c.reuse = self.reuse
         return c
 
 

@@ -116,10 +116,23 @@ class TaskGraph:
     """build_task_graph result (sched.hpp:78-88); owns the native graph."""
 
     def __init__(self, spec: ModelSpec, cfg: ParallelConfig, cost: CostModel,
-                 defer_rs: bool = False, rank: int = 0):
+                 defer_rs: bool = False, rank: int = 0, pipeline: bool = False, reuse: bool = False,
+                 recompute: bool = False):
         h = C.c_void_p()
-        N.check(N.lib.hzp_graph_build(C.byref(spec.c()), C.byref(cfg.c()), C.byref(cost.c()),
-                                      int(defer_rs), rank, C.byref(h)))
+        self.reuse_report = None
+        if pipeline or reuse or recompute:
+            # the CLI's graph: pipeline slot order, then reuse, then recompute
+            rep = N.hzp_reuse_report()
+            N.check(N.lib.hzp_graph_build_pipeline(C.byref(spec.c()), C.byref(cfg.c()), C.byref(cost.c()),
+                                                   int(defer_rs), rank, int(reuse), int(recompute),
+                                                   C.byref(rep), C.byref(h)))
+            if reuse:
+                self.reuse_report = {"r1_eliminated_ag": rep.r1_eliminated_ag, "r2_merged_rs": rep.r2_merged_rs,
+                                     "r3_eliminated_ag": rep.r3_eliminated_ag,
+                                     "extra_cached_bytes": rep.extra_cached_bytes}
+        else:
+            N.check(N.lib.hzp_graph_build(C.byref(spec.c()), C.byref(cfg.c()), C.byref(cost.c()),
+                                          int(defer_rs), rank, C.byref(h)))
         self._h = h
         self.spec, self.cfg = spec, cfg
         t = N.hzp_task()
@@ -141,8 +154,12 @@ class TaskGraph:
             self._h = None
 
 
-def build_task_graph(spec, cfg, cost, defer_rs=False, rank=0) -> TaskGraph:
-    return TaskGraph(spec, cfg, cost, defer_rs, rank)
+def build_task_graph(spec, cfg, cost, defer_rs=False, rank=0, pipeline=False, reuse=False,
+                     recompute=False) -> TaskGraph:
+    """build_task_graph (sched.hpp:90-91); with pipeline/reuse/recompute, the
+    CLI's graph (hzpsim.cpp:111-127): the rank's pipeline schedule order, then
+    apply_reuse, then recompute_rule."""
+    return TaskGraph(spec, cfg, cost, defer_rs, rank, pipeline, reuse, recompute)
 
 
 def make_pools(graph: TaskGraph, prelaunch_depth: int, rs_slots: int):

@@ -121,6 +121,45 @@ def sched_cases(ref: RefLib):
     return {"graphs": out, "prelaunch_depth": depth}
 
 
+def pipeline_cases(ref: RefLib):
+    """The CLI's graph (hzpsim.cpp:111-127): pipeline order for `rank`, then
+    apply_reuse (mode 1) or not (mode 2), then recompute_rule."""
+    out = []
+    grid = [
+        # (layers, num_mb, dp, z1, z2, z3, pp, vpp, rank, mode, recompute, defer)
+        (2, 2, 8, 8, 4, 4, 1, 1, 0, 1, False, False),   # SURVEY App. A-2 with reuse: 23 tasks
+        (4, 4, 8, 8, 4, 4, 1, 1, 0, 1, False, False),
+        (8, 2, 8, 8, 8, 8, 1, 1, 0, 1, True, False),
+        (8, 4, 4, 4, 2, 2, 2, 1, 0, 1, False, False),   # 1F1B warm-up on rank 0
+        (8, 4, 4, 4, 2, 2, 2, 1, 1, 1, False, False),
+        (8, 4, 4, 4, 2, 2, 2, 1, 0, 2, False, False),
+        (8, 4, 4, 4, 2, 2, 2, 1, 0, 1, True, False),
+        (8, 4, 4, 4, 2, 2, 2, 1, 0, 1, False, True),
+        (8, 4, 4, 4, 2, 2, 2, 2, 0, 1, False, False),   # interleaved
+        (8, 4, 4, 4, 2, 2, 2, 2, 1, 1, True, False),
+        (12, 6, 2, 2, 2, 2, 3, 2, 2, 1, False, False),
+        (12, 6, 2, 2, 2, 2, 3, 2, 1, 2, True, True),
+        (4, 3, 8, 8, 4, 4, 4, 1, 3, 1, False, False),
+    ]
+    for L, M, dp, z1, z2, z3, pp, vpp, rank, mode, rec, defer in grid:
+        tasks, summ = ref.task_graph(L, 1000000, seq=1024, num_mb=M, flops=6e6, dp=dp, z1=z1, z2=z2,
+                                     z3=z3, pp=pp, vpp=vpp, intra_bw=1e10, intra_lat=1e-6,
+                                     device_flops=1e12, defer_rs=defer, rank=rank, with_reuse=mode,
+                                     recompute=rec, depth=2, rs_slots=1)
+        out.append({
+            "layers": L, "num_mb": M, "dp": dp, "z1": z1, "z2": z2, "z3": z3, "pp": pp, "vpp": vpp,
+            "rank": rank, "reuse": mode == 1, "recompute": rec, "defer_rs": defer,
+            "ppl": 1000000, "seq": 1024, "flops": 6e6, "intra_bw": 1e10, "intra_lat": 1e-6,
+            "device_flops": 1e12,
+            "tasks": [{k: t[k] for k in ("kind", "layer", "mb", "pass", "bytes", "deps")} for t in tasks],
+            "dur": [t["dur"] for t in tasks],
+            "start": [t["start"] for t in tasks],
+            "end": [t["end"] for t in tasks],
+            "summary": summ,
+        })
+    return {"graphs": out}
+
+
 def layout_cases(ref: RefLib):
     out = []
     for dp in (1, 2, 4, 8):
@@ -174,7 +213,8 @@ def main():
     ref = RefLib()
     o = Oracle()
     for name, payload in (("numerics", numerics_cases(ref, o)), ("sched", sched_cases(ref)),
-                          ("layout", layout_cases(ref)), ("kernels", kernel_cases(ref, o))):
+                          ("layout", layout_cases(ref)),
+                          ("pipeline", pipeline_cases(ref)), ("kernels", kernel_cases(ref, o))):
         path = os.path.join(HERE, f"{name}.json")
         with open(path, "w") as fh:
             json.dump(payload, fh, indent=None, separators=(",", ":"))

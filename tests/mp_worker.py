@@ -80,7 +80,7 @@ def main():
     st = o.shard_init(dims, world, z1, z2, z3, 2024, bool(prec))
     eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=batch, num_microbatches=mbs,
                                  par=ParallelConfig(dp=world, z1=z1, z2=z2, z3=z3), device=local,
-                                 my_rank=rank))
+                                 my_rank=rank, reuse=int(os.environ.get("HZP_TEST_REUSE", "0"))))
     eng.connect()
     eng.load_state(st)
     dist.barrier()

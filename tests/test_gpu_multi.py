@@ -34,16 +34,19 @@ def test_multiprocess_kernels_match_oracle(n, z, prec):
     assert r.stdout.count(": OK") == n
 
 
-@pytest.mark.parametrize("n,z", [(2, (2, 2, 2)), (2, (2, 1, 2)), (2, (2, 2, 1)), (4, (4, 2, 2)),
-                                 (4, (4, 4, 4)), (4, (2, 4, 2))])
+@pytest.mark.parametrize("n,z,reuse", [(2, (2, 2, 2), 0), (2, (2, 1, 2), 0), (2, (2, 2, 1), 0), (4, (4, 2, 2), 0),
+                                       (4, (4, 4, 4), 0), (4, (2, 4, 2), 0), (2, (2, 2, 2), 1), (4, (4, 2, 2), 1)])
 @pytest.mark.parametrize("prec", [0, 1])
-def test_multiprocess_step_matches_oracle(n, z, prec):
+def test_multiprocess_step_matches_oracle(n, z, reuse, prec):
+    """reuse=1: the CLI's R3 reuse (microbatch 1's forward reads microbatch 0's
+    gathered layers from the side cache) over real NVLink peers."""
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n * 10 + prec),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n * 10 + prec + 4 * reuse),
            os.path.join(ROOT, "tests", "mp_worker.py"), *map(str, z), str(prec)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, HZP_TEST_REUSE=str(reuse)))
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert r.stdout.count(": OK") == n

@@ -32,14 +32,14 @@ def rel(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
 
 
-def _run(oracle, cfg, prec, mode=1, timeline=0):
+def _run(oracle, cfg, prec, mode=1, timeline=0, reuse=0):
     from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
     dims, dp, z1, z2, z3, mbs, batch, steps = cfg
     bf16 = bool(prec)
     st = oracle.shard_init(dims, dp, z1, z2, z3, 2024, bf16)
     eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=batch,
                                  num_microbatches=mbs, par=ParallelConfig(dp=dp, z1=z1, z2=z2, z3=z3),
-                                 mode=mode, timeline=timeline))
+                                 mode=mode, timeline=timeline, reuse=reuse))
     eng.load_state(st)
     for step in range(steps):
         x = oracle.make_inputs(dims, dp, mbs, batch, 2024, step)
@@ -88,6 +88,46 @@ def test_launch_log_follows_plan(gpu, oracle, mode):
     tl = eng.timeline()
     assert tl["makespan_ms"] > 0 and tl["compute_busy_ms"] > 0
     # every task starts after each of its waits ended (device clock)
+    for p in plan:
+        for w in p.waits:
+            assert tl["start_ms"][p.id] >= tl["end_ms"][w] - 1e-3
+    eng.close()
+
+
+REUSE_CONFIGS = [c for c in STEP_CONFIGS if c[5] >= 2] + [([12, 20, 8], 4, 4, 2, 2, 3, 4, 5)]
+
+
+@pytest.mark.parametrize("cfg", REUSE_CONFIGS, ids=lambda c: "{}-dp{}-z{}{}{}-mb{}".format("x".join(map(str, c[0])), *c[1:6]))
+def test_reuse_step_matches_oracle_and_no_reuse(gpu, oracle, cfg):
+    """The CLI's apply_reuse (pipeline.cpp:167-279) on the executor: at pp=1 R3
+    drops every later forward's AGs and those forwards read microbatch 0's
+    gathered layers from the side cache.  Same numbers as the oracle (which
+    runs the un-reused step) and bitwise the same as the engine without reuse."""
+    eng, st, losses, ref_losses = _run(oracle, cfg, 0, reuse=1)
+    base, _, base_losses, _ = _run(oracle, cfg, 0, reuse=0)
+    for r in range(cfg[1]):
+        assert rel(eng.param_f32(r), st.param[r]) <= 1e-5, r
+        assert rel(eng.download(r, 2), st.master[r]) <= 1e-5, r
+        assert np.array_equal(eng.param_f32(r), base.param_f32(r)), r
+    assert rel(losses, ref_losses) <= 1e-5
+    assert np.array_equal(np.asarray(losses), np.asarray(base_losses))
+    eng.close()
+    base.close()
+
+
+def test_reuse_launch_log_follows_reused_plan(gpu, oracle):
+    cfg = ([64, 128, 64], 8, 8, 4, 4, 3, 16, 1)
+    eng, st, _, _ = _run(oracle, cfg, 1, timeline=1, reuse=1)
+    log = eng.launch_log()
+    g = H.build_task_graph(H.ModelSpec(num_layers=2, params_per_layer=1, num_microbatches=3),
+                           H.ParallelConfig(dp=8, z1=8, z2=4, z3=4), H.CostModel(ranks_per_node=8), reuse=True)
+    assert g.reuse_report["r3_eliminated_ag"] == 4
+    plan = H.launch_plan(g, 2, 1)
+    assert [r[0] for r in log] == [p.id for p in plan]
+    assert [r[1] for r in log] == [p.kind for p in plan]
+    assert [r[5] for r in log] == [p.slot for p in plan]
+    assert sum(1 for r in log if r[1] == H.AG_PARAM) == 2 * 3 * 2 - 4
+    tl = eng.timeline()
     for p in plan:
         for w in p.waits:
             assert tl["start_ms"][p.id] >= tl["end_ms"][w] - 1e-3

@@ -183,3 +183,56 @@ def test_chrome_trace_matches_reference_format():
         assert e["name"] == H.KIND_NAMES[t.kind] and e["args"]["task_id"] == t.id
         assert abs(e["ts"] - tl.start[t.id] * 1e6) < 1e-6 and e["dur"] >= 0
     assert tr["displayTimeUnit"] == "ms"
+
+
+PIPE = golden("pipeline")
+
+
+@pytest.mark.parametrize("case", PIPE["graphs"],
+                         ids=lambda c: "L{layers}-M{num_mb}-pp{pp}x{vpp}-r{rank}-reuse{reuse}-rc{recompute}-d{defer_rs}".format(**c))
+def test_pipeline_reuse_recompute_bit_exact(case):
+    """The CLI's graph (hzpsim.cpp:111-127): pipeline order, apply_reuse
+    R1/R2/R3 (pipeline.cpp:167-279), recompute_rule (:281-318) — tasks, deps,
+    durations, the reuse report and the simulated timeline bit-exact."""
+    spec = hzp.ModelSpec(num_layers=case["layers"], params_per_layer=case["ppl"], seq_len=case["seq"],
+                         num_microbatches=case["num_mb"], flops_per_token_per_layer=case["flops"])
+    cfg = hzp.ParallelConfig(dp=case["dp"], z1=case["z1"], z2=case["z2"], z3=case["z3"], pp=case["pp"],
+                             vpp=case["vpp"])
+    cost = hzp.CostModel(num_nodes=1, ranks_per_node=case["dp"] * case["pp"], intra_bw=case["intra_bw"],
+                         inter_bw=case["intra_bw"], intra_latency=case["intra_lat"],
+                         device_flops=case["device_flops"])
+    g = hzp.build_task_graph(spec, cfg, cost, defer_rs=case["defer_rs"], rank=case["rank"], pipeline=True,
+                             reuse=case["reuse"], recompute=case["recompute"])
+    assert [(t.kind, t.layer, t.microbatch, t.pass_, t.bytes, t.deps) for t in g.tasks] == \
+           [(b["kind"], b["layer"], b["mb"], b["pass"], b["bytes"], b["deps"]) for b in case["tasks"]]
+    assert [t.duration for t in g.tasks] == case["dur"]
+    if case["reuse"]:
+        for k in ("r1_eliminated_ag", "r2_merged_rs", "r3_eliminated_ag", "extra_cached_bytes"):
+            assert g.reuse_report[k] == case["summary"][k], k
+    tl = hzp.simulate(g, 2, 1, hzp.ASYNC)
+    assert tl.start == case["start"] and tl.end == case["end"]
+    assert tl.makespan == case["summary"]["makespan"]
+    assert tl.compute_idle == case["summary"]["compute_idle"]
+
+
+def test_survey_a2_reuse_drops_mb1_forward_ags():
+    # SURVEY App. A-2: with the CLI's reuse at pp=1, R3 removes mb1's forward AGs -> 23 tasks
+    g = hzp.build_task_graph(hzp.ModelSpec(num_layers=2, params_per_layer=10**6, num_microbatches=2,
+                                           flops_per_token_per_layer=6e6, seq_len=1024),
+                             hzp.ParallelConfig(dp=8, z1=8, z2=4, z3=4),
+                             hzp.CostModel(ranks_per_node=8, intra_bw=1e10, inter_bw=1e10), reuse=True)
+    assert len(g.tasks) == 23
+    assert g.reuse_report == {"r1_eliminated_ag": 0, "r2_merged_rs": 0, "r3_eliminated_ag": 2,
+                              "extra_cached_bytes": 2 * g.ag_slot_bytes}
+    fwd_mb1 = [t for t in g.tasks if t.kind == hzp.hzp.FWD and t.microbatch == 1]
+    # each mb1 forward now waits on mb0's forward AG of the same layer
+    for t in fwd_mb1:
+        ag = g.tasks[t.deps[0]]
+        assert (ag.kind, ag.layer, ag.microbatch, ag.pass_) == (hzp.hzp.AG_PARAM, t.layer, 0, 0)
+
+
+def test_pipeline_order_errors():
+    spec = hzp.ModelSpec(num_layers=8, params_per_layer=1000, num_microbatches=3)
+    cost = hzp.CostModel(ranks_per_node=8)
+    with pytest.raises(N.HzpError):  # interleaved needs microbatches % pp == 0
+        hzp.build_task_graph(spec, hzp.ParallelConfig(dp=4, z1=4, z2=2, z3=2, pp=2, vpp=2), cost, pipeline=True)
