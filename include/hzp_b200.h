@@ -209,6 +209,11 @@ typedef struct {
    * lands in a per-layer side cache (full bf16 layer per layer) instead of a
    * ring slot; backward all-gathers keep the ring. */
   int reuse;
+  /* 1 = activation recomputation (recompute_rule, pipeline.cpp:281-318): a
+   * FWD-recompute task before every BWD.  GPT blocks then keep only their
+   * input and share one activation set, rebuilt by the recompute (the
+   * embedding / head keep their outputs: their recompute is a no-op). */
+  int recompute;
 } hzp_engine_config;
 
 typedef struct hzp_ctx hzp_ctx;

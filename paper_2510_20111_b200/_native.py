@@ -78,7 +78,8 @@ class hzp_engine_config(C.Structure):
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("grad_scale", C.c_double), ("device", C.c_int), ("my_rank", C.c_int),
                 ("timeline", C.c_int), ("gpt_experts", C.c_int), ("gpt_topk", C.c_int),
-                ("gpt_capacity", C.c_int), ("reuse", C.c_int)]
+                ("gpt_capacity", C.c_int), ("reuse", C.c_int),
+                ("recompute", C.c_int)]
 
 
 class hzp_launch_rec(C.Structure):

@@ -51,6 +51,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     mcfg.experts = c.gpt_experts;
     mcfg.topk = c.gpt_topk;
     mcfg.capacity = c.gpt_capacity;
+    mcfg.recompute = c.recompute;
     if (!bf16) throw std::invalid_argument("the GPT model runs in bf16 only");
     model = make_gpt_model(mcfg);
   }
@@ -78,27 +79,51 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   cost.topo.ranks_per_node = c.par.dp;
   graph = build_task_graph(spec, ParallelConfig{c.par.dp, c.par.z1, c.par.z2, c.par.z3}, cost, {});
   if (c.reuse) apply_reuse(graph);
+  if (c.recompute) recompute_rule(graph);
   pools = make_pools(graph, depth, rs_slots);
   plan = build_launch_plan(graph, pools);
   {
     const int nt = static_cast<int>(graph.tasks.size());
-    std::vector<int> consumers(nt, 0);
-    for (const Task& t : graph.tasks)
-      if ((t.kind == TaskKind::Fwd || t.kind == TaskKind::Bwd) && !t.deps.empty()) ++consumers[t.deps[0]];
+    auto is_compute = [](TaskKind k) {
+      return k == TaskKind::Fwd || k == TaskKind::Bwd || k == TaskKind::FwdRecompute;
+    };
+    std::vector<int> passes(nt, 0), last_use(nt, -1);
+    for (const Task& t : graph.tasks) {
+      if (!is_compute(t.kind)) continue;
+      if (t.deps.empty() || graph.tasks[t.deps[0]].kind != TaskKind::AgParam)
+        throw std::logic_error("compute task without its all-gather as first dependency");
+      if (t.kind != TaskKind::FwdRecompute) ++passes[t.deps[0]];
+      for (int d : t.deps)
+        if (graph.tasks[d].kind == TaskKind::AgParam) last_use[d] = t.id;
+    }
     ag_slot.assign(nt, -1);
     param_slot.assign(nt, -1);
-    for (const Task& t : graph.tasks)
+    ag_phys_wait.assign(nt, -1);
+    std::vector<int> ring;  // AG-pool issue order (plan ring rule)
+    for (const Task& t : graph.tasks) {
       if (t.kind == TaskKind::AgParam) {
-        const bool cached = consumers[t.id] > 1 && !zero_copy_ag;
+        // several passes read it (reuse): it outlives its ring slot
+        const bool cached = passes[t.id] > 1 && !zero_copy_ag;
         ag_slot[t.id] = cached ? depth + t.layer : plan.entries[t.id].slot;
         if (cached) cache_slots = L;
+        // the ring frees a slot at its occupant's FIRST consumer; a later
+        // reader (the BWD after its FWD-recompute) must finish before the
+        // slot is overwritten on the device
+        const int k = static_cast<int>(ring.size());
+        if (k >= depth && !cached) {
+          const int prev = ring[k - depth];
+          const bool prev_in_ring = ag_slot[prev] < depth;
+          if (prev_in_ring && last_use[prev] >= 0 && last_use[prev] != plan.entries[t.id].ring_wait) {
+            if (last_use[prev] > t.id) throw std::logic_error("slot reader issued after the AG that overwrites it");
+            ag_phys_wait[t.id] = last_use[prev];
+          }
+        }
       }
+      if (uses_ag_pool(t.kind)) ring.push_back(t.id);
+      if (is_compute(t.kind)) param_slot[t.id] = -2;
+    }
     for (const Task& t : graph.tasks)
-      if (t.kind == TaskKind::Fwd || t.kind == TaskKind::Bwd) {
-        if (t.deps.empty() || graph.tasks[t.deps[0]].kind != TaskKind::AgParam)
-          throw std::logic_error("compute task without its all-gather as first dependency");
-        param_slot[t.id] = ag_slot[t.deps[0]];
-      }
+      if (param_slot[t.id] == -2) param_slot[t.id] = ag_slot[t.deps[0]];
   }
 
   // ---- streams / events ----
@@ -551,6 +576,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
         if (zero_copy_ag) {
           rec_log(e, -1, e.id, e.id);  // identity: layers read the shard in place
         } else {
+          if (ag_phys_wait[e.id] >= 0) HZP_CUDA(cudaStreamWaitEvent(s, done[ag_phys_wait[e.id]], 0));
           ag_layer(e.layer, ag_slot[e.id], s);
           rec_log(e, int(e.stream), e.id, e.id);
         }
@@ -562,6 +588,14 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
           model->fwd(locals[li].mbuf, e.layer, in, layer_params(int(li), e.layer, slot), s);
         }
         launches += int64_t(locals.size()) * model->launches_per_fwd();
+        rec_log(e, 0, e.id, e.id);
+        break;
+      }
+      case TaskKind::FwdRecompute: {
+        const int slot = param_slot[e.id];
+        for (size_t li = 0; li < locals.size(); ++li)
+          model->recompute(locals[li].mbuf, e.layer, layer_params(int(li), e.layer, slot), s);
+        launches += int64_t(locals.size()) * model->launches_per_recompute(e.layer);
         rec_log(e, 0, e.id, e.id);
         break;
       }

@@ -55,6 +55,7 @@ struct Engine {
   // = the AG-buffer slot a FWD/BWD reads, ag_slot[task] = where an AG writes.
   int cache_slots = 0;
   std::vector<int> param_slot, ag_slot;
+  std::vector<int> ag_phys_wait;  // AG task -> extra wait (last reader of the slot's occupant)
 
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> done;

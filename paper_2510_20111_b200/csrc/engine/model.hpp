@@ -47,6 +47,11 @@ class Model {
                    cudaStream_t s) = 0;
   virtual void bwd(void* b, int layer, const void* params, const GradTarget& g,
                    cudaStream_t s) = 0;
+  // FWD-recompute of `layer` just before its BWD (recompute_rule,
+  // pipeline.cpp:281-318): rebuild the activations the BWD reads from the
+  // layer's saved input.  No-op for models / layers that keep them.
+  virtual void recompute(void* b, int layer, const void* params, cudaStream_t s) {}
+  virtual int64_t launches_per_recompute(int layer) const { return 0; }
   virtual const float* loss_device(void* b) const = 0;          // fp32 summed loss
   virtual int64_t launches_per_fwd() const { return 1; }
 };
@@ -58,6 +63,7 @@ struct ModelConfig {
   int batch = 1;       // MLP rows / GPT sequences per microbatch
   int layers = 0, hidden = 0, heads = 0, ffn = 0, vocab = 0, seq = 0;
   int experts = 0, topk = 2, capacity = 0;  // GPT MoE feed-forward (experts = 0: dense)
+  int recompute = 0;   // GPT: keep only block inputs; blocks share one activation set
 };
 
 std::unique_ptr<Model> make_mlp_model(const ModelConfig& c);

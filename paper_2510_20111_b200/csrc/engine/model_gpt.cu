@@ -170,7 +170,9 @@ class GptModel final : public Model {
     B->x.assign(L_ + 2, nullptr);
     for (int l = 1; l <= L_ + 1; ++l) B->x[l] = bf(T_ * h_);
     B->acts.resize(L_ + 2);
-    for (int l = 1; l <= L_; ++l) {
+    // recompute: one activation set shared by every block (rebuilt from the
+    // block's input x[l] by its FWD-recompute before the BWD reads it)
+    for (int l = 1; l <= (c_.recompute ? 1 : L_); ++l) {
       LayerActs& a = B->acts[l];
       a.ln1 = bf(T_ * h_);
       a.qkv = bf(T_ * 3 * h_);
@@ -197,6 +199,8 @@ class GptModel final : public Model {
       a.mu2 = f32(T_);
       a.rs2 = f32(T_);
     }
+    if (c_.recompute)
+      for (int l = 2; l <= L_; ++l) B->acts[l] = B->acts[1];
     B->lnf = bf(T_ * h_);
     B->muf = f32(T_);
     B->rsf = f32(T_);
@@ -230,7 +234,8 @@ class GptModel final : public Model {
   void free_rank_buffers(void* p) override {
     auto* B = static_cast<GptBuffers*>(p);
     for (auto* x : B->x) cudaFree(x);
-    for (auto& a : B->acts) {
+    for (int l = 0; l < int(B->acts.size()) && !(c_.recompute && l > 1); ++l) {
+      const LayerActs& a = B->acts[l];
       for (void* q : {(void*)a.ln1, (void*)a.qkv, (void*)a.lse, (void*)a.attn, (void*)a.xm,
                       (void*)a.ln2, (void*)a.fpre, (void*)a.fact, (void*)a.mu1, (void*)a.rs1,
                       (void*)a.mu2, (void*)a.rs2, (void*)a.logits, (void*)a.probs, (void*)a.gate,
@@ -446,6 +451,21 @@ class GptModel final : public Model {
       cross_entropy(B->logits, B->tokens, b_, S_, V_, B->loss, s);
       return;
     }
+    block_fwd(B, l, W, true, s);
+  }
+
+  void recompute(void* p, int l, const void* params, cudaStream_t s) override {
+    if (!c_.recompute || l < 1 || l > L_) return;  // embedding / head keep their outputs
+    block_fwd(static_cast<GptBuffers*>(p), l, static_cast<const uint16_t*>(params), false, s);
+  }
+  int64_t launches_per_recompute(int l) const override {
+    return c_.recompute && l >= 1 && l <= L_ ? launches_per_fwd() - (E_ > 0 ? 0 : 1) : 0;
+  }
+
+  // One transformer block.  need_out = false (FWD-recompute): only the
+  // activations the BWD reads; the dense FFN's output GEMM (x[l+1], already
+  // consumed) is skipped.
+  void block_fwd(GptBuffers* B, int l, const uint16_t* W, bool need_out, cudaStream_t s) {
     const LayerActs& a = B->acts[l];
     const BlockOff& o = bo_;
     const int64_t h3 = 3 * int64_t(h_);
@@ -466,7 +486,7 @@ class GptModel final : public Model {
     }
     layernorm_fwd(a.xm, W + o.ln2_g, W + o.ln2_b, a.ln2, a.mu2, a.rs2, int(T_), h_, s);
     if (E_ > 0) {
-      moe_fwd(a, W, B->x[l + 1], s);
+      moe_fwd(a, W, B->x[l + 1], s);  // recompute rewrites x[l+1] with identical values
       return;
     }
     {
@@ -477,7 +497,7 @@ class GptModel final : public Model {
       e.ldaux = f_;
       linear_fwd(a.ln2, W + o.w_fc1, a.fact, f_, h_, e, s);
     }
-    {
+    if (need_out) {
       Epilogue e;
       e.bias_any = W + o.b_fc2;
       e.resid = a.xm;

@@ -52,6 +52,7 @@ class EngineConfig:
     gpt_topk: int = 2
     gpt_capacity: int = 0      # slots per expert per microbatch (0 = auto)
     reuse: int = 0             # CLI parameter reuse (R3 side cache for later forwards)
+    recompute: int = 0         # activation recomputation (FWD-recompute before each BWD)
 
     def c(self) -> N.hzp_engine_config:
         c = N.hzp_engine_config()
@@ -69,6 +70,7 @@ class EngineConfig:
         c.grad_scale, c.device, c.my_rank, c.timeline = self.grad_scale, self.device, self.my_rank, self.timeline
         c.gpt_experts, c.gpt_topk, c.gpt_capacity = self.gpt_experts, self.gpt_topk, self.gpt_capacity
         c.reuse = self.reuse
+        c.recompute = self.recompute
         return c
 
 

@@ -77,12 +77,12 @@ def torch_loss(c, flat, tokens):
     return torch.nn.functional.cross_entropy(logits.reshape(-1, logits.shape[-1]), tgt.reshape(-1))
 
 
-def _engine(c, dp=1, z=(1, 1, 1), mbs=1):
+def _engine(c, dp=1, z=(1, 1, 1), mbs=1, **kw):
     from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
     return HzpEngine(EngineConfig(model=1, precision=1, gpt_layers=c["layers"], gpt_hidden=c["hidden"],
                                   gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
                                   gpt_seq=c["seq"], batch=c["batch"], num_microbatches=mbs,
-                                  par=ParallelConfig(dp=dp, z1=z[0], z2=z[1], z3=z[2])))
+                                  par=ParallelConfig(dp=dp, z1=z[0], z2=z[1], z3=z[2]), **kw))
 
 
 def _bf16_bits(x):
@@ -154,3 +154,31 @@ def test_gpt_emulated_dp_matches_single_rank(gpu):
     assert np.max(d) <= 2.5e-3 and np.mean(d > 1e-3) < 1e-2, (np.max(d), np.mean(d > 1e-3))
     e1.close()
     e2.close()
+
+
+@pytest.mark.parametrize("experts", [0, 8], ids=["dense", "moe"])
+def test_gpt_reuse_and_recompute_are_bitwise_neutral(gpu, experts):
+    """§8(f)-3 on the GPT engine: the CLI's reuse (R3: microbatch 1's forward
+    reads microbatch 0's gathered blocks from the side cache) and activation
+    recomputation (recompute_rule: one shared activation set, rebuilt by a
+    FWD-recompute before each BWD) change where data lives and what is
+    recomputed, never the arithmetic — losses and updated parameters are
+    bitwise those of the plain schedule.  dp=2 emulated (z3 = 2: real AGs)."""
+    c = dict(CFG, layers=3)
+    rng = np.random.default_rng(5)
+    tok = rng.integers(0, c["vocab"], size=(2, 2, c["batch"], c["seq"] + 1), dtype=np.int32)
+    out = {}
+    for reuse, rc in ((0, 0), (1, 0), (0, 1), (1, 1)):
+        e = _engine(c, dp=2, z=(2, 2, 2), mbs=2, reuse=reuse, recompute=rc, gpt_experts=experts)
+        e.init_random(seed=11, scale=0.04)
+        losses = [np.asarray(e.step(tok)) for _ in range(2)]
+        out[(reuse, rc)] = (losses, [e.param_f32(r) for r in range(2)])
+        if rc:
+            assert sum(1 for r in e.launch_log() if r[1] == 2) > 0  # FWD-recompute tasks ran
+        e.close()
+    base_l, base_p = out[(0, 0)]
+    for k, (l, p) in out.items():
+        for a, b in zip(l, base_l):
+            assert np.array_equal(a, b), k
+        for a, b in zip(p, base_p):
+            assert np.array_equal(a, b), k
