@@ -110,7 +110,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
         // reader (the BWD after its FWD-recompute) must finish before the
         // slot is overwritten on the device
         const int k = static_cast<int>(ring.size());
-        if (k >= depth && !cached) {
+        if (k >= depth && !cached && !zero_copy_ag) {
           const int prev = ring[k - depth];
           const bool prev_in_ring = ag_slot[prev] < depth;
           if (prev_in_ring && last_use[prev] >= 0 && last_use[prev] != plan.entries[t.id].ring_wait) {

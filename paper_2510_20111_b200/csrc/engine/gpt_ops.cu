@@ -1,6 +1,8 @@
 // Non-GEMM kernels of the GPT decoder.  See gpt_ops.cuh.
 #include <cmath>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "engine/gemm.cuh"
 #include "engine/gpt_ops.cuh"
 #include "engine/tc_ptx.cuh"
@@ -66,23 +68,51 @@ __global__ void __launch_bounds__(kT) embed_fwd_kernel(const int* __restrict__ t
   }
 }
 
-__global__ void __launch_bounds__(kT) embed_bwd_kernel(const int* __restrict__ tok,
-                                                       const uint16_t* __restrict__ dx,
-                                                       float* __restrict__ dwte,
-                                                       float* __restrict__ dwpe, int S, int h) {
-  const int t = blockIdx.x;
-  const int bi = t / S, s = t % S;
-  const int id = tok[bi * (S + 1) + s];
-  const uint4* d = reinterpret_cast<const uint4*>(dx + int64_t(t) * h);
+__global__ void embed_keys_kernel(const int* __restrict__ tok, int* __restrict__ key, int* __restrict__ val,
+                                  int T, int S) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  key[t] = tok[(t / S) * (S + 1) + t % S];
+  val[t] = t;
+}
+
+// one CTA per sorted position; the first position of each id's run sums the
+// run's rows (ascending token order: the sort is stable) into dwte[id]
+__global__ void __launch_bounds__(kT) embed_wte_grad_kernel(const int* __restrict__ key,
+                                                            const int* __restrict__ val,
+                                                            const uint16_t* __restrict__ dx,
+                                                            float* __restrict__ dwte, int T, int h) {
+  const int i = blockIdx.x;
+  const int id = key[i];
+  if (i > 0 && key[i - 1] == id) return;
+  int end = i + 1;
+  while (end < T && key[end] == id) ++end;
   for (int v = threadIdx.x; v < h / 8; v += blockDim.x) {
-    float f[8];
-    unpack8(d[v], f);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = i; j < end; ++j) {
+      float f[8];
+      unpack8(reinterpret_cast<const uint4*>(dx + int64_t(val[j]) * h)[v], f);
+      for (int q = 0; q < 8; ++q) acc[q] += f[q];
+    }
     float4* a = reinterpret_cast<float4*>(dwte + int64_t(id) * h + 8 * v);
+    a[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    a[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+__global__ void __launch_bounds__(kT) embed_wpe_grad_kernel(const uint16_t* __restrict__ dx,
+                                                            float* __restrict__ dwpe, int b, int S, int h) {
+  const int s = blockIdx.x;
+  for (int v = threadIdx.x; v < h / 8; v += blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int bi = 0; bi < b; ++bi) {
+      float f[8];
+      unpack8(reinterpret_cast<const uint4*>(dx + (int64_t(bi) * S + s) * h)[v], f);
+      for (int q = 0; q < 8; ++q) acc[q] += f[q];
+    }
     float4* p = reinterpret_cast<float4*>(dwpe + int64_t(s) * h + 8 * v);
-    atomicAdd(a, make_float4(f[0], f[1], f[2], f[3]));
-    atomicAdd(a + 1, make_float4(f[4], f[5], f[6], f[7]));
-    atomicAdd(p, make_float4(f[0], f[1], f[2], f[3]));
-    atomicAdd(p + 1, make_float4(f[4], f[5], f[6], f[7]));
+    p[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    p[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
 
@@ -256,7 +286,7 @@ __global__ void attn_rowdot_kernel(const uint16_t* __restrict__ dO, const uint16
 __global__ void __launch_bounds__(kT) cross_entropy_kernel(uint16_t* __restrict__ logits,
                                                            const int* __restrict__ tok, int S,
                                                            int V, float inv_T,
-                                                           float* __restrict__ loss) {
+                                                           float* __restrict__ row_loss) {
   __shared__ float red[32];
   const int t = blockIdx.x;
   const int bi = t / S, s = t % S;
@@ -290,7 +320,17 @@ __global__ void __launch_bounds__(kT) cross_entropy_kernel(uint16_t* __restrict_
     }
     reinterpret_cast<uint4*>(row)[v] = pack8(f);
   }
-  if (threadIdx.x == 0) atomicAdd(loss, (lse - xt) * inv_T);
+  if (threadIdx.x == 0) row_loss[t] = (lse - xt) * inv_T;
+}
+
+// *loss += sum of the row losses, in a fixed order (deterministic)
+__global__ void __launch_bounds__(1024) loss_sum_kernel(const float* __restrict__ row_loss, int T,
+                                                       float* __restrict__ loss) {
+  __shared__ float red[32];
+  float acc = 0.f;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) acc += row_loss[t];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) *loss += acc;
 }
 
 
@@ -604,9 +644,42 @@ void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint
   embed_fwd_kernel<<<b * S, kT, 0, s>>>(tokens, wte, wpe, x, S, h);
   HZP_LAUNCH_CHECK();
 }
-void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, int b, int S, int h,
-               cudaStream_t s) {
-  embed_bwd_kernel<<<b * S, kT, 0, s>>>(tokens, dx, dwte, dwpe, S, h);
+namespace {
+int key_bits(int V) {
+  int bits = 1;
+  while ((1 << bits) < V) ++bits;
+  return bits;
+}
+size_t sort_temp_bytes(int T, int V) {
+  size_t bytes = 0;
+  HZP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const int*>(nullptr),
+                                           static_cast<int*>(nullptr), static_cast<const int*>(nullptr),
+                                           static_cast<int*>(nullptr), T, 0, key_bits(V)));
+  return (bytes + 255) / 256 * 256;
+}
+}  // namespace
+
+size_t embed_bwd_ws_bytes(int T, int V) {
+  const size_t arr = (size_t(T) * 4 + 255) / 256 * 256;
+  return 4 * arr + sort_temp_bytes(T, V);
+}
+
+void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, int b, int S, int h, int V,
+               void* ws, cudaStream_t s) {
+  const int T = b * S;
+  const size_t arr = (size_t(T) * 4 + 255) / 256 * 256;
+  char* w = static_cast<char*>(ws);
+  int* key_in = reinterpret_cast<int*>(w);
+  int* val_in = reinterpret_cast<int*>(w + arr);
+  int* key = reinterpret_cast<int*>(w + 2 * arr);
+  int* val = reinterpret_cast<int*>(w + 3 * arr);
+  size_t temp = sort_temp_bytes(T, V);
+  embed_keys_kernel<<<(T + 255) / 256, 256, 0, s>>>(tokens, key_in, val_in, T, S);
+  HZP_LAUNCH_CHECK();
+  HZP_CUDA(cub::DeviceRadixSort::SortPairs(w + 4 * arr, temp, key_in, key, val_in, val, T, 0, key_bits(V), s));
+  embed_wte_grad_kernel<<<T, kT, 0, s>>>(key, val, dx, dwte, T, h);
+  HZP_LAUNCH_CHECK();
+  embed_wpe_grad_kernel<<<S, kT, 0, s>>>(dx, dwpe, b, S, h);
   HZP_LAUNCH_CHECK();
 }
 void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
@@ -673,10 +746,12 @@ void attn_rowdot(const uint16_t* dO, const uint16_t* O, const float* lse, float*
                                                                       1.f / sqrtf(float(hd)));
   HZP_LAUNCH_CHECK();
 }
-void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* loss,
+void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* row_loss, float* loss,
                    cudaStream_t s) {
   if (V % 8) throw std::invalid_argument("vocab must be a multiple of 8");
-  cross_entropy_kernel<<<b * S, kT, 0, s>>>(logits, tokens, S, V, 1.f / float(b * S), loss);
+  cross_entropy_kernel<<<b * S, kT, 0, s>>>(logits, tokens, S, V, 1.f / float(b * S), row_loss);
+  HZP_LAUNCH_CHECK();
+  loss_sum_kernel<<<1, 1024, 0, s>>>(row_loss, b * S, loss);
   HZP_LAUNCH_CHECK();
 }
 

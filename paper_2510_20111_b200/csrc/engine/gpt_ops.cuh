@@ -12,9 +12,14 @@ namespace hzp {
 // x[t] = wte[tok[t]] + wpe[t % S]; tokens laid out [b][S+1] (inputs = [:, :S]).
 void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int b, int S,
                int h, cudaStream_t s);
-// Scatter-add dx rows into fp32 scratch: dwte[tok[t]] += dx[t], dwpe[s] += dx[t].
-void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, int b, int S, int h,
-               cudaStream_t s);
+// Embedding gradient, deterministic (no float atomics): tokens are stably
+// sorted by id (CUB radix sort) and every id's rows are summed in ascending
+// token order; dwpe[s] = sum over sequences in order.  Writes the rows of
+// dwte that occur and all of dwpe (the caller zeroes dwte).  ws: a workspace
+// of embed_bwd_ws_bytes(b * S, V) bytes.
+size_t embed_bwd_ws_bytes(int T, int V);
+void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, int b, int S, int h, int V,
+               void* ws, cudaStream_t s);
 
 // LayerNorm over h (eps 1e-5): y = (x - mu) * rstd * g + beta; saves mu, rstd.
 void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
@@ -40,8 +45,9 @@ void attn_rowdot(const uint16_t* dO, const uint16_t* O, const float* lse, float*
                  int hd, cudaStream_t s);
 
 // Fused softmax cross-entropy over rows of bf16 logits [T, V]: loss +=
-// sum_t (lse - logit[target]) / T; logits <- (softmax - onehot) / T in place.
-void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* loss,
+// sum_t (lse - logit[target]) / T (row losses in row_loss [T], summed in a
+// fixed order); logits <- (softmax - onehot) / T in place.
+void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* row_loss, float* loss,
                    cudaStream_t s);
 
 }  // namespace hzp

@@ -67,6 +67,8 @@ struct GptBuffers {
   uint16_t *moe_dy = nullptr, *moe_dh = nullptr, *moe_dxp = nullptr, *moe_dlogits = nullptr;
   float* moe_dgate = nullptr;
   float* emb = nullptr;        // fp32 scratch for the embedding gradient [V*h + S*h]
+  void* emb_ws = nullptr;      // embed_bwd's sort workspace
+  float* row_loss = nullptr;   // [T] per-token loss (summed in a fixed order)
   float* loss = nullptr;
   const int* tokens = nullptr;  // current microbatch
 };
@@ -227,6 +229,8 @@ class GptModel final : public Model {
     HZP_CUDA(cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking));
     for (auto& e : B->ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     B->emb = f32(int64_t(V_) * h_ + int64_t(S_) * h_);
+    HZP_CUDA(cudaMalloc(&B->emb_ws, embed_bwd_ws_bytes(int(T_), V_)));
+    B->row_loss = f32(T_);
     B->loss = f32(1);
     HZP_CUDA(cudaMemset(B->loss, 0, 4));
     return B;
@@ -248,7 +252,7 @@ class GptModel final : public Model {
                     (void*)B->dqkv, (void*)B->dattn, (void*)B->dfc1, (void*)B->dxm, (void*)B->part,
                     (void*)B->part_side, (void*)B->moe_dy, (void*)B->moe_dh, (void*)B->moe_dxp,
                     (void*)B->moe_dlogits, (void*)B->moe_dgate,
-                    (void*)B->emb, (void*)B->loss})
+                    (void*)B->emb, B->emb_ws, (void*)B->row_loss, (void*)B->loss})
       cudaFree(q);
     for (auto e : B->ev) cudaEventDestroy(e);
     if (B->side) cudaStreamDestroy(B->side);
@@ -448,7 +452,7 @@ class GptModel final : public Model {
       Epilogue e;
       e.out_bf16 = 1;
       linear_fwd(B->lnf, W + 2 * h_, B->logits, V_, h_, e, s);
-      cross_entropy(B->logits, B->tokens, b_, S_, V_, B->loss, s);
+      cross_entropy(B->logits, B->tokens, b_, S_, V_, B->row_loss, B->loss, s);
       return;
     }
     block_fwd(B, l, W, true, s);
@@ -526,8 +530,8 @@ class GptModel final : public Model {
     }
     if (l == 0) {
       const int64_t nw = int64_t(V_) * h_, np = int64_t(S_) * h_;
-      HZP_CUDA(cudaMemsetAsync(B->emb, 0, size_t(nw + np) * 4, s));
-      embed_bwd(B->tokens, B->dx[B->cur], B->emb, B->emb + nw, b_, S_, h_, s);
+      HZP_CUDA(cudaMemsetAsync(B->emb, 0, size_t(nw) * 4, s));
+      embed_bwd(B->tokens, B->dx[B->cur], B->emb, B->emb + nw, b_, S_, h_, V_, B->emb_ws, s);
       grad_write(B->emb, nw + np, g.ptr, g.bf16, g.mode, s);
       return;
     }
