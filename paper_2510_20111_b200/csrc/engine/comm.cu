@@ -12,6 +12,8 @@
 //  * every reduction sums in ascending rank order in fp32 with IEEE
 //    round-to-nearest adds (no FMA contraction), so results are bit-identical
 //    to the reference's canonical order.
+#include <type_traits>
+
 #include "engine/comm.cuh"
 
 namespace hzp {
@@ -75,13 +77,19 @@ __global__ void __maxnreg__(kCommRegs) ag_pull_kernel(const RankTable* __restric
         for (int u = 0; u < kUnroll; ++u) st_v4(d4 + i + u * kCommThreads, v[u]);
       }
       for (; i < nv; i += kCommThreads) st_v4(d4 + i, ld_nc_v4(s4 + i));
-    } else {
-      for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
-        if (kElemBytes == 2)
-          reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(src)[i];
-        else
-          reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+    } else {  // unaligned span: element-wise, kUnroll loads in flight per thread
+      using E = typename std::conditional<kElemBytes == 2, uint16_t, uint32_t>::type;
+      const E* se = reinterpret_cast<const E*>(src);
+      E* de = reinterpret_cast<E*>(dst);
+      int64_t i = threadIdx.x;
+      for (; i + (kUnroll - 1) * kCommThreads < t.len; i += kUnroll * kCommThreads) {
+        E v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) v[u] = se[i + u * kCommThreads];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) de[i + u * kCommThreads] = v[u];
       }
+      for (; i < t.len; i += kCommThreads) de[i] = se[i];
     }
   }
 }

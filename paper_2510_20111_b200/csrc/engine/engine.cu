@@ -288,6 +288,16 @@ void Engine::build_tiles() {
       }
       runs.push_back({t.local, t.src, t.a_off, t.b_off, t.len});
     }
+  if (!emulate && locals.size() == 1) {
+    // rotate the owners: rank r reads owner r+1 first, r+2 next, ..., its own
+    // shard last, so at every moment each owner's egress serves one reader
+    // (ascending order would have every rank hit owner 0 first)
+    const int me = cfg.my_rank % geom.z3;
+    auto phase = [&](const CopyRun& r) { return (r.src % geom.z3 - me - 1 + 2 * geom.z3) % geom.z3; };
+    for (auto& runs : ag_runs)
+      std::stable_sort(runs.begin(), runs.end(),
+                       [&](const CopyRun& a, const CopyRun& b) { return phase(a) < phase(b); });
+  }
   z1_off = T.z1_off;
   z1_n = T.z1_n;
   if (dtiles) cudaFree(dtiles);
@@ -404,8 +414,8 @@ void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
       const int c1 = std::min(t1, c0 + kRsChunkTiles);
       const int64_t b0 = tiles_host[c0].b_off;
       const int64_t b1 = tiles_host[c1 - 1].b_off + tiles_host[c1 - 1].len;
-      for (int q = 0; q < geom.z2; ++q) {
-        const int g = base + q;
+      for (int j = 1; j < geom.z2; ++j) {  // rotated: peer r+1 first (one reader per owner)
+        const int g = base + (cfg.my_rank - base + j) % geom.z2;
         if (!rs_stage[g]) continue;  // this rank's own buffer is read in place
         HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(rs_stage[g]) + b0 * es,
                                  static_cast<const char*>(table.wgrad[g]) + (wslot * slot_elems + b0) * es,
