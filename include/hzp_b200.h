@@ -289,6 +289,10 @@ int hzp_gemm_profile(int on);
 int hzp_gemm_profile_read(double* flops, double* ms, int* launches);
 /* Same, plus a per-shape text table (count, ms, TFLOP/s) into text[cap]. */
 int hzp_gemm_profile_dump(double* flops, double* ms, int* launches, char* text, int cap);
+/* As read / dump, plus busy_ms = the union of the launch intervals (GEMMs on
+ * concurrent streams overlap: sum(ms) >= busy_ms). */
+int hzp_gemm_profile_read_busy(double* flops, double* ms, double* busy_ms, int* launches);
+int hzp_gemm_profile_dump_ex(double* flops, double* ms, double* busy_ms, int* launches, char* text, int cap);
 
 /* ---- kernel-level entry points (single ctx, its streams) ---------------- */
 /* Layer-wise P2P-pull all-gather of layer `layer` into AG ring slot `slot`

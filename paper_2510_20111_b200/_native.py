@@ -139,6 +139,9 @@ SIGNATURES = [
     ("hzp_gemm_profile", C.c_int, [C.c_int]),
     ("hzp_gemm_profile_read", C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_int)]),
     ("hzp_gemm_profile_dump", C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_int), C.c_char_p, C.c_int]),
+    ("hzp_gemm_profile_read_busy", C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_double), _P(C.c_int)]),
+    ("hzp_gemm_profile_dump_ex", C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_double), _P(C.c_int),
+                                           C.c_char_p, C.c_int]),
     ("hzp_ag_layer", C.c_int, [_vp, C.c_int, C.c_int]),
     ("hzp_ag_slot_download", C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64]),
     ("hzp_wgrad_upload", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_float), C.c_int64]),

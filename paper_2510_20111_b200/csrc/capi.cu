@@ -563,15 +563,26 @@ int hzp_gemm_profile_read(double* flops, double* ms, int* launches) {
   return hzp_gemm_profile_dump(flops, ms, launches, nullptr, 0);
 }
 
+int hzp_gemm_profile_read_busy(double* flops, double* ms, double* busy_ms, int* launches) {
+  return hzp_gemm_profile_dump_ex(flops, ms, busy_ms, launches, nullptr, 0);
+}
+
 int hzp_gemm_profile_dump(double* flops, double* ms, int* launches, char* text, int cap) {
+  return hzp_gemm_profile_dump_ex(flops, ms, nullptr, launches, text, cap);
+}
+
+int hzp_gemm_profile_dump_ex(double* flops, double* ms, double* busy_ms, int* launches, char* text, int cap) {
   return guarded([&] {
     GemmProfile& p = gemm_profile();
     std::map<std::string, std::array<double, 3>> agg;  // shape -> {count, ms, flops}
     double f = 0, t = 0;
+    std::vector<std::pair<float, float>> iv;  // launch [start, end] relative to the first
     for (size_t i = 0; i < p.ev.size(); ++i) {
       HZP_CUDA(cudaEventSynchronize(p.ev[i].second));
-      float x = 0;
+      float x = 0, t0 = 0;
       HZP_CUDA(cudaEventElapsedTime(&x, p.ev[i].first, p.ev[i].second));
+      HZP_CUDA(cudaEventElapsedTime(&t0, p.ev[0].first, p.ev[i].first));
+      iv.emplace_back(t0, t0 + x);
       t += x;
       f += p.flops[i];
       if (i < p.shape.size()) {
@@ -580,8 +591,25 @@ int hzp_gemm_profile_dump(double* flops, double* ms, int* launches, char* text, 
         a[1] += x;
         a[2] += p.flops[i];
       }
-      cudaEventDestroy(p.ev[i].first);
-      cudaEventDestroy(p.ev[i].second);
+    }
+    for (auto& e : p.ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    if (busy_ms) {  // union of the launch intervals (concurrent streams overlap)
+      std::sort(iv.begin(), iv.end());
+      double busy = 0, s0 = -1, e0 = -1;
+      for (const auto& [a, b] : iv) {
+        if (a > e0) {
+          if (e0 > s0) busy += e0 - s0;
+          s0 = a;
+          e0 = b;
+        } else if (b > e0) {
+          e0 = b;
+        }
+      }
+      if (e0 > s0) busy += e0 - s0;
+      *busy_ms = busy;
     }
     if (flops) *flops = f;
     if (ms) *ms = t;

@@ -295,6 +295,13 @@ def gemm_profile_read():
     return f.value, ms.value, n.value
 
 
+def gemm_profile_read_busy():
+    """(flops, summed launch ms, union-of-launches ms, launches); clears."""
+    f, ms, busy, n = C.c_double(), C.c_double(), C.c_double(), C.c_int()
+    N.check(N.lib.hzp_gemm_profile_read_busy(C.byref(f), C.byref(ms), C.byref(busy), C.byref(n)))
+    return f.value, ms.value, busy.value, n.value
+
+
 def gemm_profile_dump():
     f, ms, n = C.c_double(), C.c_double(), C.c_int()
     buf = C.create_string_buffer(1 << 16)
