@@ -54,6 +54,8 @@ struct TcParams {
   CUtensorMap tmSide; // side input (SIDE): aux for the *-grad epilogues, else resid
   CUtensorMap tmBh;   // CL == 2, K-major B: half-height boxes (each CTA loads one half)
   CUtensorMap tmBq;   // CL == 2, K-major B: quarter-height boxes (split tail units)
+  CUtensorMap tmA5, tmB5;  // MN-major operands as 5-D maps, box = two 64-wide MN chunks
+  int a5, b5;              // the 5-D maps are valid (MN extent % 64 == 0)
   int M, N, K;
   int tiles_m, tiles_n, tiles_mn, num_tiles;
   int pairs_m;        // CL == 2: ceil(tiles_m / 2); tile index space = pairs
@@ -207,16 +209,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (rank == 0)
               mbar_expect_tx(&full[stage], 2 * (A_BYTES + uint32_t(tc.w / 2) * BK * 2));
             if (A_MN) {
+              if (p.a5) {
+                tma_load_5d_pair(sa, &p.tmA5, fb, 0, k0, tc.m0 / 64, tc.zh, tc.zb);
+              } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j)
-                tma_load_4d_pair(sa + j * (BK * 128), &tmA, fb, tc.m0 + 64 * j, k0, tc.zh, tc.zb);
+                for (int j = 0; j < BM / 64; ++j)
+                  tma_load_4d_pair(sa + j * (BK * 128), &tmA, fb, tc.m0 + 64 * j, k0, tc.zh, tc.zb);
+              }
             } else {
               tma_load_4d_pair(sa, &tmA, fb, k0, tc.m0, tc.zh, tc.zb);
             }
             if (B_MN) {
-              for (int j = 0; j < tc.w / 128; ++j)
-                tma_load_4d_pair(sb + j * (BK * 128), &tmB, fb, tc.n0 + rank * (tc.w / 2) + 64 * j, k0, tc.zh,
-                                 tc.zb);
+              if (p.b5 && !split) {
+                tma_load_5d_pair(sb, &p.tmB5, fb, 0, k0, (tc.n0 + rank * (tc.w / 2)) / 64, tc.zh, tc.zb);
+              } else {
+                for (int j = 0; j < tc.w / 128; ++j)
+                  tma_load_4d_pair(sb + j * (BK * 128), &tmB, fb, tc.n0 + rank * (tc.w / 2) + 64 * j, k0, tc.zh,
+                                   tc.zb);
+              }
             } else {
               tma_load_4d_pair(sb, split ? &p.tmBq : &p.tmBh, fb, k0, tc.n0 + rank * (tc.w / 2), tc.zh, tc.zb);
             }
@@ -225,16 +235,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           if (A_MN) {
+            if (p.a5) {
+              tma_load_5d(sa, &p.tmA5, &full[stage], 0, k0, tc.m0 / 64, tc.zh, tc.zb);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_4d(sa + j * (BK * 128), &tmA, &full[stage], tc.m0 + 64 * j, k0, tc.zh, tc.zb);
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_4d(sa + j * (BK * 128), &tmA, &full[stage], tc.m0 + 64 * j, k0, tc.zh, tc.zb);
+            }
           } else {
             tma_load_4d(sa, &tmA, &full[stage], k0, tc.m0, tc.zh, tc.zb);
           }
           if (B_MN) {
+            if (p.b5) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, tc.zh, tc.zb);
+              for (int j = 0; j < BN / 128; ++j)
+                tma_load_5d(sb + j * (2 * BK * 128), &p.tmB5, &full[stage], 0, k0, tc.n0 / 64 + 2 * j, tc.zh,
+                            tc.zb);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_4d(sb + j * (BK * 128), &tmB, &full[stage], tc.n0 + 64 * j, k0, tc.zh, tc.zb);
+            }
           } else {
             tma_load_4d(sb, &tmB, &full[stage], k0, tc.n0, tc.zh, tc.zb);
           }
@@ -607,6 +628,32 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
   return make_tma_map_bf16(base, inner, outer, ld, box_outer, nh, nb, sh, sb);
 }
 
+// MN-major operand [K rows of MN contiguous elements] as the 5-D map
+// {64, K, MN / 64, nh, nb} (box {64, BK, 2, 1, 1}, 128-byte swizzle): one
+// instruction loads two 64-wide MN chunks, laid out in smem exactly as two
+// 4-D boxes.  Only when MN % 64 == 0 (the chunk dimension then bounds the
+// tail exactly); false if the driver rejects the map.
+bool make_map_mn5(const void* base, int64_t mn, int64_t K, int64_t ld, int nh, int nb, int64_t sh, int64_t sb,
+                  CUtensorMap* out) {
+  if (mn % 64 != 0 || ld % 8 != 0) return false;
+  if (nh <= 1) sh = ld * K;
+  if (nb <= 1) sb = sh * nh;
+  cuuint64_t dims[5] = {64, cuuint64_t(K), cuuint64_t(mn / 64), cuuint64_t(nh), cuuint64_t(nb)};
+  cuuint64_t strides[4] = {cuuint64_t(ld) * 2, 128, cuuint64_t(sh) * 2, cuuint64_t(sb) * 2};
+  cuuint32_t box[5] = {64, cuuint32_t(BK), 2, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return get_encode()(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool mn5_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("HZP_GEMM_MN5");
+    return e && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
 // Output map for the TMA-store epilogue: {N, M, nh, nb}, box {32, 32, 1, 1};
 // bf16 rows of 64 B use SWIZZLE_64B, fp32 rows of 128 B SWIZZLE_128B.
 CUtensorMap make_out_map(const void* base, bool f32, int64_t N, int64_t M, int64_t ld, int nh, int nb,
@@ -678,6 +725,8 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   const CUtensorMap tb = B_MN ? make_map(B, s.N, s.K, s.ldb, BK, s.nh, s.nb, s.b_sh, s.b_sb)
                               : make_map(B, s.K, s.N, s.ldb, BN, s.nh, s.nb, s.b_sh, s.b_sb);
   TcParams p;
+  p.a5 = A_MN && !mn5_disabled() && make_map_mn5(A, s.M, s.K, s.lda, s.nh, s.nb, s.a_sh, s.a_sb, &p.tmA5);
+  p.b5 = B_MN && !mn5_disabled() && make_map_mn5(B, s.N, s.K, s.ldb, s.nh, s.nb, s.b_sh, s.b_sb, &p.tmB5);
   if (STORE != 0) {
     p.tmC = make_out_map(C, STORE == 2, s.N, s.M, e.ldc, s.nh, s.nb, s.c_sh, s.c_sb);
     if (STORE == 1 && e.act == kActGelu)
