@@ -76,6 +76,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dims, mbs, batch, steps = [64, 128, 128, 64], 2, 16, 4
+    if os.environ.get("HZP_TEST_DIMS"):  # ragged shards (P not a multiple of the group sizes)
+        dims, batch = [int(d) for d in os.environ["HZP_TEST_DIMS"].split(",")], 3
     o = load_oracle()
     st = o.shard_init(dims, world, z1, z2, z3, 2024, bool(prec))
     eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=batch, num_microbatches=mbs,

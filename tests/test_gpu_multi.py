@@ -50,3 +50,19 @@ def test_multiprocess_step_matches_oracle(n, z, reuse, prec):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert r.stdout.count(": OK") == n
+
+
+@pytest.mark.parametrize("n,z", [(2, (2, 2, 2)), (4, (4, 2, 2))])
+def test_multiprocess_ragged_shards_match_oracle(n, z):
+    """P = 23 over 2 / 4 ranks: padded Z3 / Z1 shards, a layer smaller than a
+    shard, copy-engine runs of a few elements (unaligned) over NVLink."""
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29640 + n),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *map(str, z), "0"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, HZP_TEST_DIMS="5,3,2"))
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count(": OK") == n

@@ -23,6 +23,11 @@ STEP_CONFIGS = [
     ([12, 20, 8], 1, 1, 1, 1, 2, 4, 5),
     ([64, 128, 128, 64], 8, 8, 2, 2, 2, 16, 5),
     ([64, 128, 64], 8, 8, 8, 8, 1, 32, 5),
+    # ragged / degenerate shards: P = 8 over 8 ranks (1-element Z1 chunks),
+    # P = 23 (padding in the last Z3 / Z1 shards), a layer smaller than a shard
+    ([3, 2], 8, 8, 4, 4, 1, 2, 3),
+    ([5, 3, 2], 4, 4, 2, 2, 2, 3, 3),
+    ([1, 1], 2, 2, 2, 2, 1, 1, 3),
 ]
 
 
