@@ -410,8 +410,11 @@ void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
     const int t0 = rs_off[layer], t1 = rs_off[layer + 1];
     const int base = geom.z2_base(cfg.my_rank);
     int ev = 0;
-    for (int c0 = t0; c0 < t1; c0 += kRsChunkTiles, ++ev) {
-      const int c1 = std::min(t1, c0 + kRsChunkTiles);
+    // >= 4 M elements per chunk, at most ~4 chunks per layer: enough to overlap
+    // the copies with the reduce, few enough that per-copy overhead stays small
+    const int chunk = std::max(kRsChunkTiles, (t1 - t0 + 3) / 4);
+    for (int c0 = t0; c0 < t1; c0 += chunk, ++ev) {
+      const int c1 = std::min(t1, c0 + chunk);
       const int64_t b0 = tiles_host[c0].b_off;
       const int64_t b1 = tiles_host[c1 - 1].b_off + tiles_host[c1 - 1].len;
       for (int j = 1; j < geom.z2; ++j) {  // rotated: peer r+1 first (one reader per owner)
