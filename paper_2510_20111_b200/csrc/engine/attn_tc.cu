@@ -33,6 +33,7 @@ constexpr int kThreads = 192;
 
 struct AttnParams {
   CUtensorMap tmQ, tmK, tmV;  // 4-D views of qkv: {d, s, head, seq}
+  CUtensorMap tmV5;           // V as {64 d, s, 2, head, seq}: a 64-key box carries both d halves
   uint16_t* O;                // [b, S, h]
   uint16_t* P;                // [b*nh, S, S] or null
   float* lse;                 // [b*nh, S] or null
@@ -110,9 +111,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                       head, seq);
         mbar_expect_tx(&v_full[st], kTileBytes);
         for (int kc = 0; kc < 2; ++kc)
-          for (int db = 0; db < 2; ++db)
-            tma_load_4d(smem + kOffV + st * kTileBytes + kc * 16384 + db * 8192, &p.tmV, &v_full[st],
-                        db * 64, j * kBK + kc * 64, head, seq);
+          tma_load_5d(smem + kOffV + st * kTileBytes + kc * 16384, &p.tmV5, &v_full[st], 0, j * kBK + kc * 64,
+                      0, head, seq);
       }
     }
   } else if (warp == 1) {
@@ -345,9 +345,8 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
         mbar_wait(&v_empty[vs], ((j / kVSt) & 1) ^ 1);
         mbar_expect_tx(&v_full[vs], kTileBytes);
         for (int kc = 0; kc < 2; ++kc)
-          for (int db = 0; db < 2; ++db)
-            tma_load_4d(smem + k2OffV + vs * kTileBytes + kc * 16384 + db * 8192, &p.tmV, &v_full[vs],
-                        db * 64, j * kBK + kc * 64, head, seq);
+          tma_load_5d(smem + k2OffV + vs * kTileBytes + kc * 16384, &p.tmV5, &v_full[vs], 0, j * kBK + kc * 64,
+                      0, head, seq);
       }
     }
   } else if (warp == 1) {
@@ -830,6 +829,8 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
   p.tmQ = make_tma_map_bf16(qkv, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
   p.tmK = make_tma_map_bf16(qkv + h, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
   p.tmV = make_tma_map_bf16(qkv + 2 * h, kHd, S, h3, 64, nh, b, kHd, int64_t(S) * h3);
+  if (!make_map_mn5(qkv + 2 * h, kHd, S, h3, nh, b, kHd, int64_t(S) * h3, &p.tmV5))
+    throw CudaError("attention: 5-D V tensor map rejected");
   p.O = O;
   p.P = P;
   p.lse = lse;

@@ -628,24 +628,6 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
   return make_tma_map_bf16(base, inner, outer, ld, box_outer, nh, nb, sh, sb);
 }
 
-// MN-major operand [K rows of MN contiguous elements] as the 5-D map
-// {64, K, MN / 64, nh, nb} (box {64, BK, 2, 1, 1}, 128-byte swizzle): one
-// instruction loads two 64-wide MN chunks, laid out in smem exactly as two
-// 4-D boxes.  Only when MN % 64 == 0 (the chunk dimension then bounds the
-// tail exactly); false if the driver rejects the map.
-bool make_map_mn5(const void* base, int64_t mn, int64_t K, int64_t ld, int nh, int nb, int64_t sh, int64_t sb,
-                  CUtensorMap* out) {
-  if (mn % 64 != 0 || ld % 8 != 0) return false;
-  if (nh <= 1) sh = ld * K;
-  if (nb <= 1) sb = sh * nh;
-  cuuint64_t dims[5] = {64, cuuint64_t(K), cuuint64_t(mn / 64), cuuint64_t(nh), cuuint64_t(nb)};
-  cuuint64_t strides[4] = {cuuint64_t(ld) * 2, 128, cuuint64_t(sh) * 2, cuuint64_t(sb) * 2};
-  cuuint32_t box[5] = {64, cuuint32_t(BK), 2, 1, 1};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  return get_encode()(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box,
-                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 bool mn5_disabled() {
   static const bool off = [] {
     const char* e = std::getenv("HZP_GEMM_MN5");
@@ -834,6 +816,24 @@ void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, c
 
 }  // namespace
 
+// MN-major operand [K rows of MN contiguous elements] as the 5-D map
+// {64, K, MN / 64, nh, nb} (box {64, BK, 2, 1, 1}, 128-byte swizzle): one
+// instruction loads two 64-wide MN chunks, laid out in smem exactly as two
+// 4-D boxes.  Only when MN % 64 == 0 (the chunk dimension then bounds the
+// tail exactly); false if the driver rejects the map.
+bool make_map_mn5(const void* base, int64_t mn, int64_t K, int64_t ld, int nh, int nb, int64_t sh, int64_t sb,
+                  CUtensorMap* out) {
+  if (mn % 64 != 0 || ld % 8 != 0) return false;
+  if (nh <= 1) sh = ld * K;
+  if (nb <= 1) sb = sh * nh;
+  cuuint64_t dims[5] = {64, cuuint64_t(K), cuuint64_t(mn / 64), cuuint64_t(nh), cuuint64_t(nb)};
+  cuuint64_t strides[4] = {cuuint64_t(ld) * 2, 128, cuuint64_t(sh) * 2, cuuint64_t(sb) * 2};
+  cuuint32_t box[5] = {64, cuuint32_t(BK), 2, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return get_encode()(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 uint64_t& launch_counter() {
   static uint64_t n = 0;
   return n;

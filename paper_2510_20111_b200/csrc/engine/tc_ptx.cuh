@@ -377,4 +377,9 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 // strides sh / sb (elements), box {64, box_outer, 1, 1}, 128-byte swizzle.
 CUtensorMap make_tma_map_bf16(const void* base, int64_t inner, int64_t outer, int64_t ld,
                               int box_outer, int nh, int nb, int64_t sh, int64_t sb);
+// Host: MN-major operand as the 5-D map {64, K, MN / 64, nh, nb}, box
+// {64, 64, 2, 1, 1}: one load = two 64-wide MN chunks of 64 K rows (false if
+// MN % 64 != 0 or the driver rejects it).
+bool make_map_mn5(const void* base, int64_t mn, int64_t K, int64_t ld, int nh, int nb, int64_t sh, int64_t sb,
+                  CUtensorMap* out);
 }  // namespace hzp
