@@ -10,7 +10,7 @@
 //               O_g += P_g V_j    -> TMEM [256 + g*128, +128), A = P_g from TMEM
 //   warps 2-9 two softmax warpgroups (one per query tile), one thread per
 //             query row (its TMEM lane): row max over S, P = 2^(s c - m) with
-//             FFMA2 and 3/8 of the exp2 on the FMA pipe, P (bf16) written back
+//             FFMA2 and 1/4 of the exp2 on the FMA pipe, P (bf16) written back
 //             over the consumed S columns, lazy O rescale, final O / l and lse.
 // Neither S nor P ever leaves the SM.  The backward (attn_bwd_kernel, further
 // down) works per 128-key tile with P^T / dS^T kept in TMEM the same way.
@@ -25,6 +25,9 @@ namespace {
 
 using namespace tc;
 
+#ifndef HZP_ATTN_POLY_FROM
+#define HZP_ATTN_POLY_FROM 6  // forward: pairs i % 8 >= this use the FMA-pipe exp2 (2 of 8; swept 3..8 of 8 on B200: 6 best)
+#endif
 constexpr int kHd = 128;    // head dim
 constexpr int kBQ = 128;    // query rows per CTA
 constexpr int kBK = 128;    // keys per iteration
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
       const bool bump = mx > m + 8.f;
       const float mref = bump ? mx : m;
       const float corr = bump ? exp2_fast(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
-      // pass 2: P = 2^(s c - mref), FFMA2 per pair; 3 of every 8 pairs' exp2
+      // pass 2: P = 2^(s c - mref), FFMA2 per pair; 2 of every 8 pairs' exp2
       // on the FMA pipe so MUFU (16/clk/SM) stops bounding the tile.  Chunk
       // c+1's scores are loaded while chunk c is exponentiated.
       const uint64_t nm2 = f2_pack(-mref, -mref);
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
           const int i = c * 16 + ii;
           const uint64_t x = f2_fma(f2_pack(__uint_as_float(r[2 * ii]), __uint_as_float(r[2 * ii + 1])), sc2, nm2);
           uint64_t e;
-          if ((i & 7) >= 5) {
+          if ((i & 7) >= HZP_ATTN_POLY_FROM) {
             e = exp2_poly2(x);
           } else {
             float a0, a1;
