@@ -28,6 +28,9 @@ using namespace tc;
 #ifndef HZP_ATTN_POLY_FROM
 #define HZP_ATTN_POLY_FROM 6  // forward: pairs i % 8 >= this use the FMA-pipe exp2 (2 of 8; swept 3..8 of 8 on B200: 6 best)
 #endif
+#ifndef HZP_ATTN_BWD_POLY_FROM
+#define HZP_ATTN_BWD_POLY_FROM 3  // backward: pairs i % 4 >= this use the FMA-pipe exp2
+#endif
 constexpr int kHd = 128;    // head dim
 constexpr int kBQ = 128;    // query rows per CTA
 constexpr int kBK = 128;    // keys per iteration
@@ -727,7 +730,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
           const uint64_t x = f2_fma(f2_pack(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), sc2,
                                     f2_pack(nl[2 * i], nl[2 * i + 1]));
           uint64_t e;
-          if ((i & 3) == 3) {
+          if ((i & 3) >= HZP_ATTN_BWD_POLY_FROM) {
             e = exp2_poly2(x);
           } else {
             float a0, a1;
