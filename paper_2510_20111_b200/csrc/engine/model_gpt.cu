@@ -61,7 +61,7 @@ struct GptBuffers {
   // backward DAG), so they fill the SMs the dgrad chain's tail waves leave
   // idle; own column-sum partials, fork/join by events.
   cudaStream_t side = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[12] = {};
   float* part_side = nullptr;
   // MoE backward scratch
   uint16_t *moe_dy = nullptr, *moe_dh = nullptr, *moe_dxp = nullptr, *moe_dlogits = nullptr;
@@ -297,10 +297,13 @@ class GptModel final : public Model {
     return g.bf16 ? static_cast<void*>(static_cast<uint16_t*>(g.ptr) + off)
                   : static_cast<void*>(static_cast<float*>(g.ptr) + off);
   }
-  void ln_param_grads(GptBuffers* B, const GradTarget& g, int64_t g_off, int64_t b_off,
-                      cudaStream_t s) const {
-    colsum_finalize(B->part, kChunks, h_, gptr(g, g_off), g.bf16, g.mode, s);
-    colsum_finalize(B->part + int64_t(kChunks) * h_, kChunks, h_, gptr(g, b_off), g.bf16, g.mode, s);
+  // LN gamma / beta gradients from layernorm_bwd's column partials `part`
+  // ([2][kChunks][h]; B->part by default)
+  void ln_param_grads(GptBuffers* B, const GradTarget& g, int64_t g_off, int64_t b_off, cudaStream_t s,
+                      const float* part = nullptr) const {
+    if (!part) part = B->part;
+    colsum_finalize(part, kChunks, h_, gptr(g, g_off), g.bf16, g.mode, s);
+    colsum_finalize(part + int64_t(kChunks) * h_, kChunks, h_, gptr(g, b_off), g.bf16, g.mode, s);
   }
   // batched attention shapes over z = (sequence b, head)
   GemmShape attn_shape(int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int64_t a_sh,
@@ -551,7 +554,8 @@ class GptModel final : public Model {
       moe_bwd(B, a, W, g, dout, s, ws, to_side);
       layernorm_bwd(B->dattn, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_), h_,
                     s);
-      ln_param_grads(B, g, o.ln2_g, o.ln2_b, s);
+      to_side();  // the LN parameter reductions are leaves too
+      ln_param_grads(B, g, o.ln2_g, o.ln2_b, ws, B->part);
     } else {
     // MLP
     to_side();
@@ -571,7 +575,8 @@ class GptModel final : public Model {
     }
     layernorm_bwd(B->dln, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_),
                   h_, s);
-    ln_param_grads(B, g, o.ln2_g, o.ln2_b, s);
+    to_side();  // the LN parameter reductions are leaves too
+    ln_param_grads(B, g, o.ln2_g, o.ln2_b, ws, B->part);
     }
     // attention output projection
     to_side();
@@ -591,9 +596,13 @@ class GptModel final : public Model {
       Epilogue e;
       linear_dgrad(B->dqkv, W + o.w_qkv, B->dln, int(h3), h_, e, s);
     }
-    layernorm_bwd(B->dln, B->x[l], W + o.ln1_g, a.mu1, a.rs1, B->dxm, din, B->part, kChunks,
+    // ln1's partials in their own region: the side stream may still be
+    // reducing ln2's
+    float* part1 = B->part + 2 * int64_t(kChunks) * h_;
+    layernorm_bwd(B->dln, B->x[l], W + o.ln1_g, a.mu1, a.rs1, B->dxm, din, part1, kChunks,
                   int(T_), h_, s);
-    ln_param_grads(B, g, o.ln1_g, o.ln1_b, s);
+    to_side();
+    ln_param_grads(B, g, o.ln1_g, o.ln1_b, ws, part1);
     // join: the block's task ends when its weight gradients are written (the
     // RS / next block reuse the buffers they read)
     HZP_CUDA(cudaEventRecord(B->ev[nev], ws));
