@@ -36,13 +36,12 @@ def main():
                            H.ParallelConfig(), H.CostModel())
     with open(out + "_measured.json", "w") as fh:
         json.dump(measured_trace(eng, g, "hzp_b200 measured step (1.3B, N=1)"), fh)
-    # the reference simulator's view of the same graph, durations = the measured ones
+    # the reference simulator's view of the same graph (its unit cost model)
     tl = eng.timeline()
-    spec = H.ModelSpec(num_layers=L + 2, params_per_layer=1, num_microbatches=M)
     sim = H.simulate(g, 2, 1, H.ASYNC)
     with open(out + "_simulated.json", "w") as fh:
         json.dump(chrome_trace(g, sim.start, sim.end, "reference simulate() (unit cost model)"), fh)
-    print("makespan_ms", tl["makespan_ms"], "compute_idle_ms", tl["compute_idle_ms"], spec.num_layers)
+    print("makespan_ms", tl["makespan_ms"], "compute_idle_ms", tl["compute_idle_ms"])
     eng.close()
 
 
