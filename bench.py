@@ -331,7 +331,7 @@ def run_hzp(args):
                        gpt_experts=c.get("experts", 0), gpt_topk=c.get("topk", 2),
                        par=ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3), prelaunch_depth=2, rs_slots=1,
                        device=local, my_rank=rank if N > 1 else 0, reuse=int(args.reuse),
-                       recompute=int(args.recompute))
+                       recompute=int(args.recompute), wgrad_slots=args.wgrad_slots)
     eng = HzpEngine(cfg)
     if N > 1:
         eng.connect()
@@ -446,6 +446,7 @@ def run_hzp(args):
                                      f" vocab{c['vocab']} untied head)"),
                            "params": eng.P, "global_batch": N * mb * nmb, "seq_len": c["seq"],
                            "micro_batch": mb, "num_microbatches": nmb, "reuse": int(args.reuse), "recompute": int(args.recompute),
+                           "wgrad_slots": args.wgrad_slots,
                            "tokens_per_step": N * tokens_per_step,
                            "parallelism": f"dp{N} (z1={z1}, z2={z2}, z3={z3})", "prelaunch_depth": 2,
                            "rs_slots": 1, "l2": "activation working set >> 126 MB L2 (no flush needed)"},
@@ -472,6 +473,8 @@ def main():
     ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b", "moe"],
                     help="BASELINE configs[1] (default, the headline), configs[2] or configs[3]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--wgrad-slots", type=int, default=2,
+                    help="gradient buffers peers reduce-scatter from (ring; >= 2)")
     ap.add_argument("--recompute", type=int, default=0, choices=[0, 1],
                     help="activation recomputation (FWD-recompute before each BWD; GPT blocks keep inputs only)")
     ap.add_argument("--reuse", type=int, default=0, choices=[0, 1],
