@@ -89,7 +89,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -99,10 +99,14 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Samples that arrived inside [t0, t1 + one period] (all if none did)."""
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for t, ln in self.lines if t0 is None or (t0 <= t <= t1 + 0.25)]
+        if not lines:
+            lines = [ln for _, ln in self.lines]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -357,22 +361,27 @@ def run_hzp(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        eng.step_async(dev.data_ptr(), True)
-    eng.sync()
-    barrier()
-    # ---- device-timed region (inputs resident in HBM) ----
-    k0 = kernel_launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the clock sampler (an nvidia-smi process polling every 200 ms) starts
+    # before the warm-up so its own start-up does not overlap the timed steps;
+    # only the samples taken while they run are summarised
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            eng.step_async(dev.data_ptr(), True)
+        eng.sync()
+        barrier()
+        # ---- device-timed region (inputs resident in HBM) ----
+        k0 = kernel_launches()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         barrier()
+        t_on = time.perf_counter()
         ev0.record(cs)
         for _ in range(args.steps):
             eng.step_async(dev.data_ptr(), True)
         ev1.record(cs)
         ev1.synchronize()
         torch.cuda.synchronize()
+        t_off = time.perf_counter()
         barrier()
     launches = (kernel_launches() - k0) // max(1, args.steps)
     ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
@@ -432,7 +441,7 @@ def run_hzp(args):
     line = None
     if rank == 0:
         cb = cpu_reference(2, 0, "cpu_baseline", c) if (N == 1 and not args.no_cpu_baseline) else None
-        clocks = clk.summary()
+        clocks = clk.summary(t_on, t_off)
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": N,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
