@@ -15,6 +15,10 @@ SHAPES = [
     (1024, 1024, 2048),
     (8192, 2048, 128),  # CTA pairs with the tail wave split into half-width units
     (6144, 2048, 192),
+    # MN-major through the 5-D maps with a chunk past the end (MN % 128 == 64:
+    # the second 64-wide chunk of the last tile is out of bounds -> zero fill)
+    (320, 192, 256),
+    (704, 320, 128),
 ]
 
 
@@ -51,6 +55,27 @@ def test_tcgen05_gemm_matches_torch(gpu, shape, a_mn, b_mn):
     torch.cuda.synchronize()
     err16 = (C16.float() - ref).abs().max().item() / ref.abs().max().item()
     assert err16 < 1e-2, err16
+
+
+def test_gemm_profile_busy_union(gpu):
+    """hzp_gemm_profile_read_busy: GEMMs on two streams overlap, so the union
+    of the launch intervals is <= the summed launch time (and > 0)."""
+    from paper_2510_20111_b200.engine import gemm_bf16, gemm_profile, gemm_profile_read_busy
+    M = N = K = 2048
+    A, B, As, Bs, lda, ldb = _mk(M, N, K, 0, 0, gpu)
+    C1 = torch.empty(M, N, device=gpu, dtype=torch.bfloat16)
+    C2 = torch.empty(M, N, device=gpu, dtype=torch.bfloat16)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    gemm_profile(True)
+    for _ in range(4):
+        gemm_bf16(As.data_ptr(), Bs.data_ptr(), C1.data_ptr(), M, N, K, lda, ldb, N, 0, 0, 0, s1.cuda_stream)
+        gemm_bf16(As.data_ptr(), Bs.data_ptr(), C2.data_ptr(), M, N, K, lda, ldb, N, 0, 0, 0, s2.cuda_stream)
+    torch.cuda.synchronize()
+    gemm_profile(False)
+    flops, ms, busy, n = gemm_profile_read_busy()
+    assert n == 8 and flops == 8 * 2.0 * M * N * K
+    assert 0 < busy <= ms * (1 + 1e-6)
 
 
 def test_tcgen05_gemm_accumulate(gpu):
