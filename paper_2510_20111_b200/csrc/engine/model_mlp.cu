@@ -8,16 +8,19 @@
 #include <cmath>
 
 #include "engine/gemm.cuh"
+#include "engine/gpt_ops.cuh"
 #include "engine/model.hpp"
 
 namespace hzp {
 namespace {
 
 // loss += sum(y*y) / denom ; delta = y * scale  (train.cpp:127-131, 137-139).
-// ordered: one thread sums in the reference's (row-major) order.
+// ordered (fp32 tier): one thread sums in the reference's (row-major) order.
+// Otherwise every block writes the partial sum of its grid-stride elements to
+// part[blockIdx.x] and mlp_loss_sum_kernel adds them in a fixed order.
 __global__ void mlp_loss_delta_kernel(const float* __restrict__ y, int64_t n, float denom,
                                       float scale, float* __restrict__ loss, void* delta,
-                                      int delta_bf16, int ordered) {
+                                      int delta_bf16, int ordered, float* __restrict__ part) {
   __shared__ float red[32];
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -25,9 +28,8 @@ __global__ void mlp_loss_delta_kernel(const float* __restrict__ y, int64_t n, fl
     if (delta_bf16) static_cast<uint16_t*>(delta)[i] = f32_to_bf16_bits(d);
     else static_cast<float*>(delta)[i] = d;
   }
-  if (blockIdx.x != 0) return;
   if (ordered) {
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       float acc = 0.f;
       for (int64_t i = 0; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(y[i], y[i]));
       *loss = __fadd_rn(*loss, __fdiv_rn(acc, denom));
@@ -35,15 +37,24 @@ __global__ void mlp_loss_delta_kernel(const float* __restrict__ y, int64_t n, fl
     return;
   }
   float acc = 0.f;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += y[i] * y[i];
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    acc += y[i] * y[i];
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int w = 0; w < (blockDim.x + 31) / 32; ++w) s += red[w];
-    *loss += s / denom;
+    part[blockIdx.x] = s;
   }
+}
+
+__global__ void mlp_loss_sum_kernel(const float* __restrict__ part, int nparts, float denom,
+                                    float* __restrict__ loss) {
+  if (threadIdx.x != 0) return;
+  float s = 0.f;
+  for (int i = 0; i < nparts; ++i) s += part[i];
+  *loss += s / denom;
 }
 
 // Bias gradient gb[o] = sum_s d[s, o], s ascending (train.cpp:120-123), written
@@ -74,6 +85,8 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, uint16_t* __re
     y[i] = f32_to_bf16_bits(x[i]);
 }
 
+constexpr int kColChunks = 64;  // row chunks of the bf16-tier bias column sums
+
 struct MlpBuffers {
   std::vector<void*> acts;  // acts[0..nl-1] working dtype; acts[0] set per microbatch
   float* y = nullptr;       // last layer output, fp32
@@ -81,6 +94,7 @@ struct MlpBuffers {
   int cur = 0;
   float* loss = nullptr;
   void* input_bf16 = nullptr;
+  float* part = nullptr;    // bf16 tier: loss partials [256] | bias column partials [64][max dim]
 };
 
 class MlpModel final : public Model {
@@ -120,6 +134,7 @@ class MlpModel final : public Model {
     for (auto& d : b->delta) HZP_CUDA(cudaMalloc(&d, size_t(c_.batch) * maxd * es));
     HZP_CUDA(cudaMalloc(&b->loss, sizeof(float)));
     HZP_CUDA(cudaMemset(b->loss, 0, sizeof(float)));
+    HZP_CUDA(cudaMalloc(&b->part, (256 + size_t(kColChunks) * maxd) * sizeof(float)));
     return b;
   }
   void free_rank_buffers(void* p) override {
@@ -130,6 +145,7 @@ class MlpModel final : public Model {
     cudaFree(b->delta[0]);
     cudaFree(b->delta[1]);
     cudaFree(b->loss);
+    cudaFree(b->part);
     delete b;
   }
   void begin_step(void* p, cudaStream_t s) override {
@@ -174,8 +190,12 @@ class MlpModel final : public Model {
       b->cur = 0;
       const int blocks = int((n + 255) / 256 < 256 ? (n + 255) / 256 : 256);
       mlp_loss_delta_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(
-          b->y, n, denom, scale, b->loss, b->delta[0], c_.bf16, c_.bf16 ? 0 : 1);
+          b->y, n, denom, scale, b->loss, b->delta[0], c_.bf16, c_.bf16 ? 0 : 1, b->part);
       HZP_LAUNCH_CHECK();
+      if (c_.bf16) {
+        mlp_loss_sum_kernel<<<1, 32, 0, s>>>(b->part, blocks < 1 ? 1 : blocks, denom, b->loss);
+        HZP_LAUNCH_CHECK();
+      }
     }
   }
 
@@ -198,8 +218,13 @@ class MlpModel final : public Model {
     {
       void* gb = g.bf16 ? static_cast<void*>(static_cast<uint16_t*>(g.ptr) + int64_t(in) * out)
                         : static_cast<void*>(static_cast<float*>(g.ptr) + int64_t(in) * out);
-      colsum_kernel<<<(out + 255) / 256, 256, 0, s>>>(d, c_.bf16, B, out, gb, g.bf16, g.mode);
-      HZP_LAUNCH_CHECK();
+      if (c_.bf16 && out % 8 == 0) {  // column partials over row chunks, then a fixed-order sum
+        colsum_partial(static_cast<const uint16_t*>(d), B, out, b->part + 256, kColChunks, s);
+        colsum_finalize(b->part + 256, kColChunks, out, gb, g.bf16, g.mode, s);
+      } else {  // fp32 tier: the reference's ascending-row order
+        colsum_kernel<<<(out + 255) / 256, 256, 0, s>>>(d, c_.bf16, B, out, gb, g.bf16, g.mode);
+        HZP_LAUNCH_CHECK();
+      }
     }
     // dgrad: prev[s, in] = (sum_o d[s, o] W[o, in]) * (1 - a^2), a = acts[l]
     if (l > 0) {
