@@ -222,6 +222,8 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   if (const char* c = std::getenv("HZP_AG_CE")) ag_ce = std::atoi(c) != 0;
   if (const char* c = std::getenv("HZP_RS_CE")) rs_ce = std::atoi(c) != 0;
   if (const char* c = std::getenv("HZP_Z1_CE")) z1_ce = std::atoi(c) != 0;
+  if (const char* c = std::getenv("HZP_RS_CHUNKS")) rs_chunks = std::max(1, std::atoi(c));
+  if (const char* c = std::getenv("HZP_RS_PAR")) rs_par = std::atoi(c) != 0;
   build_tiles();
 }
 
@@ -246,6 +248,8 @@ Engine::~Engine() {
   for (auto p : z1_stage) cudaFree(p);
   if (z1_copy_stream) cudaStreamDestroy(z1_copy_stream);
   if (rs_red_stream) cudaStreamDestroy(rs_red_stream);
+  for (auto st : rs_copy_streams) cudaStreamDestroy(st);
+  for (auto e : rs_par_ev) cudaEventDestroy(e);
   for (auto p : rs_stage) cudaFree(p);
   cudaFree(dtiles);
   cudaFree(dinputs);
@@ -393,6 +397,12 @@ void Engine::setup_rs_staging() {
     rs_ev.resize(64);
     for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  if (rs_par) {
+    rs_copy_streams.resize(geom.z2 - 1);
+    for (auto& st : rs_copy_streams) HZP_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    rs_par_ev.resize(size_t(geom.z2) * 64);
+    for (auto& e : rs_par_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   for (int w = 0; w < int(wslots); ++w) {
     RankTable t = table;
     for (int r = 0; r < cfg.par.dp; ++r)
@@ -410,9 +420,18 @@ void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
     const int t0 = rs_off[layer], t1 = rs_off[layer + 1];
     const int base = geom.z2_base(cfg.my_rank);
     int ev = 0;
-    // >= 4 M elements per chunk, at most ~4 chunks per layer: enough to overlap
-    // the copies with the reduce, few enough that per-copy overhead stays small
-    const int chunk = std::max(kRsChunkTiles, (t1 - t0 + 3) / 4);
+    if (rs_par) {  // fork: every copy stream starts after the producer's work on s
+      cudaEvent_t f = rs_par_ev[0];
+      HZP_CUDA(cudaEventRecord(f, s));
+      for (auto st : rs_copy_streams) HZP_CUDA(cudaStreamWaitEvent(st, f, 0));
+    }
+    // at most rs_chunks chunks per layer and >= 64 MB per peer copy: enough to
+    // overlap the copies with the reduce, few enough that per-copy overhead
+    // stays small (N=4 sweep, bf16: a 64 MB layer is fastest as one chunk, a
+    // 1 GB layer with 4; profiles/r01_rs_sweep_n4.jsonl)
+    const int64_t seg_bytes = t1 <= t0 ? 0 : (tiles_host[t1 - 1].b_off + tiles_host[t1 - 1].len - tiles_host[t0].b_off) * es;
+    const int nch = int(std::max<int64_t>(1, std::min<int64_t>(rs_chunks, seg_bytes / kRsMinChunkBytes)));
+    const int chunk = std::max(kRsChunkTiles, (t1 - t0 + nch - 1) / nch);
     for (int c0 = t0; c0 < t1; c0 += chunk, ++ev) {
       const int c1 = std::min(t1, c0 + chunk);
       const int64_t b0 = tiles_host[c0].b_off;
@@ -420,9 +439,15 @@ void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
       for (int j = 1; j < geom.z2; ++j) {  // rotated: peer r+1 first (one reader per owner)
         const int g = base + (cfg.my_rank - base + j) % geom.z2;
         if (!rs_stage[g]) continue;  // this rank's own buffer is read in place
+        cudaStream_t cs = rs_par ? rs_copy_streams[j - 1] : s;
         HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(rs_stage[g]) + b0 * es,
                                  static_cast<const char*>(table.wgrad[g]) + (wslot * slot_elems + b0) * es,
-                                 (b1 - b0) * es, cudaMemcpyDeviceToDevice, s));
+                                 (b1 - b0) * es, cudaMemcpyDeviceToDevice, cs));
+        if (rs_par) {
+          cudaEvent_t pe = rs_par_ev[size_t(geom.z2) * (1 + ev % 63) + j];
+          HZP_CUDA(cudaEventRecord(pe, cs));
+          HZP_CUDA(cudaStreamWaitEvent(rs_red_stream, pe, 0));
+        }
       }
       cudaEvent_t e = rs_ev[ev % rs_ev.size()];
       HZP_CUDA(cudaEventRecord(e, s));
