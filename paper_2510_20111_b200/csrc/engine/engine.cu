@@ -224,6 +224,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   if (const char* c = std::getenv("HZP_Z1_CE")) z1_ce = std::atoi(c) != 0;
   if (const char* c = std::getenv("HZP_RS_CHUNKS")) rs_chunks = std::max(1, std::atoi(c));
   if (const char* c = std::getenv("HZP_RS_PAR")) rs_par = std::atoi(c) != 0;
+  if (const char* c = std::getenv("HZP_AG_PAR")) ag_par = std::atoi(c) != 0;
   build_tiles();
 }
 
@@ -249,6 +250,8 @@ Engine::~Engine() {
   if (z1_copy_stream) cudaStreamDestroy(z1_copy_stream);
   if (rs_red_stream) cudaStreamDestroy(rs_red_stream);
   for (auto st : rs_copy_streams) cudaStreamDestroy(st);
+  for (auto st : ag_copy_streams) cudaStreamDestroy(st);
+  for (auto e : ag_par_ev) cudaEventDestroy(e);
   for (auto e : rs_par_ev) cudaEventDestroy(e);
   for (auto p : rs_stage) cudaFree(p);
   cudaFree(dtiles);
@@ -301,6 +304,14 @@ void Engine::build_tiles() {
     for (auto& runs : ag_runs)
       std::stable_sort(runs.begin(), runs.end(),
                        [&](const CopyRun& a, const CopyRun& b) { return phase(a) < phase(b); });
+    if (ag_par && geom.z3 > 2 && ag_copy_streams.empty()) {
+      int lo = 0, hi = 0;
+      HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      ag_copy_streams.resize(geom.z3 - 1);
+      for (auto& st : ag_copy_streams) HZP_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+      ag_par_ev.resize(geom.z3);
+      for (auto& e : ag_par_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
   }
   z1_off = T.z1_off;
   z1_n = T.z1_n;
@@ -313,10 +324,24 @@ void Engine::build_tiles() {
 void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
   if (ag_ce && !emulate) {  // multi-process: NVLink leg on the copy engines
     const int es = bf16 ? 2 : 4;
+    const bool par = !ag_copy_streams.empty();
+    const int me = cfg.my_rank % geom.z3;
+    if (par) {  // fork after everything already on s (slot reuse waits included)
+      HZP_CUDA(cudaEventRecord(ag_par_ev[0], s));
+      for (auto st : ag_copy_streams) HZP_CUDA(cudaStreamWaitEvent(st, ag_par_ev[0], 0));
+    }
     for (const CopyRun& r : ag_runs[layer])
       HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(table.ag_slots[r.local]) + (slot * slot_elems + r.dst_off) * es,
                                static_cast<const char*>(table.param[r.src]) + r.src_off * es, r.len * es,
-                               cudaMemcpyDeviceToDevice, s));
+                               cudaMemcpyDeviceToDevice,
+                               par && r.src % geom.z3 != me
+                                   ? ag_copy_streams[(r.src % geom.z3 - me - 1 + 2 * geom.z3) % geom.z3]
+                                   : s));
+    if (par)  // join: the AG task ends when every owner's copies have landed
+      for (size_t i = 0; i < ag_copy_streams.size(); ++i) {
+        HZP_CUDA(cudaEventRecord(ag_par_ev[1 + i], ag_copy_streams[i]));
+        HZP_CUDA(cudaStreamWaitEvent(s, ag_par_ev[1 + i], 0));
+      }
     ++launches;
     return;
   }

@@ -77,6 +77,10 @@ struct Engine {
   };
   std::vector<std::vector<CopyRun>> ag_runs;
   bool ag_ce = true;   // HZP_AG_CE=0 to use the SM pull
+  // HZP_AG_PAR=1: each owner's runs on its own copy stream (all owners read at once)
+  bool ag_par = false;
+  std::vector<cudaStream_t> ag_copy_streams;
+  std::vector<cudaEvent_t> ag_par_ev;  // [0] fork, [1 + i] join of stream i
   // RS with the NVLink leg on the copy engines: each remote Z2 member's
   // gradient-buffer segment is copied into a local staging slot, then the
   // (now HBM-local) reduction kernel runs on a table whose remote wgrad
