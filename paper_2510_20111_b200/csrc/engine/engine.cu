@@ -225,6 +225,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   if (const char* c = std::getenv("HZP_RS_CHUNKS")) rs_chunks = std::max(1, std::atoi(c));
   if (const char* c = std::getenv("HZP_RS_PAR")) rs_par = std::atoi(c) != 0;
   if (const char* c = std::getenv("HZP_AG_PAR")) ag_par = std::atoi(c) != 0;
+  if (const char* c = std::getenv("HZP_RS_MIN_CHUNK_MB")) rs_min_chunk_bytes = std::max<int64_t>(1, std::atoll(c)) << 20;
   build_tiles();
 }
 
@@ -450,12 +451,16 @@ void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
       HZP_CUDA(cudaEventRecord(f, s));
       for (auto st : rs_copy_streams) HZP_CUDA(cudaStreamWaitEvent(st, f, 0));
     }
-    // at most rs_chunks chunks per layer and >= 64 MB per peer copy: enough to
+    // at most rs_chunks chunks per layer and a floor per peer copy: enough to
     // overlap the copies with the reduce, few enough that per-copy overhead
-    // stays small (N=4 sweep, bf16: a 64 MB layer is fastest as one chunk, a
-    // 1 GB layer with 4; profiles/r01_rs_sweep_n4.jsonl)
+    // stays small.  Floor 8 MB with one peer, 64 MB with several concurrent
+    // peer streams (bf16 sweeps: N=2 256 MB layer 399 vs 319 GB/s with the
+    // 8 MB floor; N=4 64 MB layer 377 as one chunk vs 327 as two, 1 GB best
+    // with 4; profiles/r01_rs_sweep_n4.jsonl, r01_rs_chunk_n2.jsonl)
+    const int64_t floor_bytes =
+        rs_min_chunk_bytes > 0 ? rs_min_chunk_bytes : (int64_t(rs_par && geom.z2 > 2 ? 64 : 8) << 20);
     const int64_t seg_bytes = t1 <= t0 ? 0 : (tiles_host[t1 - 1].b_off + tiles_host[t1 - 1].len - tiles_host[t0].b_off) * es;
-    const int nch = int(std::max<int64_t>(1, std::min<int64_t>(rs_chunks, seg_bytes / kRsMinChunkBytes)));
+    const int nch = int(std::max<int64_t>(1, std::min<int64_t>(rs_chunks, seg_bytes / floor_bytes)));
     const int chunk = std::max(kRsChunkTiles, (t1 - t0 + nch - 1) / nch);
     for (int c0 = t0; c0 < t1; c0 += chunk, ++ev) {
       const int c1 = std::min(t1, c0 + chunk);

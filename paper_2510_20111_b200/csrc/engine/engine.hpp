@@ -98,7 +98,7 @@ struct Engine {
   std::vector<cudaStream_t> rs_copy_streams;
   std::vector<cudaEvent_t> rs_par_ev;
   static constexpr int kRsChunkTiles = 128;  // 4 M elements per pipelined chunk
-  static constexpr int64_t kRsMinChunkBytes = int64_t(64) << 20;  // per peer copy
+  int64_t rs_min_chunk_bytes = 0;  // per peer copy, 0 = auto (HZP_RS_MIN_CHUNK_MB)
   bool rs_ce = true;
   // Z1 with DZP replicas (R > 1): the remote replicas' gradient segments of
   // this rank's chunk are copied (copy engines) into double-buffered local
