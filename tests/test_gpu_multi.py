@@ -66,3 +66,20 @@ def test_multiprocess_ragged_shards_match_oracle(n, z):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert r.stdout.count(": OK") == n
+
+
+@pytest.mark.parametrize("n,z", [(4, (4, 4, 4)), (4, (4, 2, 2))])
+@pytest.mark.parametrize("knobs", [{"HZP_RS_PAR": "0"}, {"HZP_AG_PAR": "1"}])
+def test_multiprocess_copy_stream_variants_match_oracle(n, z, knobs):
+    """The copy-engine stream layouts besides the defaults (one rotated RS copy
+    stream; one AG copy stream per owner) give the same bitwise step."""
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    port = 29660 + n + 2 * ("HZP_AG_PAR" in knobs) + 4 * (z[1] == 2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *map(str, z), "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=dict(os.environ, **knobs))
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count(": OK") == n
