@@ -141,6 +141,36 @@ typedef struct {
 int hzp_simulate(const hzp_graph* g, int depth, int rs_slots, int mode, double* start,
                  double* end, hzp_sim_summary* summary);
 
+/* Static-memory ledger (replaces hzp::ledger, memory.hpp:47 / memory.cpp:35-45):
+ * per-rank bytes of bf16 params / fp32 grads / master / m / v shards. */
+typedef struct {
+  int64_t params_bf16, grads_fp32, replica_fp32, momentum_fp32, variance_fp32, total_static;
+} hzp_ledger;
+int hzp_memory_ledger(const hzp_model_spec* spec, const hzp_parallel* par, hzp_ledger* out);
+
+/* Pool occupancy / fragmentation / peak gradient-buffer bytes of a timeline
+ * (replaces hzp::memory_trace, sched.hpp:139-149 / sched.cpp:389-466).  With
+ * start == end == NULL the timeline is simulate(g, depth, rs_slots, mode);
+ * otherwise start[i] / end[i] are MEASURED task times (e.g. hzp_timeline) and
+ * the release points, busy time and memory samples are derived from them by
+ * the same rules.  static_bytes = ledger.total_static.  Samples (time, bytes
+ * incl. static) are written up to cap; n_samples is the full count. */
+typedef struct {
+  int64_t peak_bytes;             /* static + peak dynamic */
+  double fragmentation;           /* (reserved pools - max live pools) / reserved */
+  int64_t peak_grad_buffer_bytes; /* live unsharded-gradient buffers x rs slot bytes */
+  int64_t peak_memory;            /* Timeline::peak_memory (dynamic only) */
+  double makespan;
+  int n_samples;
+} hzp_memory_report;
+int hzp_memory_trace(const hzp_graph* g, int depth, int rs_slots, int mode, const double* start,
+                     const double* end, int64_t static_bytes, hzp_memory_report* out, double* sample_t,
+                     int64_t* sample_bytes, int cap);
+/* Model FLOPs / (makespan x peak_flops) (replaces hzp::utilization_report,
+ * sched.hpp:151-152 / sched.cpp:468-477); timeline chosen as above. */
+int hzp_utilization_report(const hzp_graph* g, int depth, int rs_slots, int mode, const double* start,
+                           const double* end, double peak_flops, double* out);
+
 /* LaunchPlan (new): the per-task issue record the device executor follows.
  * slot = k % depth for the k-th AG-pool task, k % rs_slots for the k-th RS
  * task, -1 otherwise; ring_wait = the task whose completion frees that slot

@@ -314,7 +314,10 @@ class RefLib:
                         ("ag_slot_count", C.c_int), ("rs_slot_count", C.c_int),
                         ("ag_slot_bytes", C.c_longlong), ("rs_slot_bytes", C.c_longlong),
                         ("r1_eliminated_ag", C.c_int), ("r2_merged_rs", C.c_int),
-                        ("r3_eliminated_ag", C.c_int), ("extra_cached_bytes", C.c_longlong)]
+                        ("r3_eliminated_ag", C.c_int), ("extra_cached_bytes", C.c_longlong),
+                        ("total_static", C.c_longlong), ("peak_bytes", C.c_longlong),
+                        ("utilization", C.c_double), ("n_samples", C.c_int),
+                        ("sample_time_sum", C.c_double), ("sample_bytes_sum", C.c_longlong)]
         cap = 6 * layers * num_mb * max(1, vpp) + 4 * layers + 8
         ints = lambda: np.zeros(cap, dtype=np.int32)  # noqa: E731
         dbl = lambda: np.zeros(cap, dtype=np.float64)  # noqa: E731

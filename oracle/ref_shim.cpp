@@ -236,6 +236,12 @@ struct RefSimOut {
   long long ag_slot_bytes, rs_slot_bytes;
   int r1_eliminated_ag, r2_merged_rs, r3_eliminated_ag;  // ReuseReport (pipeline.hpp:44-49)
   long long extra_cached_bytes;
+  // memory_trace / utilization_report (sched.cpp:389-477)
+  long long total_static, peak_bytes;
+  double utilization;  // peak_flops = device_flops
+  int n_samples;
+  double sample_time_sum;
+  long long sample_bytes_sum;
 };
 
 int ref_task_graph(long long layers, long long ppl, long long seq, long long mbsize,
@@ -317,6 +323,16 @@ int ref_task_graph(long long layers, long long ppl, long long seq, long long mbs
     sim->r2_merged_rs = rep.r2_merged_rs;
     sim->r3_eliminated_ag = rep.r3_eliminated_ag;
     sim->extra_cached_bytes = rep.extra_cached_bytes;
+    sim->total_static = hzp::ledger(spec, cfg).total_static;
+    sim->peak_bytes = mem.peak_bytes;
+    sim->utilization = hzp::utilization_report(tl, spec, device_flops);
+    sim->n_samples = static_cast<int>(mem.samples.size());
+    sim->sample_time_sum = 0.0;
+    sim->sample_bytes_sum = 0;
+    for (const auto& [t, b] : mem.samples) {
+      sim->sample_time_sum += t;
+      sim->sample_bytes_sum += b;
+    }
     return n;
   } catch (const std::exception& e) {
     g_err = e.what();

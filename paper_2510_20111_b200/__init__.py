@@ -10,8 +10,8 @@ library has not been built.
 from . import _native  # noqa: F401  (raises ImportError when the .so is missing)
 from .hzp import (ASYNC, VANILLA, CostModel, ModelSpec, ParallelConfig, SchedError,  # noqa: F401
                   TaskGraph, ValidationError, build_process_groups, build_task_graph,
-                  derive_prelaunch_depth, launch_plan, make_pools, shard_elems, simulate,
-                  validate_config)
+                  derive_prelaunch_depth, launch_plan, ledger, make_pools, memory_trace, shard_elems,
+                  simulate, utilization_report, validate_config)
 from .engine import BF16, FP32, GPT, MLP, EngineConfig, HzpEngine  # noqa: F401
 
 __version__ = "0.1.0"

@@ -56,6 +56,17 @@ class hzp_sim_summary(C.Structure):
                 ("compute_busy", C.c_double)]
 
 
+class hzp_ledger(C.Structure):
+    _fields_ = [("params_bf16", C.c_int64), ("grads_fp32", C.c_int64), ("replica_fp32", C.c_int64),
+                ("momentum_fp32", C.c_int64), ("variance_fp32", C.c_int64), ("total_static", C.c_int64)]
+
+
+class hzp_memory_report(C.Structure):
+    _fields_ = [("peak_bytes", C.c_int64), ("fragmentation", C.c_double),
+                ("peak_grad_buffer_bytes", C.c_int64), ("peak_memory", C.c_int64),
+                ("makespan", C.c_double), ("n_samples", C.c_int)]
+
+
 class hzp_plan_entry(C.Structure):
     _fields_ = [("id", C.c_int), ("kind", C.c_int), ("layer", C.c_int), ("microbatch", C.c_int),
                 ("stream", C.c_int), ("slot", C.c_int), ("ring_wait", C.c_int),
@@ -111,6 +122,11 @@ SIGNATURES = [
     ("hzp_make_pools", C.c_int, [_vp, C.c_int, C.c_int, _P(hzp_pool), _P(hzp_pool)]),
     ("hzp_simulate", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_double), _P(C.c_double),
                                _P(hzp_sim_summary)]),
+    ("hzp_memory_ledger", C.c_int, [_P(hzp_model_spec), _P(hzp_parallel), _P(hzp_ledger)]),
+    ("hzp_memory_trace", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_double), _P(C.c_double), C.c_int64,
+                                   _P(hzp_memory_report), _P(C.c_double), _P(C.c_int64), C.c_int]),
+    ("hzp_utilization_report", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_double), _P(C.c_double),
+                                         C.c_double, _P(C.c_double)]),
     ("hzp_plan_entry_get", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(hzp_plan_entry)]),
     ("hzp_comm_tiles", C.c_int, [_P(hzp_parallel), C.c_int64, _P(C.c_int64), _P(C.c_int64), C.c_int,
                                  C.c_int, C.c_int, _P(hzp_comm_tile), C.c_int, _P(C.c_int),

@@ -225,6 +225,59 @@ int hzp_simulate(const hzp_graph* g, int depth, int rs_slots, int mode, double* 
   });
 }
 
+int hzp_memory_ledger(const hzp_model_spec* spec, const hzp_parallel* par, hzp_ledger* out) {
+  if (!spec || !par || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    const MemoryLedger m = ledger(to_spec(spec), to_cfg(par));
+    *out = {m.params_bf16, m.grads_fp32, m.replica_fp32, m.momentum_fp32, m.variance_fp32, m.total_static};
+  });
+}
+
+namespace {
+// simulate() or the measured start / end times, with derived fields
+Timeline timeline_of(const hzp_graph* g, const PoolSet& pools, int mode, const double* start, const double* end) {
+  if (!start != !end) throw std::invalid_argument("start and end must both be given or both be NULL");
+  if (!start) return simulate(g->g, pools, mode == HZP_MODE_VANILLA ? SchedMode::Vanilla : SchedMode::Async);
+  Timeline tl;
+  tl.mode = mode == HZP_MODE_VANILLA ? SchedMode::Vanilla : SchedMode::Async;
+  tl.entries.resize(g->g.tasks.size());
+  for (size_t i = 0; i < tl.entries.size(); ++i) {
+    tl.entries[i].start = start[i];
+    tl.entries[i].end = end[i];
+  }
+  finish_timeline(g->g, pools, tl);
+  return tl;
+}
+}  // namespace
+
+int hzp_memory_trace(const hzp_graph* g, int depth, int rs_slots, int mode, const double* start,
+                     const double* end, int64_t static_bytes, hzp_memory_report* out, double* sample_t,
+                     int64_t* sample_bytes, int cap) {
+  if (!g || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    const PoolSet pools = make_pools(g->g, depth, rs_slots);
+    const Timeline tl = timeline_of(g, pools, mode, start, end);
+    MemoryLedger led;
+    led.total_static = static_bytes;
+    const MemoryTraceResult m = memory_trace(tl, led, pools);
+    *out = {m.peak_bytes, m.fragmentation, m.peak_grad_buffer_bytes, tl.peak_memory, tl.makespan,
+            static_cast<int>(m.samples.size())};
+    for (int i = 0; i < cap && i < static_cast<int>(m.samples.size()); ++i) {
+      if (sample_t) sample_t[i] = m.samples[i].first;
+      if (sample_bytes) sample_bytes[i] = m.samples[i].second;
+    }
+  });
+}
+
+int hzp_utilization_report(const hzp_graph* g, int depth, int rs_slots, int mode, const double* start,
+                           const double* end, double peak_flops, double* out) {
+  if (!g || !out) return HZP_ERR_ARG;
+  return guarded([&] {
+    const PoolSet pools = make_pools(g->g, depth, rs_slots);
+    *out = utilization_report(timeline_of(g, pools, mode, start, end), g->g.spec, peak_flops);
+  });
+}
+
 int hzp_plan_entry_get(const hzp_graph* cg, int depth, int rs_slots, int i, hzp_plan_entry* out) {
   auto* g = const_cast<hzp_graph*>(cg);
   if (!g || !out) return HZP_ERR_ARG;
@@ -387,6 +440,9 @@ int hzp_state_upload(hzp_ctx* ctx, int rank, int field, const void* host, int64_
     void* p = field_ptr(e, li, field, &es, &cnt);
     if (n != cnt) throw std::invalid_argument("element count mismatch");
     HZP_CUDA(cudaSetDevice(e.cfg.device));
+    // the engine's streams are non-blocking: a step issued with step_async may
+    // still be reading / writing this buffer
+    HZP_CUDA(cudaDeviceSynchronize());
     HZP_CUDA(cudaMemcpy(p, host, size_t(n) * es, cudaMemcpyHostToDevice));
   });
 }
@@ -707,7 +763,10 @@ int hzp_zero_grads(hzp_ctx* ctx) {
   if (!ctx) return HZP_ERR_ARG;
   return guarded([&] {
     Engine& e = *ctx->e;
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    HZP_CUDA(cudaDeviceSynchronize());  // see hzp_state_upload
     for (auto& l : e.locals) HZP_CUDA(cudaMemset(e.arenas[l.rank].grad, 0, size_t(e.geom.s2) * 4));
+    HZP_CUDA(cudaDeviceSynchronize());
   });
 }
 

@@ -408,6 +408,75 @@ struct RingState {
   }
 };
 
+// Interval bookkeeping for the memory sweeps: each hold adds +amount at t0
+// and -amount at t1; sweeps visit events by time, equal times in insertion
+// order (a stable sort), which fixes how coincident frees and allocations
+// count toward a peak.
+struct Events {
+  std::vector<std::pair<double, std::int64_t>> ev;
+  void hold(double t0, double t1, std::int64_t amount) {
+    ev.emplace_back(t0, amount);
+    ev.emplace_back(t1, -amount);
+  }
+  void sort() {
+    std::stable_sort(ev.begin(), ev.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  }
+  std::int64_t peak() {
+    sort();
+    std::int64_t live = 0, top = 0;
+    for (const auto& [t, d] : ev) top = std::max(top, live += d);
+    return top;
+  }
+};
+
+// Everything a timeline derives from its tasks' start / end times: release
+// points (an AG's buffer lives until its LAST consumer ends, its pool slot
+// until its FIRST consumer ends), makespan, compute busy / idle
+// (sched.cpp:341-350) and the dynamic-memory samples (pool slots + the
+// unsharded gradients each RS consumes).  `dur` = the busy time per task.
+void derive_timeline(const TaskGraph& graph, const PoolSet& pools, const std::vector<double>& dur, Timeline& tl) {
+  const int n = static_cast<int>(graph.tasks.size());
+  const std::vector<int> fc = first_consumers(graph);
+  std::vector<double> last_use(n, 0.0);
+  for (const auto& t : graph.tasks)
+    for (int d : t.deps) last_use[d] = std::max(last_use[d], tl.entries[t.id].end);
+  double last_compute = 0.0;
+  for (int id = 0; id < n; ++id) {
+    auto& e = tl.entries[id];
+    e.buffer_release = std::max(e.end, last_use[id]);
+    e.pool_release = fc[id] >= 0 ? tl.entries[fc[id]].end : e.end;
+    tl.makespan = std::max(tl.makespan, e.end);
+    if (e.stream == StreamId::Compute) {
+      tl.compute_busy += dur[id];
+      last_compute = std::max(last_compute, e.end);
+    }
+  }
+  tl.compute_idle = last_compute - tl.compute_busy;
+  Events mem;
+  for (int id = 0; id < n; ++id) {
+    const Task& t = graph.tasks[id];
+    const auto& e = tl.entries[id];
+    if (uses_ag_pool(t.kind)) {
+      mem.hold(e.start, e.buffer_release, pools.ag.slot_bytes);
+    } else if (t.kind == TaskKind::RsGrad) {
+      mem.hold(e.start, e.end, pools.rs.slot_bytes);
+      for (int d : t.deps)
+        if (graph.tasks[d].kind == TaskKind::Bwd && graph.tasks[d].layer == t.layer)
+          mem.hold(tl.entries[d].end, e.end, graph.grad_buf_bytes);
+    }
+  }
+  mem.sort();
+  std::int64_t live = 0;
+  for (const auto& [t, d] : mem.ev) {
+    live += d;
+    if (!tl.memory_samples.empty() && tl.memory_samples.back().first == t)
+      tl.memory_samples.back().second = std::max(tl.memory_samples.back().second, live);
+    else
+      tl.memory_samples.emplace_back(t, live);
+    tl.peak_memory = std::max(tl.peak_memory, live);
+  }
+}
+
 }  // namespace
 
 Timeline simulate(const TaskGraph& graph, const PoolSet& pools, SchedMode mode) {
@@ -455,22 +524,80 @@ Timeline simulate(const TaskGraph& graph, const PoolSet& pools, SchedMode mode) 
     e.end = t1[id];
     e.bytes = t.bytes;
   }
-  std::vector<double> last_use(n, 0.0);
-  for (const auto& t : graph.tasks)
-    for (int d : t.deps) last_use[d] = std::max(last_use[d], t1[t.id]);
-  double last_compute = 0.0;
+  std::vector<double> dur(n);
+  for (int id = 0; id < n; ++id) dur[id] = graph.tasks[id].duration;
+  derive_timeline(graph, pools, dur, tl);
+  return tl;
+}
+
+void finish_timeline(const TaskGraph& graph, const PoolSet& pools, Timeline& tl) {
+  const int n = static_cast<int>(graph.tasks.size());
+  if (static_cast<int>(tl.entries.size()) != n) throw std::invalid_argument("timeline / graph size mismatch");
+  std::vector<double> dur(n);
   for (int id = 0; id < n; ++id) {
+    const Task& t = graph.tasks[id];
     auto& e = tl.entries[id];
-    e.buffer_release = std::max(t1[id], last_use[id]);
-    e.pool_release = fc[id] >= 0 ? t1[fc[id]] : t1[id];
-    tl.makespan = std::max(tl.makespan, t1[id]);
-    if (e.stream == StreamId::Compute) {
-      tl.compute_busy += graph.tasks[id].duration;
-      last_compute = std::max(last_compute, t1[id]);
+    e.task_id = id;
+    e.kind = t.kind;
+    e.layer = t.layer;
+    e.microbatch = t.microbatch;
+    e.stream = stream_of(t.kind);
+    e.bytes = t.bytes;
+    dur[id] = e.end - e.start;
+  }
+  tl.makespan = tl.compute_busy = tl.compute_idle = 0.0;
+  tl.memory_samples.clear();
+  tl.peak_memory = 0;
+  derive_timeline(graph, pools, dur, tl);
+}
+
+MemoryTraceResult memory_trace(const Timeline& timeline, const MemoryLedger& ledger, const PoolSet& pools) {
+  MemoryTraceResult out;
+  out.peak_bytes = ledger.total_static + timeline.peak_memory;
+  out.samples.reserve(timeline.memory_samples.size());
+  for (const auto& [t, live] : timeline.memory_samples) out.samples.emplace_back(t, ledger.total_static + live);
+
+  Events ag, rs, grad;
+  for (const auto& e : timeline.entries) {
+    if (uses_ag_pool(e.kind)) ag.hold(e.start, e.pool_release, pools.ag.slot_bytes);  // ring slot
+    else if (e.kind == TaskKind::RsGrad) rs.hold(e.start, e.end, pools.rs.slot_bytes);
+  }
+  // gradient buffers, counted: BWD(l, mb) end -> end of the RS that consumes it
+  std::map<std::pair<int, int>, double> open;  // (layer, mb) -> BWD end
+  std::map<int, double> last_rs;               // layer -> latest RS end
+  for (const auto& e : timeline.entries) {
+    if (e.kind == TaskKind::Bwd) {
+      open[{e.layer, e.microbatch}] = e.end;
+    } else if (e.kind == TaskKind::RsGrad) {
+      const auto it = open.find({e.layer, e.microbatch});
+      if (it != open.end()) {
+        grad.hold(it->second, e.end, 1);
+        open.erase(it);
+      }
+      last_rs[e.layer] = std::max(last_rs[e.layer], e.end);
     }
   }
-  tl.compute_idle = last_compute - tl.compute_busy;
-  return tl;
+  // a BWD whose RS was merged away (reuse R2) holds its buffer until the
+  // layer's last RS ends
+  for (const auto& [key, t_bwd] : open) {
+    const auto it = last_rs.find(key.first);
+    if (it != last_rs.end() && it->second > t_bwd) grad.hold(t_bwd, it->second, 1);
+  }
+  const std::int64_t live_pools =
+      std::min(ag.peak(), pools.ag.capacity) + std::min(rs.peak(), pools.rs.capacity);
+  const std::int64_t reserved = pools.ag.capacity + pools.rs.capacity;
+  out.fragmentation = reserved > 0 ? static_cast<double>(reserved - live_pools) / static_cast<double>(reserved) : 0.0;
+  out.peak_grad_buffer_bytes = grad.peak() * pools.rs.slot_bytes;
+  return out;
+}
+
+double utilization_report(const Timeline& timeline, const ModelSpec& spec, double peak_flops) {
+  // forward + backward = 3 x forward FLOPs over every token of every layer
+  const double model_flops = 3.0 * spec.flops_per_token_per_layer * static_cast<double>(spec.seq_len) *
+                             static_cast<double>(spec.micro_batch_size) *
+                             static_cast<double>(spec.num_microbatches) * static_cast<double>(spec.num_layers);
+  if (timeline.makespan <= 0.0 || peak_flops <= 0.0) return 0.0;
+  return model_flops / (timeline.makespan * peak_flops);
 }
 
 LaunchPlan build_launch_plan(const TaskGraph& graph, const PoolSet& pools) {

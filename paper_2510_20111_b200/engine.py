@@ -157,7 +157,14 @@ class HzpEngine:
 
     def save_checkpoint(self, path: str) -> None:
         """One .npz per driven rank: param (working dtype), grad, master, m, v
-        shards and the Adam step — the reference's ShardedState (train.hpp:73-83)."""
+        shards and the Adam step — the reference's ShardedState (train.hpp:73-83).
+
+        ``grad`` is this rank's Z2 shard as the reduce-scatter left it.  With
+        DZP replicas (dp / z2 > 1) the reference all-reduces it across the
+        replicas (train.cpp:326-341); here that sum is formed only inside the
+        fused Z1 kernel (registers), so the saved ``grad`` is the per-replica
+        shard, not the reference's all-reduced one.  Resuming is unaffected:
+        the first reduce-scatter of the next step overwrites it."""
         import os
         os.makedirs(path, exist_ok=True)
         for r in self.driven_ranks():
@@ -165,7 +172,9 @@ class HzpEngine:
                      grad=self.download(r, F_GRAD), master=self.download(r, F_MASTER),
                      mom=self.download(r, F_MOM), var=self.download(r, F_VAR),
                      adam_step=np.int64(self.get_step(r)), P=np.int64(self.P),
-                     layout=np.array([self.cfg.par.dp, self.cfg.par.z1, self.cfg.par.z2, self.cfg.par.z3]))
+                     layout=np.array([self.cfg.par.dp, self.cfg.par.z1, self.cfg.par.z2, self.cfg.par.z3]),
+                     precision=np.int64(self.cfg.precision), model=np.int64(self.cfg.model),
+                     layers=np.array(self.layers, dtype=np.int64).reshape(-1, 2))
 
     def load_checkpoint(self, path: str) -> None:
         import os
@@ -174,6 +183,14 @@ class HzpEngine:
             if int(z["P"]) != self.P or list(z["layout"]) != [self.cfg.par.dp, self.cfg.par.z1,
                                                               self.cfg.par.z2, self.cfg.par.z3]:
                 raise ValueError("checkpoint layout does not match this ctx")
+            if "precision" not in z or int(z["precision"]) != self.cfg.precision:
+                raise ValueError("checkpoint precision does not match this ctx "
+                                 "(a bf16 working copy would be reinterpreted as fp32 or truncated)")
+            if int(z["model"]) != self.cfg.model or [tuple(x) for x in z["layers"]] != \
+                    [tuple(x) for x in self.layers]:
+                raise ValueError("checkpoint model / layer table does not match this ctx")
+            if z["param"].dtype != self._field_shape(F_PARAM)[1]:
+                raise ValueError("checkpoint param dtype does not match the working precision")
             self.upload(r, F_PARAM, z["param"])
             self.upload(r, F_GRAD, z["grad"])
             self.upload(r, F_MASTER, z["master"])

@@ -190,6 +190,49 @@ def simulate(graph: TaskGraph, depth: int = 2, rs_slots: int = 1, mode: int = AS
     return Timeline(list(s)[:n], list(e)[:n], summ.makespan, summ.compute_idle, summ.compute_busy)
 
 
+def ledger(spec: ModelSpec, cfg: ParallelConfig) -> dict:
+    """Per-rank static bytes of the sharded states (memory.hpp:47)."""
+    m = N.hzp_ledger()
+    N.check(N.lib.hzp_memory_ledger(C.byref(spec.c()), C.byref(cfg.c()), C.byref(m)))
+    return {f: getattr(m, f) for f, _ in N.hzp_ledger._fields_}
+
+
+def _times(graph, start, end):
+    if start is None:
+        return None, None
+    n = len(graph.tasks)
+    if len(start) != n or len(end) != n:
+        raise ValueError("one start / end time per task")
+    return (C.c_double * n)(*start), (C.c_double * n)(*end)
+
+
+def memory_trace(graph: TaskGraph, depth: int = 2, rs_slots: int = 1, mode: int = ASYNC,
+                 static_bytes: int = 0, start=None, end=None) -> dict:
+    """memory_trace (sched.hpp:139-149) of simulate(graph, ...) or, with
+    start / end, of a measured timeline: peak bytes (static + dynamic), pool
+    fragmentation, peak gradient-buffer bytes and the (time, bytes) samples."""
+    s, e = _times(graph, start, end)
+    out = N.hzp_memory_report()
+    N.check(N.lib.hzp_memory_trace(graph._h, depth, rs_slots, mode, s, e, static_bytes, C.byref(out),
+                                   None, None, 0))
+    cap = max(1, out.n_samples)
+    ts, bs = (C.c_double * cap)(), (C.c_int64 * cap)()
+    N.check(N.lib.hzp_memory_trace(graph._h, depth, rs_slots, mode, s, e, static_bytes, C.byref(out),
+                                   ts, bs, cap))
+    r = {f: getattr(out, f) for f, _ in N.hzp_memory_report._fields_}
+    r["samples"] = list(zip(list(ts)[: out.n_samples], list(bs)[: out.n_samples]))
+    return r
+
+
+def utilization_report(graph: TaskGraph, peak_flops: float, depth: int = 2, rs_slots: int = 1,
+                       mode: int = ASYNC, start=None, end=None) -> float:
+    """Model FLOPs / (makespan x peak) (sched.hpp:151-152)."""
+    s, e = _times(graph, start, end)
+    v = C.c_double()
+    N.check(N.lib.hzp_utilization_report(graph._h, depth, rs_slots, mode, s, e, peak_flops, C.byref(v)))
+    return v.value
+
+
 @dataclass
 class PlanEntry:
     id: int

@@ -12,9 +12,9 @@ pytestmark = pytest.mark.gpu
 DIMS, DP, Z, MBS, BATCH = [12, 20, 8], 4, (4, 2, 2), 2, 4
 
 
-def _engine(timeline=0):
+def _engine(timeline=0, precision=0):
     from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
-    return HzpEngine(EngineConfig(model=0, precision=0, dims=DIMS, batch=BATCH, num_microbatches=MBS,
+    return HzpEngine(EngineConfig(model=0, precision=precision, dims=DIMS, batch=BATCH, num_microbatches=MBS,
                                   par=ParallelConfig(dp=DP, z1=Z[0], z2=Z[1], z3=Z[2]), timeline=timeline))
 
 
@@ -35,6 +35,20 @@ def test_checkpoint_round_trip_is_bitwise(gpu, oracle, tmp_path):
     for r in range(DP):
         for f in range(5):
             assert np.array_equal(a.download(r, f), b.download(r, f)), (r, f)
+    a.close()
+    b.close()
+
+
+def test_checkpoint_rejects_other_precision(gpu, oracle, tmp_path):
+    """A bf16 checkpoint (param = uint16 bit patterns) must not load into an
+    fp32 ctx (same element count) and vice versa."""
+    st = oracle.shard_init(DIMS, DP, *Z, 2024, True)
+    a = _engine(precision=1)
+    a.load_state(st)
+    a.save_checkpoint(str(tmp_path))
+    b = _engine(precision=0)
+    with pytest.raises(ValueError, match="precision"):
+        b.load_checkpoint(str(tmp_path))
     a.close()
     b.close()
 
