@@ -224,54 +224,218 @@ def run_reference(args):
     return 0
 
 
+# ---- same-config workloads (the reference's own model on both arms) --------
+# configs[0]: the reference's CPU case exactly (train.cpp:484-512, 540;
+# SURVEY §8(d)-1): MLP {12, 20, 8}, 4 ranks z = (4, 2, 2), 4 rows per rank,
+# 1 microbatch, 10 steps, seed 2024, fp32.  mlp-slice: a GEMM-sized MLP the
+# reference can still time on a CPU, mixed precision.
+MLP_CASES = {
+    "mlp": dict(dims=[12, 20, 8], dp=4, z=(4, 2, 2), batch=4, mbs=1, steps=10, prec=0,
+                workload="BASELINE configs[0]: MLP{12,20,8} fp32, 4 ranks z=(4,2,2), B=4, 10 steps, seed 2024"),
+    "mlp-slice": dict(dims=[1024, 4096, 1024], dp=4, z=(4, 2, 2), batch=64, mbs=2, steps=2, prec=1,
+                      workload="SURVEY §8(d)-2 MLP slice {1024,4096,1024} mixed bf16, 4 ranks z=(4,2,2), "
+                               "2 microbatches x 64 rows, seed 2024"),
+}
+
+
+def ref_mlp(case, steps, cores=1):
+    """The reference's train_step_hzp<float> (oracle/_ref = its sources
+    compiled unmodified) on the same config: rows/s on `cores` concurrent
+    single-threaded processes (the reference has no threading)."""
+    import numpy as np
+    from oracle import load_ref
+    ref = load_ref()
+    if ref is None:
+        return None
+    d = np.asarray(case["dims"], dtype=np.int32)
+    z1, z2, z3 = case["z"]
+
+    def one(_=None):
+        losses = np.zeros(case["dp"], np.float32)
+        sec = ref.L.ref_time_steps_f32(d, len(d) - 1, case["dp"], z1, z2, z3, case["mbs"], case["batch"], 2024,
+                                       steps, case["prec"], losses)
+        return sec, losses
+
+    if cores > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(cores) as pool:
+            res = pool.map(one, range(cores))
+    else:
+        res = [one()]
+    rows = case["dp"] * case["mbs"] * case["batch"]
+    return {"value": sum(rows / sec for sec, _ in res), "sec_per_step": res[0][0], "cores": cores,
+            "losses": [float(x) for x in res[0][1]]}
+
+
+def hzp_mlp(case, steps, warmup, local):
+    """The same config on the B200 engine: all dp ranks emulated on one GPU
+    (the kernels of the multi-rank path), device-timed and e2e (host inputs
+    copied in, losses copied out, every step)."""
+    import numpy as np
+    import torch
+    from oracle import load_oracle  # input generator (the reference's run_case seeding)
+    from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
+    from paper_2510_20111_b200.engine import kernel_launches
+    o = load_oracle()
+    z1, z2, z3 = case["z"]
+    dims, dp, mbs, B = case["dims"], case["dp"], case["mbs"], case["batch"]
+    eng = HzpEngine(EngineConfig(model=0, precision=case["prec"], dims=dims, batch=B, num_microbatches=mbs,
+                                 par=ParallelConfig(dp=dp, z1=z1, z2=z2, z3=z3), device=local))
+    eng.load_state(o.shard_init(dims, dp, z1, z2, z3, 2024, bool(case["prec"])))
+    xs = [o.make_inputs(dims, dp, mbs, B, 2024, s) for s in range(steps)]
+    host = [torch.from_numpy(x).pin_memory() for x in xs]
+    dev = [h.to(f"cuda:{local}") for h in host]
+    cs = torch.cuda.ExternalStream(eng.stream(0), device=f"cuda:{local}")
+    for i in range(warmup):
+        eng.step_async(dev[i % steps].data_ptr(), True)
+    eng.sync()
+    eng.load_state(o.shard_init(dims, dp, z1, z2, z3, 2024, bool(case["prec"])))  # restart from step 0
+    k0 = kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
+    for s in range(steps):
+        eng.step_async(dev[s].data_ptr(), True)
+    e1.record(cs)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    launches = (kernel_launches() - k0) // steps
+    eng.load_state(o.shard_init(dims, dp, z1, z2, z3, 2024, bool(case["prec"])))
+    t0 = time.perf_counter()
+    for s in range(steps):
+        losses = eng.step(host[s].numpy(), on_device=False)
+    e2e_s = (time.perf_counter() - t0) / steps
+    eng.close()
+    rows = dp * mbs * B
+    return {"ms": ms, "value": rows / (ms / 1e3), "e2e": rows / e2e_s, "e2e_ms": e2e_s * 1e3,
+            "losses": [float(x) for x in losses], "launches": int(launches),
+            "h2d": int(xs[0].nbytes), "d2h": 4 * dp}
+
+
+def same_config(which="mlp", cores=1, local=0, warmup=3):
+    """Both arms on the identical workload (same model, ranks, rows, steps,
+    precision and inputs): the like-for-like comparison."""
+    case = MLP_CASES[which]
+    g = hzp_mlp(case, case["steps"], warmup, local)
+    r = ref_mlp(case, case["steps"], cores)
+    out = {"same_config": True, "workload": case["workload"], "unit": "rows/s",
+           "hzp": {"value": round(g["value"], 1), "e2e": round(g["e2e"], 1), "ms_per_step": round(g["ms"], 4),
+                   "loss_final": g["losses"]},
+           "reference": None, "ratio": None, "e2e_ratio": None}
+    if r:
+        out["reference"] = {"value": round(r["value"], 1), "cores": r["cores"],
+                            "ms_per_step": round(r["sec_per_step"] * 1e3, 4), "loss_final": r["losses"]}
+        out["ratio"] = round(g["value"] / r["value"], 1)
+        out["e2e_ratio"] = round(g["e2e"] / r["value"], 1)
+    return out
+
+
+def run_mlp(args):
+    """--model mlp | mlp-slice: the same-config line (both arms share it)."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    case = MLP_CASES[args.model]
+    if args.impl == "reference":
+        cores = usable_cores()
+        r = ref_mlp(case, case["steps"], cores)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhzpref.so not built"}))
+            return 0
+        line = {"metric": METRIC, "value": round(r["value"], 2), "unit": "rows/s", "n_gpus": args.gpus,
+                "steps": case["steps"], "warmup": 0, "ms_per_step": round(r["sec_per_step"] * 1e3, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (run_case seeding)", "impl": "reference", "same_config": True,
+                "config": {"workload": case["workload"]},
+                "cpu_baseline": {"value": round(r["value"], 2), "unit": "rows/s", "cores": r["cores"],
+                                 "kind": "reference", "sample": f"{case['steps']} steps per process"},
+                "e2e": {"value": round(r["value"], 2), "unit": "rows/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    import torch
+    torch.cuda.set_device(local)
+    g = hzp_mlp(case, case["steps"], args.warmup, local)
+    r = ref_mlp(case, case["steps"], 1) if not args.no_cpu_baseline else None
+    line = {"metric": METRIC, "value": round(g["value"], 1), "unit": "rows/s", "n_gpus": 1,
+            "steps": case["steps"], "warmup": args.warmup, "ms_per_step": round(g["ms"], 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if case["prec"] == 0 else "bf16", "data": "synthetic (run_case seeding)",
+            "same_config": True, "config": {"workload": case["workload"], "parallelism": "dp4 emulated on 1 GPU"},
+            "gpu_launches": g["launches"], "loss_final": g["losses"],
+            "e2e": {"value": round(g["e2e"], 1), "unit": "rows/s", "h2d_bytes_per_step": g["h2d"],
+                    "d2h_bytes_per_step": g["d2h"], "ms_per_step": round(g["e2e_ms"], 4)},
+            "cpu_baseline": ({"value": round(r["value"], 2), "unit": "rows/s", "cores": 1, "kind": "reference",
+                              "sample": f"the same {case['steps']} steps, 1 thread",
+                              "loss_final": r["losses"]} if r else None)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def usable_cores():
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        import psutil
+        cores = max(1, min(cores, int(psutil.virtual_memory().available // (1 << 30)) - 2))
+    except Exception:  # noqa: BLE001
+        pass
+    return max(1, min(cores, 64))
+
+
 NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU
 
 
+NVLINK_MEASURED_GBPS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
 def collectives(eng, N, local, max_over_ranks, barrier, z2, z3, iters=5):
-    """AG / RS bus bandwidth of one 1.3B transformer layer (the step's own
-    collective, through the ctx: copy-engine NVLink leg by default) and an NCCL
-    comparator on the same bytes.  busbw = (N-1)/N x layer bytes / time
-    (nccl-tests convention)."""
+    """The step's own AG / RS of one 1.3B transformer layer through the ctx
+    (hzp_collective_time: back-to-back on the collective's stream, CUDA
+    events, max over ranks) and an NCCL comparator on the same bytes.
+
+    With the flat layout a layer sits inside ONE member's shard, so the AG is
+    a broadcast from that owner (NVLS multimem.st: the layer crosses the
+    owner's link once) and the RS a reduce at that owner (multimem.ld_reduce:
+    the bf16 sum crosses the owner's link once).  owner_link = layer bytes /
+    time is the utilisation of that link; busbw = (g-1)/g x layer bytes /
+    time is the nccl-tests convention of the balanced collective."""
     import torch
     import torch.distributed as dist
     off, n = eng.layers[1]
     nbytes = n * 2  # bf16 working copy / bf16 gradient wire
-    out = {"layer_elems": int(n), "layer_bytes": int(nbytes), "nvlink_peak_GBps": NVLINK_GBPS}
+    out = {"layer_elems": int(n), "layer_bytes": int(nbytes), "nvlink_peak_GBps": NVLINK_GBPS,
+           "nvlink_measured_GBps": NVLINK_MEASURED_GBPS}
+    for name, g in (("ag", z3), ("rs", z2)):
+        if g <= 1:  # z3 = 1: layers read the shard in place; z2 = 1: RS fused into wgrad
+            out[name] = None
+            continue
+        eng.collective_time(name, 1, 2)
+        ms = max_over_ranks(eng.collective_time(name, 1, iters))
+        bw = (g - 1) / g * nbytes / (ms / 1e3) / 1e9
+        link = nbytes / (ms / 1e3) / 1e9
+        out[name] = {"group": g, "ms": round(ms, 4), "busbw_GBps": round(bw, 1),
+                     "owner_link_GBps": round(link, 1), "owner_link_frac": round(link / NVLINK_GBPS, 3),
+                     "owner_link_frac_of_measured": round(link / NVLINK_MEASURED_GBPS, 3)}
 
-    def timed(fn, stream_ptr):
-        st = torch.cuda.ExternalStream(stream_ptr, device=f"cuda:{local}") if stream_ptr else None
+    def timed(fn):
         for _ in range(2):
             fn()
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if st is not None:
-            e0.record(st)
-        else:
-            e0.record()
+        e0.record()
         for _ in range(iters):
             fn()
-        if st is not None:
-            e1.record(st)
-        else:
-            e1.record()
+        e1.record()
         e1.synchronize()
         return max_over_ranks(e0.elapsed_time(e1) / iters)
 
-    for name, fn, sid, g in (("ag", lambda: eng.ag_layer(1, 0), 1, z3), ("rs", lambda: eng.rs_layer(1, 0), 2, z2)):
-        if g <= 1:  # z3 = 1: layers read the shard in place; z2 = 1: RS fused into wgrad
-            out[name] = None
-            continue
-        ms = timed(fn, eng.stream(sid))
-        bw = (g - 1) / g * nbytes / (ms / 1e3) / 1e9
-        out[name] = {"group": g, "ms": round(ms, 4), "busbw_GBps": round(bw, 1), "frac": round(bw / NVLINK_GBPS, 3)}
     try:  # NCCL comparator (setup only; never on the step's data path)
         g = dist.new_group(backend="nccl")
         full = torch.empty(n - n % N, dtype=torch.bfloat16, device=f"cuda:{local}")
         part = torch.empty(full.numel() // N, dtype=torch.bfloat16, device=f"cuda:{local}")
         for name, fn in (("nccl_all_gather", lambda: dist.all_gather_into_tensor(full, part, group=g)),
                          ("nccl_reduce_scatter", lambda: dist.reduce_scatter_tensor(part, full, group=g))):
-            ms = timed(fn, None)
+            ms = timed(fn)
             bw = (N - 1) / N * full.numel() * 2 / (ms / 1e3) / 1e9
             out[name] = {"ms": round(ms, 4), "busbw_GBps": round(bw, 1)}
         dist.destroy_process_group(g)
@@ -432,15 +596,31 @@ def run_hzp(args):
     eng.set_timeline(False)
     idle = max_over_ranks(tl["compute_idle_ms"])
     mk = max_over_ranks(tl["makespan_ms"])
+    # in-step collective task durations (AG-param / RS of the decoder blocks;
+    # CUDA events around each task on its stream, so they include the wait
+    # for the slowest peer)
+    kinds = {r[0]: (r[1], r[2]) for r in eng.launch_log() if r[4] >= 0}
+    in_step = {}
+    for name, kind in (("ag", 3), ("rs", 4)):
+        d = sorted(tl["end_ms"][i] - tl["start_ms"][i] for i, (k, l) in kinds.items()
+                   if k == kind and 1 <= l <= c["layers"])
+        if d:
+            in_step[name] = {"tasks": len(d), "median_ms": round(statistics.median(d), 4),
+                             "max_ms": round(d[-1], 4)}
     exposed = {"compute_idle_ms": round(idle, 3), "makespan_ms": round(mk, 3),
                "frac": round(idle / mk, 4) if mk else None,
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}
     colls = collectives(eng, N, local, max_over_ranks, barrier, z2, z3) if N > 1 else None
+    if colls is not None:
+        colls["in_step"] = in_step
     z1r = z1_roofline(eng, N, local, max_over_ranks, barrier, hbm, z1, z2, z3)
     line = None
     if rank == 0:
         cb = cpu_reference(2, 0, "cpu_baseline", c) if (N == 1 and not args.no_cpu_baseline) else None
+        # the like-for-like comparison next to the headline: the reference's
+        # own CPU case (configs[0]) on both arms
+        same = same_config("mlp", 1, local) if (N == 1 and not args.no_cpu_baseline) else None
         clocks = clk.summary(t_on, t_off)
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": N,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
@@ -462,7 +642,8 @@ def run_hzp(args):
                 "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roof, "exposed_comm": exposed, "collectives": colls, "z1_adam": z1r,
                 "cpu_baseline": ({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-                                 if cb else None)}
+                                 if cb else None),
+                "same_config": same}
         print(json.dumps(line), flush=True)
     eng.close()
     if N > 1:
@@ -479,8 +660,9 @@ def main():
     ap.add_argument("--impl", default="hzp", choices=["hzp", "reference"])
     ap.add_argument("--batch", type=int, default=4, help="sequences per microbatch per GPU")
     ap.add_argument("--microbatches", type=int, default=2)
-    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b", "moe"],
-                    help="BASELINE configs[1] (default, the headline), configs[2] or configs[3]")
+    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b", "moe", "mlp", "mlp-slice"],
+                    help="BASELINE configs[1] (default, the headline), configs[2], configs[3], "
+                         "configs[0] (mlp: the reference's own CPU case) or the MLP slice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--wgrad-slots", type=int, default=2,
                     help="gradient buffers peers reduce-scatter from (ring; >= 2)")
@@ -489,6 +671,8 @@ def main():
     ap.add_argument("--reuse", type=int, default=0, choices=[0, 1],
                     help="the CLI's parameter reuse (R3: later forwards read microbatch 0's gathered layers)")
     args = ap.parse_args()
+    if args.model in MLP_CASES:
+        return run_mlp(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_hzp(args)

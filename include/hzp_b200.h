@@ -257,8 +257,13 @@ int hzp_ctx_layout(const hzp_ctx* ctx, int64_t* P, int64_t* s1, int64_t* s2, int
                    int* num_layers);
 int hzp_ctx_layer_range(const hzp_ctx* ctx, int layer, int64_t* offset, int64_t* size);
 
-/* Multi-process P2P wiring (one process per GPU): export this rank's
- * peer-visible arena as an opaque handle, then import every peer's. */
+/* Multi-process wiring (one process per GPU): hzp_ctx_ipc_handle writes this
+ * rank's share record (pid + POSIX fds of its cuMem arena and, on a group's
+ * first rank, of the Z3 / Z2 NVLS multicast objects; opaque bytes to the
+ * caller); after an all-gather of the records over the control plane,
+ * hzp_ctx_open_peers maps every peer's arena (pidfd_getfd +
+ * cuMemImportFromShareableHandle) and binds this rank's AG / gradient rings
+ * into its groups' multicast objects.  All ranks must call it concurrently. */
 int hzp_ctx_ipc_handle(hzp_ctx* ctx, void* buf, size_t* len);
 int hzp_ctx_open_peers(hzp_ctx* ctx, const void* handles, size_t handle_len, int n_ranks);
 
@@ -341,6 +346,12 @@ int hzp_rs_layer(hzp_ctx* ctx, int layer, int wslot);
  * Adam (train.cpp:171-189) on the Z1 chunk, round-to-bf16 and P2P-store the
  * working copy into the Z3 owners (train.cpp:361-379).  grad_out (device
  * or NULL) optionally receives each driven rank's reduced Z1 gradient chunk. */
+/* Device-timed (CUDA events on the collective's own stream, no host sync
+ * between iterations) back-to-back runs of the step's own collective for one
+ * layer: kind 0 = AG (the layer-wise all-gather into ring slots), 1 = RS
+ * (reduce-scatter into the grad shard; accumulates, so measurement only).
+ * Starts with a device-side barrier of all ranks. */
+int hzp_collective_time(hzp_ctx* ctx, int kind, int layer, int iters, double* ms_per_iter);
 int hzp_z1_adam_step(hzp_ctx* ctx);
 int hzp_zero_grads(hzp_ctx* ctx);
 /* Device-wide barrier over all dp ranks (no-op in emulation mode). */

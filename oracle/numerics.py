@@ -273,6 +273,8 @@ class RefLib:
         L.ref_derive_prelaunch_depth.argtypes = [C.c_longlong, C.c_longlong] + [C.c_int] * 4 + [C.c_longlong]
         L.ref_time_train_step_f32.argtypes = [_i32p] + [C.c_int] * 7 + [C.c_ulonglong, C.c_int]
         L.ref_time_train_step_f32.restype = C.c_double
+        L.ref_time_steps_f32.argtypes = [_i32p] + [C.c_int] * 7 + [C.c_ulonglong, C.c_int, C.c_int, _f32p]
+        L.ref_time_steps_f32.restype = C.c_double
 
     def run_states(self, dims, dp, z1, z2, z3, mbs, batch, seed, steps, bf16_working,
                    dtype=np.float32):

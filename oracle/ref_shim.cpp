@@ -368,4 +368,25 @@ double ref_time_train_step_f32(const int* dims, int nl, int dp, int z1, int z2, 
   return std::chrono::duration<double>(t1 - t0).count() / (steps > 0 ? steps : 1);
 }
 
+// The reference's train_step_hzp<float> on `steps` run_case-seeded steps
+// (per-(step, rank, mb) batches, train.cpp:501-508, generated before the
+// clock starts), fp32 (bf16_working 0) or mixed (1); seconds per step.
+// Optionally returns the final per-rank losses.
+double ref_time_steps_f32(const int* dims, int nl, int dp, int z1, int z2, int z3, int mbs, int batch,
+                          unsigned long long seed, int steps, int bf16_working, float* losses) {
+  const auto shape = shape_of(dims, nl);
+  const auto cfg = cfg_of(dp, z1, z2, z3);
+  auto states = hzp::shard_init<float>(shape, cfg, seed, bf16_working != 0);
+  const hzp::AdamParams adam;
+  std::vector<hzp::RankBatches<float>> all;
+  for (int s = 0; s < steps; ++s) all.push_back(batches_for<float>(shape, dp, mbs, batch, seed, s));
+  std::vector<float> l;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int s = 0; s < steps; ++s) l = hzp::train_step_hzp(states, shape, cfg, all[s], batch, adam, bf16_working != 0);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (losses)
+    for (int r = 0; r < dp && r < static_cast<int>(l.size()); ++r) losses[r] = l[r];
+  return std::chrono::duration<double>(t1 - t0).count() / (steps > 0 ? steps : 1);
+}
+
 }  // extern "C"

@@ -162,6 +162,7 @@ SIGNATURES = [
     ("hzp_ag_slot_download", C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64]),
     ("hzp_wgrad_upload", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_float), C.c_int64]),
     ("hzp_rs_layer", C.c_int, [_vp, C.c_int, C.c_int]),
+    ("hzp_collective_time", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_double)]),
     ("hzp_z1_adam_step", C.c_int, [_vp]),
     ("hzp_zero_grads", C.c_int, [_vp]),
     ("hzp_barrier", C.c_int, [_vp]),

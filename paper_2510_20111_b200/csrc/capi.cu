@@ -366,16 +366,13 @@ int hzp_ctx_ipc_handle(hzp_ctx* ctx, void* buf, size_t* len) {
   if (!ctx || !len) return HZP_ERR_ARG;
   return guarded([&] {
     Engine& e = *ctx->e;
-    if (e.emulate) throw std::invalid_argument("emulation ctx has no IPC handle");
-    if (!buf || *len < sizeof(cudaIpcMemHandle_t)) {
-      *len = sizeof(cudaIpcMemHandle_t);
+    if (!buf || *len < sizeof(ShareRecord)) {
+      *len = sizeof(ShareRecord);
       throw std::invalid_argument("buffer too small");
     }
-    HZP_CUDA(cudaSetDevice(e.cfg.device));
-    cudaIpcMemHandle_t h;
-    HZP_CUDA(cudaIpcGetMemHandle(&h, e.arenas[e.cfg.my_rank].base));
-    std::memcpy(buf, &h, sizeof(h));
-    *len = sizeof(h);
+    const ShareRecord r = e.share_record();
+    std::memcpy(buf, &r, sizeof(r));
+    *len = sizeof(r);
   });
 }
 
@@ -384,36 +381,11 @@ int hzp_ctx_open_peers(hzp_ctx* ctx, const void* handles, size_t handle_len, int
   return guarded([&] {
     Engine& e = *ctx->e;
     if (e.emulate) return;
-    if (n_ranks != e.cfg.par.dp || handle_len != sizeof(cudaIpcMemHandle_t))
-      throw std::invalid_argument("need one cudaIpcMemHandle_t per dp rank");
-    HZP_CUDA(cudaSetDevice(e.cfg.device));
-    const Arena& mine = e.arenas[e.cfg.my_rank];
-    const size_t p_off = 0;
-    const size_t g_off = static_cast<char*>(static_cast<void*>(mine.grad)) - static_cast<char*>(mine.base);
-    const size_t w_off = mine.wgrad ? static_cast<char*>(mine.wgrad) - static_cast<char*>(mine.base) : 0;
-    const size_t f_off = reinterpret_cast<char*>(mine.flags) - static_cast<char*>(mine.base);
-    for (int r = 0; r < n_ranks; ++r) {
-      if (r == e.cfg.my_rank) continue;
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, static_cast<const char*>(handles) + r * handle_len, sizeof(h));
-      void* p = nullptr;
-      HZP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-      Arena& a = e.arenas[r];
-      a.base = p;
-      a.owned = false;
-      a.bytes = mine.bytes;
-      a.param = static_cast<char*>(p) + p_off;
-      a.grad = reinterpret_cast<float*>(static_cast<char*>(p) + g_off);
-      a.wgrad = mine.wgrad ? static_cast<char*>(p) + w_off : nullptr;
-      a.flags = reinterpret_cast<uint64_t*>(static_cast<char*>(p) + f_off);
-      e.table.param[r] = a.param;
-      e.table.grad[r] = a.grad;
-      e.table.wgrad[r] = a.wgrad;
-      e.table.flags[r] = a.flags;
-    }
-    HZP_CUDA(cudaMemcpy(e.dtable, &e.table, sizeof(RankTable), cudaMemcpyHostToDevice));
-    e.setup_rs_staging();
-    e.peers_open = true;
+    if (handle_len != sizeof(ShareRecord)) throw std::invalid_argument("need one share record per dp rank");
+    std::vector<ShareRecord> recs(n_ranks);
+    for (int r = 0; r < n_ranks; ++r)
+      std::memcpy(&recs[r], static_cast<const char*>(handles) + r * handle_len, sizeof(ShareRecord));
+    e.open_peers(recs.data(), n_ranks);
   });
 }
 
@@ -704,7 +676,8 @@ int hzp_ag_slot_download(hzp_ctx* ctx, int rank, int slot, void* host, int64_t n
     const int li = e.local_index(rank);
     if (li < 0 || slot < 0 || slot >= e.depth || n > e.slot_elems) throw std::invalid_argument("bad args");
     const int es = e.bf16 ? 2 : 4;
-    HZP_CUDA(cudaMemcpy(host, static_cast<char*>(e.locals[li].ag) + int64_t(slot) * e.slot_elems * es,
+    HZP_CUDA(cudaDeviceSynchronize());
+    HZP_CUDA(cudaMemcpy(host, static_cast<char*>(e.arenas[rank].ag) + int64_t(slot) * e.slot_elems * es,
                         size_t(n) * es, cudaMemcpyDeviceToHost));
   });
 }
@@ -743,8 +716,38 @@ int hzp_rs_layer(hzp_ctx* ctx, int layer, int wslot) {
   return guarded([&] {
     Engine& e = *ctx->e;
     if (e.direct_grad) throw std::invalid_argument("z2 == 1: the reduce-scatter is fused into wgrad");
-    e.rs_layer(layer, wslot, false, e.st[2]);
+    e.rs_layer(layer, wslot, false, ++e.rs_seq, e.st[2]);
     HZP_CUDA(cudaStreamSynchronize(e.st[2]));
+  });
+}
+
+int hzp_collective_time(hzp_ctx* ctx, int kind, int layer, int iters, double* ms_per_iter) {
+  if (!ctx || !ms_per_iter || iters < 1) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    if (layer < 0 || layer >= static_cast<int>(e.layers.size())) throw std::invalid_argument("layer out of range");
+    if (kind == 0 && e.zero_copy_ag) throw std::invalid_argument("z3 == 1: the all-gather is the identity");
+    if (kind == 1 && e.direct_grad) throw std::invalid_argument("z2 == 1: the reduce-scatter is fused into wgrad");
+    if (kind != 0 && kind != 1) throw std::invalid_argument("kind: 0 = AG, 1 = RS");
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    cudaStream_t s = e.st[kind == 0 ? 1 : 2];
+    HZP_CUDA(cudaDeviceSynchronize());
+    e.barrier(s);  // all ranks start together
+    cudaEvent_t a, b;
+    HZP_CUDA(cudaEventCreate(&a));
+    HZP_CUDA(cudaEventCreate(&b));
+    HZP_CUDA(cudaEventRecord(a, s));
+    for (int i = 0; i < iters; ++i) {
+      if (kind == 0) e.ag_layer(layer, i % e.depth, s);
+      else e.rs_layer(layer, 0, false, ++e.rs_seq, s);
+    }
+    HZP_CUDA(cudaEventRecord(b, s));
+    HZP_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    HZP_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_iter = ms / iters;
   });
 }
 

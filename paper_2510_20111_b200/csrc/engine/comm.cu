@@ -1,17 +1,23 @@
-// P2P collective kernels (sm_100a).  See comm.cuh for the contract.
+// Collective kernels (sm_100a).  See comm.cuh for the contract.
 //
 // Design notes (B200):
-//  * pull, not push: a rank reads what it needs straight out of its peers'
-//    HBM through NVLink 5 / NVSwitch (peer pointers are IPC-mapped device
-//    addresses), so there is no staging copy and no rendezvous inside a pass.
-//  * 16-byte vector loads, UNROLL of them in flight per thread before any
-//    use: a peer load costs ~2 us, so bandwidth needs deep memory-level
-//    parallelism rather than many threads.
-//  * CTA count is bounded (`ctas`) so the comm kernels leave most of the 148
-//    SMs to the tcgen05 GEMMs running concurrently on the compute stream.
-//  * every reduction sums in ascending rank order in fp32 with IEEE
-//    round-to-nearest adds (no FMA contraction), so results are bit-identical
-//    to the reference's canonical order.
+//  * AG = owner push through NVLS multicast: the owner reads its span from
+//    its own HBM (16-byte ld.global.nc) and issues multimem.st.v4 to the Z3
+//    group's multicast AG slot; NVSwitch replicates each store into every
+//    member's slot, so the owner's NVLink egress is the layer once (a pull
+//    by the z3 - 1 readers moved it z3 - 1 times) and readers stay idle.
+//  * RS = reduce at the segment owner: bf16 wire through
+//    multimem.ld_reduce.add.acc::f32 (the switch reads every member's slot
+//    and returns the fp32-accumulated sum rounded to bf16: the owner's
+//    ingress is the layer once), fp32 wire by an ordered pull (ascending rank,
+//    __fadd_rn, bit-identical to the reference's canonical order,
+//    SPEC.md:208,241).
+//  * register-only (no shared memory): these kernels co-reside with the
+//    persistent tcgen05 GEMM (which takes ~all of an SM's shared memory) on
+//    every SM instead of waiting for it to drain; 128 threads capped at 80
+//    registers fit beside the GEMM's 320 x 168.
+//  * UNROLL 16-byte vectors in flight per thread before any use (NVLink
+//    round trips are ~2 us).
 #include <type_traits>
 
 #include "engine/comm.cuh"
@@ -20,13 +26,11 @@ namespace hzp {
 namespace {
 
 constexpr int kThreads = 256;  // Z1 / optimizer kernels (run alone)
-// AG / RS run beside a persistent tcgen05 GEMM CTA on every SM: 128 threads
-// capped at 80 registers (10 K) fit next to the GEMM's 320 x 168 (53.7 K) in
-// the 64 K register file, so neither kernel waits for the other to drain.
 constexpr int kCommThreads = 128;
 constexpr int kCommRegs = 80;
 constexpr int kUnroll = 8;    // AG: 16-byte vectors in flight per thread
 constexpr int kUnrollRS = 4;  // RS: per source
+constexpr int kUnrollMC = 8;  // RS through multimem.ld_reduce
 
 __device__ __forceinline__ void fadd4(float4& a, const float4& b) {
   a.x = __fadd_rn(a.x, b.x);
@@ -49,79 +53,147 @@ __device__ __forceinline__ void bf8_to_f8(uint4 v, float4& lo, float4& hi) {
   hi = make_float4(__uint_as_float(v.z << 16), __uint_as_float(v.z & 0xFFFF0000u),
                    __uint_as_float(v.w << 16), __uint_as_float(v.w & 0xFFFF0000u));
 }
+__device__ __forceinline__ float round_bf16(float f) { return bf16_bits_to_f32(f32_to_bf16_bits(f)); }
+__device__ __forceinline__ void round4_bf16(float4& a) {
+  a.x = round_bf16(a.x);
+  a.y = round_bf16(a.y);
+  a.z = round_bf16(a.z);
+  a.w = round_bf16(a.w);
+}
 
-// ---------------------------------------------------------------------------
-// AG: copy tile from owner shard to local slot.  Elements are moved as raw
-// bits (bit-exact by construction).
-template <int kElemBytes>
-__global__ void __maxnreg__(kCommRegs) ag_pull_kernel(const RankTable* __restrict__ T,
-                                                           const CommTile* __restrict__ tiles,
-                                                           int ntiles, int slot,
-                                                           int64_t slot_elems) {
-  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-    const CommTile t = tiles[ti];
-    char* dst = static_cast<char*>(T->ag_slots[t.local]) +
-                (slot * slot_elems + t.a_off) * kElemBytes;
-    const char* src = static_cast<const char*>(T->param[t.src]) + t.b_off * kElemBytes;
-    const int64_t bytes = int64_t(t.len) * kElemBytes;
-    if (t.vec) {
-      const int64_t nv = bytes / 16;
-      const uint4* s4 = reinterpret_cast<const uint4*>(src);
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
-      int64_t i = threadIdx.x;
-      for (; i + (kUnroll - 1) * kCommThreads < nv; i += kUnroll * kCommThreads) {
-        uint4 v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = ld_nc_v4(s4 + i + u * kCommThreads);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) st_v4(d4 + i + u * kCommThreads, v[u]);
-      }
-      for (; i < nv; i += kCommThreads) st_v4(d4 + i, ld_nc_v4(s4 + i));
-    } else {  // unaligned span: element-wise, kUnroll loads in flight per thread
-      using E = typename std::conditional<kElemBytes == 2, uint16_t, uint32_t>::type;
-      const E* se = reinterpret_cast<const E*>(src);
-      E* de = reinterpret_cast<E*>(dst);
-      int64_t i = threadIdx.x;
-      for (; i + (kUnroll - 1) * kCommThreads < t.len; i += kUnroll * kCommThreads) {
-        E v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = se[i + u * kCommThreads];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) de[i + u * kCommThreads] = v[u];
-      }
-      for (; i < t.len; i += kCommThreads) de[i] = se[i];
-    }
+// NVLS multicast primitives (sm_90+; on B200 through NVSwitch)
+__device__ __forceinline__ void mc_st_v4(void* p, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 mc_ld_reduce_bf16x8(const void* p) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+// In-kernel gate (multi-process): wait for the peers' flags before touching
+// their slots.
+__device__ __forceinline__ void gate_wait(const RankTable* __restrict__ T, const FlagGate& g) {
+  if (!g.mask) return;
+  const int q = threadIdx.x;
+  if (q < kMaxRanks && (g.mask >> q & 1)) {
+    const uint64_t* f = T->flags[g.me] + g.kind * kMaxRanks + q;
+    while (ld_acquire_sys(f) < g.value) __nanosleep(64);
   }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
-// RS: grad[local][a_off + i] (+)= sum_{q=0..z2-1} wire(wgrad[base+q][slot][b_off + i])
-template <bool kBf16Wire>
-__global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restrict__ T,
-                                                           const CommTile* __restrict__ tiles,
-                                                           int ntiles, int wslot,
-                                                           int64_t wslot_elems, int z2,
-                                                           int assign, float scale, int split) {
-  // `split` CTAs share a tile (part = blockIdx % split takes every split-th
-  // group of kUnrollRS x kCommThreads vectors): HBM-local reduces want more
-  // CTAs in flight than NVLink pulls do.
+// AG: owner tile -> slot of every member of the owner's Z3 group.  Raw bits
+// (bit-exact by construction).
+template <int kEB, bool kMC>
+__global__ void __maxnreg__(kCommRegs) ag_push_kernel(const RankTable* __restrict__ T,
+                                                      const CommTile* __restrict__ tiles, int ntiles,
+                                                      int slot, int64_t slot_elems, int z3, FlagGate gate) {
+  gate_wait(T, gate);
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const CommTile t = tiles[ti];
+    const char* src = static_cast<const char*>(T->param[t.src]) + t.b_off * kEB;
+    const int64_t dst_off = (slot * slot_elems + t.a_off) * kEB;
+    const int base = t.src - t.src % z3;
+    char* const mc = kMC ? static_cast<char*>(T->ag_mc) + dst_off : nullptr;  // hoisted past the asm clobbers
+    if (t.vec) {
+      const int64_t nv = int64_t(t.len) * kEB / 16;
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      int64_t i = threadIdx.x;
+      for (; i < nv; i += kUnroll * kCommThreads) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t j = i + u * kCommThreads;
+          if (j < nv) v[u] = ld_nc_v4(s4 + j);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t j = i + u * kCommThreads;
+          if (j >= nv) continue;
+          if (kMC) {
+            mc_st_v4(mc + j * 16, v[u]);
+          } else {
+            for (int q = base; q < base + z3; ++q) st_v4(static_cast<char*>(T->ag[q]) + dst_off + j * 16, v[u]);
+          }
+        }
+      }
+    } else {  // unaligned head / tail: element-wise unicast stores to every member
+      using E = typename std::conditional<kEB == 2, uint16_t, uint32_t>::type;
+      const E* se = reinterpret_cast<const E*>(src);
+      for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
+        const E v = se[i];
+        for (int q = base; q < base + z3; ++q)
+          reinterpret_cast<E*>(static_cast<char*>(T->ag[q]) + dst_off)[i] = v;
+      }
+    }
+  }
+  if (kMC) __threadfence_system();  // stores performed before the owner posts AgDone
+}
+
+// ---------------------------------------------------------------------------
+// RS at the segment owner:
+//   grad[a_off + i] (+)= scale * reduce_{q in Z2 group}(wire(wgrad[q][wslot][b_off + i]))
+template <bool kBf16Wire, int kMode>
+__global__ void __maxnreg__(kCommRegs) rs_reduce_kernel(const RankTable* __restrict__ T,
+                                                        const CommTile* __restrict__ tiles, int ntiles,
+                                                        int wslot, int64_t wslot_elems, int z2, int assign,
+                                                        float scale, FlagGate gate) {
   constexpr int kEB = kBf16Wire ? 2 : 4;
+  constexpr bool kRound = kBf16Wire && kMode != kRsOrdered;
   const bool do_scale = scale != 1.0f;
-  const int part = int(blockIdx.x) % split;
-  for (int ti = int(blockIdx.x) / split; ti < ntiles; ti += int(gridDim.x) / split) {
+  gate_wait(T, gate);
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
     float* g = T->grad[T->global_rank[t.local]] + t.a_off;  // local index -> global rank
     const int64_t woff = (int64_t(wslot) * wslot_elems + t.b_off) * kEB;
-    if (t.vec) {
-      // kUnrollRS 16-byte vectors per thread and source in flight before any
-      // use (peer loads are ~2 us away); sources summed in ascending order.
+    const char* const mcw = kMode == kRsMulticast ? static_cast<const char*>(T->wgrad_mc) + woff : nullptr;
+    if (kMode == kRsMulticast && t.vec) {
+      // one in-switch reduction per 16 bytes: 8 bf16 of every member summed
+      // (fp32 accumulate), returned as 8 bf16; kUnrollMC in flight per thread
+      const int64_t nv = t.len / 8;
+      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += int64_t(kUnrollMC) * kCommThreads) {
+        uint4 v[kUnrollMC];
+#pragma unroll
+        for (int u = 0; u < kUnrollMC; ++u) {
+          const int64_t i = i0 + int64_t(u) * kCommThreads;
+          v[u] = i < nv ? mc_ld_reduce_bf16x8(mcw + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnrollMC; ++u) {
+          const int64_t i = i0 + int64_t(u) * kCommThreads;
+          if (i >= nv) continue;
+          float4 lo, hi;
+          bf8_to_f8(v[u], lo, hi);
+          if (do_scale) {
+            lo.x = __fmul_rn(lo.x, scale); lo.y = __fmul_rn(lo.y, scale);
+            lo.z = __fmul_rn(lo.z, scale); lo.w = __fmul_rn(lo.w, scale);
+            hi.x = __fmul_rn(hi.x, scale); hi.y = __fmul_rn(hi.y, scale);
+            hi.z = __fmul_rn(hi.z, scale); hi.w = __fmul_rn(hi.w, scale);
+          }
+          float4* g4 = reinterpret_cast<float4*>(g) + i * 2;
+          float4 a = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[0];
+          float4 b = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[1];
+          fadd4(a, lo);
+          fadd4(b, hi);
+          g4[0] = a;
+          g4[1] = b;
+        }
+      }
+    } else if (t.vec) {
       constexpr int kPer = kBf16Wire ? 8 : 4;  // elements per 16-byte load
       const int64_t nv = t.len / kPer;
-      for (int64_t i0 = threadIdx.x + int64_t(part) * kUnrollRS * kCommThreads; i0 < nv;
-           i0 += int64_t(kUnrollRS) * kCommThreads * split) {
+      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += int64_t(kUnrollRS) * kCommThreads) {
         float4 lo[kUnrollRS], hi[kUnrollRS];
         uint4 v[kUnrollRS];
         {
+          // every source's vectors in flight before any use; ascending order
           const char* p = static_cast<const char*>(T->wgrad[t.src]) + woff;
 #pragma unroll
           for (int u = 0; u < kUnrollRS; ++u) {
@@ -133,23 +205,30 @@ __global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restric
             if (kBf16Wire) bf8_to_f8(v[u], lo[u], hi[u]);
             else lo[u] = as_f4(v[u]);
           }
-        }
-        for (int q = 1; q < z2; ++q) {
-          const char* p = static_cast<const char*>(T->wgrad[t.src + q]) + woff;
+          for (int q = 1; q < z2; ++q) {
+            const char* pq = static_cast<const char*>(T->wgrad[t.src + q]) + woff;
 #pragma unroll
-          for (int u = 0; u < kUnrollRS; ++u) {
-            const int64_t i = i0 + int64_t(u) * kCommThreads;
-            v[u] = i < nv ? ld_nc_v4(p + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+            for (int u = 0; u < kUnrollRS; ++u) {
+              const int64_t i = i0 + int64_t(u) * kCommThreads;
+              v[u] = i < nv ? ld_nc_v4(pq + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnrollRS; ++u) {
+              if (kBf16Wire) {
+                float4 a, b;
+                bf8_to_f8(v[u], a, b);
+                fadd4(lo[u], a);
+                fadd4(hi[u], b);
+              } else {
+                fadd4(lo[u], as_f4(v[u]));
+              }
+            }
           }
+          if (kRound) {
 #pragma unroll
-          for (int u = 0; u < kUnrollRS; ++u) {
-            if (kBf16Wire) {
-              float4 a, b;
-              bf8_to_f8(v[u], a, b);
-              fadd4(lo[u], a);
-              fadd4(hi[u], b);
-            } else {
-              fadd4(lo[u], as_f4(v[u]));
+            for (int u = 0; u < kUnrollRS; ++u) {
+              round4_bf16(lo[u]);
+              round4_bf16(hi[u]);
             }
           }
         }
@@ -176,8 +255,7 @@ __global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restric
           }
         }
       }
-    } else {
-      if (part != 0) continue;
+    } else {  // unaligned head / tail: ordered unicast sum (rounded like the switch)
       for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
         float s = 0.f;
         for (int q = 0; q < z2; ++q) {
@@ -186,6 +264,7 @@ __global__ void __maxnreg__(kCommRegs) rs_pull_kernel(const RankTable* __restric
                                     : reinterpret_cast<const float*>(p)[i];
           s = q == 0 ? v : __fadd_rn(s, v);
         }
+        if (kRound) s = round_bf16(s);
         if (do_scale) s = __fmul_rn(s, scale);
         g[i] = __fadd_rn(assign ? 0.f : g[i], s);
       }
@@ -291,31 +370,18 @@ __global__ void __launch_bounds__(kThreads) z1_adam_kernel(const RankTable* __re
 }
 
 // ---------------------------------------------------------------------------
-// Cross-GPU signals: monotonic 64-bit counters in every rank's peer-visible
-// arena, written with st.release.sys, polled with ld.acquire.sys.
-__global__ void signal_kernel(const RankTable* __restrict__ T, int me, int kind, int first,
-                              int count, int stride, uint64_t value, int wait_kind,
-                              uint64_t wait_value) {
+// Cross-GPU flags: monotonic 64-bit counters in every rank's arena, written
+// with st.release.sys, polled with ld.acquire.sys.
+__global__ void flags_kernel(const RankTable* __restrict__ T, int me, int post_kind, uint64_t post_mask,
+                             uint64_t post_value, int wait_kind, uint64_t wait_mask, uint64_t wait_value) {
   const int q = threadIdx.x;
-  if (q < count) {
-    const int r = first + q * stride;
+  if (post_mask >> q & 1) {
     __threadfence_system();
-    st_release_sys(T->flags[r] + kind * kMaxRanks + me, value);
+    st_release_sys(T->flags[q] + post_kind * kMaxRanks + me, post_value);
   }
-  if (wait_kind >= 0 && q < count) {
-    const int r = first + q * stride;
-    const uint64_t* f = T->flags[me] + wait_kind * kMaxRanks + r;
+  if (wait_mask >> q & 1) {
+    const uint64_t* f = T->flags[me] + wait_kind * kMaxRanks + q;
     while (ld_acquire_sys(f) < wait_value) __nanosleep(64);
-  }
-  __syncthreads();
-}
-
-__global__ void wait_kernel(const RankTable* __restrict__ T, int me, int kind, int first,
-                            int count, int stride, uint64_t value) {
-  const int q = threadIdx.x;
-  if (q < count) {
-    const uint64_t* f = T->flags[me] + kind * kMaxRanks + first + q * stride;
-    while (ld_acquire_sys(f) < value) __nanosleep(64);
   }
   __syncthreads();
 }
@@ -324,28 +390,39 @@ int grid_for(int ntiles, int ctas) { return ntiles < ctas ? (ntiles > 0 ? ntiles
 
 }  // namespace
 
-void launch_ag_pull(const RankTable* T, const CommTile* tiles, int ntiles, int slot,
-                    int64_t slot_elems, bool bf16, int ctas, cudaStream_t s) {
+void launch_ag_push(const RankTable* T, const CommTile* tiles, int ntiles, int slot, int64_t slot_elems,
+                    int z3, bool bf16, bool multicast, FlagGate gate, int ctas, cudaStream_t s) {
   if (ntiles <= 0) return;
-  if (bf16)
-    ag_pull_kernel<2><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems);
-  else
-    ag_pull_kernel<4><<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems);
+  const int grid = grid_for(ntiles, ctas);
+  if (bf16) {
+    if (multicast) ag_push_kernel<2, true><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
+    else ag_push_kernel<2, false><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
+  } else {
+    if (multicast) ag_push_kernel<4, true><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
+    else ag_push_kernel<4, false><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
+  }
   HZP_LAUNCH_CHECK();
 }
 
-void launch_rs_pull(const RankTable* T, const CommTile* tiles, int ntiles, int wslot,
-                    int64_t wslot_elems, int z2, bool bf16_wire, bool assign, float scale,
-                    int ctas, cudaStream_t s, int split) {
+void launch_rs_reduce(const RankTable* T, const CommTile* tiles, int ntiles, int wslot, int64_t wslot_elems,
+                      int z2, bool bf16_wire, RsMode mode, bool assign, float scale, FlagGate gate, int ctas,
+                      cudaStream_t s) {
   if (ntiles <= 0) return;
-  split = split < 1 ? 1 : split;
-  const int grid = grid_for(ntiles, ctas) * split;
-  if (bf16_wire)
-    rs_pull_kernel<true><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2, assign,
-                                                       scale, split);
-  else
-    rs_pull_kernel<false><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2, assign,
-                                                        scale, split);
+  const int grid = grid_for(ntiles, ctas);
+  if (!bf16_wire) {
+    if (mode != kRsOrdered) throw std::invalid_argument("fp32 wire reduces in order only (bit-exact tier)");
+    rs_reduce_kernel<false, kRsOrdered><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2,
+                                                                      assign, scale, gate);
+  } else if (mode == kRsMulticast) {
+    rs_reduce_kernel<true, kRsMulticast><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2,
+                                                                       assign, scale, gate);
+  } else if (mode == kRsOrderedRound) {
+    rs_reduce_kernel<true, kRsOrderedRound><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems,
+                                                                          z2, assign, scale, gate);
+  } else {
+    rs_reduce_kernel<true, kRsOrdered><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, wslot, wslot_elems, z2,
+                                                                     assign, scale, gate);
+  }
   HZP_LAUNCH_CHECK();
 }
 
@@ -362,16 +439,10 @@ void launch_z1_adam(const RankTable* T, const CommTile* tiles, int ntiles, int z
   HZP_LAUNCH_CHECK();
 }
 
-void launch_signal(const RankTable* T, int me, int kind, int first, int count, int stride,
-                   uint64_t value, int wait_kind, uint64_t wait_value, cudaStream_t s) {
-  signal_kernel<<<1, kMaxRanks, 0, s>>>(T, me, kind, first, count, stride, value, wait_kind,
-                                        wait_value);
-  HZP_LAUNCH_CHECK();
-}
-
-void launch_wait(const RankTable* T, int me, int kind, int first, int count, int stride,
-                 uint64_t value, cudaStream_t s) {
-  wait_kernel<<<1, kMaxRanks, 0, s>>>(T, me, kind, first, count, stride, value);
+void launch_flags(const RankTable* T, int me, int post_kind, uint64_t post_mask, uint64_t post_value,
+                  int wait_kind, uint64_t wait_mask, uint64_t wait_value, cudaStream_t s) {
+  if (!post_mask && !wait_mask) return;
+  flags_kernel<<<1, kMaxRanks, 0, s>>>(T, me, post_kind, post_mask, post_value, wait_kind, wait_mask, wait_value);
   HZP_LAUNCH_CHECK();
 }
 

@@ -19,6 +19,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <unistd.h>
+
 #include "engine/engine.hpp"
 #include "engine/gemm.cuh"
 
@@ -149,10 +151,16 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
 
   // ---- per-rank peer-visible arenas ----
   const int es = bf16 ? 2 : 4;
-  const size_t p_bytes = align_up(size_t(geom.s3) * es, 256);
-  const size_t g_bytes = align_up(size_t(geom.s2) * 4, 256);
-  const size_t w_bytes = direct_grad ? 0 : align_up(size_t(wslots) * slot_elems * es, 256);
-  const size_t f_bytes = align_up(sizeof(uint64_t) * kNumFlagKinds * kMaxRanks, 256);
+  const bool shared = !emulate && c.par.dp > 1;  // one process per GPU: cuMem + NVLS
+  const size_t al = shared ? symm_granularity(c.device) : 256;
+  lay.param = 0;
+  lay.grad = align_up(size_t(geom.s3) * es, 256);
+  lay.flags = lay.grad + align_up(size_t(geom.s2) * 4, 256);
+  lay.ag = align_up(lay.flags + sizeof(uint64_t) * kNumFlagKinds * kMaxRanks, al);
+  lay.ag_bytes = zero_copy_ag ? 0 : align_up(size_t(depth + cache_slots) * slot_elems * es, al);
+  lay.wgrad = lay.ag + lay.ag_bytes;
+  lay.wgrad_bytes = direct_grad ? 0 : align_up(size_t(wslots) * slot_elems * es, al);
+  lay.total = align_up(lay.wgrad + lay.wgrad_bytes, al);
   arenas.resize(c.par.dp);
   std::vector<int> mine;
   if (emulate) {
@@ -162,27 +170,30 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     if (c.my_rank >= c.par.dp) throw std::invalid_argument("my_rank out of range");
     mine.push_back(c.my_rank);
   }
+  if (shared && !multicast_supported(c.device))
+    throw CudaError("multi-process mode needs NVLS multicast (NVSwitch); this device has none");
   for (int r : mine) {
     Arena& a = arenas[r];
-    a.bytes = p_bytes + g_bytes + w_bytes + f_bytes;
-    HZP_CUDA(cudaMalloc(&a.base, a.bytes));
+    if (shared) {
+      a.symm = symm_alloc(c.device, lay.total);
+      a.base = reinterpret_cast<void*>(a.symm.va);
+    } else {
+      HZP_CUDA(cudaMalloc(&a.base, lay.total));
+      a.cuda_malloc = true;
+    }
+    a.bytes = lay.total;
     HZP_CUDA(cudaMemset(a.base, 0, a.bytes));
-    a.owned = true;
+    carve(a);
   }
-  auto carve = [&](Arena& a) {
-    char* b = static_cast<char*>(a.base);
-    a.param = b;
-    a.grad = reinterpret_cast<float*>(b + p_bytes);
-    a.wgrad = w_bytes ? b + p_bytes + g_bytes : nullptr;
-    a.flags = reinterpret_cast<uint64_t*>(b + p_bytes + g_bytes + w_bytes);
-  };
-  for (int r : mine) carve(arenas[r]);
+  if (shared) {  // the group's first rank creates the multicast objects
+    if (!zero_copy_ag && c.my_rank % geom.z3 == 0) ag_mc = mc_create(geom.z3, lay.ag_bytes);
+    if (!direct_grad && bf16 && c.my_rank % geom.z2 == 0) wg_mc = mc_create(geom.z2, lay.wgrad_bytes);
+  }
 
   // ---- driven ranks ----
   for (int r : mine) {
     LocalRank lr;
     lr.rank = r;
-    HZP_CUDA(cudaMalloc(&lr.ag, size_t(depth + cache_slots) * slot_elems * es));
     HZP_CUDA(cudaMalloc(&lr.master, size_t(geom.s1) * 4));
     HZP_CUDA(cudaMalloc(&lr.mom, size_t(geom.s1) * 4));
     HZP_CUDA(cudaMalloc(&lr.var, size_t(geom.s1) * 4));
@@ -204,10 +215,10 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     table.param[r] = arenas[r].param;
     table.grad[r] = arenas[r].grad;
     table.wgrad[r] = arenas[r].wgrad;
+    table.ag[r] = arenas[r].ag;
     table.flags[r] = arenas[r].flags;
   }
   for (size_t i = 0; i < locals.size(); ++i) {
-    table.ag_slots[i] = locals[i].ag;
     table.master[i] = locals[i].master;
     table.mom[i] = locals[i].mom;
     table.var[i] = locals[i].var;
@@ -216,45 +227,93 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   }
   HZP_CUDA(cudaMalloc(&dtable, sizeof(RankTable)));
   HZP_CUDA(cudaMemcpy(dtable, &table, sizeof(RankTable), cudaMemcpyHostToDevice));
-  peers_open = emulate || c.par.dp == 1;
-  debug_sync = std::getenv("HZP_DEBUG_SYNC") != nullptr;
-  if (const char* c = std::getenv("HZP_COMM_CTAS")) comm_ctas = std::max(1, std::atoi(c));  // tuning knob
-  if (const char* c = std::getenv("HZP_AG_CE")) ag_ce = std::atoi(c) != 0;
-  if (const char* c = std::getenv("HZP_RS_CE")) rs_ce = std::atoi(c) != 0;
-  if (const char* c = std::getenv("HZP_Z1_CE")) z1_ce = std::atoi(c) != 0;
-  if (const char* c = std::getenv("HZP_RS_CHUNKS")) rs_chunks = std::max(1, std::atoi(c));
-  if (const char* c = std::getenv("HZP_RS_PAR")) rs_par = std::atoi(c) != 0;
-  if (const char* c = std::getenv("HZP_AG_PAR")) ag_par = std::atoi(c) != 0;
-  if (const char* c = std::getenv("HZP_RS_MIN_CHUNK_MB")) rs_min_chunk_bytes = std::max<int64_t>(1, std::atoll(c)) << 20;
+  peers_open = !shared;
+  debug_sync = std::getenv("HZP_DEBUG_SYNC") != nullptr;  // debugging aid: serialise every task
   build_tiles();
+}
+
+void Engine::carve(Arena& a) const {
+  char* b = static_cast<char*>(a.base);
+  a.param = b + lay.param;
+  a.grad = reinterpret_cast<float*>(b + lay.grad);
+  a.flags = reinterpret_cast<uint64_t*>(b + lay.flags);
+  a.ag = lay.ag_bytes ? b + lay.ag : nullptr;
+  a.wgrad = lay.wgrad_bytes ? b + lay.wgrad : nullptr;
+}
+
+ShareRecord Engine::share_record() const {
+  if (emulate || cfg.par.dp == 1) throw std::invalid_argument("only a multi-process ctx shares its arena");
+  ShareRecord r;
+  r.magic = kShareMagic;
+  r.rank = cfg.my_rank;
+  r.pid = static_cast<int32_t>(getpid());
+  r.arena_fd = arenas[cfg.my_rank].symm.fd;
+  r.arena_bytes = static_cast<int64_t>(lay.total);
+  r.ag_mc_fd = ag_mc.fd;
+  r.wg_mc_fd = wg_mc.fd;
+  r.ag_mc_bytes = static_cast<int64_t>(lay.ag_bytes);
+  r.wg_mc_bytes = static_cast<int64_t>(lay.wgrad_bytes);
+  return r;
+}
+
+void Engine::open_peers(const ShareRecord* rec, int n) {
+  if (emulate || cfg.par.dp == 1) return;
+  if (peers_open) throw std::invalid_argument("peers already opened");
+  if (n != cfg.par.dp) throw std::invalid_argument("need one share record per dp rank");
+  for (int r = 0; r < n; ++r)
+    if (rec[r].magic != kShareMagic || rec[r].rank != r || rec[r].arena_bytes != int64_t(lay.total))
+      throw std::invalid_argument("share record " + std::to_string(r) + " does not match this layout");
+  HZP_CUDA(cudaSetDevice(cfg.device));
+  const int me = cfg.my_rank;
+  for (int r = 0; r < n; ++r) {
+    if (r == me) continue;
+    Arena& a = arenas[r];
+    a.symm = symm_import(cfg.device, rec[r].pid, rec[r].arena_fd, lay.total);
+    a.base = reinterpret_cast<void*>(a.symm.va);
+    a.bytes = lay.total;
+    carve(a);
+    table.param[r] = a.param;
+    table.grad[r] = a.grad;
+    table.wgrad[r] = a.wgrad;
+    table.ag[r] = a.ag;
+    table.flags[r] = a.flags;
+  }
+  // bind this rank's AG / gradient regions into its groups' multicast
+  // objects (mc_attach blocks until every member has added its device)
+  const Arena& mine = arenas[me];
+  if (lay.ag_bytes) {
+    const ShareRecord& lead = rec[geom.z3_base(me)];
+    if (me != lead.rank) ag_mc = mc_import(lead.pid, lead.ag_mc_fd, lay.ag_bytes);
+    mc_attach(ag_mc, cfg.device, mine.symm, lay.ag);
+    table.ag_mc = reinterpret_cast<void*>(ag_mc.va);
+  }
+  if (lay.wgrad_bytes && bf16) {
+    const ShareRecord& lead = rec[geom.z2_base(me)];
+    if (me != lead.rank) wg_mc = mc_import(lead.pid, lead.wg_mc_fd, lay.wgrad_bytes);
+    mc_attach(wg_mc, cfg.device, mine.symm, lay.wgrad);
+    table.wgrad_mc = reinterpret_cast<void*>(wg_mc.va);
+  }
+  HZP_CUDA(cudaMemcpy(dtable, &table, sizeof(RankTable), cudaMemcpyHostToDevice));
+  HZP_CUDA(cudaDeviceSynchronize());
+  peers_open = true;
 }
 
 Engine::~Engine() {
   cudaDeviceSynchronize();
   for (auto& l : locals) {
-    cudaFree(l.ag);
     cudaFree(l.master);
     cudaFree(l.mom);
     cudaFree(l.var);
     cudaFree(l.dbg);
     model->free_rank_buffers(l.mbuf);
   }
+  mc_release(ag_mc);
+  mc_release(wg_mc);
   for (auto& a : arenas) {
-    if (a.base && a.owned) cudaFree(a.base);
-    else if (a.base) cudaIpcCloseMemHandle(a.base);
+    if (a.cuda_malloc) cudaFree(a.base);
+    else if (a.symm.va) symm_release(a.symm);
   }
   cudaFree(dtable);
-  for (auto d : dtable_staged) cudaFree(d);
-  for (auto e : rs_ev) cudaEventDestroy(e);
-  for (auto& ch : z1_chunks) cudaFree(ch.table);
-  for (auto p : z1_stage) cudaFree(p);
-  if (z1_copy_stream) cudaStreamDestroy(z1_copy_stream);
-  if (rs_red_stream) cudaStreamDestroy(rs_red_stream);
-  for (auto st : rs_copy_streams) cudaStreamDestroy(st);
-  for (auto st : ag_copy_streams) cudaStreamDestroy(st);
-  for (auto e : ag_par_ev) cudaEventDestroy(e);
-  for (auto e : rs_par_ev) cudaEventDestroy(e);
-  for (auto p : rs_stage) cudaFree(p);
   cudaFree(dtiles);
   cudaFree(dinputs);
   cudaFreeHost(hloss);
@@ -281,219 +340,68 @@ void Engine::build_tiles() {
   TileTables T = build_comm_tiles(geom, lr, ranks, bf16 ? 2 : 4, direct_grad);
   ag_off = T.ag_off;
   rs_off = T.rs_off;
-  tiles_host = T.tiles;
-  ag_runs.assign(ag_off.size() > 0 ? ag_off.size() - 1 : 0, {});
-  for (size_t l = 0; l + 1 < ag_off.size(); ++l)
-    for (int i = ag_off[l]; i < ag_off[l + 1]; ++i) {
-      const CommTile& t = T.tiles[i];
-      auto& runs = ag_runs[l];
-      if (!runs.empty()) {
-        CopyRun& r = runs.back();
-        if (r.local == t.local && r.src == t.src && r.dst_off + r.len == t.a_off && r.src_off + r.len == t.b_off) {
-          r.len += t.len;
-          continue;
-        }
-      }
-      runs.push_back({t.local, t.src, t.a_off, t.b_off, t.len});
-    }
-  if (!emulate && locals.size() == 1) {
-    // rotate the owners: rank r reads owner r+1 first, r+2 next, ..., its own
-    // shard last, so at every moment each owner's egress serves one reader
-    // (ascending order would have every rank hit owner 0 first)
-    const int me = cfg.my_rank % geom.z3;
-    auto phase = [&](const CopyRun& r) { return (r.src % geom.z3 - me - 1 + 2 * geom.z3) % geom.z3; };
-    for (auto& runs : ag_runs)
-      std::stable_sort(runs.begin(), runs.end(),
-                       [&](const CopyRun& a, const CopyRun& b) { return phase(a) < phase(b); });
-    if (ag_par && geom.z3 > 2 && ag_copy_streams.empty()) {
-      int lo = 0, hi = 0;
-      HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      ag_copy_streams.resize(geom.z3 - 1);
-      for (auto& st : ag_copy_streams) HZP_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
-      ag_par_ev.resize(geom.z3);
-      for (auto& e : ag_par_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-  }
   z1_off = T.z1_off;
   z1_n = T.z1_n;
+  // members of this rank's Z3 group whose shard holds part of each layer
+  ag_owners.assign(layers.size(), 0);
+  if (!emulate)
+    for (size_t l = 0; l < layers.size(); ++l) {
+      const int base = geom.z3_base(cfg.my_rank);
+      const int j0 = static_cast<int>(layers[l].off / geom.s3);
+      const int j1 = static_cast<int>((layers[l].off + layers[l].size - 1) / geom.s3);
+      for (int j = j0; j <= j1 && j < geom.z3; ++j) ag_owners[l] |= 1ull << (base + j);
+    }
   if (dtiles) cudaFree(dtiles);
   HZP_CUDA(cudaMalloc(&dtiles, std::max<size_t>(1, T.tiles.size()) * sizeof(CommTile)));
   if (!T.tiles.empty())
     HZP_CUDA(cudaMemcpy(dtiles, T.tiles.data(), T.tiles.size() * sizeof(CommTile), cudaMemcpyHostToDevice));
 }
 
+// AG task: every member posts "slot free" (its ring wait is already on the
+// stream), the owner(s) of the layer multicast their spans once every member
+// is ready and post "landed"; every member waits for all the layer's owners.
 void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
-  if (ag_ce && !emulate) {  // multi-process: NVLink leg on the copy engines
-    const int es = bf16 ? 2 : 4;
-    const bool par = !ag_copy_streams.empty();
-    const int me = cfg.my_rank % geom.z3;
-    if (par) {  // fork after everything already on s (slot reuse waits included)
-      HZP_CUDA(cudaEventRecord(ag_par_ev[0], s));
-      for (auto st : ag_copy_streams) HZP_CUDA(cudaStreamWaitEvent(st, ag_par_ev[0], 0));
-    }
-    for (const CopyRun& r : ag_runs[layer])
-      HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(table.ag_slots[r.local]) + (slot * slot_elems + r.dst_off) * es,
-                               static_cast<const char*>(table.param[r.src]) + r.src_off * es, r.len * es,
-                               cudaMemcpyDeviceToDevice,
-                               par && r.src % geom.z3 != me
-                                   ? ag_copy_streams[(r.src % geom.z3 - me - 1 + 2 * geom.z3) % geom.z3]
-                                   : s));
-    if (par)  // join: the AG task ends when every owner's copies have landed
-      for (size_t i = 0; i < ag_copy_streams.size(); ++i) {
-        HZP_CUDA(cudaEventRecord(ag_par_ev[1 + i], ag_copy_streams[i]));
-        HZP_CUDA(cudaStreamWaitEvent(s, ag_par_ev[1 + i], 0));
-      }
+  if (zero_copy_ag) throw std::invalid_argument("z3 == 1: the all-gather is the identity (layers read the shard)");
+  const int t0 = ag_off[layer], nt = ag_off[layer + 1] - t0;
+  if (emulate) {
+    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, false, FlagGate{}, kCommCtas, s);
     ++launches;
     return;
   }
-  launch_ag_pull(dtable, dtiles + ag_off[layer], ag_off[layer + 1] - ag_off[layer], slot,
-                 slot_elems, bf16, comm_ctas, s);
-  ++launches;
+  // the waits run in single-CTA flag kernels, so the data kernel's CTAs
+  // (one per SM, beside the GEMM) never spin
+  const int me = cfg.my_rank;
+  const uint64_t seq = ++ag_seq;
+  const uint64_t grp = rank_mask(geom.z3_base(me), geom.z3);
+  launch_flags(dtable, me, kFlagAgReady, grp, seq, kFlagAgReady, nt > 0 ? grp : 0, seq, s);
+  if (nt > 0)
+    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, true, FlagGate{}, kCommCtas, s);
+  launch_flags(dtable, me, kFlagAgDone, nt > 0 ? grp : 0, seq, kFlagAgDone, ag_owners[layer], seq, s);
+  launches += nt > 0 ? 3 : 2;
 }
 
-void Engine::setup_z1_staging() {
-  if (emulate || !z1_ce || geom.replicas() <= 1) return;
-  const int t_end = z1_off + z1_n;
-  // chunk boundaries: whole tiles, <= kZ1ChunkElems elements
-  std::vector<std::pair<int, int>> ranges;
-  for (int t = z1_off; t < t_end;) {
-    int64_t n = 0;
-    int u = t;
-    while (u < t_end && (u == t || n + tiles_host[u].len <= kZ1ChunkElems)) n += tiles_host[u++].len;
-    ranges.push_back({t, u});
-    t = u;
-  }
-  z1_stage.assign(cfg.par.dp, nullptr);
-  for (int r = 0; r < cfg.par.dp; ++r)
-    if (local_index(r) < 0) {
-      // a rank is a remote replica source if some chunk tile reads from it
-      bool used = false;
-      for (int t = z1_off; t < t_end && !used; ++t)
-        for (int b = 1; b < geom.replicas() && !used; ++b) used = tiles_host[t].src + b * geom.z2 == r;
-      for (int t = z1_off; t < t_end && !used; ++t) used = tiles_host[t].src == r;
-      if (used) HZP_CUDA(cudaMalloc(&z1_stage[r], size_t(2 * kZ1ChunkElems) * 4));
-    }
-  for (size_t c = 0; c < ranges.size(); ++c) {
-    Z1Chunk ch;
-    ch.t0 = ranges[c].first;
-    ch.t1 = ranges[c].second;
-    RankTable t = table;
-    for (int r = 0; r < cfg.par.dp; ++r) {
-      if (!z1_stage[r]) continue;
-      // rank r's grad offsets read by this chunk form one contiguous range
-      int64_t lo = INT64_MAX, hi = -1;
-      for (int u = ch.t0; u < ch.t1; ++u) {
-        const CommTile& x = tiles_host[u];
-        bool reads = false;
-        for (int b = 0; b < geom.replicas(); ++b) reads = reads || x.src + b * geom.z2 == r;
-        if (!reads) continue;
-        lo = std::min<int64_t>(lo, x.b_off);
-        hi = std::max<int64_t>(hi, x.b_off + x.len);
-      }
-      if (hi < 0) continue;
-      float* buf = static_cast<float*>(z1_stage[r]) + (c & 1) * kZ1ChunkElems;
-      t.grad[r] = buf - lo;  // the kernel indexes grad[r] + b_off
-      ch.copies.push_back({0, r, 0, lo, hi - lo});
-    }
-    HZP_CUDA(cudaMalloc(&ch.table, sizeof(RankTable)));
-    HZP_CUDA(cudaMemcpy(ch.table, &t, sizeof(RankTable), cudaMemcpyHostToDevice));
-    z1_chunks.push_back(ch);
-  }
-  int lo = 0, hi = 0;
-  HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HZP_CUDA(cudaStreamCreateWithPriority(&z1_copy_stream, cudaStreamNonBlocking, hi));
-  if (rs_ev.empty()) {
-    rs_ev.resize(64);
-    for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-}
-
-void Engine::setup_rs_staging() {
-  setup_z1_staging();
-  if (emulate || direct_grad || geom.z2 <= 1 || !rs_ce) return;
-  const int es = bf16 ? 2 : 4;
-  const int base = geom.z2_base(cfg.my_rank);
-  rs_stage.assign(cfg.par.dp, nullptr);
-  for (int q = 0; q < geom.z2; ++q)
-    if (base + q != cfg.my_rank) HZP_CUDA(cudaMalloc(&rs_stage[base + q], size_t(slot_elems) * es));
-  int lo = 0, hi = 0;
-  HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HZP_CUDA(cudaStreamCreateWithPriority(&rs_red_stream, cudaStreamNonBlocking, hi));
-  if (rs_ev.empty()) {
-    rs_ev.resize(64);
-    for (auto& e : rs_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  if (rs_par) {
-    rs_copy_streams.resize(geom.z2 - 1);
-    for (auto& st : rs_copy_streams) HZP_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
-    rs_par_ev.resize(size_t(geom.z2) * 64);
-    for (auto& e : rs_par_ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  for (int w = 0; w < int(wslots); ++w) {
-    RankTable t = table;
-    for (int r = 0; r < cfg.par.dp; ++r)
-      if (rs_stage[r]) t.wgrad[r] = static_cast<char*>(rs_stage[r]) - int64_t(w) * slot_elems * es;
-    RankTable* d = nullptr;
-    HZP_CUDA(cudaMalloc(&d, sizeof(RankTable)));
-    HZP_CUDA(cudaMemcpy(d, &t, sizeof(RankTable), cudaMemcpyHostToDevice));
-    dtable_staged.push_back(d);
-  }
-}
-
-void Engine::rs_layer(int layer, int wslot, bool assign, cudaStream_t s) {
-  if (!dtable_staged.empty()) {
-    const int es = bf16 ? 2 : 4;
-    const int t0 = rs_off[layer], t1 = rs_off[layer + 1];
-    const int base = geom.z2_base(cfg.my_rank);
-    int ev = 0;
-    if (rs_par) {  // fork: every copy stream starts after the producer's work on s
-      cudaEvent_t f = rs_par_ev[0];
-      HZP_CUDA(cudaEventRecord(f, s));
-      for (auto st : rs_copy_streams) HZP_CUDA(cudaStreamWaitEvent(st, f, 0));
-    }
-    // at most rs_chunks chunks per layer and a floor per peer copy: enough to
-    // overlap the copies with the reduce, few enough that per-copy overhead
-    // stays small.  Floor 8 MB with one peer, 64 MB with several concurrent
-    // peer streams (bf16 sweeps: N=2 256 MB layer 399 vs 319 GB/s with the
-    // 8 MB floor; N=4 64 MB layer 377 as one chunk vs 327 as two, 1 GB best
-    // with 4; profiles/r01_rs_sweep_n4.jsonl, r01_rs_chunk_n2.jsonl)
-    const int64_t floor_bytes =
-        rs_min_chunk_bytes > 0 ? rs_min_chunk_bytes : (int64_t(rs_par && geom.z2 > 2 ? 64 : 8) << 20);
-    const int64_t seg_bytes = t1 <= t0 ? 0 : (tiles_host[t1 - 1].b_off + tiles_host[t1 - 1].len - tiles_host[t0].b_off) * es;
-    const int nch = int(std::max<int64_t>(1, std::min<int64_t>(rs_chunks, seg_bytes / floor_bytes)));
-    const int chunk = std::max(kRsChunkTiles, (t1 - t0 + nch - 1) / nch);
-    for (int c0 = t0; c0 < t1; c0 += chunk, ++ev) {
-      const int c1 = std::min(t1, c0 + chunk);
-      const int64_t b0 = tiles_host[c0].b_off;
-      const int64_t b1 = tiles_host[c1 - 1].b_off + tiles_host[c1 - 1].len;
-      for (int j = 1; j < geom.z2; ++j) {  // rotated: peer r+1 first (one reader per owner)
-        const int g = base + (cfg.my_rank - base + j) % geom.z2;
-        if (!rs_stage[g]) continue;  // this rank's own buffer is read in place
-        cudaStream_t cs = rs_par ? rs_copy_streams[j - 1] : s;
-        HZP_CUDA(cudaMemcpyAsync(static_cast<char*>(rs_stage[g]) + b0 * es,
-                                 static_cast<const char*>(table.wgrad[g]) + (wslot * slot_elems + b0) * es,
-                                 (b1 - b0) * es, cudaMemcpyDeviceToDevice, cs));
-        if (rs_par) {
-          cudaEvent_t pe = rs_par_ev[size_t(geom.z2) * (1 + ev % 63) + j];
-          HZP_CUDA(cudaEventRecord(pe, cs));
-          HZP_CUDA(cudaStreamWaitEvent(rs_red_stream, pe, 0));
-        }
-      }
-      cudaEvent_t e = rs_ev[ev % rs_ev.size()];
-      HZP_CUDA(cudaEventRecord(e, s));
-      HZP_CUDA(cudaStreamWaitEvent(rs_red_stream, e, 0));
-      launch_rs_pull(dtable_staged[wslot], dtiles + c0, c1 - c0, wslot, slot_elems, geom.z2, bf16, assign,
-                     static_cast<float>(cfg.grad_scale), comm_ctas, rs_red_stream, 4);
-    }
-    cudaEvent_t e = rs_ev[ev % rs_ev.size()];
-    HZP_CUDA(cudaEventRecord(e, rs_red_stream));
-    HZP_CUDA(cudaStreamWaitEvent(s, e, 0));  // the RS task ends when its last reduce does
+// RS task (sequence number seq): every member posts "gradient slot written";
+// the owner of (layer ∩ its Z2 segment) waits for all members, reduces; every
+// member posts "done" (BWD reuses a slot once every member posted done for
+// the RS that read it).
+void Engine::rs_layer(int layer, int wslot, bool assign, uint64_t seq, cudaStream_t s) {
+  if (direct_grad) throw std::invalid_argument("z2 == 1: the reduce-scatter is fused into the wgrad GEMM");
+  const int t0 = rs_off[layer], nt = rs_off[layer + 1] - t0;
+  const float scale = static_cast<float>(cfg.grad_scale);
+  if (emulate) {
+    launch_rs_reduce(dtable, dtiles + t0, nt, wslot, slot_elems, geom.z2, bf16,
+                     bf16 ? kRsOrderedRound : kRsOrdered, assign, scale, FlagGate{}, kCommCtas, s);
     ++launches;
     return;
   }
-  launch_rs_pull(dtable, dtiles + rs_off[layer], rs_off[layer + 1] - rs_off[layer], wslot,
-                 slot_elems, geom.z2, bf16, assign, static_cast<float>(cfg.grad_scale), comm_ctas, s);
-  ++launches;
+  const int me = cfg.my_rank;
+  const uint64_t grp = rank_mask(geom.z2_base(me), geom.z2);
+  launch_flags(dtable, me, kFlagRsReady, grp, seq, kFlagRsReady, nt > 0 ? grp : 0, seq, s);
+  if (nt > 0)
+    launch_rs_reduce(dtable, dtiles + t0, nt, wslot, slot_elems, geom.z2, bf16, bf16 ? kRsMulticast : kRsOrdered,
+                     assign, scale, FlagGate{}, kCommCtas, s);
+  launch_flags(dtable, me, kFlagRsDone, grp, seq, 0, 0, 0, s);
+  launches += nt > 0 ? 3 : 2;
 }
 
 void Engine::z1_adam(cudaStream_t s) {
@@ -512,32 +420,6 @@ void Engine::z1_adam(cudaStream_t s) {
   a.omb2 = one - a.b2;
   a.bc1 = one - static_cast<float>(std::pow(static_cast<double>(a.b1), step));
   a.bc2 = one - static_cast<float>(std::pow(static_cast<double>(a.b2), step));
-  if (!z1_chunks.empty()) {
-    // chunk c's copy (copy engines, z1_copy_stream) overlaps chunk c-1's
-    // kernel (s); buffer c & 1 is reused by chunk c+2 only after chunk c's
-    // kernel retired
-    std::vector<cudaEvent_t> done_k(z1_chunks.size());
-    cudaEvent_t e0 = rs_ev[0];
-    HZP_CUDA(cudaEventRecord(e0, s));  // grads complete (the caller's barrier)
-    HZP_CUDA(cudaStreamWaitEvent(z1_copy_stream, e0, 0));
-    for (size_t c = 0; c < z1_chunks.size(); ++c) {
-      const Z1Chunk& ch = z1_chunks[c];
-      if (c >= 2) HZP_CUDA(cudaStreamWaitEvent(z1_copy_stream, done_k[c - 2], 0));
-      for (const CopyRun& r : ch.copies)
-        HZP_CUDA(cudaMemcpyAsync(static_cast<float*>(z1_stage[r.src]) + (c & 1) * kZ1ChunkElems,
-                                 table.grad[r.src] + r.src_off, size_t(r.len) * 4, cudaMemcpyDeviceToDevice,
-                                 z1_copy_stream));
-      cudaEvent_t ec = rs_ev[1 + (2 * c) % (rs_ev.size() - 1)];
-      HZP_CUDA(cudaEventRecord(ec, z1_copy_stream));
-      HZP_CUDA(cudaStreamWaitEvent(s, ec, 0));
-      launch_z1_adam(ch.table, dtiles + ch.t0, ch.t1 - ch.t0, geom.z2, geom.replicas(), &a, 1, bf16,
-                     l0.dbg != nullptr, 8 * kNumSMs, s);
-      done_k[c] = rs_ev[1 + (2 * c + 1) % (rs_ev.size() - 1)];
-      HZP_CUDA(cudaEventRecord(done_k[c], s));
-    }
-    ++launches;
-    return;
-  }
   launch_z1_adam(dtable, dtiles + z1_off, z1_n, geom.z2, geom.replicas(), &a, 1, bf16,
                  l0.dbg != nullptr, 8 * kNumSMs, s);  // HBM-bound, never beside a GEMM
   ++launches;
@@ -546,8 +428,8 @@ void Engine::z1_adam(cudaStream_t s) {
 void Engine::barrier(cudaStream_t s) {
   if (emulate || cfg.par.dp == 1) return;
   ++barrier_epoch;
-  launch_signal(dtable, cfg.my_rank, kFlagBarrier, 0, cfg.par.dp, 1, barrier_epoch, kFlagBarrier,
-                barrier_epoch, s);
+  const uint64_t all = rank_mask(0, cfg.par.dp);
+  launch_flags(dtable, cfg.my_rank, kFlagBarrier, all, barrier_epoch, kFlagBarrier, all, barrier_epoch, s);
   ++launches;
 }
 
@@ -555,7 +437,7 @@ const void* Engine::layer_params(int li, int layer, int slot) const {
   const int es = bf16 ? 2 : 4;
   if (zero_copy_ag)  // z3 == 1: this rank's shard is the whole working copy
     return static_cast<const char*>(arenas[locals[li].rank].param) + layers[layer].off * es;
-  return static_cast<const char*>(locals[li].ag) + (int64_t(slot) * slot_elems) * es;
+  return static_cast<const char*>(arenas[locals[li].rank].ag) + (int64_t(slot) * slot_elems) * es;
 }
 
 GradTarget Engine::grad_target(int li, int layer, int wslot, int mb) const {
@@ -676,8 +558,8 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
           // the gradient buffer is free once RS k - wslots finished everywhere
           if (k >= wslots) HZP_CUDA(cudaStreamWaitEvent(s, done[rs_ids[k - wslots]], 0));
           if (!emulate && geom.z2 > 1 && seq0 + k >= uint64_t(wslots)) {
-            launch_wait(dtable, cfg.my_rank, kFlagRsDone, geom.z2_base(cfg.my_rank), geom.z2, 1,
-                        seq0 + k + 1 - wslots, s);
+            launch_flags(dtable, cfg.my_rank, 0, 0, 0, kFlagRsDone, rank_mask(geom.z2_base(cfg.my_rank), geom.z2),
+                         seq0 + k + 1 - wslots, s);
             ++launches;
           }
         }
@@ -694,17 +576,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
         if (direct_grad) {
           rec_log(e, -1, e.id - 1, e.id);  // fused into the BWD's wgrad epilogue
         } else {
-          if (!emulate && geom.z2 > 1) {  // publish + wait for every Z2 peer's gradient
-            launch_signal(dtable, cfg.my_rank, kFlagRsReady, geom.z2_base(cfg.my_rank), geom.z2, 1,
-                          seq, kFlagRsReady, seq, s);
-            ++launches;
-          }
-          rs_layer(e.layer, static_cast<int>((seq - 1) % wslots), e.microbatch == 0, s);
-          if (!emulate && geom.z2 > 1) {
-            launch_signal(dtable, cfg.my_rank, kFlagRsDone, geom.z2_base(cfg.my_rank), geom.z2, 1,
-                          seq, -1, 0, s);
-            ++launches;
-          }
+          rs_layer(e.layer, static_cast<int>((seq - 1) % wslots), e.microbatch == 0, seq, s);
           rec_log(e, int(e.stream), e.id, e.id);
         }
         break;

@@ -1,6 +1,8 @@
 // Device engine: one hzp_ctx drives one GPU and either one dp rank (one
-// process per GPU, peers reached through CUDA IPC over NVLink/NVSwitch) or
-// all dp ranks emulated on that GPU (single-process parity mode).
+// process per GPU; peers' arenas mapped over NVLink/NVSwitch from shared
+// cuMem allocations, AG / gradient rings bound to NVLS multicast objects) or
+// all dp ranks emulated on that GPU (single-process parity mode: the same
+// kernels with unicast stores / ordered loads in place of multimem).
 #pragma once
 
 #include <memory>
@@ -10,22 +12,32 @@
 #include "hzp_b200.h"
 #include "engine/comm.cuh"
 #include "engine/model.hpp"
+#include "engine/symm.hpp"
 
 namespace hzp {
 
+// One dp rank's peer-visible memory, carved from one allocation:
+//   [ param s3 | grad s2 fp32 | flags | AG ring + reuse cache | gradient ring ]
+// (multi-process: a cuMem allocation; the AG and gradient regions start at
+// multicast-granularity offsets so they can be bound to the group objects).
 struct Arena {
   void* base = nullptr;
   size_t bytes = 0;
-  bool owned = false;  // allocated here (else IPC-mapped)
+  SymmBuf symm;        // multi-process: exported (own) or imported (peer) mapping
+  bool cuda_malloc = false;
   void* param = nullptr;
   float* grad = nullptr;
-  void* wgrad = nullptr;
   uint64_t* flags = nullptr;
+  void* ag = nullptr;     // [depth + cache_slots][slot_elems]: ring, then the reuse cache
+  void* wgrad = nullptr;  // [wslots][slot_elems] wire dtype (null when z2 == 1)
+};
+
+struct ArenaLayout {
+  size_t param = 0, grad = 0, flags = 0, ag = 0, ag_bytes = 0, wgrad = 0, wgrad_bytes = 0, total = 0;
 };
 
 struct LocalRank {
   int rank = 0;
-  void* ag = nullptr;  // [depth + cache_slots][slot_elems]: ring, then the reuse cache
   float* master = nullptr;
   float* mom = nullptr;
   float* var = nullptr;
@@ -68,65 +80,24 @@ struct Engine {
   RankTable* dtable = nullptr;
 
   CommTile* dtiles = nullptr;
-  std::vector<int> ag_off, rs_off;  // [nlocal_layers + 1] per layer tile ranges
-  // AG through the copy engines (no SMs taken from the concurrent GEMMs): the
-  // layer's tiles merged into contiguous (owner -> slot) runs
-  struct CopyRun {
-    int local, src;
-    int64_t dst_off, src_off, len;
-  };
-  std::vector<std::vector<CopyRun>> ag_runs;
-  bool ag_ce = true;   // HZP_AG_CE=0 to use the SM pull
-  // HZP_AG_PAR=1: each owner's runs on its own copy stream (all owners read at once)
-  bool ag_par = false;
-  std::vector<cudaStream_t> ag_copy_streams;
-  std::vector<cudaEvent_t> ag_par_ev;  // [0] fork, [1 + i] join of stream i
-  // RS with the NVLink leg on the copy engines: each remote Z2 member's
-  // gradient-buffer segment is copied into a local staging slot, then the
-  // (now HBM-local) reduction kernel runs on a table whose remote wgrad
-  // entries point at the staging slots (one table per ring slot).
-  std::vector<void*> rs_stage;                // [dp] staging slot per remote member (or null)
-  std::vector<RankTable*> dtable_staged;      // [wslots]
-  // The copy of chunk c+1 overlaps the HBM-local reduce of chunk c: copies
-  // on the RS stream, reduces on rs_red_stream, chained by rs_ev.
-  std::vector<CommTile> tiles_host;
-  cudaStream_t rs_red_stream = nullptr;
-  std::vector<cudaEvent_t> rs_ev;
-  // each peer's copies on its own stream, all peers pulled at once (HZP_RS_PAR=0:
-  // one stream, peers in rotated order; 441 vs 576 GB/s for a 1 GB layer at N=4)
-  bool rs_par = true;
-  std::vector<cudaStream_t> rs_copy_streams;
-  std::vector<cudaEvent_t> rs_par_ev;
-  static constexpr int kRsChunkTiles = 128;  // 4 M elements per pipelined chunk
-  int64_t rs_min_chunk_bytes = 0;  // per peer copy, 0 = auto (HZP_RS_MIN_CHUNK_MB)
-  bool rs_ce = true;
-  // Z1 with DZP replicas (R > 1): the remote replicas' gradient segments of
-  // this rank's chunk are copied (copy engines) into double-buffered local
-  // staging, chunk by chunk, while the fused Z1 kernel consumes the previous
-  // chunk through a table whose remote grad entries point at the staging.
-  bool z1_ce = false;  // HZP_Z1_CE=1 (7B dp=4: 36.6 vs 31.3 ms SM pull, so off)
-  struct Z1Chunk {
-    int t0, t1;                       // tile range (within the Z1 tiles)
-    RankTable* table;                 // device table for this chunk
-    std::vector<CopyRun> copies;      // CopyRun.src = global rank; dst_off into its staging buffer
-  };
-  std::vector<Z1Chunk> z1_chunks;
-  std::vector<void*> z1_stage;        // [dp]: 2 x kZ1ChunkElems fp32 per remote replica rank
-  cudaStream_t z1_copy_stream = nullptr;
-  static constexpr int64_t kZ1ChunkElems = int64_t(16) << 20;
-  void setup_z1_staging();   // HZP_RS_CE=0 to use the SM pull (dp=4: 184.5 -> 160.1 ms with both CE legs)
-  void setup_rs_staging();
+  std::vector<int> ag_off, rs_off;  // [L + 1] per layer tile ranges
+  std::vector<uint64_t> ag_owners;  // [L] Z3 members owning part of layer l (multi-process)
   int z1_off = 0, z1_n = 0;
+  ArenaLayout lay;
+  McGroup ag_mc, wg_mc;  // NVLS objects of this rank's Z3 / Z2 group (multi-process)
+  // AG / RS launch one short-lived 128-thread CTA per tile (<= 64 KB, ~10 us):
+  // one fits beside a resident persistent GEMM CTA, and a comm CTA that lands
+  // on an SM between two GEMMs delays the next GEMM's CTA there by one tile at
+  // most (a grid-stride CTA would hold it for the whole collective)
+  static constexpr int kCommCtas = 1 << 16;
 
   void* dinputs = nullptr;
   size_t input_bytes_per_mb = 0;
   float* hloss = nullptr;  // pinned [nlocal]
 
-  uint64_t rs_seq = 0, barrier_epoch = 0;
+  uint64_t rs_seq = 0, ag_seq = 0, barrier_epoch = 0;
   std::vector<hzp_launch_rec> log;
   int64_t launches = 0;
-  int comm_ctas = kNumSMs;  // one 256-thread CTA per SM, beside the persistent GEMM
-  int rs_chunks = 4;        // copy-engine RS: at most this many pipelined chunks per layer (HZP_RS_CHUNKS)
   bool peers_open = false;
   bool debug_sync = false;
 
@@ -135,9 +106,12 @@ struct Engine {
 
   int local_index(int rank) const;
   void build_tiles();
+  void carve(Arena& a) const;
+  ShareRecord share_record() const;
+  void open_peers(const ShareRecord* records, int n);
   void step(const void* inputs, bool on_device, float* losses_out);
   void ag_layer(int layer, int slot, cudaStream_t s);
-  void rs_layer(int layer, int wslot, bool assign, cudaStream_t s);
+  void rs_layer(int layer, int wslot, bool assign, uint64_t seq, cudaStream_t s);
   void z1_adam(cudaStream_t s);
   void barrier(cudaStream_t s);
   GradTarget grad_target(int li, int layer, int wslot, int mb) const;

@@ -103,6 +103,12 @@ std::vector<SlotRun> slot_runs(const TaskGraph& g) {
 
 }  // namespace
 
+std::vector<ScheduleSlot> graph_slots(const TaskGraph& graph) {
+  std::vector<ScheduleSlot> out;
+  for (const SlotRun& r : slot_runs(graph)) out.push_back({r.pass, r.mb, r.vstage});
+  return out;
+}
+
 ReuseReport apply_reuse(TaskGraph& graph) {
   const std::vector<SlotRun> runs = slot_runs(graph);
   // (pass, mb, vstage, layer) -> AG id;  (mb, vstage, layer) -> RS id

@@ -55,32 +55,31 @@ TileTables build_comm_tiles(const ShardGeom& g, const std::vector<Range64>& laye
   TileTables T;
   auto& tiles = T.tiles;
   const int L = static_cast<int>(layers.size());
-  // AG: per layer, per driven rank, the owner spans of the layer's range.
+  // AG (owner push): per layer, per driven rank o, the part of the layer o
+  // owns (layer ∩ o's Z3 shard).  o stores it into the AG slot of every
+  // member of its Z3 group (one multimem.st on NVLS; the union over the
+  // group's owners covers the layer once).
   T.ag_off.assign(L + 1, 0);
   for (int l = 0; l < L; ++l) {
     T.ag_off[l] = static_cast<int>(tiles.size());
     for (size_t li = 0; li < local_ranks.size(); ++li) {
-      const int r = local_ranks[li];
-      const int base = g.z3_base(r);
-      int64_t e = layers[l].off;
-      const int64_t end = layers[l].off + layers[l].size;
-      while (e < end) {
-        const int owner = static_cast<int>(e / g.s3);
-        const int64_t stop = std::min(end, (owner + 1) * g.s3);
-        const int64_t offs[2] = {e - layers[l].off, e - owner * g.s3};
-        const int eb[2] = {es, es};
-        split_run(offs, eb, 2, stop - e, 16 / es, [&](int64_t p, int64_t n, bool v) {
-          CommTile t{};
-          t.a_off = offs[0] + p;
-          t.b_off = offs[1] + p;
-          t.len = static_cast<int32_t>(n);
-          t.local = static_cast<int16_t>(li);
-          t.src = static_cast<int16_t>(base + owner);
-          t.vec = v;
-          tiles.push_back(t);
-        });
-        e = stop;
-      }
+      const int o = local_ranks[li];
+      const int i3 = o % g.z3;
+      const int64_t e0 = std::max(layers[l].off, i3 * g.s3);
+      const int64_t e1 = std::min(layers[l].off + layers[l].size, (i3 + 1) * g.s3);
+      if (e0 >= e1) continue;
+      const int64_t offs[2] = {e0 - layers[l].off, e0 - i3 * g.s3};
+      const int eb[2] = {es, es};
+      split_run(offs, eb, 2, e1 - e0, 16 / es, [&](int64_t p, int64_t n, bool v) {
+        CommTile t{};
+        t.a_off = offs[0] + p;
+        t.b_off = offs[1] + p;
+        t.len = static_cast<int32_t>(n);
+        t.local = static_cast<int16_t>(li);
+        t.src = static_cast<int16_t>(o);
+        t.vec = v;
+        tiles.push_back(t);
+      });
     }
   }
   T.ag_off[L] = static_cast<int>(tiles.size());

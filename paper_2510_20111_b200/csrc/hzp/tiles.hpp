@@ -14,12 +14,12 @@
 namespace hzp {
 
 struct CommTile {
-  int64_t a_off;   // AG: dst (slot) offset | RS: grad offset | Z1: chunk offset
-  int64_t b_off;   // AG: src (shard) offset | RS: gradient-buffer offset | Z1: grad-shard offset
+  int64_t a_off;   // AG: slot offset | RS: grad offset | Z1: chunk offset
+  int64_t b_off;   // AG: offset in the owner's shard | RS: gradient-buffer offset | Z1: grad-shard offset
   int64_t c_off;   // Z1: param-shard offset
   uint64_t mask;   // Z1: push targets, bit q = global rank q
   int32_t len;     // elements
-  int16_t local;   // index of the destination rank among the ctx's driven ranks
+  int16_t local;   // index of the rank among the ctx's driven ranks (AG: the owner; RS / Z1: the destination)
   int16_t src;     // AG: owner rank | RS: Z2 group base | Z1: Z2 segment index j
   int32_t vec;     // 1 = every address 16-byte aligned and len a multiple of the vector
   int32_t pad_;

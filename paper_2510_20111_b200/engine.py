@@ -288,6 +288,12 @@ class HzpEngine:
     def rs_layer(self, layer: int, wslot: int) -> None:
         N.check(N.lib.hzp_rs_layer(self._h, layer, wslot))
 
+    def collective_time(self, kind: str, layer: int, iters: int = 5) -> float:
+        """ms per back-to-back AG ("ag") or RS ("rs") of `layer`, CUDA-event timed."""
+        v = C.c_double()
+        N.check(N.lib.hzp_collective_time(self._h, {"ag": 0, "rs": 1}[kind], layer, iters, C.byref(v)))
+        return v.value
+
     def z1_adam_step(self) -> None:
         N.check(N.lib.hzp_z1_adam_step(self._h))
 

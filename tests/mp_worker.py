@@ -15,6 +15,7 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from oracle import load_oracle  # noqa: E402
 from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig  # noqa: E402
@@ -35,7 +36,7 @@ def kernels(z1, z2, z3, prec):
     eng.load_state(st)
     dist.barrier()
     ok = True
-    for l, (off, n) in enumerate(eng.layers):
+    for l, (off, n) in enumerate(eng.layers if z3 > 1 else []):  # z3 = 1: the AG is the identity
         eng.ag_layer(l, 0)
         g0 = rank - rank % z3
         want = o.all_gather(st.param[g0:g0 + z3])[off:off + n]
@@ -43,7 +44,7 @@ def kernels(z1, z2, z3, prec):
         if prec:
             got = (got.astype(np.uint32) << 16).view(np.float32)
         ok &= bool(np.array_equal(got, want))
-    if z2 > 1 and prec == 0:
+    if z2 > 1:
         rng = np.random.default_rng(5)
         grads = rng.standard_normal((world, st.s2 * z2)).astype(np.float32)
         eng.zero_grads()
@@ -55,9 +56,19 @@ def kernels(z1, z2, z3, prec):
             torch.cuda.synchronize()
             dist.barrier()
         g0 = rank - rank % z2
-        seg = o.reduce_scatter(grads[g0:g0 + z2])[rank % z2]
         got = eng.download(rank, 1)
-        ok &= bool(np.array_equal(got, 0 + seg))
+        lo = (rank % z2) * st.s2
+        nv = max(0, min(st.s2, st.P - lo))
+        if prec == 0:  # fp32 wire: ordered pull, bit-exact
+            seg = o.reduce_scatter(grads[g0:g0 + z2])[rank % z2]
+            ok &= bool(np.array_equal(got[:nv], (0 + seg)[:nv]))
+        else:  # bf16 wire: multimem.ld_reduce in the switch vs the unicast model
+            from test_gpu_comm import rs_bf16_model
+            want = rs_bf16_model(o, grads[g0:g0 + z2])[lo:lo + nv]
+            exact = float(np.mean(got[:nv].view(np.uint32) == want.view(np.uint32))) if nv else 1.0
+            err = float(np.max(np.abs(got[:nv] - want)) / max(np.max(np.abs(want)), 1e-30)) if nv else 0.0
+            print(f"rank {rank}: bf16 multimem RS vs model: exact {exact:.6f} max rel {err:.3g}", flush=True)
+            ok &= err <= 2.0 ** -7
     print(f"rank {rank}: {'OK' if ok else 'FAIL'} kernels", flush=True)
     dist.barrier()
     eng.close()

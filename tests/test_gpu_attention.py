@@ -21,7 +21,9 @@ def _ref(q, k, v, do):
     return o.detach(), lse.detach(), q.grad, k.grad, v.grad
 
 
-@pytest.mark.parametrize("b,nh,S", [(1, 1, 128), (2, 2, 256), (1, 4, 512), (2, 1, 1024)])
+# (4, 16, 2048) is the bench shape (1.3B config: b = 4 sequences per microbatch,
+# 16 heads, S = 2048): the LPT-ordered two-tile forward and the full backward grid
+@pytest.mark.parametrize("b,nh,S", [(1, 1, 128), (2, 2, 256), (1, 4, 512), (2, 1, 1024), (4, 16, 2048)])
 def test_fused_attention_fwd_bwd(gpu, b, nh, S):
     from paper_2510_20111_b200 import _native as N
     hd, h = 128, 128 * nh

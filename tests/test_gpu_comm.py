@@ -1,11 +1,15 @@
-"""Parity of the P2P collective kernels against the oracle (tier A, bitwise).
+"""Parity of the collective kernels against the oracle (tier A, bitwise).
 
-All dp ranks are emulated on one GPU (peer pointers are local device
-pointers), which exercises the exact kernels the multi-GPU path runs; the
-multi-process path is covered by tests/test_gpu_multi.py on >= 2 GPUs.
+All dp ranks are emulated on one GPU: the AG / RS / Z1 kernels of the
+multi-GPU path run over the same tile tables, with the NVLS primitive
+replaced by its unicast model (owner stores to every member's slot; the
+reducer sums the members' slots in ascending order, bf16 wire rounded to
+bf16 like the switch).  The multi-process path (multimem over NVSwitch) is
+covered by tests/test_gpu_multi.py on >= 2 GPUs.
 
   AG  : slot contents == oracle all_gather of the Z3 group (collective.cpp:44-67)
-  RS  : grad shards == 0 + ascending-rank sum (collective.cpp:69-97, train.cpp:313-322)
+  RS  : grad shards == 0 + ascending-rank sum (collective.cpp:69-97, train.cpp:313-322);
+        bf16 wire: the same sum of the bf16-rounded gradients, rounded to bf16
   Z1  : master/m/v/param shards after the fused replica-reduce + Adam + bf16
         push == oracle train_step_hzp (train.cpp:326-379)
 """
@@ -82,6 +86,50 @@ def test_rs_pull_bitwise(gpu, oracle, cfg):
     for r in range(dp):
         got = eng.download(r, 2 - 1)  # F_GRAD
         assert np.array_equal(got.view(np.uint32), want[r].view(np.uint32)), r
+    eng.close()
+
+
+def bf16_rne(o, x):
+    return o.bf16_round(np.ascontiguousarray(x, np.float32)).astype(np.float32)
+
+
+def rs_bf16_model(o, grads):
+    """The bf16-wire reduce: each member's gradient rounded to bf16 (the wgrad
+    GEMM's bf16 store), summed in fp32 in ascending rank order, the sum
+    rounded to bf16 (multimem.ld_reduce .acc::f32 returns bf16)."""
+    w = [bf16_rne(o, g) for g in grads]
+    s = w[0].copy()
+    for x in w[1:]:
+        s = (s + x).astype(np.float32)
+    return bf16_rne(o, s)
+
+
+@pytest.mark.parametrize("cfg", [c for c in CONFIGS if c[3] > 1], ids=_ids)
+def test_rs_bf16_wire_bitwise(gpu, oracle, cfg):
+    dims, dp, z1, z2, z3 = cfg
+    st = oracle.shard_init(dims, dp, z1, z2, z3, 7, True)
+    rng = np.random.default_rng(3)
+    eng = _engine(dims, dp, z1, z2, z3, 1, mbs=2)
+    eng.load_state(st)
+    eng.zero_grads()
+    want = np.zeros((dp, st.s2), np.float32)
+    for mb in range(2):
+        full = rng.standard_normal((dp, st.s2 * z2)).astype(np.float32)
+        for l, (off, n) in enumerate(eng.layers):
+            for r in range(dp):
+                eng.wgrad_upload(r, l, mb % 2, full[r, off:off + n])
+            eng.rs_layer(l, mb % 2)
+        for g0 in range(0, dp, z2):
+            red = rs_bf16_model(oracle, full[g0:g0 + z2])
+            for i in range(z2):
+                seg = red[i * st.s2:(i + 1) * st.s2]
+                want[g0 + i] = (want[g0 + i] + seg).astype(np.float32)
+    for r in range(dp):
+        got = eng.download(r, 1)
+        P = eng.P
+        lo = (r % z2) * st.s2
+        n_valid = max(0, min(st.s2, P - lo))
+        assert np.array_equal(got[:n_valid].view(np.uint32), want[r][:n_valid].view(np.uint32)), r
     eng.close()
 
 

@@ -15,6 +15,9 @@ CFG = dict(layers=2, hidden=256, heads=2, ffn=1024, vocab=512, seq=256, batch=2)
 # the 1.3B block width: CTA-pair GEMMs (incl. split tail waves), the h = 2048
 # register-resident LayerNorm kernels, two-tile attention, bias column sums
 CFG_WIDE = dict(layers=1, hidden=2048, heads=16, ffn=8192, vocab=1024, seq=512, batch=2)
+# the bench's exact shapes (BASELINE configs[1]): S = 2048, 16 heads, b = 4
+# sequences per microbatch, the 50304-way head / cross-entropy
+CFG_BENCH = dict(layers=1, hidden=2048, heads=16, ffn=8192, vocab=50304, seq=2048, batch=4)
 
 
 def layout(c):
@@ -90,7 +93,7 @@ def _bf16_bits(x):
             ((np.ascontiguousarray(x, np.float32).view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("c", [CFG, CFG_WIDE], ids=["small", "wide"])
+@pytest.mark.parametrize("c", [CFG, CFG_WIDE, CFG_BENCH], ids=["small", "wide", "bench"])
 def test_gpt_gradient_matches_torch(gpu, c):
     eng = _engine(c)
     master = init_params(c)

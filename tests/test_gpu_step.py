@@ -28,6 +28,10 @@ STEP_CONFIGS = [
     ([3, 2], 8, 8, 4, 4, 1, 2, 3),
     ([5, 3, 2], 4, 4, 2, 2, 2, 3, 3),
     ([1, 1], 2, 2, 2, 2, 1, 1, 3),
+    # SURVEY §8(d)-2 parity size: {256, 1024, 256}, B = 8 rows per microbatch,
+    # dp = 4 with the CPU config's hierarchy and flat; multi-tile tcgen05 GEMMs
+    ([256, 1024, 256], 4, 4, 2, 2, 2, 8, 3),
+    ([256, 1024, 256], 4, 4, 4, 4, 2, 8, 3),
 ]
 
 

@@ -4,8 +4,9 @@ tile tables through the C-ABI (no GPU needed); rank 0 gathers everything and
 checks the multi-rank invariants the device kernels rely on:
 
   * every rank derives the identical launch order / slot plan;
-  * AG tiles of rank r cover each layer exactly once, each element pulled
-    from its Z3 owner  (e // s3, train.cpp:229-249);
+  * AG tiles: rank r pushes exactly the part of each layer inside its own
+    Z3 shard (e // s3 == r % z3, train.cpp:229-249); the owners of a Z3
+    group together cover each layer exactly once;
   * RS tiles of a Z2 group partition (layer ∩ segment) across its members;
   * Z1 tiles of a Z1 group partition [0, P), and every element is pushed to
     exactly the group members q with q % z3 == e // s3 (train.cpp:361-379).
@@ -98,18 +99,18 @@ def test_multirank_plans_and_tiles(world, z, dims, es):
         assert p.exitcode == 0
     # identical plans on every rank
     assert all(v["plan"] == allv[0]["plan"] for v in allv)
-    for r, v in enumerate(allv):
-        T = v["tiles"]
+    for g0 in range(0, world, z3):
         for l, (lo, ln) in enumerate(layers):
             cov = np.zeros(ln, np.int32)
-            for (a, b, c, m, n, src, vec) in T[v["ag"][l]:v["ag"][l + 1]]:
-                cov[a:a + n] += 1
-                owner = src - (r - r % z3)
-                assert 0 <= owner < z3
-                assert owner * s3 + b == lo + a  # pulled from the element's owner
-                if vec:
-                    assert (a * es) % 16 == 0 and (b * es) % 16 == 0 and (n * es) % 16 == 0
-            assert np.all(cov == 1), (r, l)
+            for r in range(g0, g0 + z3):
+                v = allv[r]
+                for (a, b, c, m, n, src, vec) in v["tiles"][v["ag"][l]:v["ag"][l + 1]]:
+                    assert src == r  # the owner pushes its own span
+                    cov[a:a + n] += 1
+                    assert (r % z3) * s3 + b == lo + a  # offset in the owner's shard
+                    if vec:
+                        assert (a * es) % 16 == 0 and (b * es) % 16 == 0 and (n * es) % 16 == 0
+            assert np.all(cov == 1), (g0, l)
     if z2 > 1:
         for g0 in range(0, world, z2):
             for l, (lo, ln) in enumerate(layers):
