@@ -33,11 +33,12 @@ UNIT = "tokens/s"
 
 # BASELINE.json configs[1] dims (SURVEY App. A-5 proposal; untied LM head)
 GPT13B = dict(layers=24, hidden=2048, heads=16, ffn=8192, vocab=50304, seq=2048)
-# BASELINE configs[2]: 7B dense decoder, hierarchical ZeRO-3 group 4 x ZeRO-1 group 2
-GPT7B = dict(layers=32, hidden=4096, heads=32, ffn=16384, vocab=50304, seq=2048)
-# BASELINE configs[3]: MoE 16 experts top-2 (SURVEY App. A-5 dims, GELU experts of
-# width 4864), hierarchical ZeRO-3 group 2 x ZeRO-1 group 4
-MOE = dict(layers=16, hidden=2048, heads=16, ffn=4864, vocab=50304, seq=2048, experts=16, topk=2)
+# BASELINE configs[2]: 7B dense decoder (L32 h4096, SwiGLU 11008,
+# vocab 32000 -> 6.7 B parameters), hierarchical ZeRO-3 group 4 x ZeRO-1 group 2
+GPT7B = dict(layers=32, hidden=4096, heads=32, ffn=11008, vocab=32000, seq=2048, swiglu=1)
+# BASELINE configs[3]: MoE 16 SwiGLU experts of width 4864, top-2 (SURVEY App. A-5:
+# 495 M parameters per layer, ~8 B total), hierarchical ZeRO-3 group 2 x ZeRO-1 group 4
+MOE = dict(layers=16, hidden=2048, heads=16, ffn=4864, vocab=50304, seq=2048, experts=16, topk=2, swiglu=1)
 MODELS = {"1.3b": GPT13B, "7b": GPT7B, "moe": MOE}
 
 
@@ -164,7 +165,8 @@ def cpu_reference(steps: int, warmup: int, label: str, c=None):
     sample_tok = mbs * rows
     sample_flops_tok = 6.0 * (dims[0] * dims[1] + dims[1] * dims[2])
     c = c or GPT13B
-    ffn = c.get("topk", 1) * 2 * c["hidden"] * c["ffn"] if c.get("experts") else 2 * c["hidden"] * c["ffn"]
+    per_ex = (3 if c.get("swiglu") else 2) * c["hidden"] * c["ffn"]
+    ffn = c.get("topk", 1) * per_ex if c.get("experts") else per_ex
     model_flops_tok = 6.0 * (c["layers"] * (4 * c["hidden"] ** 2 + ffn) + c["vocab"] * c["hidden"])
     raw = sample_tok / sec
     equiv = raw * sample_flops_tok / model_flops_tok
@@ -477,6 +479,33 @@ def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, z1=1, z2=1, z3
             "note": "includes the two device-wide barriers around the kernel (no-op at N=1)"}
 
 
+def simulator_prediction(c, N, z1, z2, z3, nmb, mb, depth):
+    """The reference's own simulator (the drop-in's bit-exact simulate) on this
+    step's task graph, with SURVEY App. A-6's B200 cost model (720 GB/s
+    intra-node = the 80 % NVLink target, 10 us latency, 1 PFLOP/s achieved):
+    predicted compute-idle fraction in async and vanilla mode, to set beside
+    the measured one."""
+    from paper_2510_20111_b200 import hzp as H
+    h, f, S = c["hidden"], c["ffn"], c["seq"]
+    per_ex = (3 if c.get("swiglu") else 2) * h * f
+    ffn = per_ex * (c.get("topk", 1) if c.get("experts") else 1)
+    ppl = 4 * h * h + (c.get("experts", 0) or 1) * per_ex
+    spec = H.ModelSpec(num_layers=c["layers"], params_per_layer=ppl, seq_len=S, micro_batch_size=mb,
+                       num_microbatches=nmb, flops_per_token_per_layer=2 * (4 * h * h + ffn) + 4 * S * h)
+    out = {}
+    try:
+        g = H.build_task_graph(spec, H.ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3),
+                               H.CostModel(num_nodes=1, ranks_per_node=N, intra_bw=720e9, inter_bw=720e9,
+                                           intra_latency=10e-6, device_flops=1e15))
+        for name, m in (("async", H.ASYNC), ("vanilla", H.VANILLA)):
+            tl = H.simulate(g, depth, 1, m)
+            out[name] = {"compute_idle_frac": round(tl.compute_idle / tl.makespan, 4),
+                         "makespan_ms": round(tl.makespan * 1e3, 3)}
+    except Exception as exc:  # noqa: BLE001
+        out["error"] = str(exc)[:200]
+    return out
+
+
 def run_hzp(args):
     import numpy as np
     import torch
@@ -497,21 +526,32 @@ def run_hzp(args):
                        gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
                        gpt_seq=c["seq"], batch=mb, num_microbatches=nmb,
                        gpt_experts=c.get("experts", 0), gpt_topk=c.get("topk", 2),
-                       par=ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3), prelaunch_depth=2, rs_slots=1,
+                       gpt_swiglu=c.get("swiglu", 0),
+                       par=ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3), prelaunch_depth=args.depth, rs_slots=1,
+                       mode=0 if args.mode == "vanilla" else 1,
                        device=local, my_rank=rank if N > 1 else 0, reuse=int(args.reuse),
                        recompute=int(args.recompute), wgrad_slots=args.wgrad_slots)
     eng = HzpEngine(cfg)
     if N > 1:
         eng.connect()
-    eng.init_random(seed=1234 + 0, scale=0.04)
+    # the reference's shard_init with seeded_uniform(P, 2024) x 0.02 weights
+    # (train.cpp:17-27, 224-253), streamed on the host
+    eng.init_seeded(2024, 0.02)
     if N > 1:
         dist.barrier()
     tokens_per_step = mb * c["seq"] * nmb  # per GPU
-    rng = np.random.default_rng(rank)
-    # pinned host token batches (e2e leg) and a resident device copy (device leg)
-    shape = (1, nmb, mb, c["seq"] + 1)
-    host = torch.from_numpy(rng.integers(0, c["vocab"], size=shape, dtype=np.int32)).pin_memory()
-    dev = host.to(f"cuda:{local}")
+    # run_case-seeded token ids, one stream per (step, rank, microbatch)
+    # (train.cpp:501-508): a distinct batch for every timed step
+    from paper_2510_20111_b200.engine import make_tokens
+    per_mb = mb * (c["seq"] + 1)
+    n_in = max(args.steps, 5)
+
+    def tokens(step):
+        return np.stack([make_tokens(2024, step, rank, k, per_mb, c["vocab"]).reshape(mb, c["seq"] + 1)
+                         for k in range(nmb)])[None]
+
+    host = [torch.from_numpy(tokens(i)).pin_memory() for i in range(n_in)]
+    dev = [h.to(f"cuda:{local}") for h in host]
     cs = torch.cuda.ExternalStream(eng.stream(0), device=f"cuda:{local}")
 
     def barrier():
@@ -529,8 +569,8 @@ def run_hzp(args):
     # before the warm-up so its own start-up does not overlap the timed steps;
     # only the samples taken while they run are summarised
     with ClockSampler(local) as clk:
-        for _ in range(args.warmup):
-            eng.step_async(dev.data_ptr(), True)
+        for i in range(args.warmup):
+            eng.step_async(dev[i % n_in].data_ptr(), True)
         eng.sync()
         barrier()
         # ---- device-timed region (inputs resident in HBM) ----
@@ -540,8 +580,8 @@ def run_hzp(args):
         barrier()
         t_on = time.perf_counter()
         ev0.record(cs)
-        for _ in range(args.steps):
-            eng.step_async(dev.data_ptr(), True)
+        for i in range(args.steps):
+            eng.step_async(dev[i % n_in].data_ptr(), True)
         ev1.record(cs)
         ev1.synchronize()
         torch.cuda.synchronize()
@@ -555,15 +595,15 @@ def run_hzp(args):
     barrier()
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 5))
-    for _ in range(e2e_steps):
-        loss = eng.step(host.numpy(), on_device=False)
+    for i in range(e2e_steps):
+        loss = eng.step(host[i % n_in].numpy(), on_device=False)
     e2e_s = max_over_ranks(time.perf_counter() - t0) / e2e_steps
     e2e = {"value": N * tokens_per_step / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": int(host.numel() * 4), "d2h_bytes_per_step": 4 * 1,
+           "h2d_bytes_per_step": int(host[0].numel() * 4), "d2h_bytes_per_step": 4 * 1,
            "ms_per_step": e2e_s * 1e3, "loss": float(loss[0])}
     # ---- roofline of the dominant kernel (tcgen05 GEMM), one extra profiled step ----
     gemm_profile(True)
-    eng.step_async(dev.data_ptr(), True)
+    eng.step_async(dev[0].data_ptr(), True)
     eng.sync()
     gemm_profile(False)
     gf, gms, gbusy, gn = gemm_profile_read_busy()
@@ -590,7 +630,7 @@ def run_hzp(args):
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
     # ---- exposed comm: compute-stream idle of one recorded step (sched.cpp:341-350) ----
     eng.set_timeline(True)
-    eng.step_async(dev.data_ptr(), True)
+    eng.step_async(dev[0].data_ptr(), True)
     eng.sync()
     tl = eng.timeline()
     eng.set_timeline(False)
@@ -607,7 +647,8 @@ def run_hzp(args):
         if d:
             in_step[name] = {"tasks": len(d), "median_ms": round(statistics.median(d), 4),
                              "max_ms": round(d[-1], 4)}
-    exposed = {"compute_idle_ms": round(idle, 3), "makespan_ms": round(mk, 3),
+    sim = simulator_prediction(c, N, z1, z2, z3, nmb, mb, args.depth)
+    exposed = {"compute_idle_ms": round(idle, 3), "makespan_ms": round(mk, 3), "simulator": sim,
                "frac": round(idle / mk, 4) if mk else None,
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}
@@ -625,19 +666,22 @@ def run_hzp(args):
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": N,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (uniform random token ids; hash-uniform init weights)",
+                "data": ("synthetic: run_case-seeded mt19937_64 token ids per (step, rank, microbatch); "
+                         "shard_init of seeded_uniform(P, 2024) x 0.02 weights"),
                 "config": {"workload": {"7b": "BASELINE configs[2]: 7B-class GPT decoder, hierarchical ZeRO",
                                         "moe": "BASELINE configs[3]: MoE 16 experts top-2, hierarchical ZeRO",
                                         "1.3b": "BASELINE configs[1]: 1.3B-class GPT decoder, flat ZeRO-3"}[args.model],
                            "model": (f"gpt-{args.model}-class (L{c['layers']} h{c['hidden']} {c['heads']} heads "
-                                     f"ffn{c['ffn']}" + (f" x {c['experts']} experts top-{c['topk']}"
+                                     f"{'SwiGLU ' if c.get('swiglu') else ''}ffn{c['ffn']}"
+                                     + (f" x {c['experts']} experts top-{c['topk']}"
                                                          if c.get("experts") else "") +
                                      f" vocab{c['vocab']} untied head)"),
                            "params": eng.P, "global_batch": N * mb * nmb, "seq_len": c["seq"],
                            "micro_batch": mb, "num_microbatches": nmb, "reuse": int(args.reuse), "recompute": int(args.recompute),
                            "wgrad_slots": args.wgrad_slots,
                            "tokens_per_step": N * tokens_per_step,
-                           "parallelism": f"dp{N} (z1={z1}, z2={z2}, z3={z3})", "prelaunch_depth": 2,
+                           "parallelism": f"dp{N} (z1={z1}, z2={z2}, z3={z3})", "prelaunch_depth": args.depth,
+                           "mode": args.mode,
                            "rs_slots": 1, "l2": "activation working set >> 126 MB L2 (no flush needed)"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roof, "exposed_comm": exposed, "collectives": colls, "z1_adam": z1r,
@@ -664,6 +708,9 @@ def main():
                     help="BASELINE configs[1] (default, the headline), configs[2], configs[3], "
                          "configs[0] (mlp: the reference's own CPU case) or the MLP slice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="async", choices=["async", "vanilla"],
+                    help="scheduler mode (sched.cpp:280-284: vanilla blocks compute on every issued collective)")
+    ap.add_argument("--depth", type=int, default=2, help="AG prefetch depth (ring slots), BASELINE configs[4]: 1-4")
     ap.add_argument("--wgrad-slots", type=int, default=2,
                     help="gradient buffers peers reduce-scatter from (ring; >= 2)")
     ap.add_argument("--recompute", type=int, default=0, choices=[0, 1],

@@ -244,6 +244,10 @@ typedef struct {
    * input and share one activation set, rebuilt by the recompute (the
    * embedding / head keep their outputs: their recompute is a no-op). */
   int recompute;
+  /* GPT only: 1 = SwiGLU feed-forward (LLaMA-style: fc1 [2 gpt_ffn, h] = gate
+   * | up, act = silu(gate) * up, fc2 [h, gpt_ffn], no FFN biases), for the
+   * dense blocks and every MoE expert. */
+  int gpt_swiglu;
 } hzp_engine_config;
 
 typedef struct hzp_ctx hzp_ctx;
@@ -286,6 +290,20 @@ int hzp_state_init_random(hzp_ctx* ctx, uint64_t seed, double scale);
  * inputs_on_device != 0: `inputs` is a device pointer; else a host pointer
  * (copied H2D on the ctx's stream inside the step).  losses_out
  * (host, [local_ranks], optional) receives per-rank summed losses (D2H). */
+/* Reference-faithful synthetic inputs (replace shard_init / seeded_uniform /
+ * run_case seeding, train.cpp:17-27, 224-253, 501-508):
+ *   hzp_seeded_span: out[i] = float(seeded_uniform(P, seed)[first + i]) * scale
+ *     (0 past P: the zero padding of the flat vector);
+ *   hzp_state_init_seeded: every driven rank's master chunk = that vector's
+ *     Z1 chunk, working copy = its Z3 shard (bf16 RNE in bf16 mode), m = v =
+ *     grad = 0, step 0 (scale 1 = the reference's shard_init bit for bit);
+ *   hzp_make_tokens: the run_case stream of (step, rank, microbatch),
+ *     mt19937_64(seed ^ 0x9E3779B97F4A7C15 * (step*1024 + rank*32 + mb + 1)),
+ *     token = floor(((raw >> 11) * 2^-53) * vocab). */
+int hzp_seeded_span(uint64_t seed, int64_t P, int64_t first, int64_t n, double scale, float* out);
+int hzp_state_init_seeded(hzp_ctx* ctx, uint64_t seed, double scale);
+int hzp_make_tokens(uint64_t seed, int step, int rank, int microbatch, int64_t n, int vocab, int32_t* out);
+
 int hzp_step(hzp_ctx* ctx, const void* inputs, int inputs_on_device, float* losses_out);
 int hzp_sync(hzp_ctx* ctx);
 

@@ -90,7 +90,7 @@ class hzp_engine_config(C.Structure):
                 ("grad_scale", C.c_double), ("device", C.c_int), ("my_rank", C.c_int),
                 ("timeline", C.c_int), ("gpt_experts", C.c_int), ("gpt_topk", C.c_int),
                 ("gpt_capacity", C.c_int), ("reuse", C.c_int),
-                ("recompute", C.c_int)]
+                ("recompute", C.c_int), ("gpt_swiglu", C.c_int)]
 
 
 class hzp_launch_rec(C.Structure):
@@ -163,6 +163,9 @@ SIGNATURES = [
     ("hzp_wgrad_upload", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_float), C.c_int64]),
     ("hzp_rs_layer", C.c_int, [_vp, C.c_int, C.c_int]),
     ("hzp_collective_time", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _P(C.c_double)]),
+    ("hzp_seeded_span", C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_double, _P(C.c_float)]),
+    ("hzp_state_init_seeded", C.c_int, [_vp, C.c_uint64, C.c_double]),
+    ("hzp_make_tokens", C.c_int, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, _P(C.c_int32)]),
     ("hzp_z1_adam_step", C.c_int, [_vp]),
     ("hzp_zero_grads", C.c_int, [_vp]),
     ("hzp_barrier", C.c_int, [_vp]),

@@ -6,6 +6,7 @@
 #include <array>
 #include <cstdio>
 #include <map>
+#include <random>
 #include <cstring>
 #include <string>
 
@@ -495,6 +496,87 @@ int hzp_state_init_random(hzp_ctx* ctx, uint64_t seed, double scale) {
     }
     HZP_CUDA(cudaDeviceSynchronize());
   });
+}
+
+// ---- reference-faithful synthetic state / inputs (train.cpp:17-27, 224-253, 501-508) ----
+namespace {
+inline float seeded_value(std::mt19937_64& rng) {
+  // seeded_uniform<float>: (raw >> 11) * 2^-53 - 0.5 in double, then float
+  return static_cast<float>(static_cast<double>(rng() >> 11) * 0x1p-53 - 0.5);
+}
+inline uint16_t bf16_rne_host(float f) {  // bf16_round (kernels.hpp:37-50), non-NaN inputs
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+}  // namespace
+
+int hzp_seeded_span(uint64_t seed, int64_t P, int64_t first, int64_t n, double scale, float* out) {
+  if (!out || first < 0 || n < 0) return HZP_ERR_ARG;
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    rng.discard(static_cast<unsigned long long>(std::min(first, P)));
+    const float sc = static_cast<float>(scale);
+    for (int64_t i = 0; i < n; ++i) out[i] = first + i < P ? seeded_value(rng) * sc : 0.0f;
+  });
+}
+
+int hzp_state_init_seeded(hzp_ctx* ctx, uint64_t seed, double scale) {
+  if (!ctx) return HZP_ERR_ARG;
+  return guarded([&] {
+    Engine& e = *ctx->e;
+    HZP_CUDA(cudaSetDevice(e.cfg.device));
+    HZP_CUDA(cudaDeviceSynchronize());
+    const ShardGeom& g = e.geom;
+    const float sc = static_cast<float>(scale);
+    constexpr int64_t kChunk = int64_t(1) << 24;
+    std::vector<float> buf(kChunk);
+    std::vector<uint16_t> bbuf(kChunk);
+    for (auto& l : e.locals) {
+      const int r = l.rank;
+      // this rank's Z1 master chunk and Z3 working-copy shard of the padded
+      // flat vector seeded_uniform(P, seed) * scale, streamed in one pass
+      const int64_t m0 = int64_t(r % g.z1) * g.s1, p0 = int64_t(r % g.z3) * g.s3;
+      const int64_t lo = std::min(m0, p0), hi = std::max(m0 + g.s1, p0 + g.s3);
+      std::mt19937_64 rng(seed);
+      rng.discard(static_cast<unsigned long long>(std::min(lo, g.P)));
+      auto* master = l.master;
+      auto* param = static_cast<char*>(e.arenas[r].param);
+      for (int64_t c0 = lo; c0 < hi; c0 += kChunk) {
+        const int64_t n = std::min(kChunk, hi - c0);
+        for (int64_t i = 0; i < n; ++i) buf[i] = c0 + i < g.P ? seeded_value(rng) * sc : 0.0f;
+        const int64_t a = std::max(c0, m0), b = std::min(c0 + n, m0 + g.s1);
+        if (a < b) HZP_CUDA(cudaMemcpy(master + (a - m0), buf.data() + (a - c0), size_t(b - a) * 4, cudaMemcpyHostToDevice));
+        const int64_t x = std::max(c0, p0), y = std::min(c0 + n, p0 + g.s3);
+        if (x < y) {
+          if (e.bf16) {
+            for (int64_t i = x; i < y; ++i) bbuf[i - x] = bf16_rne_host(buf[i - c0]);
+            HZP_CUDA(cudaMemcpy(param + (x - p0) * 2, bbuf.data(), size_t(y - x) * 2, cudaMemcpyHostToDevice));
+          } else {
+            HZP_CUDA(cudaMemcpy(param + (x - p0) * 4, buf.data() + (x - c0), size_t(y - x) * 4, cudaMemcpyHostToDevice));
+          }
+        }
+      }
+      HZP_CUDA(cudaMemset(l.mom, 0, size_t(g.s1) * 4));
+      HZP_CUDA(cudaMemset(l.var, 0, size_t(g.s1) * 4));
+      HZP_CUDA(cudaMemset(e.arenas[r].grad, 0, size_t(g.s2) * 4));
+      l.adam_step = 0;
+    }
+    HZP_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+int hzp_make_tokens(uint64_t seed, int step, int rank, int microbatch, int64_t n, int vocab, int32_t* out) {
+  if (!out || n < 0 || vocab < 1) return HZP_ERR_ARG;
+  // run_case's per-(step, rank, microbatch) stream (train.cpp:506-507);
+  // token = floor(u * vocab), u = (raw >> 11) * 2^-53
+  std::mt19937_64 rng(seed ^ (0x9E3779B97F4A7C15ull * (uint64_t(step) * 1024ull + uint64_t(rank) * 32ull +
+                                                       uint64_t(microbatch) + 1)));
+  for (int64_t i = 0; i < n; ++i) {
+    const int t = static_cast<int>(static_cast<double>(rng() >> 11) * 0x1p-53 * vocab);
+    out[i] = t < vocab ? t : vocab - 1;
+  }
+  return HZP_OK;
 }
 
 int hzp_step(hzp_ctx* ctx, const void* inputs, int inputs_on_device, float* losses_out) {

@@ -25,7 +25,10 @@
 namespace hzp {
 namespace {
 
-constexpr int kThreads = 256;  // Z1 / optimizer kernels (run alone)
+// Z1 / optimizer kernel: it runs beside the backward's persistent GEMMs, so
+// it is shaped like the collectives (128 threads, <= 80 registers, one
+// short-lived CTA per tile)
+constexpr int kThreads = 128;
 constexpr int kCommThreads = 128;
 constexpr int kCommRegs = 80;
 constexpr int kUnroll = 8;    // AG: 16-byte vectors in flight per thread
@@ -285,7 +288,7 @@ __device__ __forceinline__ float adam_one(float g, float& m, float& v, float& w,
 }
 
 template <bool kBf16Param>
-__global__ void __launch_bounds__(kThreads) z1_adam_kernel(const RankTable* __restrict__ T,
+__global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int z2, int replicas,
                                                            AdamArgs a, int dbg) {

@@ -71,7 +71,8 @@ enum FlagKind {
   kFlagRsDone = 2,   // RS finished on the poster (its reads of peers' slots too)
   kFlagAgReady = 3,  // AG slot free on the poster (AG sequence number)
   kFlagAgDone = 4,   // owner's span landed in every member's slot
-  kNumFlagKinds = 5
+  kFlagGradReady = 5,  // a layer's gradient final on the poster (and its param reads done)
+  kNumFlagKinds = 6
 };
 
 // Optional in-kernel gate: spin until flags[me][kind][q] >= value for every

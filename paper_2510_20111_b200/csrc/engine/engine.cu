@@ -54,6 +54,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     mcfg.topk = c.gpt_topk;
     mcfg.capacity = c.gpt_capacity;
     mcfg.recompute = c.recompute;
+    mcfg.swiglu = c.gpt_swiglu;
     if (!bf16) throw std::invalid_argument("the GPT model runs in bf16 only");
     model = make_gpt_model(mcfg);
   }
@@ -134,6 +135,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   HZP_CUDA(cudaStreamCreateWithPriority(&st[0], cudaStreamNonBlocking, lo));
   HZP_CUDA(cudaStreamCreateWithPriority(&st[1], cudaStreamNonBlocking, hi));
   HZP_CUDA(cudaStreamCreateWithPriority(&st[2], cudaStreamNonBlocking, hi));
+  HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, lo));
   const int n = static_cast<int>(plan.entries.size());
   done.resize(n);
   for (auto& e : done) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -148,6 +150,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   HZP_CUDA(cudaEventCreate(&ev_step0));
   HZP_CUDA(cudaEventCreate(&ev_step1));
   HZP_CUDA(cudaEventCreateWithFlags(&ev_opt, cudaEventDisableTiming));
+  HZP_CUDA(cudaEventCreateWithFlags(&ev_z1, cudaEventDisableTiming));
 
   // ---- per-rank peer-visible arenas ----
   const int es = bf16 ? 2 : 4;
@@ -323,7 +326,9 @@ Engine::~Engine() {
   cudaEventDestroy(ev_step0);
   cudaEventDestroy(ev_step1);
   cudaEventDestroy(ev_opt);
+  cudaEventDestroy(ev_z1);
   for (auto s : st) cudaStreamDestroy(s);
+  if (opt_stream) cudaStreamDestroy(opt_stream);
 }
 
 int Engine::local_index(int rank) const {
@@ -342,6 +347,15 @@ void Engine::build_tiles() {
   rs_off = T.rs_off;
   z1_off = T.z1_off;
   z1_n = T.z1_n;
+  z1_layer_off = T.z1_layer_off;
+  z1_wait_mask.assign(layers.size(), 0);
+  if (!emulate)
+    for (size_t l = 0; l < layers.size(); ++l)
+      for (int i = z1_layer_off[l]; i < z1_layer_off[l + 1]; ++i) {
+        const CommTile& t = T.tiles[i];
+        for (int b = 0; b < geom.replicas(); ++b) z1_wait_mask[l] |= 1ull << (t.src + b * geom.z2);
+        z1_wait_mask[l] |= t.mask;
+      }
   // members of this rank's Z3 group whose shard holds part of each layer
   ag_owners.assign(layers.size(), 0);
   if (!emulate)
@@ -360,7 +374,7 @@ void Engine::build_tiles() {
 // AG task: every member posts "slot free" (its ring wait is already on the
 // stream), the owner(s) of the layer multicast their spans once every member
 // is ready and post "landed"; every member waits for all the layer's owners.
-void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
+void Engine::ag_layer(int layer, int slot, cudaStream_t s, bool ready_posted) {
   if (zero_copy_ag) throw std::invalid_argument("z3 == 1: the all-gather is the identity (layers read the shard)");
   const int t0 = ag_off[layer], nt = ag_off[layer + 1] - t0;
   if (emulate) {
@@ -373,7 +387,7 @@ void Engine::ag_layer(int layer, int slot, cudaStream_t s) {
   const int me = cfg.my_rank;
   const uint64_t seq = ++ag_seq;
   const uint64_t grp = rank_mask(geom.z3_base(me), geom.z3);
-  launch_flags(dtable, me, kFlagAgReady, grp, seq, kFlagAgReady, nt > 0 ? grp : 0, seq, s);
+  launch_flags(dtable, me, kFlagAgReady, ready_posted ? 0 : grp, seq, kFlagAgReady, nt > 0 ? grp : 0, seq, s);
   if (nt > 0)
     launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, true, FlagGate{}, kCommCtas, s);
   launch_flags(dtable, me, kFlagAgDone, nt > 0 ? grp : 0, seq, kFlagAgDone, ag_owners[layer], seq, s);
@@ -404,12 +418,11 @@ void Engine::rs_layer(int layer, int wslot, bool assign, uint64_t seq, cudaStrea
   launches += nt > 0 ? 3 : 2;
 }
 
-void Engine::z1_adam(cudaStream_t s) {
+AdamArgs Engine::next_adam_args() {
   // Bias corrections exactly as the reference (train.cpp:179-180 with T=float):
   // (T)1 - (T)std::pow((T)beta, step), std::pow(float, int) promoting to double.
-  LocalRank& l0 = locals.front();
   for (auto& l : locals) l.adam_step += 1;
-  const int step = l0.adam_step;
+  const int step = locals.front().adam_step;
   AdamArgs a;
   a.lr = static_cast<float>(cfg.lr);
   a.b1 = static_cast<float>(cfg.beta1);
@@ -420,9 +433,29 @@ void Engine::z1_adam(cudaStream_t s) {
   a.omb2 = one - a.b2;
   a.bc1 = one - static_cast<float>(std::pow(static_cast<double>(a.b1), step));
   a.bc2 = one - static_cast<float>(std::pow(static_cast<double>(a.b2), step));
+  return a;
+}
+
+void Engine::z1_adam(cudaStream_t s) {
+  const AdamArgs a = next_adam_args();
   launch_z1_adam(dtable, dtiles + z1_off, z1_n, geom.z2, geom.replicas(), &a, 1, bf16,
-                 l0.dbg != nullptr, 8 * kNumSMs, s);  // HBM-bound, never beside a GEMM
+                 locals.front().dbg != nullptr, kCommCtas, s);  // HBM-bound
   ++launches;
+}
+
+void Engine::z1_layer(int layer, const AdamArgs& a, cudaStream_t s) {
+  if (!emulate && cfg.par.dp > 1) {
+    // announce "layer final here" to every rank, wait for the ranks this
+    // layer's Z1 reads gradients from / pushes parameters into
+    const uint64_t seq = ++grad_seq;
+    launch_flags(dtable, cfg.my_rank, kFlagGradReady, rank_mask(0, cfg.par.dp), seq, kFlagGradReady,
+                 z1_wait_mask[layer], seq, s);
+    ++launches;
+  }
+  const int t0 = z1_layer_off[layer], nt = z1_layer_off[layer + 1] - t0;
+  launch_z1_adam(dtable, dtiles + t0, nt, geom.z2, geom.replicas(), &a, 1, bf16, locals.front().dbg != nullptr,
+                 kCommCtas, s);
+  launches += nt > 0;
 }
 
 void Engine::barrier(cudaStream_t s) {
@@ -469,6 +502,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
   HZP_CUDA(cudaEventRecord(ev_step0, cs));
   HZP_CUDA(cudaStreamWaitEvent(st[1], ev_step0, 0));
   HZP_CUDA(cudaStreamWaitEvent(st[2], ev_step0, 0));
+  HZP_CUDA(cudaStreamWaitEvent(opt_stream, ev_step0, 0));
   const char* in_dev = static_cast<const char*>(inputs);
   if (!on_device) {
     HZP_CUDA(cudaMemcpyAsync(dinputs, inputs, in_total, cudaMemcpyHostToDevice, cs));
@@ -510,6 +544,49 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
   int opt_id = -1;
   for (const auto& e : plan.entries)
     if (e.kind == TaskKind::OptStep) opt_id = e.id;
+  // async mode: each layer's Z1 (replica reduce + Adam + bf16 push, covering
+  // AR-dzp(l) and AG-post-step(l)) is enqueued on the RS stream right after
+  // the task that makes the layer's gradient final (its last RS; its last BWD
+  // when z2 == 1 fuses the RS into the wgrad GEMM), overlapping the rest of
+  // the backward.  Vanilla mode keeps the reference's tail order.
+  const bool early_z1 = cfg.mode != HZP_MODE_VANILLA;
+  std::vector<int> final_of(n, -1);  // task id -> layer whose gradient it finalises
+  if (early_z1) {
+    std::vector<int> last(layers.size(), -1);
+    for (const auto& t : graph.tasks)
+      if ((direct_grad && t.kind == TaskKind::Bwd) || (!direct_grad && t.kind == TaskKind::RsGrad))
+        last[t.layer] = std::max(last[t.layer], t.id);
+    for (size_t l = 0; l < layers.size(); ++l)
+      if (last[l] >= 0) final_of[last[l]] = static_cast<int>(l);
+  }
+  AdamArgs adam{};
+  bool adam_ready = false;
+  int z1_issued = 0;
+  // multi-process AG: every member posts "slot free" for AG k from its
+  // compute stream as soon as the task that releases the slot (the ring wait:
+  // first consumer of the slot's previous occupant, or its last reader) ends,
+  // so an owner's multicast waits on the members' compute progress only, not
+  // on their AG streams.  post_after[t] = AG sequence number to post after
+  // compute task t (monotone); AGs with no ring wait are free at step start.
+  const bool post_ready_early = !emulate && !zero_copy_ag && cfg.par.dp > 1;
+  std::vector<uint64_t> post_after(n, 0);
+  uint64_t post_at_start = 0;
+  if (post_ready_early) {
+    uint64_t k = ag_seq;
+    for (const auto& e : plan.entries) {
+      if (e.kind != TaskKind::AgParam) continue;
+      const uint64_t q = ++k;
+      const int freed = std::max(e.ring_wait, ag_phys_wait[e.id]);
+      if (freed < 0) post_at_start = std::max(post_at_start, q);
+      else post_after[freed] = std::max(post_after[freed], q);
+    }
+    uint64_t run = post_at_start;  // keep the posted values monotone in issue order
+    for (int t = 0; t < n; ++t)
+      if (post_after[t]) post_after[t] = run = std::max(run, post_after[t]);
+    if (post_at_start)
+      launch_flags(dtable, cfg.my_rank, kFlagAgReady, rank_mask(geom.z3_base(cfg.my_rank), geom.z3), post_at_start,
+                   0, 0, 0, cs);
+  }
 
   for (const auto& e : plan.entries) {
     cudaStream_t s = st[static_cast<int>(e.stream)];
@@ -520,6 +597,12 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
       for (int k = 1; k < 3; ++k)
         if (last_comm_ev[k] >= 0) HZP_CUDA(cudaStreamWaitEvent(s, done[last_comm_ev[k]], 0));
     }
+    if (e.kind == TaskKind::OptStep) {
+      // cross-stream / cross-rank waits of the optimizer step happen before
+      // its start event: they count as idle (exposed), not as compute
+      if (early_z1 && z1_issued) HZP_CUDA(cudaStreamWaitEvent(s, ev_z1, 0));
+      barrier(s);  // early: every push landed; tail: every rank's RS complete
+    }
     if (cfg.timeline) HZP_CUDA(cudaEventRecord(tev0[e.id], s));
     switch (e.kind) {
       case TaskKind::AgParam:
@@ -527,7 +610,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
           rec_log(e, -1, e.id, e.id);  // identity: layers read the shard in place
         } else {
           if (ag_phys_wait[e.id] >= 0) HZP_CUDA(cudaStreamWaitEvent(s, done[ag_phys_wait[e.id]], 0));
-          ag_layer(e.layer, ag_slot[e.id], s);
+          ag_layer(e.layer, ag_slot[e.id], s, post_ready_early);
           rec_log(e, int(e.stream), e.id, e.id);
         }
         break;
@@ -582,15 +665,14 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
         break;
       }
       case TaskKind::ArDzp:
-        rec_log(e, -1, opt_id, opt_id);  // folded into the fused Z1 kernel
+        // folded into the fused Z1 kernel(s): per layer (async) or the tail
+        rec_log(e, early_z1 ? 2 : -1, early_z1 ? e.id : opt_id, early_z1 ? e.id : opt_id);
         break;
       case TaskKind::OptStep: {
-        barrier(s);  // every rank's RS complete; nobody reads param shards any more
-        z1_adam(s);
-        barrier(s);  // every push landed, every grad pull done
+        if (!early_z1) z1_adam(s);  // the reference's tail order (vanilla)
         int first = e.id, last = e.id;
         for (const auto& x : plan.entries)
-          if (x.kind == TaskKind::ArDzp || x.kind == TaskKind::AgPostStep) {
+          if ((!early_z1 && x.kind == TaskKind::ArDzp) || x.kind == TaskKind::AgPostStep) {
             first = std::min(first, x.id);
             last = std::max(last, x.id);
           }
@@ -605,6 +687,21 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
     }
     if (cfg.timeline) HZP_CUDA(cudaEventRecord(tev1[e.id], s));
     HZP_CUDA(cudaEventRecord(done[e.id], s));
+    if (post_after[e.id])  // this compute task freed AG ring slots
+      launch_flags(dtable, cfg.my_rank, kFlagAgReady, rank_mask(geom.z3_base(cfg.my_rank), geom.z3),
+                   post_after[e.id], 0, 0, 0, s);
+    if (e.kind == TaskKind::OptStep && !early_z1) barrier(s);  // every push landed, every grad pull done
+    if (final_of[e.id] >= 0) {  // this task made a layer's gradient final: its Z1 now
+      cudaStream_t zs = opt_stream;  // its own stream: later RSs never queue behind it
+      HZP_CUDA(cudaStreamWaitEvent(zs, done[e.id], 0));
+      if (!adam_ready) {
+        adam = next_adam_args();
+        adam_ready = true;
+      }
+      z1_layer(final_of[e.id], adam, zs);
+      HZP_CUDA(cudaEventRecord(ev_z1, zs));
+      ++z1_issued;
+    }
     if (e.stream != StreamId::Compute) last_comm_ev[static_cast<int>(e.stream)] = e.id;
     if (debug_sync) {  // HZP_DEBUG_SYNC=1: serialise every task across all ranks
       HZP_CUDA(cudaDeviceSynchronize());

@@ -70,6 +70,7 @@ struct Engine {
   std::vector<int> ag_phys_wait;  // AG task -> extra wait (last reader of the slot's occupant)
 
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t opt_stream = nullptr;  // per-layer Z1 kernels (async mode)
   std::vector<cudaEvent_t> done;
   std::vector<cudaEvent_t> tev0, tev1;
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr, ev_opt = nullptr;
@@ -83,6 +84,9 @@ struct Engine {
   std::vector<int> ag_off, rs_off;  // [L + 1] per layer tile ranges
   std::vector<uint64_t> ag_owners;  // [L] Z3 members owning part of layer l (multi-process)
   int z1_off = 0, z1_n = 0;
+  std::vector<int> z1_layer_off;       // [L + 1] Z1 tiles per layer
+  std::vector<uint64_t> z1_wait_mask;  // [L] ranks whose GradReady(l) this rank's Z1(l) needs
+  cudaEvent_t ev_z1 = nullptr;         // last per-layer Z1 of the step (async mode)
   ArenaLayout lay;
   McGroup ag_mc, wg_mc;  // NVLS objects of this rank's Z3 / Z2 group (multi-process)
   // AG / RS launch one short-lived 128-thread CTA per tile (<= 64 KB, ~10 us):
@@ -95,7 +99,7 @@ struct Engine {
   size_t input_bytes_per_mb = 0;
   float* hloss = nullptr;  // pinned [nlocal]
 
-  uint64_t rs_seq = 0, ag_seq = 0, barrier_epoch = 0;
+  uint64_t rs_seq = 0, ag_seq = 0, grad_seq = 0, barrier_epoch = 0;
   std::vector<hzp_launch_rec> log;
   int64_t launches = 0;
   bool peers_open = false;
@@ -110,9 +114,15 @@ struct Engine {
   ShareRecord share_record() const;
   void open_peers(const ShareRecord* records, int n);
   void step(const void* inputs, bool on_device, float* losses_out);
-  void ag_layer(int layer, int slot, cudaStream_t s);
+  // ready_posted: the step posted this AG's "slot free" from the compute
+  // stream already (at the task that released the slot); else post it here
+  void ag_layer(int layer, int slot, cudaStream_t s, bool ready_posted = false);
   void rs_layer(int layer, int wslot, bool assign, uint64_t seq, cudaStream_t s);
-  void z1_adam(cudaStream_t s);
+  void z1_adam(cudaStream_t s);  // every layer at once (test entry / vanilla mode)
+  AdamArgs next_adam_args();     // advances the Adam step of every driven rank
+  // Z1 of one layer as soon as its gradient is final everywhere it is read
+  // from and its parameters are no longer read anywhere this step
+  void z1_layer(int layer, const AdamArgs& a, cudaStream_t s);
   void barrier(cudaStream_t s);
   GradTarget grad_target(int li, int layer, int wslot, int mb) const;
   const void* layer_params(int li, int layer, int slot) const;

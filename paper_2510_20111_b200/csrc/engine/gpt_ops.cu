@@ -639,6 +639,83 @@ __global__ void __launch_bounds__(256) colsum_finalize4_kernel(const float* __re
 
 }  // namespace
 
+namespace {
+
+// SwiGLU: one thread per 8 columns (16-byte loads of gate, up, dact);
+// silu(x) = x * sigmoid(x), silu'(x) = sigmoid(x) * (1 + x * (1 - sigmoid(x))).
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  return uint32_t(f32_to_bf16_bits(a)) | (uint32_t(f32_to_bf16_bits(b)) << 16);
+}
+
+__global__ void __launch_bounds__(256) swiglu_fwd_kernel(const uint16_t* __restrict__ pre, uint16_t* __restrict__ act,
+                                                         int64_t rows, int f) {
+  const int vec = f / 8;
+  const int64_t n = rows * vec;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / vec;
+    const int c = int(i - r * vec) * 8;
+    const uint4 g = *reinterpret_cast<const uint4*>(pre + r * 2 * f + c);
+    const uint4 u = *reinterpret_cast<const uint4*>(pre + r * 2 * f + f + c);
+    const uint32_t gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float g0 = bf_lo(gv[k]), g1 = bf_hi(gv[k]);
+      o[k] = pack_bf2(g0 * sigmoid_f(g0) * bf_lo(uv[k]), g1 * sigmoid_f(g1) * bf_hi(uv[k]));
+    }
+    *reinterpret_cast<uint4*>(act + r * f + c) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) swiglu_bwd_kernel(const uint16_t* __restrict__ pre,
+                                                         const uint16_t* __restrict__ dact,
+                                                         uint16_t* __restrict__ dpre, int64_t rows, int f) {
+  const int vec = f / 8;
+  const int64_t n = rows * vec;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / vec;
+    const int c = int(i - r * vec) * 8;
+    const uint4 g = *reinterpret_cast<const uint4*>(pre + r * 2 * f + c);
+    const uint4 u = *reinterpret_cast<const uint4*>(pre + r * 2 * f + f + c);
+    const uint4 d = *reinterpret_cast<const uint4*>(dact + r * f + c);
+    const uint32_t gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w}, dv[4] = {d.x, d.y, d.z, d.w};
+    uint32_t og[4], ou[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float gg[2] = {bf_lo(gv[k]), bf_hi(gv[k])}, uu[2] = {bf_lo(uv[k]), bf_hi(uv[k])},
+                  dd[2] = {bf_lo(dv[k]), bf_hi(dv[k])};
+      float rg[2], ru[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float sg = sigmoid_f(gg[j]);
+        ru[j] = dd[j] * gg[j] * sg;                                 // d up   = dact * silu(gate)
+        rg[j] = dd[j] * uu[j] * sg * (1.0f + gg[j] * (1.0f - sg));  // d gate = dact * up * silu'(gate)
+      }
+      og[k] = pack_bf2(rg[0], rg[1]);
+      ou[k] = pack_bf2(ru[0], ru[1]);
+    }
+    *reinterpret_cast<uint4*>(dpre + r * 2 * f + c) = make_uint4(og[0], og[1], og[2], og[3]);
+    *reinterpret_cast<uint4*>(dpre + r * 2 * f + f + c) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+  }
+}
+
+}  // namespace
+
+void swiglu_fwd(const uint16_t* pre, uint16_t* act, int64_t rows, int f, cudaStream_t s) {
+  if (f % 8) throw std::invalid_argument("swiglu: f % 8 != 0");
+  swiglu_fwd_kernel<<<8 * kNumSMs, 256, 0, s>>>(pre, act, rows, f);
+  HZP_LAUNCH_CHECK();
+}
+
+void swiglu_bwd(const uint16_t* pre, const uint16_t* dact, uint16_t* dpre, int64_t rows, int f, cudaStream_t s) {
+  if (f % 8) throw std::invalid_argument("swiglu: f % 8 != 0");
+  swiglu_bwd_kernel<<<8 * kNumSMs, 256, 0, s>>>(pre, dact, dpre, rows, f);
+  HZP_LAUNCH_CHECK();
+}
+
 void embed_fwd(const int* tokens, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int b, int S,
                int h, cudaStream_t s) {
   embed_fwd_kernel<<<b * S, kT, 0, s>>>(tokens, wte, wpe, x, S, h);

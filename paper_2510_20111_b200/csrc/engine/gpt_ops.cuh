@@ -50,4 +50,11 @@ void attn_rowdot(const uint16_t* dO, const uint16_t* O, const float* lse, float*
 void cross_entropy(uint16_t* logits, const int* tokens, int b, int S, int V, float* row_loss, float* loss,
                    cudaStream_t s);
 
+// SwiGLU feed-forward activation over rows of the fc1 output pre [rows, 2f]
+// (gate = columns [0, f), up = [f, 2f)):  act[r, j] = silu(gate) * up, bf16.
+void swiglu_fwd(const uint16_t* pre, uint16_t* act, int64_t rows, int f, cudaStream_t s);
+// Its backward from dact [rows, f]: dpre[r, j] = dact * up * silu'(gate),
+// dpre[r, f + j] = dact * silu(gate).
+void swiglu_bwd(const uint16_t* pre, const uint16_t* dact, uint16_t* dpre, int64_t rows, int f, cudaStream_t s);
+
 }  // namespace hzp

@@ -63,6 +63,7 @@ struct ModelConfig {
   int batch = 1;       // MLP rows / GPT sequences per microbatch
   int layers = 0, hidden = 0, heads = 0, ffn = 0, vocab = 0, seq = 0;
   int experts = 0, topk = 2, capacity = 0;  // GPT MoE feed-forward (experts = 0: dense)
+  int swiglu = 0;      // GPT: SwiGLU feed-forward (fc1 [2f, h] gate | up, fc2 [h, f], no FFN biases)
   int recompute = 0;   // GPT: keep only block inputs; blocks share one activation set
 };
 

@@ -6,9 +6,12 @@
 //                  ln1_g ln1_b [h] | w_qkv [3h, h] | b_qkv [3h] | w_o [h, h] | b_o [h] |
 //                  ln2_g ln2_b [h] | w_fc1 [f, h] | b_fc1 [f] | w_fc2 [h, f] | b_fc2 [h]
 //   layer L+1      head: lnf_g lnf_b [h] | w_head [V, h]  (untied)
+// SwiGLU variant (BASELINE configs[2] / [3] dims): the FFN is
+//                  w_fc1 [2f, h] (rows [0, f) gate, [f, 2f) up) | w_fc2 [h, f], no biases;
+//                  act = silu(gate) * up.
 // MoE variant (experts E > 0, BASELINE configs[3]): the FFN part of a block is
 //                  ln2_g ln2_b [h] | w_router [E, h] | E x (w_fc1 [f, h] | b_fc1 [f] |
-//                  w_fc2 [h, f] | b_fc2 [h])
+//                  w_fc2 [h, f] | b_fc2 [h])     (SwiGLU: E x (w_fc1 [2f, h] | w_fc2 [h, f]))
 // with top-K routing (renormalised gates), capacity-bounded deterministic
 // dispatch (moe_ops.cuh) and the E expert products as single batched
 // tcgen05 GEMMs over [E, C] slots (per-expert weights via the batch stride).
@@ -56,6 +59,7 @@ struct GptBuffers {
   uint16_t* dx[2] = {nullptr, nullptr};
   int cur = 0;
   uint16_t *dln = nullptr, *dqkv = nullptr, *dattn = nullptr, *dfc1 = nullptr, *dxm = nullptr;
+  uint16_t* dact = nullptr;  // SwiGLU: grad of the activation [T, f] (dfc1 is [T, 2f])
   float* part = nullptr;       // column-sum partials
   // weight gradients of a block run on a side stream (they are leaves of the
   // backward DAG), so they fill the SMs the dgrad chain's tail waves leave
@@ -65,6 +69,7 @@ struct GptBuffers {
   float* part_side = nullptr;
   // MoE backward scratch
   uint16_t *moe_dy = nullptr, *moe_dh = nullptr, *moe_dxp = nullptr, *moe_dlogits = nullptr;
+  uint16_t* moe_dact = nullptr;  // SwiGLU experts: [E*C, f]
   float* moe_dgate = nullptr;
   float* emb = nullptr;        // fp32 scratch for the embedding gradient [V*h + S*h]
   void* emb_ws = nullptr;      // embed_bwd's sort workspace
@@ -89,6 +94,8 @@ class GptModel final : public Model {
     L_ = c.layers;
     E_ = c.experts;
     K_ = c.topk > 0 ? c.topk : 2;
+    sw_ = c.swiglu != 0;
+    f1_ = sw_ ? 2 * f_ : f_;  // fc1 output width
     if (E_ > 0) {
       if (E_ > 64 || K_ > 4 || K_ > E_ || E_ % 8) throw std::invalid_argument("MoE: experts % 8 == 0, <= 64, topk <= 4");
       const int64_t autoc = (int64_t(K_) * T_ * 5 / 4 + E_ - 1) / E_;
@@ -113,10 +120,10 @@ class GptModel final : public Model {
     bo_.ln2_b = take(h_);
     if (E_ > 0) bo_.w_router = take(int64_t(E_) * h_);
     const int64_t ex0 = o;
-    bo_.w_fc1 = take(int64_t(f_) * h_);
-    bo_.b_fc1 = take(f_);
+    bo_.w_fc1 = take(int64_t(f1_) * h_);
+    bo_.b_fc1 = sw_ ? -1 : take(f_);
     bo_.w_fc2 = take(int64_t(h_) * f_);
-    bo_.b_fc2 = take(h_);
+    bo_.b_fc2 = sw_ ? -1 : take(h_);
     if (E_ > 0) {
       bo_.ex_stride = o - ex0;
       o = ex0 + int64_t(E_) * bo_.ex_stride;
@@ -144,11 +151,12 @@ class GptModel final : public Model {
     // 6 * dense params * tokens + causal attention (QK^T and PV, fwd + bwd = 3x):
     // 3 * 2 * 2 * S^2/2 * h * b * L
     // MoE: the active parameters per token (K experts + router)
-    const double ffn = E_ > 0 ? double(K_) * 2.0 * h_ * f_ + double(E_) * h_ : 2.0 * h_ * f_;
+    const double per_ex = (sw_ ? 3.0 : 2.0) * h_ * f_;
+    const double ffn = E_ > 0 ? double(K_) * per_ex + double(E_) * h_ : per_ex;
     const double dense = double(L_) * (4.0 * h_ * h_ + ffn) + double(V_) * h_;
     return 6.0 * dense * double(T_) + 6.0 * double(S_) * S_ * h_ * b_ * L_;
   }
-  int64_t launches_per_fwd() const override { return 9; }
+  int64_t launches_per_fwd() const override { return 9 + (sw_ ? 1 : 0); }
 
   void* alloc_rank_buffers() override {
     auto* B = new GptBuffers();
@@ -183,7 +191,7 @@ class GptModel final : public Model {
       a.xm = bf(T_ * h_);
       a.ln2 = bf(T_ * h_);
       const int64_t frows = E_ > 0 ? int64_t(E_) * C_ : T_;
-      a.fpre = bf(frows * f_);
+      a.fpre = bf(frows * f1_);
       a.fact = bf(frows * f_);
       if (E_ > 0) {
         a.logits = f32(T_ * E_);
@@ -215,10 +223,12 @@ class GptModel final : public Model {
     B->dln = bf(T_ * h_);
     B->dqkv = bf(T_ * 3 * h_);
     B->dattn = bf(T_ * h_);
-    B->dfc1 = bf(T_ * f_);
+    B->dfc1 = bf(T_ * f1_);
+    if (sw_) B->dact = bf(T_ * f_);
     if (E_ > 0) {
       B->moe_dy = bf(int64_t(E_) * C_ * h_);
-      B->moe_dh = bf(int64_t(E_) * C_ * f_);
+      B->moe_dh = bf(int64_t(E_) * C_ * f1_);
+      if (sw_) B->moe_dact = bf(int64_t(E_) * C_ * f_);
       B->moe_dxp = bf(int64_t(E_) * C_ * h_);
       B->moe_dlogits = bf(T_ * E_);
       B->moe_dgate = f32(T_ * K_);
@@ -348,7 +358,13 @@ class GptModel final : public Model {
     moe_route(a.logits, int(T_), E_, K_, a.probs, a.sel, a.gate, s);
     moe_dispatch(a.sel, int(T_), E_, K_, C_, a.pos, a.slot_tok, a.slot_k, s);
     moe_gather(a.ln2, a.slot_tok, int(EC), h_, a.xp, s);
-    {  // H_e = GELU(Xp_e W1_e^T + b1_e)  (pre-activation kept for the backward)
+    if (sw_) {  // H_e = silu(Xp_e Wg_e^T) * (Xp_e Wu_e^T)  (fc1 output kept for the backward)
+      GemmShape sh = expert_shape(C_, f1_, h_, h_, h_, 0, 0, int64_t(C_) * h_, o.ex_stride, int64_t(C_) * f1_);
+      Epilogue e;
+      e.ldc = f1_;
+      gemm_tc_bf16(a.xp, W + o.w_fc1, a.fpre, sh, e, s);
+      swiglu_fwd(a.fpre, a.fact, EC, f_, s);
+    } else {  // H_e = GELU(Xp_e W1_e^T + b1_e)  (pre-activation kept for the backward)
       GemmShape sh = expert_shape(C_, f_, h_, h_, h_, 0, 0, int64_t(C_) * h_, o.ex_stride, int64_t(C_) * f_);
       Epilogue e;
       e.bias_any = W + o.b_fc1;
@@ -359,11 +375,13 @@ class GptModel final : public Model {
       e.ldc = f_;
       gemm_tc_bf16(a.xp, W + o.w_fc1, a.fact, sh, e, s);
     }
-    {  // Y_e = H_e W2_e^T + b2_e
+    {  // Y_e = H_e W2_e^T (+ b2_e)
       GemmShape sh = expert_shape(C_, h_, f_, f_, f_, 0, 0, int64_t(C_) * f_, o.ex_stride, int64_t(C_) * h_);
       Epilogue e;
-      e.bias_any = W + o.b_fc2;
-      e.bias_sh = o.ex_stride;
+      if (!sw_) {
+        e.bias_any = W + o.b_fc2;
+        e.bias_sh = o.ex_stride;
+      }
       e.ldc = h_;
       gemm_tc_bf16(a.fact, W + o.w_fc2, a.y, sh, e, s);
     }
@@ -387,12 +405,18 @@ class GptModel final : public Model {
       e.out_bf16 = g.bf16;
       e.ldc = f_;
       gemm_tc_bf16(B->moe_dy, a.fact, gptr(g, o.w_fc2), sh, e, ws);
-      for (int x = 0; x < E_; ++x) {
+      for (int x = 0; x < E_ && !sw_; ++x) {
         colsum_partial(B->moe_dy + int64_t(x) * C_ * h_, C_, h_, B->part_side, kChunks, ws);
         colsum_finalize(B->part_side, kChunks, h_, gptr(g, o.b_fc2 + x * o.ex_stride), g.bf16, g.mode, ws);
       }
     }
-    {  // dH_e = GELU'(pre) * (dY_e W2_e)
+    if (sw_) {  // dH_e = SwiGLU'(fc1 out) applied to dY_e W2_e
+      GemmShape sh = expert_shape(C_, f_, h_, h_, f_, 0, 1, int64_t(C_) * h_, o.ex_stride, int64_t(C_) * f_);
+      Epilogue e;
+      e.ldc = f_;
+      gemm_tc_bf16(B->moe_dy, W + o.w_fc2, B->moe_dact, sh, e, s);
+      swiglu_bwd(a.fpre, B->moe_dact, B->moe_dh, EC, f_, s);
+    } else {  // dH_e = GELU'(pre) * (dY_e W2_e)
       GemmShape sh = expert_shape(C_, f_, h_, h_, f_, 0, 1, int64_t(C_) * h_, o.ex_stride, int64_t(C_) * f_);
       Epilogue e;
       e.act = kActGeluGrad;
@@ -402,20 +426,20 @@ class GptModel final : public Model {
       gemm_tc_bf16(B->moe_dy, W + o.w_fc2, B->moe_dh, sh, e, s);
     }
     to_side();
-    {  // dW1_e [f, h] = dH_e^T Xp_e ; db1_e = colsum dH_e
-      GemmShape sh = expert_shape(f_, h_, C_, f_, h_, 1, 1, int64_t(C_) * f_, int64_t(C_) * h_, o.ex_stride);
+    {  // dW1_e [f1, h] = dH_e^T Xp_e ; db1_e = colsum dH_e
+      GemmShape sh = expert_shape(f1_, h_, C_, f1_, h_, 1, 1, int64_t(C_) * f1_, int64_t(C_) * h_, o.ex_stride);
       Epilogue e;
       e.mode = g.mode;
       e.out_bf16 = g.bf16;
       e.ldc = h_;
       gemm_tc_bf16(B->moe_dh, a.xp, gptr(g, o.w_fc1), sh, e, ws);
-      for (int x = 0; x < E_; ++x) {
+      for (int x = 0; x < E_ && !sw_; ++x) {
         colsum_partial(B->moe_dh + int64_t(x) * C_ * f_, C_, f_, B->part_side, kChunks, ws);
         colsum_finalize(B->part_side, kChunks, f_, gptr(g, o.b_fc1 + x * o.ex_stride), g.bf16, g.mode, ws);
       }
     }
     {  // dXp_e = dH_e W1_e
-      GemmShape sh = expert_shape(C_, h_, f_, f_, h_, 0, 1, int64_t(C_) * f_, o.ex_stride, int64_t(C_) * h_);
+      GemmShape sh = expert_shape(C_, h_, f1_, f1_, h_, 0, 1, int64_t(C_) * f1_, o.ex_stride, int64_t(C_) * h_);
       Epilogue e;
       e.ldc = h_;
       gemm_tc_bf16(B->moe_dh, W + o.w_fc1, B->moe_dxp, sh, e, s);
@@ -496,7 +520,10 @@ class GptModel final : public Model {
       moe_fwd(a, W, B->x[l + 1], s);  // recompute rewrites x[l+1] with identical values
       return;
     }
-    {
+    if (sw_) {
+      linear_fwd(a.ln2, W + o.w_fc1, a.fpre, f1_, h_, Epilogue{}, s);
+      swiglu_fwd(a.fpre, a.fact, T_, f_, s);
+    } else {
       Epilogue e;
       e.bias_any = W + o.b_fc1;
       e.act = kActGelu;
@@ -506,7 +533,7 @@ class GptModel final : public Model {
     }
     if (need_out) {
       Epilogue e;
-      e.bias_any = W + o.b_fc2;
+      if (!sw_) e.bias_any = W + o.b_fc2;
       e.resid = a.xm;
       e.ldres = h_;
       linear_fwd(a.fact, W + o.w_fc2, B->x[l + 1], h_, f_, e, s);
@@ -560,7 +587,10 @@ class GptModel final : public Model {
     // MLP
     to_side();
     linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, o.b_fc2, B, ws);
-    {
+    if (sw_) {
+      linear_dgrad(dout, W + o.w_fc2, B->dact, h_, f_, Epilogue{}, s);
+      swiglu_bwd(a.fpre, B->dact, B->dfc1, T_, f_, s);
+    } else {
       Epilogue e;
       e.act = kActGeluGrad;
       e.aux = a.fpre;
@@ -568,10 +598,10 @@ class GptModel final : public Model {
       linear_dgrad(dout, W + o.w_fc2, B->dfc1, h_, f_, e, s);
     }
     to_side();
-    linear_wgrad(B->dfc1, a.ln2, f_, h_, g, o.w_fc1, o.b_fc1, B, ws);
+    linear_wgrad(B->dfc1, a.ln2, f1_, h_, g, o.w_fc1, o.b_fc1, B, ws);
     {
       Epilogue e;
-      linear_dgrad(B->dfc1, W + o.w_fc1, B->dln, f_, h_, e, s);
+      linear_dgrad(B->dfc1, W + o.w_fc1, B->dln, f1_, h_, e, s);
     }
     layernorm_bwd(B->dln, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_),
                   h_, s);
@@ -614,6 +644,8 @@ class GptModel final : public Model {
   ModelConfig c_;
   int h_, nh_, hd_, f_, V_, S_, b_, L_;
   int E_ = 0, K_ = 2, C_ = 0;  // MoE experts, top-k, slots per expert (E_ = 0: dense FFN)
+  bool sw_ = false;            // SwiGLU feed-forward
+  int f1_ = 0;                 // fc1 output width (2f for SwiGLU)
   int64_t T_;
   BlockOff bo_;
   std::vector<LayerRange> ranges_;

@@ -109,37 +109,44 @@ TileTables build_comm_tiles(const ShardGeom& g, const std::vector<Range64>& laye
     }
   }
   T.rs_off[L] = static_cast<int>(tiles.size());
-  // Z1: each driven rank's chunk ∩ [0, P), cut at Z2 and Z3 segment bounds.
+  // Z1: each driven rank's chunk ∩ [0, P), cut at Z2 and Z3 segment bounds
+  // and at layer bounds; grouped by layer (z1_layer_off) so the optimizer
+  // step of a layer can run as soon as that layer's gradient is final.
   T.z1_off = static_cast<int>(tiles.size());
-  for (size_t li = 0; li < local_ranks.size(); ++li) {
-    const int r = local_ranks[li];
-    const int i1 = r % g.z1;
-    int64_t e = i1 * g.s1;
-    const int64_t end = std::min(int64_t(i1 + 1) * g.s1, g.P);
-    while (e < end) {
-      const int j2 = static_cast<int>(e / g.s2), j3 = static_cast<int>(e / g.s3);
-      const int64_t stop = std::min({end, (j2 + 1) * g.s2, (j3 + 1) * g.s3});
-      const int64_t offs[3] = {e - i1 * g.s1, e - j2 * g.s2, e - j3 * g.s3};
-      // master/m/v and grads are fp32 (16-byte float4); the param stream is
-      // stored 4 elements at a time (float4 or 4 x bf16 = 8 bytes), so all
-      // three need offset % 4 == 0: model that as 4-byte elements.
-      const int eb[3] = {4, 4, 4};
-      const uint64_t mask = z1_targets(g, r, j3);
-      split_run(offs, eb, 3, stop - e, 4, [&](int64_t p, int64_t n, bool v) {
-        CommTile t{};
-        t.a_off = offs[0] + p;
-        t.b_off = offs[1] + p;
-        t.c_off = offs[2] + p;
-        t.mask = mask;
-        t.len = static_cast<int32_t>(n);
-        t.local = static_cast<int16_t>(li);
-        t.src = static_cast<int16_t>(j2);
-        t.vec = v;
-        tiles.push_back(t);
-      });
-      e = stop;
+  T.z1_layer_off.assign(L + 1, T.z1_off);
+  for (int l = 0; l < L; ++l) {
+    T.z1_layer_off[l] = static_cast<int>(tiles.size());
+    for (size_t li = 0; li < local_ranks.size(); ++li) {
+      const int r = local_ranks[li];
+      const int i1 = r % g.z1;
+      int64_t e = std::max(int64_t(i1) * g.s1, layers[l].off);
+      const int64_t end = std::min({int64_t(i1 + 1) * g.s1, g.P, layers[l].off + layers[l].size});
+      while (e < end) {
+        const int j2 = static_cast<int>(e / g.s2), j3 = static_cast<int>(e / g.s3);
+        const int64_t stop = std::min({end, (j2 + 1) * g.s2, (j3 + 1) * g.s3});
+        const int64_t offs[3] = {e - i1 * g.s1, e - j2 * g.s2, e - j3 * g.s3};
+        // master/m/v and grads are fp32 (16-byte float4); the param stream is
+        // stored 4 elements at a time (float4 or 4 x bf16 = 8 bytes), so all
+        // three need offset % 4 == 0: model that as 4-byte elements.
+        const int eb[3] = {4, 4, 4};
+        const uint64_t mask = z1_targets(g, r, j3);
+        split_run(offs, eb, 3, stop - e, 4, [&](int64_t p, int64_t n, bool v) {
+          CommTile t{};
+          t.a_off = offs[0] + p;
+          t.b_off = offs[1] + p;
+          t.c_off = offs[2] + p;
+          t.mask = mask;
+          t.len = static_cast<int32_t>(n);
+          t.local = static_cast<int16_t>(li);
+          t.src = static_cast<int16_t>(j2);
+          t.vec = v;
+          tiles.push_back(t);
+        });
+        e = stop;
+      }
     }
   }
+  T.z1_layer_off[L] = static_cast<int>(tiles.size());
   T.z1_n = static_cast<int>(tiles.size()) - T.z1_off;
   return T;
 }

@@ -30,6 +30,7 @@ struct TileTables {
   std::vector<int> ag_off;  // [L + 1]
   std::vector<int> rs_off;  // [L + 1]
   int z1_off = 0, z1_n = 0;
+  std::vector<int> z1_layer_off;  // [L + 1]: Z1 tiles of layer l (every driven rank)
 };
 
 struct Range64 {

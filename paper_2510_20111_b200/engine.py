@@ -53,6 +53,7 @@ class EngineConfig:
     gpt_capacity: int = 0      # slots per expert per microbatch (0 = auto)
     reuse: int = 0             # CLI parameter reuse (R3 side cache for later forwards)
     recompute: int = 0         # activation recomputation (FWD-recompute before each BWD)
+    gpt_swiglu: int = 0        # GPT: SwiGLU feed-forward (dense blocks and MoE experts)
 
     def c(self) -> N.hzp_engine_config:
         c = N.hzp_engine_config()
@@ -71,6 +72,7 @@ class EngineConfig:
         c.gpt_experts, c.gpt_topk, c.gpt_capacity = self.gpt_experts, self.gpt_topk, self.gpt_capacity
         c.reuse = self.reuse
         c.recompute = self.recompute
+        c.gpt_swiglu = self.gpt_swiglu
         return c
 
 
@@ -198,6 +200,12 @@ class HzpEngine:
             self.upload(r, F_VAR, z["var"])
             self.set_step(r, int(z["adam_step"]))
 
+    def init_seeded(self, seed: int = 2024, scale: float = 1.0) -> None:
+        """shard_init (train.cpp:224-253) on the device: master / working copy
+        = seeded_uniform(P, seed) * scale, sharded (scale 1: bitwise the
+        reference's)."""
+        N.check(N.lib.hzp_state_init_seeded(self._h, seed, scale))
+
     def init_random(self, seed: int = 1234, scale: float = 0.04) -> None:
         N.check(N.lib.hzp_state_init_random(self._h, seed, scale))
 
@@ -302,6 +310,19 @@ class HzpEngine:
 
     def barrier(self) -> None:
         N.check(N.lib.hzp_barrier(self._h))
+
+
+def seeded_span(seed: int, P: int, first: int, n: int, scale: float = 1.0) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    N.check(N.lib.hzp_seeded_span(seed, P, first, n, scale, out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
+def make_tokens(seed: int, step: int, rank: int, mb: int, n: int, vocab: int) -> np.ndarray:
+    """run_case's per-(step, rank, microbatch) token stream (train.cpp:506-507)."""
+    out = np.empty(n, np.int32)
+    N.check(N.lib.hzp_make_tokens(seed, step, rank, mb, n, vocab, out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
 
 
 def kernel_launches() -> int:

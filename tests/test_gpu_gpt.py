@@ -20,11 +20,18 @@ CFG_WIDE = dict(layers=1, hidden=2048, heads=16, ffn=8192, vocab=1024, seq=512, 
 CFG_BENCH = dict(layers=1, hidden=2048, heads=16, ffn=8192, vocab=50304, seq=2048, batch=4)
 
 
+# SwiGLU FFN (BASELINE configs[2] / [3]): fc1 [2f, h] = gate | up, no FFN biases
+CFG_SWIGLU = dict(layers=2, hidden=256, heads=2, ffn=704, vocab=512, seq=256, batch=2, swiglu=1)
+
+
 def layout(c):
     h, f, V, S, L = c["hidden"], c["ffn"], c["vocab"], c["seq"], c["layers"]
     blk = [("ln1_g", (h,)), ("ln1_b", (h,)), ("w_qkv", (3 * h, h)), ("b_qkv", (3 * h,)),
-           ("w_o", (h, h)), ("b_o", (h,)), ("ln2_g", (h,)), ("ln2_b", (h,)), ("w_fc1", (f, h)),
-           ("b_fc1", (f,)), ("w_fc2", (h, f)), ("b_fc2", (h,))]
+           ("w_o", (h, h)), ("b_o", (h,)), ("ln2_g", (h,)), ("ln2_b", (h,))]
+    if c.get("swiglu"):
+        blk += [("w_fc1", (2 * f, h)), ("w_fc2", (h, f))]
+    else:
+        blk += [("w_fc1", (f, h)), ("b_fc1", (f,)), ("w_fc2", (h, f)), ("b_fc2", (h,))]
     names, off = [], 0
     for n, shp in [("wte", (V, h)), ("wpe", (S, h))]:
         names.append((n, shp, off))
@@ -74,7 +81,11 @@ def torch_loss(c, flat, tokens):
         o = (att @ v).transpose(1, 2).reshape(x.shape[0], S, h)
         x = x + o @ g("w_o").t() + g("b_o")
         a = torch.nn.functional.layer_norm(x, (h,), g("ln2_g"), g("ln2_b"), 1e-5)
-        x = x + gelu(a @ g("w_fc1").t() + g("b_fc1")) @ g("w_fc2").t() + g("b_fc2")
+        if c.get("swiglu"):
+            gate, up = (a @ g("w_fc1").t()).split(c["ffn"], dim=-1)
+            x = x + (torch.nn.functional.silu(gate) * up) @ g("w_fc2").t()
+        else:
+            x = x + gelu(a @ g("w_fc1").t() + g("b_fc1")) @ g("w_fc2").t() + g("b_fc2")
     a = torch.nn.functional.layer_norm(x, (h,), P["lnf_g"], P["lnf_b"], 1e-5)
     logits = a @ P["w_head"].t()
     return torch.nn.functional.cross_entropy(logits.reshape(-1, logits.shape[-1]), tgt.reshape(-1))
@@ -85,6 +96,7 @@ def _engine(c, dp=1, z=(1, 1, 1), mbs=1, **kw):
     return HzpEngine(EngineConfig(model=1, precision=1, gpt_layers=c["layers"], gpt_hidden=c["hidden"],
                                   gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
                                   gpt_seq=c["seq"], batch=c["batch"], num_microbatches=mbs,
+                                  gpt_swiglu=c.get("swiglu", 0),
                                   par=ParallelConfig(dp=dp, z1=z[0], z2=z[1], z3=z[2]), **kw))
 
 
@@ -93,7 +105,7 @@ def _bf16_bits(x):
             ((np.ascontiguousarray(x, np.float32).view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("c", [CFG, CFG_WIDE, CFG_BENCH], ids=["small", "wide", "bench"])
+@pytest.mark.parametrize("c", [CFG, CFG_WIDE, CFG_BENCH, CFG_SWIGLU], ids=["small", "wide", "bench", "swiglu"])
 def test_gpt_gradient_matches_torch(gpu, c):
     eng = _engine(c)
     master = init_params(c)

@@ -12,6 +12,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 CFG = dict(layers=1, hidden=256, heads=2, ffn=512, vocab=512, seq=256, batch=2, experts=8, topk=2)
+# SwiGLU experts (BASELINE configs[3]: 16 x SwiGLU): fc1 [2f, h] = gate | up, no biases
+CFG_SWIGLU = dict(CFG, ffn=320, swiglu=1)
 
 
 def layout(c):
@@ -19,7 +21,10 @@ def layout(c):
     blk = [("ln1_g", (h,)), ("ln1_b", (h,)), ("w_qkv", (3 * h, h)), ("b_qkv", (3 * h,)),
            ("w_o", (h, h)), ("b_o", (h,)), ("ln2_g", (h,)), ("ln2_b", (h,)), ("w_router", (E, h))]
     for e in range(E):
-        blk += [(f"e{e}.w_fc1", (f, h)), (f"e{e}.b_fc1", (f,)), (f"e{e}.w_fc2", (h, f)), (f"e{e}.b_fc2", (h,))]
+        if c.get("swiglu"):
+            blk += [(f"e{e}.w_fc1", (2 * f, h)), (f"e{e}.w_fc2", (h, f))]
+        else:
+            blk += [(f"e{e}.w_fc1", (f, h)), (f"e{e}.b_fc1", (f,)), (f"e{e}.w_fc2", (h, f)), (f"e{e}.b_fc2", (h,))]
     names, off = [], 0
     for n, shp in [("wte", (V, h)), ("wpe", (S, h))]:
         names.append((n, shp, off))
@@ -78,8 +83,12 @@ def torch_loss(c, flat, tokens):
             ti, ki = (topi == e).nonzero(as_tuple=True)
             if ti.numel() == 0:
                 continue
-            hh = gelu(a2[ti] @ g(f"e{e}.w_fc1").t() + g(f"e{e}.b_fc1"))
-            y = hh @ g(f"e{e}.w_fc2").t() + g(f"e{e}.b_fc2")
+            if c.get("swiglu"):
+                gate, up = (a2[ti] @ g(f"e{e}.w_fc1").t()).split(c["ffn"], dim=-1)
+                y = (torch.nn.functional.silu(gate) * up) @ g(f"e{e}.w_fc2").t()
+            else:
+                hh = gelu(a2[ti] @ g(f"e{e}.w_fc1").t() + g(f"e{e}.b_fc1"))
+                y = hh @ g(f"e{e}.w_fc2").t() + g(f"e{e}.b_fc2")
             out = out.index_add(0, ti, gates[ti, ki, None] * y)
         x = x + out.view_as(x)
     a = torch.nn.functional.layer_norm(x, (h,), P["lnf_g"], P["lnf_b"], 1e-5)
@@ -92,14 +101,15 @@ def _bf16_bits(x):
     return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
 
 
-def test_moe_gradient_matches_torch(gpu):
+@pytest.mark.parametrize("c", [CFG, CFG_SWIGLU], ids=["gelu", "swiglu"])
+def test_moe_gradient_matches_torch(gpu, c):
     from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
-    c = CFG
     T = c["batch"] * c["seq"]
     eng = HzpEngine(EngineConfig(model=1, precision=1, gpt_layers=c["layers"], gpt_hidden=c["hidden"],
                                  gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
                                  gpt_seq=c["seq"], batch=c["batch"], num_microbatches=1,
                                  gpt_experts=c["experts"], gpt_topk=c["topk"], gpt_capacity=T,
+                                 gpt_swiglu=c.get("swiglu", 0),
                                  par=ParallelConfig()))
     master = init_params(c)
     work = _bf16_bits(master)

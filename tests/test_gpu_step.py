@@ -92,8 +92,15 @@ def test_launch_log_follows_plan(gpu, oracle, mode):
     assert [r[1] for r in log] == [p.kind for p in plan]
     assert [r[5] for r in log] == [p.slot for p in plan]          # ring slots bit-exact
     fused = [r for r in log if r[1] == H.OPT_STEP][0]
-    ids = [p.id for p in plan if p.kind in (H.AR_DZP, H.AG_POST_STEP)]
+    # async: each layer's Z1 (covering AR-dzp(l)) ran on the RS stream right
+    # after the layer's last RS; the OPT record covers OPT + AG-post-step.
+    # vanilla: one Z1 at the tail covers AR-dzp, OPT and AG-post-step.
+    kinds = (H.AG_POST_STEP,) if mode == 1 else (H.AR_DZP, H.AG_POST_STEP)
+    ids = [p.id for p in plan if p.kind in kinds]
     assert (fused[6], fused[7]) == (min(ids + [fused[0]]), max(ids + [fused[0]]))
+    for r in log:
+        if r[1] == H.AR_DZP:
+            assert (r[4], r[6], r[7]) == ((2, r[0], r[0]) if mode == 1 else (-1, fused[0], fused[0]))
     tl = eng.timeline()
     assert tl["makespan_ms"] > 0 and tl["compute_busy_ms"] > 0
     # every task starts after each of its waits ended (device clock)
@@ -140,4 +147,21 @@ def test_reuse_launch_log_follows_reused_plan(gpu, oracle):
     for p in plan:
         for w in p.waits:
             assert tl["start_ms"][p.id] >= tl["end_ms"][w] - 1e-3
+    eng.close()
+
+
+@pytest.mark.parametrize("prec", [0, 1], ids=["fp32", "bf16"])
+def test_device_seeded_init_is_reference_shard_init(gpu, oracle, prec):
+    """hzp_state_init_seeded (scale 1) == the reference's shard_init
+    (train.cpp:224-253) bit for bit, every rank and field."""
+    from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
+    dims, dp, z1, z2, z3 = [64, 128, 72], 8, 8, 4, 2
+    st = oracle.shard_init(dims, dp, z1, z2, z3, 2024, bool(prec))
+    eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=4,
+                                 par=ParallelConfig(dp=dp, z1=z1, z2=z2, z3=z3)))
+    eng.init_seeded(2024, 1.0)
+    for r in range(dp):
+        assert np.array_equal(eng.param_f32(r).view(np.uint32), st.param[r].view(np.uint32)), r
+        assert np.array_equal(eng.download(r, 2).view(np.uint32), st.master[r].view(np.uint32)), r
+        assert not eng.download(r, 3).any() and not eng.download(r, 1).any()
     eng.close()

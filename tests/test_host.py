@@ -236,3 +236,20 @@ def test_pipeline_order_errors():
     cost = hzp.CostModel(ranks_per_node=8)
     with pytest.raises(N.HzpError):  # interleaved needs microbatches % pp == 0
         hzp.build_task_graph(spec, hzp.ParallelConfig(dp=4, z1=4, z2=2, z3=2, pp=2, vpp=2), cost, pipeline=True)
+
+
+def test_seeded_span_and_tokens_follow_the_reference_streams(oracle):
+    """Product-side seeded_uniform (train.cpp:17-27) and run_case token stream
+    (train.cpp:506-507) vs the oracle's restatement, which is pinned to the
+    reference (tests/test_oracle.py)."""
+    import numpy as np
+    from paper_2510_20111_b200.engine import make_tokens, seeded_span
+    ref = oracle.seeded_uniform(5000, 2024, np.float32)
+    assert np.array_equal(seeded_span(2024, 5000, 0, 5000), ref)
+    got = seeded_span(2024, 4321, 1234, 4000, 0.02)
+    assert np.array_equal(got[:4321 - 1234], ref[1234:4321] * np.float32(0.02))
+    assert not got[4321 - 1234:].any()  # the zero padding past P
+    for step, rank, mb in ((0, 0, 0), (3, 5, 1), (9, 2, 3)):
+        u = oracle.seeded_uniform(777, oracle.batch_seed(2024, step, rank, mb), np.float64) + 0.5
+        assert np.array_equal(make_tokens(2024, step, rank, mb, 777, 50304),
+                              np.floor(u * 50304).astype(np.int32))
