@@ -479,6 +479,41 @@ def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, z1=1, z2=1, z3
             "note": "includes the two device-wide barriers around the kernel (no-op at N=1)"}
 
 
+def memory_report(eng, tl, N, z1, z2, z3, nmb, args):
+    """memory_trace (sched.cpp:389-466, the drop-in's bit-exact port) of this
+    step's task graph on the simulated timeline AND on the measured one (the
+    CUDA-event start / end of every task of one recorded step), next to what
+    the device actually reserves for the AG ring / reuse cache and the
+    gradient ring.  peak_grad_buffer_bytes (live unsharded gradients x fp32
+    layer bytes) is the reference's sizing of the gradient ring (SURVEY
+    §7.3-9); the device ring holds wgrad_slots layers in the wire dtype."""
+    from paper_2510_20111_b200 import hzp as H
+    ppl = max(n for _, n in eng.layers)
+    c = MODELS[args.model]
+    # the engine's graph (one task-graph layer per engine layer, pp = 1); the
+    # simulated times use SURVEY App. A-6's B200 cost model
+    spec = H.ModelSpec(num_layers=eng.num_layers, params_per_layer=ppl, seq_len=c["seq"],
+                       micro_batch_size=args.batch, num_microbatches=nmb, flops_per_token_per_layer=2.0 * ppl)
+    cfg = H.ParallelConfig(dp=N, z1=z1, z2=z2, z3=z3)
+    g = H.build_task_graph(spec, cfg, H.CostModel(num_nodes=1, ranks_per_node=N, intra_bw=720e9, inter_bw=720e9,
+                                                  intra_latency=10e-6, device_flops=1e15),
+                           reuse=bool(args.reuse), recompute=bool(args.recompute))
+    led = H.ledger(H.ModelSpec(num_layers=1, params_per_layer=eng.P), cfg)
+    mode = H.VANILLA if args.mode == "vanilla" else H.ASYNC
+    keys = ("peak_bytes", "fragmentation", "peak_grad_buffer_bytes", "peak_memory")
+    sim = H.memory_trace(g, args.depth, 1, mode, led["total_static"])
+    meas = H.memory_trace(g, args.depth, 1, mode, led["total_static"], start=tl["start_ms"], end=tl["end_ms"])
+    slot = ((ppl + 127) // 128) * 128
+    return {"static_ledger_bytes": led["total_static"],
+            "simulated": {k: sim[k] for k in keys}, "measured": {k: meas[k] for k in keys},
+            "measured_live_grad_buffers": meas["peak_grad_buffer_bytes"] // max(1, 4 * ppl),
+            "device_reserved": {"ag_ring_bytes": 0 if z3 == 1 else args.depth * slot * 2,
+                                "grad_ring_bytes": 0 if z2 == 1 else args.wgrad_slots * slot * 2,
+                                "grad_ring_slots": 0 if z2 == 1 else args.wgrad_slots,
+                                "note": "z3 = 1: layers read the shard in place; z2 = 1: RS fused into the "
+                                        "wgrad GEMM (no ring)"}}
+
+
 def simulator_prediction(c, N, z1, z2, z3, nmb, mb, depth):
     """The reference's own simulator (the drop-in's bit-exact simulate) on this
     step's task graph, with SURVEY App. A-6's B200 cost model (720 GB/s
@@ -652,6 +687,7 @@ def run_hzp(args):
                "frac": round(idle / mk, 4) if mk else None,
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}
+    mem = memory_report(eng, tl, N, z1, z2, z3, nmb, args)
     colls = collectives(eng, N, local, max_over_ranks, barrier, z2, z3) if N > 1 else None
     if colls is not None:
         colls["in_step"] = in_step
@@ -685,6 +721,7 @@ def run_hzp(args):
                            "rs_slots": 1, "l2": "activation working set >> 126 MB L2 (no flush needed)"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
                 "roofline": roof, "exposed_comm": exposed, "collectives": colls, "z1_adam": z1r,
+                "memory": mem,
                 "cpu_baseline": ({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
                                  if cb else None),
                 "same_config": same}

@@ -913,8 +913,13 @@ int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const floa
     auto* dq = static_cast<uint16_t*>(dqkv);
     auto* ds = static_cast<uint16_t*>(dsT);
     attn_rowdot(static_cast<const uint16_t*>(dO), static_cast<const uint16_t*>(O), lse, D, b, nh, S, 128, st);
-    attention_bwd_tc(q, static_cast<const uint16_t*>(dO), lse, D, dq, ds, b, nh, S, h, st);
-    attention_dq(q, ds, dq, b, nh, S, h, st);
+    if (ds) {  // legacy: dS^T through HBM + GEMM dQ
+      attention_bwd_tc(q, static_cast<const uint16_t*>(dO), lse, D, dq, ds, b, nh, S, h, st);
+      attention_dq(q, ds, dq, b, nh, S, h, st);
+    } else {   // production: dQ pass recomputing P / dS in TMEM
+      attention_bwd_tc(q, static_cast<const uint16_t*>(dO), lse, D, dq, nullptr, b, nh, S, h, st);
+      attention_dq_tc(q, static_cast<const uint16_t*>(dO), D, dq, b, nh, S, h, st);
+    }
   });
 }
 

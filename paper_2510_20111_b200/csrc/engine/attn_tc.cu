@@ -762,10 +762,12 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
-      uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0 + half * 32);
+      if (p.dsT) {  // legacy dQ path (dQ = dS K as a GEMM over dS^T in HBM)
+        uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0 + half * 32);
 #pragma unroll
-      for (int j4 = 0; j4 < 4; ++j4)
-        dsg[j4] = make_uint4(dsw[4 * j4], dsw[4 * j4 + 1], dsw[4 * j4 + 2], dsw[4 * j4 + 3]);
+        for (int j4 = 0; j4 < 4; ++j4)
+          dsg[j4] = make_uint4(dsw[4 * j4], dsw[4 * j4 + 1], dsw[4 * j4 + 2], dsw[4 * j4 + 3]);
+      }
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
@@ -786,6 +788,223 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
       for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) dkg[c * 4 + i] = pack8f(o + 8 * i);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dQ without dS in HBM: one CTA per (128-query tile, head, sequence), walking
+// the 64-key sub-tiles k < query tile end, the key-tile backward's structure
+// with the roles of queries and keys swapped (rows of every TMEM accumulator
+// are QUERIES):
+//   S   = Q K_a^T          TMEM S[b]  (64 cols)  P  = exp2(S c - lse2_q)
+//   dP  = dO V_a^T         TMEM dP[b] (64 cols)  dS = P (dP - D_q) / sqrt(d)
+//   dQ += dS K_a           TMEM [256,384)        (A = dS from TMEM, K_a as MN-major B)
+// P / dS are recomputed from lse (two extra 128x64x128 products per sub-tile
+// instead of a [b*nh, S, S] dS^T round trip through HBM).  Q / dO stay in
+// smem; K_a / V_a are a 4-deep ring; S / dP double-buffered in TMEM so the
+// products of sub-tile a+1 run while the softmax warps process sub-tile a.
+// Every query row's -lse log2 e and -D / sqrt(d) are two scalars of its
+// thread.  Heaviest query tiles are launched first.
+struct AttnDqParams {
+  CUtensorMap tmQ, tmdO;  // 128-row boxes
+  CUtensorMap tmK, tmV;   // 64-row boxes
+  const float* V;         // [2][z][S]: -rowsum(dO * O) / sqrt(d) | -lse log2(e)
+  int64_t zS;
+  uint16_t* dqkv;         // dQ written into the q third
+  int S, h, nh, nq;
+  float scale_log2, scale;
+};
+
+constexpr int kKTile = kBQ2 * kHd * 2;                 // 16 KB: 64 keys
+constexpr int kKStages = 4;
+constexpr int kDOffQ = 0;                              // 32 KB
+constexpr int kDOffdO = kTileBytes;                    // 32 KB
+constexpr int kDOffK = 2 * kTileBytes;                 // 4 x 16 KB
+constexpr int kDOffV = kDOffK + kKStages * kKTile;     // 4 x 16 KB
+constexpr int kDOffBar = kDOffV + kKStages * kKTile;
+constexpr size_t kDSmem = size_t(kDOffBar) + 256 + 1024;
+static_assert(kDSmem <= 232448, "attention dQ smem budget");
+
+__global__ void __launch_bounds__(kThreadsB, 1) attn_dq_kernel(const __grid_constant__ AttnDqParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kDOffBar);
+  uint64_t* qd_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [kKStages]
+  uint64_t* kv_empty = bar + 5;  // [kKStages]
+  uint64_t* s_full = bar + 9;    // [2]
+  uint64_t* p_full = bar + 11;   // [2]
+  uint64_t* acc_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int qt = p.nq - 1 - int(blockIdx.z);  // heaviest (most key tiles) first
+  const int head = blockIdx.x, seq = blockIdx.y;
+  const int q0 = qt * kBQ;
+  const int nit = (q0 + kBQ) / kBQ2;  // 64-key sub-tiles up to the tile's last query
+  const int z = seq * p.nh + head;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qd_full, 1);
+    for (int i = 0; i < kKStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+    }
+    mbar_init(acc_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S[b] = b*128, dP[b] = b*128 + 64, dQ 256
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qd_full, 2 * kTileBytes);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_4d(smem + kDOffQ + c * 16384, &p.tmQ, qd_full, c * 64, q0, head, seq);
+        tma_load_4d(smem + kDOffdO + c * 16384, &p.tmdO, qd_full, c * 64, q0, head, seq);
+      }
+      for (int a = 0; a < nit; ++a) {
+        const int ks = a % kKStages;
+        const uint32_t kph = (a / kKStages) & 1;
+        mbar_wait(&kv_empty[ks], kph ^ 1);
+        mbar_expect_tx(&kv_full[ks], 2 * kKTile);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_4d(smem + kDOffK + ks * kKTile + c * 8192, &p.tmK, &kv_full[ks], c * 64, a * kBQ2, head, seq);
+          tma_load_4d(smem + kDOffV + ks * kKTile + c * 8192, &p.tmV, &kv_full[ks], c * 64, a * kBQ2, head, seq);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = make_idesc(128, 64, 0, 0);    // Q / dO K-major, K_a / V_a K-major (N = 64 keys)
+      constexpr uint32_t kIdAcc = make_idesc(128, 128, 0, 1); // A = dS from TMEM, K_a MN-major
+      const uint32_t sq = smem_u32(smem + kDOffQ), sdo = smem_u32(smem + kDOffdO);
+      auto accumulate = [&](int i) {
+        const int b = i & 1;
+        const uint32_t ph = (i >> 1) & 1;
+        const int ks = i % kKStages;
+        mbar_wait(&p_full[b], ph);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(smem + kDOffK + ks * kKTile);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 keys (16 per step: 8 packed columns)
+          const uint32_t ac = b * 128 + (kk >> 1) * 32 + (kk & 1) * 8;
+          tc_mma_ts(tmem + 256, tmem + ac, smem_desc(sk + kk * 2048, 8192, 1024), kIdAcc,
+                    (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&kv_empty[ks]);
+      };
+      mbar_wait(qd_full, 0);
+      for (int a = 0; a < nit; ++a) {
+        const int b = a & 1;
+        const int ks = a % kKStages;
+        mbar_wait(&kv_full[ks], (a / kKStages) & 1);
+        tc_fence_after();  // region b is free: accumulate(a-2) read it, issued earlier (in-order MMAs)
+        const uint32_t sk = smem_u32(smem + kDOffK + ks * kKTile);
+        const uint32_t sv = smem_u32(smem + kDOffV + ks * kKTile);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K = 128 head dims
+          const uint32_t oq = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t ok = (kk >> 2) * 8192 + (kk & 3) * 32;
+          tc_mma(tmem + b * 128, smem_desc(sq + oq, 16, 1024), smem_desc(sk + ok, 16, 1024), kIdS, kk > 0);
+          tc_mma(tmem + b * 128 + 64, smem_desc(sdo + oq, 16, 1024), smem_desc(sv + ok, 16, 1024), kIdS,
+                 kk > 0);
+        }
+        tc_commit(&s_full[b]);
+        if (a >= 1) accumulate(a - 1);
+      }
+      accumulate(nit - 1);
+      tc_commit(acc_done);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;     // which 32 of the sub-tile's 64 keys
+    const int row = quarter * 32 + lane;  // query q0 + row
+    const int q = q0 + row;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const float nl = p.V[p.zS + int64_t(z) * p.S + q];  // -lse log2 e
+    const float nd = p.V[int64_t(z) * p.S + q];         // -D / sqrt(d)
+    const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), dsc2 = f2_pack(p.scale, p.scale);
+    const uint64_t nl2 = f2_pack(nl, nl), nd2 = f2_pack(nd, nd);
+    for (int a = 0; a < nit; ++a) {
+      const int b = a & 1;
+      const uint32_t ph = (a >> 1) & 1;
+      mbar_wait(&s_full[b], ph);
+      tc_fence_after();
+      uint32_t rs[32], rd[32];
+      tmem_ld32_nw(tmem + lane_off + b * 128 + half * 32, rs);
+      tmem_ld32_nw(tmem + lane_off + b * 128 + 64 + half * 32, rd);
+      tmem_wait_ld32(rs);
+      tmem_pin32(rd);
+      // keys a*64 + half*32 + c with c > lim lie above the diagonal (masked);
+      // only the last two sub-tiles have any, warp-uniformly known
+      const int lim = q - (a * kBQ2 + half * 32);
+      const bool masked = __any_sync(0xffffffffu, lim < 31);
+      uint32_t dsw[16];
+      auto body = [&](auto mask_tag) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t x = f2_fma(f2_pack(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), sc2, nl2);
+          uint64_t e;
+          if ((i & 3) >= HZP_ATTN_BWD_POLY_FROM) {
+            e = exp2_poly2(x);
+          } else {
+            float a0, a1;
+            f2_unpack(x, a0, a1);
+            e = f2_pack(exp2_fast(a0), exp2_fast(a1));
+          }
+          if (decltype(mask_tag)::value) {
+            float e0, e1;
+            f2_unpack(e, e0, e1);
+            e = f2_pack(2 * i > lim ? 0.f : e0, 2 * i + 1 > lim ? 0.f : e1);
+          }
+          const uint64_t dsv =
+              f2_mul(e, f2_fma(f2_pack(__uint_as_float(rd[2 * i]), __uint_as_float(rd[2 * i + 1])), dsc2, nd2));
+          float d0, d1;
+          f2_unpack(dsv, d0, d1);
+          dsw[i] = bf16x2(d0, d1);
+        }
+      };
+      if (masked) body(std::true_type{});
+      else body(std::false_type{});
+      // dS (bf16 pairs) over the consumed S columns this warp read: the A of dQ += dS K_a
+      tmem_st16_nw(tmem + lane_off + b * 128 + half * 32, dsw);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    const int64_t rowbase = (int64_t(seq) * p.S + q) * (3 * int64_t(p.h)) + int64_t(head) * kHd;
+    uint4* dqg = reinterpret_cast<uint4*>(p.dqkv + rowbase);
+#pragma unroll 1
+    for (int c = half * 2; c < half * 2 + 2; ++c) {  // each half writes 64 of the 128 dims
+      uint32_t r[32];
+      float o[32];
+      tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dqg[c * 4 + i] = pack8f(o + 8 * i);
     }
     tc_fence_before();
   }
@@ -858,6 +1077,34 @@ void attention_fwd_tc(const uint16_t* qkv, uint16_t* O, uint16_t* P, float* lse,
   }
   dim3 grid(nh, b, S / kBQ);
   attn_fwd_kernel<<<grid, kThreads, kSmem, stream>>>(p);
+  HZP_LAUNCH_CHECK();
+}
+
+void attention_dq_tc(const uint16_t* qkv, const uint16_t* dO, const float* D, uint16_t* dqkv, int b, int nh,
+                     int S, int h, cudaStream_t stream) {
+  if (h != nh * kHd || S % kBQ) throw std::invalid_argument("fused attention needs head dim 128, S % 128 == 0");
+  static bool attr = false;
+  if (!attr) {
+    HZP_CUDA(cudaFuncSetAttribute(attn_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDSmem)));
+    attr = true;
+  }
+  AttnDqParams p;
+  const int64_t h3 = 3 * int64_t(h);
+  p.tmQ = make_tma_map_bf16(qkv, kHd, S, h3, 128, nh, b, kHd, int64_t(S) * h3);
+  p.tmdO = make_tma_map_bf16(dO, kHd, S, h, 128, nh, b, kHd, int64_t(S) * h);
+  p.tmK = make_tma_map_bf16(qkv + h, kHd, S, h3, kBQ2, nh, b, kHd, int64_t(S) * h3);
+  p.tmV = make_tma_map_bf16(qkv + 2 * h, kHd, S, h3, kBQ2, nh, b, kHd, int64_t(S) * h3);
+  p.V = D;
+  p.zS = int64_t(b) * nh * S;
+  p.dqkv = dqkv;
+  p.S = S;
+  p.h = h;
+  p.nh = nh;
+  p.nq = S / kBQ;
+  p.scale = 1.f / std::sqrt(float(kHd));
+  p.scale_log2 = 1.4426950408889634f * p.scale;
+  dim3 grid(nh, b, S / kBQ);
+  attn_dq_kernel<<<grid, kThreadsB, kDSmem, stream>>>(p);
   HZP_LAUNCH_CHECK();
 }
 

@@ -99,6 +99,7 @@ __global__ void __maxnreg__(kCommRegs) ag_push_kernel(const RankTable* __restric
                                                       const CommTile* __restrict__ tiles, int ntiles,
                                                       int slot, int64_t slot_elems, int z3, FlagGate gate) {
   gate_wait(T, gate);
+  const uint64_t pol = l2_evict_first_policy();
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
     const char* src = static_cast<const char*>(T->param[t.src]) + t.b_off * kEB;
@@ -114,7 +115,7 @@ __global__ void __maxnreg__(kCommRegs) ag_push_kernel(const RankTable* __restric
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const int64_t j = i + u * kCommThreads;
-          if (j < nv) v[u] = ld_nc_v4(s4 + j);
+          if (j < nv) v[u] = ld_nc_stream_v4(s4 + j, pol);
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -152,6 +153,7 @@ __global__ void __maxnreg__(kCommRegs) rs_reduce_kernel(const RankTable* __restr
   constexpr bool kRound = kBf16Wire && kMode != kRsOrdered;
   const bool do_scale = scale != 1.0f;
   gate_wait(T, gate);
+  const uint64_t pol = l2_evict_first_policy();
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
     float* g = T->grad[T->global_rank[t.local]] + t.a_off;  // local index -> global rank
@@ -181,12 +183,12 @@ __global__ void __maxnreg__(kCommRegs) rs_reduce_kernel(const RankTable* __restr
             hi.z = __fmul_rn(hi.z, scale); hi.w = __fmul_rn(hi.w, scale);
           }
           float4* g4 = reinterpret_cast<float4*>(g) + i * 2;
-          float4 a = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[0];
-          float4 b = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : g4[1];
+          float4 a = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : as_f4(ld_stream_v4(g4, pol));
+          float4 b = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : as_f4(ld_stream_v4(g4 + 1, pol));
           fadd4(a, lo);
           fadd4(b, hi);
-          g4[0] = a;
-          g4[1] = b;
+          st_stream_v4(g4, as_u4(a), pol);
+          st_stream_v4(g4 + 1, as_u4(b), pol);
         }
       }
     } else if (t.vec) {
@@ -292,6 +294,7 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int z2, int replicas,
                                                            AdamArgs a, int dbg) {
+  const uint64_t pol = l2_evict_first_policy();
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
     float* mw = T->master[t.local] + t.a_off;
@@ -310,12 +313,12 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
           const int64_t i = i0 + int64_t(u) * kThreads;
           ok[u] = i < nv;
           if (!ok[u]) continue;
-          g[u] = as_f4(ld_v4(T->grad[t.src] + t.b_off + 4 * i));
+          g[u] = as_f4(ld_stream_v4(T->grad[t.src] + t.b_off + 4 * i, pol));
           for (int b = 1; b < replicas; ++b)
-            fadd4(g[u], as_f4(ld_v4(T->grad[t.src + b * z2] + t.b_off + 4 * i)));
-          m[u] = reinterpret_cast<const float4*>(mm)[i];
-          v[u] = reinterpret_cast<const float4*>(mv)[i];
-          w[u] = reinterpret_cast<const float4*>(mw)[i];
+            fadd4(g[u], as_f4(ld_stream_v4(T->grad[t.src + b * z2] + t.b_off + 4 * i, pol)));
+          m[u] = as_f4(ld_stream_v4(mm + 4 * i, pol));
+          v[u] = as_f4(ld_stream_v4(mv + 4 * i, pol));
+          w[u] = as_f4(ld_stream_v4(mw + 4 * i, pol));
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -326,9 +329,9 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
           adam_one(g[u].y, m[u].y, v[u].y, w[u].y, a);
           adam_one(g[u].z, m[u].z, v[u].z, w[u].z, a);
           adam_one(g[u].w, m[u].w, v[u].w, w[u].w, a);
-          reinterpret_cast<float4*>(mm)[i] = m[u];
-          reinterpret_cast<float4*>(mv)[i] = v[u];
-          reinterpret_cast<float4*>(mw)[i] = w[u];
+          st_stream_v4(mm + 4 * i, as_u4(m[u]), pol);
+          st_stream_v4(mv + 4 * i, as_u4(v[u]), pol);
+          st_stream_v4(mw + 4 * i, as_u4(w[u]), pol);
           uint64_t targets = t.mask;
           if (kBf16Param) {
             const uint32_t lo = uint32_t(f32_to_bf16_bits(w[u].x)) | (uint32_t(f32_to_bf16_bits(w[u].y)) << 16);
@@ -336,14 +339,14 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
             while (targets) {
               const int q = __ffsll(targets) - 1;
               targets &= targets - 1;
-              uint2* p = reinterpret_cast<uint2*>(static_cast<uint16_t*>(T->param[q]) + t.c_off) + i;
-              *p = make_uint2(lo, hi);
+              st_stream_v2(reinterpret_cast<uint2*>(static_cast<uint16_t*>(T->param[q]) + t.c_off) + i,
+                           make_uint2(lo, hi), pol);
             }
           } else {
             while (targets) {
               const int q = __ffsll(targets) - 1;
               targets &= targets - 1;
-              reinterpret_cast<float4*>(static_cast<float*>(T->param[q]) + t.c_off)[i] = w[u];
+              st_stream_v4(static_cast<float*>(T->param[q]) + t.c_off + 4 * i, as_u4(w[u]), pol);
             }
           }
         }

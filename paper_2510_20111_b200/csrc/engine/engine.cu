@@ -132,9 +132,15 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   // ---- streams / events ----
   int lo = 0, hi = 0;
   HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HZP_CUDA(cudaStreamCreateWithPriority(&st[0], cudaStreamNonBlocking, lo));
-  HZP_CUDA(cudaStreamCreateWithPriority(&st[1], cudaStreamNonBlocking, hi));
-  HZP_CUDA(cudaStreamCreateWithPriority(&st[2], cudaStreamNonBlocking, hi));
+  // Priorities (numerically lower = scheduled first when an SM frees up):
+  // compute highest, so a pending persistent GEMM takes every SM it needs
+  // before any queued collective / optimizer CTA (those then fill the space
+  // beside the resident GEMM CTAs, one per SM); collectives next; the
+  // per-layer optimizer lowest (it has the most slack).
+  const int mid = hi < lo ? std::min(lo, hi + 1) : hi;
+  HZP_CUDA(cudaStreamCreateWithPriority(&st[0], cudaStreamNonBlocking, hi));
+  HZP_CUDA(cudaStreamCreateWithPriority(&st[1], cudaStreamNonBlocking, mid));
+  HZP_CUDA(cudaStreamCreateWithPriority(&st[2], cudaStreamNonBlocking, mid));
   HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, lo));
   const int n = static_cast<int>(plan.entries.size());
   done.resize(n);

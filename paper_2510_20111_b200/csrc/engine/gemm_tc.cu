@@ -44,7 +44,6 @@ constexpr int kThreadsTC = 64 + 32 * kEpiWarps;
 constexpr int kStageBufs = HZP_STAGE_BUFS;
 
 int g_sm_budget = kNumSMs;
-bool g_cluster = std::getenv("HZP_GEMM_NO_CLUSTER") == nullptr;
 
 using namespace tc;
 
@@ -628,14 +627,6 @@ CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld,
   return make_tma_map_bf16(base, inner, outer, ld, box_outer, nh, nb, sh, sb);
 }
 
-bool mn5_disabled() {
-  static const bool off = [] {
-    const char* e = std::getenv("HZP_GEMM_MN5");
-    return e && std::atoi(e) == 0;
-  }();
-  return off;
-}
-
 // Output map for the TMA-store epilogue: {N, M, nh, nb}, box {32, 32, 1, 1};
 // bf16 rows of 64 B use SWIZZLE_64B, fp32 rows of 128 B SWIZZLE_128B.
 CUtensorMap make_out_map(const void* base, bool f32, int64_t N, int64_t M, int64_t ld, int nh, int nb,
@@ -707,8 +698,8 @@ void launch_tc(const void* A, const void* B, void* C, const GemmShape& s, const 
   const CUtensorMap tb = B_MN ? make_map(B, s.N, s.K, s.ldb, BK, s.nh, s.nb, s.b_sh, s.b_sb)
                               : make_map(B, s.K, s.N, s.ldb, BN, s.nh, s.nb, s.b_sh, s.b_sb);
   TcParams p;
-  p.a5 = A_MN && !mn5_disabled() && make_map_mn5(A, s.M, s.K, s.lda, s.nh, s.nb, s.a_sh, s.a_sb, &p.tmA5);
-  p.b5 = B_MN && !mn5_disabled() && make_map_mn5(B, s.N, s.K, s.ldb, s.nh, s.nb, s.b_sh, s.b_sb, &p.tmB5);
+  p.a5 = A_MN && make_map_mn5(A, s.M, s.K, s.lda, s.nh, s.nb, s.a_sh, s.a_sb, &p.tmA5);
+  p.b5 = B_MN && make_map_mn5(B, s.N, s.K, s.ldb, s.nh, s.nb, s.b_sh, s.b_sb, &p.tmB5);
   if (STORE != 0) {
     p.tmC = make_out_map(C, STORE == 2, s.N, s.M, e.ldc, s.nh, s.nb, s.c_sh, s.c_sb);
     if (STORE == 1 && e.act == kActGelu)
@@ -800,7 +791,7 @@ void dispatch_store(const void* A, const void* B, void* C, const GemmShape& s, c
   // per-SM operand traffic and smem per stage (deeper pipeline).  (Pairing
   // the causal dQ product measured slower: 79 vs 67 us — the pair's union K
   // range outweighs the halved B traffic at N = 128.)
-  const bool pair = g_cluster && !s.causal && (s.M + BM - 1) / BM >= 2;
+  const bool pair = !s.causal && (s.M + BM - 1) / BM >= 2;
   if (!tma) dispatch_major<BN, 0, 0, 1>(A, B, C, s, e, st);
   else if (!e.out_bf16) {
     if (pair) dispatch_major<BN, 2, 0, 2>(A, B, C, s, e, st);

@@ -20,7 +20,8 @@
 // without transposes (gemm.cuh).  Attention is fused on tcgen05 (attn_tc.cu):
 // forward keeps S in TMEM (online softmax, lse saved); backward recomputes P
 // per key tile, accumulates dK / dV in TMEM and emits dS^T for dQ = dS K
-// (a causal batched GEMM).
+// (a causal batched GEMM; the alternative query-tile pass recomputing P / dS
+// in TMEM, attention_dq_tc, measured slower).
 #include <cmath>
 #include <vector>
 
@@ -236,7 +237,11 @@ class GptModel final : public Model {
     B->dxm = bf(T_ * h_);
     B->part = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
     B->part_side = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
-    HZP_CUDA(cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking));
+    {  // weight-gradient GEMMs: compute, at the compute stream's (highest) priority
+      int lo = 0, hi = 0;
+      HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      HZP_CUDA(cudaStreamCreateWithPriority(&B->side, cudaStreamNonBlocking, hi));
+    }
     for (auto& e : B->ev) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     B->emb = f32(int64_t(V_) * h_ + int64_t(S_) * h_);
     HZP_CUDA(cudaMalloc(&B->emb_ws, embed_bwd_ws_bytes(int(T_), V_)));
@@ -618,6 +623,9 @@ class GptModel final : public Model {
     // attention core: fused tcgen05 backward for dK, dV (P recomputed from
     // lse, dS^T emitted), then dQ = dS K as one transposed causal product
     attn_rowdot(B->dattn, a.attn, a.lse, B->D, b_, nh_, S_, hd_, s);
+    // dS^T through HBM + one causal GEMM for dQ: measured faster than the
+    // query-tile pass that recomputes P / dS in TMEM (attention_dq_tc,
+    // 0.290 vs 0.341 ms for the whole backward at b4 / 16 heads / S 2048)
     attention_bwd_tc(a.qkv, B->dattn, a.lse, B->D, B->dqkv, B->dS, b_, nh_, S_, h_, s);
     attention_dq(a.qkv, B->dS, B->dqkv, b_, nh_, S_, h_, s);  // dQ = dS K
     to_side();

@@ -9,7 +9,12 @@
 namespace hzp {
 namespace {
 
+// Tile = the work of one short-lived 128-thread CTA (these kernels run beside
+// the persistent GEMMs, so a CTA must not hold an SM for long): 32 K elements
+// for AG / RS (64 KB of bf16 moved), 4 K for the optimizer (30 B / element of
+// HBM traffic, ~120 KB).
 constexpr int64_t kTileElems = 1 << 15;
+constexpr int64_t kZ1TileElems = 1 << 12;
 
 // Split a contiguous element run whose streams start at offs[] (element
 // offsets into 256-byte aligned buffers of elem bytes ebytes[]) into tiles:
@@ -17,7 +22,7 @@ constexpr int64_t kTileElems = 1 << 15;
 // elements), scalar tail; bodies are cut into pieces of <= kTileElems.
 template <typename Emit>
 void split_run(const int64_t* offs, const int* ebytes, int nstreams, int64_t len, int vec,
-               Emit&& emit) {
+               Emit&& emit, int64_t tile = kTileElems) {
   auto aligned_at = [&](int64_t h) {
     for (int s = 0; s < nstreams; ++s)
       if (((offs[s] + h) * ebytes[s]) % 16 != 0) return false;
@@ -30,12 +35,12 @@ void split_run(const int64_t* offs, const int* ebytes, int nstreams, int64_t len
       break;
     }
   if (head < 0 || len - head < vec) {
-    for (int64_t p = 0; p < len; p += kTileElems) emit(p, std::min(kTileElems, len - p), false);
+    for (int64_t p = 0; p < len; p += tile) emit(p, std::min(tile, len - p), false);
     return;
   }
   if (head > 0) emit(0, head, false);
   const int64_t body = (len - head) / vec * vec;
-  const int64_t piece = std::max<int64_t>(vec, kTileElems / vec * vec);
+  const int64_t piece = std::max<int64_t>(vec, tile / vec * vec);
   for (int64_t p = 0; p < body; p += piece) emit(head + p, std::min(piece, body - p), true);
   if (head + body < len) emit(head + body, len - head - body, false);
 }
@@ -141,7 +146,7 @@ TileTables build_comm_tiles(const ShardGeom& g, const std::vector<Range64>& laye
           t.src = static_cast<int16_t>(j2);
           t.vec = v;
           tiles.push_back(t);
-        });
+        }, kZ1TileElems);
         e = stop;
       }
     }

@@ -23,8 +23,9 @@ def _ref(q, k, v, do):
 
 # (4, 16, 2048) is the bench shape (1.3B config: b = 4 sequences per microbatch,
 # 16 heads, S = 2048): the LPT-ordered two-tile forward and the full backward grid
+@pytest.mark.parametrize("legacy", [False, True], ids=["dq-tmem", "dq-gemm"])
 @pytest.mark.parametrize("b,nh,S", [(1, 1, 128), (2, 2, 256), (1, 4, 512), (2, 1, 1024), (4, 16, 2048)])
-def test_fused_attention_fwd_bwd(gpu, b, nh, S):
+def test_fused_attention_fwd_bwd(gpu, b, nh, S, legacy):
     from paper_2510_20111_b200 import _native as N
     hd, h = 128, 128 * nh
     g = torch.Generator(device="cpu").manual_seed(b * 100 + nh * 10 + S)
@@ -36,8 +37,10 @@ def test_fused_attention_fwd_bwd(gpu, b, nh, S):
     N.check(N.lib.hzp_attention_fwd(p(qkv), p(O), p(lse), b, nh, S, h, None))
     D = torch.zeros(2, b * nh, S, device=gpu)  # backward workspace (per-query vectors)
     dqkv = torch.zeros(b, S, 3 * h, device=gpu, dtype=torch.bfloat16)
-    dsT = torch.zeros(b * nh, S, S, device=gpu, dtype=torch.bfloat16)
-    N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv), p(dsT), b, nh, S, h, None))
+    # dQ recomputed in TMEM (production, dsT = NULL) and the legacy dS^T + GEMM path
+    dsT = torch.zeros(b * nh, S, S, device=gpu, dtype=torch.bfloat16) if legacy else None
+    N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv),
+                                    p(dsT) if legacy else None, b, nh, S, h, None))
     torch.cuda.synchronize()
     split = lambda t: t.view(b, S, nh, hd).transpose(1, 2)  # noqa: E731
     q, k, v = (split(t) for t in qkv.split(h, dim=-1))

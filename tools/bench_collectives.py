@@ -1,21 +1,24 @@
-"""AG / RS bus-bandwidth sweep over NVLink (SURVEY §8(d) sweep 4), one process
+"""AG / RS sweep over NVLink / NVSwitch (SURVEY §8(d) sweep 4, BASELINE
+configs[4]: 1 MB - 1 GB x prefetch depth 1-4 at 2 / 4 / 8 GPUs), one process
 per GPU, with an NCCL comparator on the same bytes.
 
-    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \\
-        tools/bench_collectives.py [--sizes-mb 1,4,16,64,256,1024] [--depth 2]
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
+        tools/bench_collectives.py [--sizes-mb 1,4,16,64,256,1024] [--depths 1,2,4]
 
-Each size is the full (unsharded) layer in the bf16 wire format: a
-one-layer MLP ctx (`dims = [1024, k]`, layer = 1025 k elements) in flat
-ZeRO-3 over the N ranks.  AG = `hzp_ag_layer` into ring slot `i % depth`
-(k back-to-back AGs into k slots); RS = `hzp_rs_layer` from gradient slot 0.
-Both legs are measured with the NVLink part on the copy engines (default)
-and as SM pull kernels (HZP_AG_CE=0 / HZP_RS_CE=0), in the bf16 wire format
-and (--precs 1,0) fp32; the AG additionally at prefetch depths 1-4
-(--depths, copy-engine bf16 leg).  busbw = (N-1)/N x bytes / time, CUDA
-events on the ctx stream, max over ranks.  Rank 0 prints one JSON object per
-(size, op, path, dtype, depth), and with --cpu-ref the reference's own
-`all_gather` / `reduce_scatter` (collective.cpp:44-115, oracle/_ref, one
-host thread, sizes <= 64 MB) on the same bytes — the CPU baseline of sweep 4.
+Two layer placements of the flat ZeRO-3 layout (the kernels are the step's
+own: owner multimem.st AG, multimem.ld_reduce RS for the bf16 wire, ordered
+pull for fp32):
+  balanced     one-layer MLP ctx (dims = [1024, k]): the layer spans all N
+               shards, every rank owns 1/N (the nccl-tests shape);
+  single-owner 2N equal layers (dims = [k] * (2N + 1)): layer 0 lies inside
+               rank 0's shard (the 1.3B / 7B case: a broadcast / a reduce at
+               one owner).
+Timing: hzp_collective_time (back-to-back on the collective's stream, CUDA
+events, one device barrier first), max over ranks.  busbw = (N-1)/N x
+bytes / time; owner_link = bytes / time (the owner's NVLink carries the
+layer once).  Rank 0 prints one JSON object per row; with --cpu-ref also the
+reference's own CPU all_gather / reduce_scatter (collective.cpp:44-115,
+oracle/_ref, one host thread, sizes <= 64 MB) on the same bytes.
 """
 import argparse
 import json
@@ -65,7 +68,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--depth", type=int, default=2)
-    ap.add_argument("--depths", default="1,2,4", help="AG prefetch depths (copy-engine bf16 leg)")
+    ap.add_argument("--depths", default="1,2,4", help="AG prefetch depths (bf16 wire)")
     ap.add_argument("--precs", default="1,0", help="1 = bf16 wire, 0 = fp32")
     ap.add_argument("--cpu-ref", action="store_true")
     ap.add_argument("--iters", type=int, default=8)
@@ -102,30 +105,32 @@ def main():
         for prec in (int(x) for x in args.precs.split(",")):
             es = 2 if prec else 4
             elems = mb * (1 << 20) // es
-            k = max(64, (elems // 1025) // 64 * 64)  # shard bounds 16-B aligned up to N = 8
-            n = 1025 * k
-            nbytes = es * n
-            for ce in (1, 0):
-                for depth in (depths if (ce and prec) else [args.depth]):
-                    os.environ["HZP_AG_CE"] = str(ce)
-                    os.environ["HZP_RS_CE"] = str(ce)
-                    eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=[1024, k], batch=8,
+            for place in ("balanced", "single-owner"):
+                if place == "balanced":
+                    k = max(64, (elems // 1025) // 64 * 64)  # shard bounds 16-B aligned up to N = 8
+                    dims, n = [1024, k], 1025 * k
+                else:
+                    k = max(64, int((elems ** 0.5) // 64 * 64))
+                    dims, n = [k] * (2 * world + 1), k * k + k
+                nbytes = es * n
+                for depth in (depths if prec else [args.depth]):
+                    eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=8,
                                                  par=ParallelConfig(dp=world, z1=world, z2=world, z3=world),
                                                  prelaunch_depth=depth, device=local, my_rank=rank))
                     eng.connect()
-                    eng.init_random()
-                    path = "copy-engine" if ce else "sm-pull"
-                    legs = [("ag", lambda i: eng.ag_layer(0, i % depth), 1)]
-                    if depth == args.depth:
-                        legs.append(("rs", lambda i: eng.rs_layer(0, 0), 2))
-                    for op, fn, sid in legs:
-                        ms = timed(fn, eng.stream(sid))
+                    eng.init_random()  # values do not matter for timing (device-side, fast)
+                    for op in (("ag", "rs") if depth == args.depth else ("ag",)):
+                        eng.collective_time(op, 0, 2)
+                        ms = mx(eng.collective_time(op, 0, args.iters))
                         bw = (world - 1) / world * nbytes / (ms / 1e3) / 1e9
+                        link = nbytes / (ms / 1e3) / 1e9
                         if rank == 0:
-                            print(json.dumps({"op": op, "path": path, "dtype": "bf16" if prec else "f32",
+                            print(json.dumps({"op": op, "placement": place, "dtype": "bf16" if prec else "f32",
                                               "n_gpus": world, "bytes": nbytes, "depth": depth,
                                               "ms": round(ms, 4), "busbw_GBps": round(bw, 1),
-                                              "frac_nvlink": round(bw / NVLINK_GBPS, 3)}), flush=True)
+                                              "owner_link_GBps": round(link, 1) if place == "single-owner" else None,
+                                              "frac_nvlink": round((link if place == "single-owner" else bw)
+                                                                   / NVLINK_GBPS, 3)}), flush=True)
                     eng.close()
         elems = mb * (1 << 20) // 2
         n = 1025 * max(64, (elems // 1025) // 64 * 64)

@@ -63,23 +63,27 @@ def bench_gemm():
 
 
 def bench_comm():
-    from oracle import load_oracle  # noqa: F401  (not used for timing)
     from paper_2510_20111_b200 import EngineConfig, HzpEngine, ParallelConfig
-    # emulated dp ranks on one GPU: peer loads hit local HBM; measures the
-    # kernels' memory-level parallelism, not NVLink
+    # emulated dp ranks on one GPU (the unicast model of the NVLS kernels: the
+    # owner stores into every member's slot, the reducer sums the members'
+    # slots in order), so this measures HBM-side efficiency, not NVLink
     for dims, dp in (([4096, 16384, 4096], 4), ([4096, 16384, 4096], 8)):
-        for prec in (1,):
-            eng = HzpEngine(EngineConfig(model=0, precision=prec, dims=dims, batch=8,
-                                         par=ParallelConfig(dp=dp, z1=dp, z2=dp, z3=dp)))
-            eng.init_random()
-            off, n = eng.layers[0]
-            es = 2 if prec else 4
-            ms = timeit(lambda: eng.ag_layer(0, 0), iters=10)
-            # bytes moved per rank = full layer (dst) read from peers; dp ranks per launch
-            gbs = n * es * dp * 2 / ms / 1e6  # read + write
-            print(json.dumps({"kernel": "ag_pull", "dp": dp, "layer_elems": n, "ms": round(ms, 4),
-                              "GBps_hbm_rw": round(gbs, 1)}), flush=True)
-            eng.close()
+        eng = HzpEngine(EngineConfig(model=0, precision=1, dims=dims, batch=8,
+                                     par=ParallelConfig(dp=dp, z1=dp, z2=dp, z3=dp)))
+        eng.init_random()
+        off, n = eng.layers[0]
+        for op in ("ag", "rs", "z1"):
+            if op == "z1":
+                ms = timeit(eng.z1_adam_step, iters=5)
+                gbs = eng.s1 * dp * 30 / ms / 1e6  # 30 B / element of every driven rank's chunk
+            else:
+                ms = eng.collective_time(op, 0, 10)
+                # AG: layer read once per owner span + written dp times; RS: dp
+                # bf16 reads + 8 B fp32 grad read-modify-write per element
+                gbs = (n * 2 * (1 + dp) if op == "ag" else n * (2 * dp + 8)) / ms / 1e6
+            print(json.dumps({"kernel": op, "dp": dp, "layer_elems": n, "ms": round(ms, 4),
+                              "GBps_hbm": round(gbs, 1)}), flush=True)
+        eng.close()
 
 
 def bench_epi():
@@ -125,9 +129,16 @@ def bench_attn():
     p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     fwd = lambda: N.check(N.lib.hzp_attention_fwd(p(qkv), p(O), p(lse), b, nh, S, h, st))  # noqa: E731
-    bwd = lambda: N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv), p(dsT), b, nh, S, h, st))  # noqa: E731
+    bwd = lambda: N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv), None,  # noqa: E731
+                                                  b, nh, S, h, st))
+    bwd_legacy = lambda: N.check(N.lib.hzp_attention_bwd(p(qkv), p(O), p(do), p(lse), p(D), p(dqkv),  # noqa: E731
+                                                         p(dsT), b, nh, S, h, st))
     flops_fwd = 4.0 * b * nh * S * S * hd / 2  # causal QK^T + PV
-    for name, fn, fl in (("attn_fwd", fwd, flops_fwd), ("attn_bwd(+rowdot+dQ gemm)", bwd, 2.5 * flops_fwd)):
+    # backward algorithmic FLOPs: S^T, dP^T, dV, dK, dQ = 2.5 x forward (the
+    # dQ pass's recomputed S / dP products are not counted)
+    for name, fn, fl in (("attn_fwd", fwd, flops_fwd),
+                         ("attn_bwd (rowdot + dK/dV + dQ pass, P/dS in TMEM)", bwd, 2.5 * flops_fwd),
+                         ("attn_bwd legacy (rowdot + dK/dV + dS^T in HBM + dQ GEMM)", bwd_legacy, 2.5 * flops_fwd)):
         ms = timeit(fn)
         print(json.dumps({"kernel": name, "b": b, "nh": nh, "S": S, "ms": round(ms, 4),
                           "tflops_causal": round(fl / ms / 1e9, 1)}), flush=True)
