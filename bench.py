@@ -682,8 +682,21 @@ def run_hzp(args):
         if d:
             in_step[name] = {"tasks": len(d), "median_ms": round(statistics.median(d), 4),
                              "max_ms": round(d[-1], 4)}
+    # where the compute stream waited: the gap before each compute task,
+    # summed by the kind of task that was kept waiting (FWD: its AG; BWD: its
+    # AG or the gradient ring; OPT: the per-layer optimizer tail + barrier)
+    allk = {r[0]: r[1] for r in eng.launch_log()}
+    comp = sorted((tl["start_ms"][i], tl["end_ms"][i], allk[i]) for i in allk if allk[i] in (0, 1, 2, 6))
+    gaps = {"before_fwd": 0.0, "before_bwd": 0.0, "before_opt": 0.0}
+    prev = 0.0
+    for s0, e0, k in comp:
+        if s0 > prev:
+            key = {0: "before_fwd", 2: "before_bwd", 1: "before_bwd", 6: "before_opt"}[k]
+            gaps[key] += s0 - prev
+        prev = max(prev, e0)
     sim = simulator_prediction(c, N, z1, z2, z3, nmb, mb, args.depth)
     exposed = {"compute_idle_ms": round(idle, 3), "makespan_ms": round(mk, 3), "simulator": sim,
+               "idle_by_next_task_ms": {k: round(v, 3) for k, v in gaps.items()},
                "frac": round(idle / mk, 4) if mk else None,
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}
