@@ -116,55 +116,6 @@ __global__ void __launch_bounds__(kT) embed_wpe_grad_kernel(const uint16_t* __re
   }
 }
 
-__global__ void __launch_bounds__(kT) layernorm_fwd_kernel(const uint16_t* __restrict__ x,
-                                                           const uint16_t* __restrict__ g,
-                                                           const uint16_t* __restrict__ be,
-                                                           uint16_t* __restrict__ y,
-                                                           float* __restrict__ mu,
-                                                           float* __restrict__ rs, int h) {
-  __shared__ float red[32];
-  const int r = blockIdx.x;
-  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
-  float v[kMaxVec][8];
-  float s = 0.f;
-  const int nv = h / 8;
-#pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = threadIdx.x + k * kT;
-    if (i < nv) {
-      unpack8(xr[i], v[k]);
-      for (int j = 0; j < 8; ++j) s += v[k][j];
-    }
-  }
-  const float mean = block_sum(s, red) / h;
-  float q = 0.f;
-#pragma unroll
-  for (int k = 0; k < kMaxVec; ++k)
-    if (threadIdx.x + k * kT < nv)
-      for (int j = 0; j < 8; ++j) {
-        const float d = v[k][j] - mean;
-        q += d * d;
-      }
-  const float rstd = rsqrtf(block_sum(q, red) / h + 1e-5f);
-  if (threadIdx.x == 0) {
-    mu[r] = mean;
-    rs[r] = rstd;
-  }
-  const uint4* gr = reinterpret_cast<const uint4*>(g);
-  const uint4* br = reinterpret_cast<const uint4*>(be);
-  uint4* yr = reinterpret_cast<uint4*>(y + int64_t(r) * h);
-#pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = threadIdx.x + k * kT;
-    if (i < nv) {
-      float gg[8], bb[8], o[8];
-      unpack8(gr[i], gg);
-      unpack8(br[i], bb);
-      for (int j = 0; j < 8; ++j) o[j] = (v[k][j] - mean) * rstd * gg[j] + bb[j];
-      yr[i] = pack8(o);
-    }
-  }
-}
 
 __global__ void __launch_bounds__(kT) layernorm_bwd_kernel(
     const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
@@ -356,6 +307,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_warp_kernel(
     const int i = lane + 32 * k;
     if (i < nv) {
       unpack8(xr[i], v[k]);
+#pragma unroll
       for (int j = 0; j < 8; ++j) s += v[k][j];
     }
   }
@@ -512,23 +464,31 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const uint16_t* __restrict_
 }
 
 // dx = rstd (dy g - mean(dy g) - xhat mean(dy g xhat)) (+ resid); warp per row.
-template <int NVL>
+// WPR warps per row (h = 4096 uses 2: one warp holding 16 x 2 x 8 floats of a
+// row would spill), each owning NVL / WPR of the row's 16-byte vectors; the
+// two row sums are combined across the row's warps through shared memory.
+template <int NVL, int WPR = 1>
 __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint16_t* __restrict__ dy,
                                                         const uint16_t* __restrict__ x,
                                                         const uint16_t* __restrict__ g,
                                                         const float* __restrict__ mu, const float* __restrict__ rs,
                                                         const uint16_t* __restrict__ resid,
                                                         uint16_t* __restrict__ dx, int rows, int h) {
-  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float m = mu[r], rstd = rs[r];
-  const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
-  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
-  float xh[NVL][8], dg[NVL][8];
+  constexpr int kV = NVL / WPR > 0 ? NVL / WPR : 1;  // vectors per lane (dispatched with WPR | NVL)
+  __shared__ float red[8][2];
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (8 / WPR) + w / WPR, part = w % WPR;
+  const bool live = r < rows;
+  if (WPR == 1 && !live) return;
+  const int rr = live ? r : rows - 1;
+  const float m = mu[rr], rstd = rs[rr];
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(rr) * h);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(rr) * h);
+  float xh[kV][8], dg[kV][8];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int k = 0; k < NVL; ++k) {
-    const int i = lane + 32 * k;
+  for (int k = 0; k < kV; ++k) {
+    const int i = lane + 32 * (part + WPR * k);
     float d[8], gg[8];
     unpack8(__ldg(dyr + i), d);
     unpack8(__ldg(xr + i), xh[k]);
@@ -541,11 +501,26 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint16_t* __restri
       s2 += dg[k][j] * xh[k][j];
     }
   }
-  const float a1 = warp_sum(s1) / h, a2 = warp_sum(s2) / h;
+  float t1 = warp_sum(s1), t2 = warp_sum(s2);
+  if (WPR > 1) {
+    if (lane == 0) {
+      red[w][0] = t1;
+      red[w][1] = t2;
+    }
+    __syncthreads();
+    t1 = t2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < WPR; ++q) {  // fixed order: deterministic
+      t1 += red[w - part + q][0];
+      t2 += red[w - part + q][1];
+    }
+    if (!live) return;
+  }
+  const float a1 = t1 / h, a2 = t2 / h;
   uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
 #pragma unroll
-  for (int k = 0; k < NVL; ++k) {
-    const int i = lane + 32 * k;
+  for (int k = 0; k < kV; ++k) {
+    const int i = lane + 32 * (part + WPR * k);
     float o[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
@@ -761,14 +736,14 @@ void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, 
 }
 void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
                    float* mu, float* rstd, int rows, int h, cudaStream_t s) {
-  if (h % 8 || h > 8 * kT * kMaxVec) throw std::invalid_argument("layernorm: h % 8 != 0 or > 8192");
+  if (h % 8) throw std::invalid_argument("layernorm: h % 8 != 0");
   bool handled = h % 256 == 0;
   if (handled) {
     HZP_NVL_SWITCH(h / 256, (ln_fwd_kernel<NVL><<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h)));
   }
   if (!handled) {
-    if (h <= 32 * 8 * kWV) layernorm_fwd_warp_kernel<<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h);
-    else layernorm_fwd_kernel<<<rows, kT, 0, s>>>(x, g, beta, y, mu, rstd, h);
+    if (h > 32 * 8 * kWV) throw std::invalid_argument("layernorm: h > 4096 must be 256 x {12, 16}");
+    layernorm_fwd_warp_kernel<<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h);
   }
   HZP_LAUNCH_CHECK();
 }
@@ -777,8 +752,13 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
                    int rows, int h, cudaStream_t s) {
   bool handled = h % 256 == 0;
   if (handled) {  // dx pass (warp per row) + column pass for dgamma / dbeta
-    HZP_NVL_SWITCH(h / 256, (ln_bwd_dx_kernel<NVL><<<(rows + 7) / 8, 256, 0, s>>>(dy, x, g, mu, rstd, resid, dx,
-                                                                                   rows, h)));
+    if (h / 256 > 8) {  // two warps per row beyond h = 2048 (no spills)
+      HZP_NVL_SWITCH(h / 256, (ln_bwd_dx_kernel<NVL, 2><<<(rows + 3) / 4, 256, 0, s>>>(dy, x, g, mu, rstd, resid,
+                                                                                         dx, rows, h)));
+    } else {
+      HZP_NVL_SWITCH(h / 256, (ln_bwd_dx_kernel<(NVL > 8 ? 8 : NVL)><<<(rows + 7) / 8, 256, 0, s>>>(
+                                   dy, x, g, mu, rstd, resid, dx, rows, h)));
+    }
   }
   if (handled) {
     HZP_LAUNCH_CHECK();
