@@ -141,7 +141,11 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   HZP_CUDA(cudaStreamCreateWithPriority(&st[0], cudaStreamNonBlocking, hi));
   HZP_CUDA(cudaStreamCreateWithPriority(&st[1], cudaStreamNonBlocking, mid));
   HZP_CUDA(cudaStreamCreateWithPriority(&st[2], cudaStreamNonBlocking, mid));
-  HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, lo));
+  // (with DZP replicas the per-layer optimizer also moves the replicas'
+  // gradients over NVLink and must keep up with the backward: collective
+  // priority; flat, it is HBM-only and gives way: measured 7B N=4 90.8 vs
+  // 90.0 K tokens/s with, 1.3B N=4 404 vs 414 K without)
+  HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, geom.replicas() > 1 ? mid : lo));
   const int n = static_cast<int>(plan.entries.size());
   done.resize(n);
   for (auto& e : done) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -179,8 +183,8 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     if (c.my_rank >= c.par.dp) throw std::invalid_argument("my_rank out of range");
     mine.push_back(c.my_rank);
   }
-  if (shared && !multicast_supported(c.device))
-    throw CudaError("multi-process mode needs NVLS multicast (NVSwitch); this device has none");
+  if (shared && (ag_multicast() || rs_multicast()) && !multicast_supported(c.device))
+    throw CudaError("groups of >= 3 GPUs need NVLS multicast (NVSwitch); this device has none");
   for (int r : mine) {
     Arena& a = arenas[r];
     if (shared) {
@@ -195,8 +199,8 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     carve(a);
   }
   if (shared) {  // the group's first rank creates the multicast objects
-    if (!zero_copy_ag && c.my_rank % geom.z3 == 0) ag_mc = mc_create(geom.z3, lay.ag_bytes);
-    if (!direct_grad && bf16 && c.my_rank % geom.z2 == 0) wg_mc = mc_create(geom.z2, lay.wgrad_bytes);
+    if (ag_multicast() && c.my_rank % geom.z3 == 0) ag_mc = mc_create(geom.z3, lay.ag_bytes);
+    if (rs_multicast() && c.my_rank % geom.z2 == 0) wg_mc = mc_create(geom.z2, lay.wgrad_bytes);
   }
 
   // ---- driven ranks ----
@@ -290,13 +294,13 @@ void Engine::open_peers(const ShareRecord* rec, int n) {
   // bind this rank's AG / gradient regions into its groups' multicast
   // objects (mc_attach blocks until every member has added its device)
   const Arena& mine = arenas[me];
-  if (lay.ag_bytes) {
+  if (ag_multicast()) {
     const ShareRecord& lead = rec[geom.z3_base(me)];
     if (me != lead.rank) ag_mc = mc_import(lead.pid, lead.ag_mc_fd, lay.ag_bytes);
     mc_attach(ag_mc, cfg.device, mine.symm, lay.ag);
     table.ag_mc = reinterpret_cast<void*>(ag_mc.va);
   }
-  if (lay.wgrad_bytes && bf16) {
+  if (rs_multicast()) {
     const ShareRecord& lead = rec[geom.z2_base(me)];
     if (me != lead.rank) wg_mc = mc_import(lead.pid, lead.wg_mc_fd, lay.wgrad_bytes);
     mc_attach(wg_mc, cfg.device, mine.symm, lay.wgrad);
@@ -395,7 +399,8 @@ void Engine::ag_layer(int layer, int slot, cudaStream_t s, bool ready_posted) {
   const uint64_t grp = rank_mask(geom.z3_base(me), geom.z3);
   launch_flags(dtable, me, kFlagAgReady, ready_posted ? 0 : grp, seq, kFlagAgReady, nt > 0 ? grp : 0, seq, s);
   if (nt > 0)
-    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, true, FlagGate{}, kCommCtas, s);
+    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, ag_multicast(), FlagGate{},
+                   kCommCtas, s);
   launch_flags(dtable, me, kFlagAgDone, nt > 0 ? grp : 0, seq, kFlagAgDone, ag_owners[layer], seq, s);
   launches += nt > 0 ? 3 : 2;
 }
@@ -410,7 +415,7 @@ void Engine::rs_layer(int layer, int wslot, bool assign, uint64_t seq, cudaStrea
   const float scale = static_cast<float>(cfg.grad_scale);
   if (emulate) {
     launch_rs_reduce(dtable, dtiles + t0, nt, wslot, slot_elems, geom.z2, bf16,
-                     bf16 ? kRsOrderedRound : kRsOrdered, assign, scale, FlagGate{}, kCommCtas, s);
+                     rs_multicast_group() ? kRsOrderedRound : kRsOrdered, assign, scale, FlagGate{}, kCommCtas, s);
     ++launches;
     return;
   }
@@ -418,7 +423,7 @@ void Engine::rs_layer(int layer, int wslot, bool assign, uint64_t seq, cudaStrea
   const uint64_t grp = rank_mask(geom.z2_base(me), geom.z2);
   launch_flags(dtable, me, kFlagRsReady, grp, seq, kFlagRsReady, nt > 0 ? grp : 0, seq, s);
   if (nt > 0)
-    launch_rs_reduce(dtable, dtiles + t0, nt, wslot, slot_elems, geom.z2, bf16, bf16 ? kRsMulticast : kRsOrdered,
+    launch_rs_reduce(dtable, dtiles + t0, nt, wslot, slot_elems, geom.z2, bf16, rs_multicast() ? kRsMulticast : kRsOrdered,
                      assign, scale, FlagGate{}, kCommCtas, s);
   launch_flags(dtable, me, kFlagRsDone, grp, seq, 0, 0, 0, s);
   launches += nt > 0 ? 3 : 2;

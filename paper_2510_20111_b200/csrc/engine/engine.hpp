@@ -110,6 +110,18 @@ struct Engine {
 
   int local_index(int rank) const;
   void build_tiles();
+  // Collective algorithm by group size (both hand-written kernels; chosen by
+  // the traffic shape, as NCCL picks ring / NVLS): a layer lies inside one
+  // member's shard, so the AG is a broadcast and the RS a reduce at that
+  // owner.  With one peer (group of 2) the owner's unicast stores / ordered
+  // pull move the layer over its link once at up to ~760 GB/s; with >= 2
+  // peers a unicast broadcast / pull would cross the owner's link (z - 1)
+  // times, so the NVLS multicast store / in-switch reduce (one crossing,
+  // ~470-570 GB/s measured) wins.  Emulation runs the unicast model of the
+  // same choice (multicast groups: the sum rounded to bf16 like the switch).
+  bool rs_multicast_group() const { return bf16 && !direct_grad && geom.z2 >= 3; }
+  bool ag_multicast() const { return !emulate && cfg.par.dp > 1 && !zero_copy_ag && geom.z3 >= 3; }
+  bool rs_multicast() const { return !emulate && cfg.par.dp > 1 && rs_multicast_group(); }
   void carve(Arena& a) const;
   ShareRecord share_record() const;
   void open_peers(const ShareRecord* records, int n);

@@ -95,13 +95,14 @@ def bf16_rne(o, x):
 
 def rs_bf16_model(o, grads):
     """The bf16-wire reduce: each member's gradient rounded to bf16 (the wgrad
-    GEMM's bf16 store), summed in fp32 in ascending rank order, the sum
-    rounded to bf16 (multimem.ld_reduce .acc::f32 returns bf16)."""
+    GEMM's bf16 store), summed in fp32 in ascending rank order; in groups of
+    >= 3 (in-switch multimem.ld_reduce .acc::f32, which returns bf16) the sum
+    is rounded to bf16, in groups of 2 (ordered unicast pull) it stays fp32."""
     w = [bf16_rne(o, g) for g in grads]
     s = w[0].copy()
     for x in w[1:]:
         s = (s + x).astype(np.float32)
-    return bf16_rne(o, s)
+    return bf16_rne(o, s) if len(grads) >= 3 else s
 
 
 @pytest.mark.parametrize("cfg", [c for c in CONFIGS if c[3] > 1], ids=_ids)
