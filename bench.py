@@ -645,12 +645,15 @@ def run_hzp(args):
     burst, sustained, hbm, src = peaks()
     achieved = gf / (gms / 1e3) / 1e12
     traffic, traffic_src = None, None
-    tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gemm_dram_traffic.json")
+    import glob  # the newest ncu capture of this kernel (tools/gemm_traffic.py, refreshed per round)
+    caps = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                         "r*_gemm_dram_traffic.json")))
+    tf = caps[-1] if caps else ""
     if os.path.exists(tf):  # committed ncu capture of this kernel (DRAM bytes per launch, one step)
         with open(tf) as fh:
             tj = json.load(fh)
         traffic = int(tj["dram_bytes_per_launch"])
-        traffic_src = (f"profiles/r01_gemm_dram_traffic.json: ncu dram__bytes_read+write per launch over "
+        traffic_src = (f"profiles/{os.path.basename(tf)}: ncu dram__bytes_read+write per launch over "
                        f"{tj['launches']} launches; algorithmic {int(tj['algorithmic_bytes_per_launch'])} B "
                        f"(ratio {tj['ratio']:.2f})")
     roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": sustained, "unit": "TFLOP/s",

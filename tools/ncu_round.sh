@@ -16,3 +16,10 @@ for k in "gemm_tc_kernel:300" "attn_fwd2_kernel:10" "attn_bwd_kernel:10" "z1_ada
       -o gpurun_out/${tag}_ncu_$name $CMD > gpurun_out/${tag}_ncu_$name.log 2>&1
   echo "$name rc=$?"
 done
+# GEMM DRAM traffic per launch (bench.py roofline.traffic): per-shape launch
+# counts of one step + ncu DRAM bytes of every gemm_tc launch of that step
+python tools/gemm_traffic.py shapes gpurun_out/${tag}_gemm_shapes.json > /dev/null 2>&1 && \
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:gemm_tc --csv --log-file gpurun_out/${tag}_gemm_dram.csv python tools/gemm_traffic.py run \
+    > gpurun_out/${tag}_gemm_dram.log 2>&1
+echo "gemm dram rc=$?"
