@@ -199,13 +199,6 @@ int hzp_comm_tiles(const hzp_parallel* par, int64_t P, const int64_t* layer_off,
                    const int64_t* layer_size, int num_layers, int rank, int working_bytes,
                    hzp_comm_tile* out, int cap, int* n_out, int* ag_off, int* rs_off,
                    int* z1_off, int* z1_n);
-/* The replica-push tiles of `rank` (DZP replicas, dp / z2 >= 2): after a
- * layer's gradient is final on `rank` (segment j = rank % z2 of replica
- * b = rank / z2) it stores, per tile, len elements from its grad shard at
- * b_off into rank src's staging slot c_off (= b) at a_off (offset in src's
- * Z1 chunk).  Empty when dp / z2 == 1. */
-int hzp_comm_push_tiles(const hzp_parallel* par, int64_t P, const int64_t* layer_off, const int64_t* layer_size,
-                        int num_layers, int rank, hzp_comm_tile* out, int cap, int* n_out);
 
 /* ---- device engine ------------------------------------------------------ */
 /* Model families.  HZP_MODEL_MLP is the reference's model (tanh MLP, loss

@@ -131,8 +131,6 @@ SIGNATURES = [
     ("hzp_comm_tiles", C.c_int, [_P(hzp_parallel), C.c_int64, _P(C.c_int64), _P(C.c_int64), C.c_int,
                                  C.c_int, C.c_int, _P(hzp_comm_tile), C.c_int, _P(C.c_int),
                                  _P(C.c_int), _P(C.c_int), _P(C.c_int), _P(C.c_int)]),
-    ("hzp_comm_push_tiles", C.c_int, [_P(hzp_parallel), C.c_int64, _P(C.c_int64), _P(C.c_int64), C.c_int,
-                                      C.c_int, _P(hzp_comm_tile), C.c_int, _P(C.c_int)]),
     ("hzp_ctx_create", C.c_int, [_P(hzp_engine_config), _P(_vp)]),
     ("hzp_ctx_destroy", None, [_vp]),
     ("hzp_ctx_layout", C.c_int, [_vp, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64), _P(C.c_int64),

@@ -323,21 +323,6 @@ int hzp_comm_tiles(const hzp_parallel* par, int64_t P, const int64_t* layer_off,
   });
 }
 
-int hzp_comm_push_tiles(const hzp_parallel* par, int64_t P, const int64_t* layer_off, const int64_t* layer_size,
-                        int num_layers, int rank, hzp_comm_tile* out, int cap, int* n_out) {
-  if (!par || !layer_off || !layer_size || !n_out) return HZP_ERR_ARG;
-  return guarded([&] {
-    const ParallelConfig c = to_cfg(par);
-    if (rank < 0 || rank >= c.dp || c.dp > kMaxRanks) throw std::invalid_argument("rank / dp out of range");
-    std::vector<Range64> lr;
-    for (int l = 0; l < num_layers; ++l) lr.push_back({layer_off[l], layer_size[l]});
-    const TileTables T = build_comm_tiles(ShardGeom(P, c), lr, {rank}, 2, c.z2 == 1);
-    const int b0 = T.push_layer_off.front(), b1 = T.push_layer_off.back();
-    *n_out = b1 - b0;
-    if (out) std::memcpy(out, T.tiles.data() + b0, sizeof(CommTile) * std::min(cap, b1 - b0));
-  });
-}
-
 // ---- engine ---------------------------------------------------------------
 int hzp_ctx_create(const hzp_engine_config* cfg, hzp_ctx** out) {
   if (!cfg || !out) return HZP_ERR_ARG;

@@ -289,23 +289,14 @@ __device__ __forceinline__ float adam_one(float g, float& m, float& v, float& w,
   return w;
 }
 
-// stage_stride > 0: the replicas' gradients of this chunk were pushed into
-// the local staging slots T->stage[me] + b * stage_stride (replica b) by their
-// Z2-segment owners (replica_push_kernel); else they are read from the
-// segment owners' grad shards directly (flat: R = 1, all local).
 template <bool kBf16Param>
 __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int z2, int replicas,
-                                                           AdamArgs a, int dbg, int64_t stage_stride) {
+                                                           AdamArgs a, int dbg) {
   const uint64_t pol = l2_evict_first_policy();
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
-    // replica b's gradient of this tile: gsrc(b) + element
-    const float* st = stage_stride ? T->stage[T->global_rank[t.local]] + t.a_off : nullptr;
-    auto gsrc = [&](int b) -> const float* {
-      return st ? st + b * stage_stride : T->grad[t.src + b * z2] + t.b_off;
-    };
     float* mw = T->master[t.local] + t.a_off;
     float* mm = T->mom[t.local] + t.a_off;
     float* mv = T->var[t.local] + t.a_off;
@@ -322,8 +313,9 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
           const int64_t i = i0 + int64_t(u) * kThreads;
           ok[u] = i < nv;
           if (!ok[u]) continue;
-          g[u] = as_f4(ld_stream_v4(gsrc(0) + 4 * i, pol));
-          for (int b = 1; b < replicas; ++b) fadd4(g[u], as_f4(ld_stream_v4(gsrc(b) + 4 * i, pol)));
+          g[u] = as_f4(ld_stream_v4(T->grad[t.src] + t.b_off + 4 * i, pol));
+          for (int b = 1; b < replicas; ++b)
+            fadd4(g[u], as_f4(ld_stream_v4(T->grad[t.src + b * z2] + t.b_off + 4 * i, pol)));
           m[u] = as_f4(ld_stream_v4(mm + 4 * i, pol));
           v[u] = as_f4(ld_stream_v4(mv + 4 * i, pol));
           w[u] = as_f4(ld_stream_v4(mw + 4 * i, pol));
@@ -361,8 +353,8 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
       }
     } else {
       for (int64_t i = threadIdx.x; i < t.len; i += kThreads) {
-        float g = gsrc(0)[i];
-        for (int b = 1; b < replicas; ++b) g = __fadd_rn(g, gsrc(b)[i]);
+        float g = T->grad[t.src][t.b_off + i];
+        for (int b = 1; b < replicas; ++b) g = __fadd_rn(g, T->grad[t.src + b * z2][t.b_off + i]);
         if (gd) gd[i] = g;
         float m = mm[i], v = mv[i], w = mw[i];
         adam_one(g, m, v, w, a);
@@ -381,40 +373,6 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
       }
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Replica push: q's final gradient of a Z1 chunk's part -> the chunk owner's
-// staging slot (unicast stores over NVLink: fire-and-forget, so it keeps up
-// where the Z1 kernel's replica LOADS were latency-bound).
-__global__ void __maxnreg__(kCommRegs) replica_push_kernel(const RankTable* __restrict__ T,
-                                                           const CommTile* __restrict__ tiles, int ntiles,
-                                                           int64_t stage_stride) {
-  const uint64_t pol = l2_evict_first_policy();
-  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-    const CommTile t = tiles[ti];
-    const float* src = T->grad[T->global_rank[t.local]] + t.b_off;
-    float* dst = T->stage[t.src] + t.c_off * stage_stride + t.a_off;
-    if (t.vec) {
-      const int64_t nv = t.len / 4;
-      for (int64_t i = threadIdx.x; i < nv; i += kUnroll * kCommThreads) {
-        uint4 v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t j = i + u * kCommThreads;
-          if (j < nv) v[u] = ld_stream_v4(src + 4 * j, pol);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t j = i + u * kCommThreads;
-          if (j < nv) st_v4(dst + 4 * j, v[u]);
-        }
-      }
-    } else {
-      for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) dst[i] = src[i];
-    }
-  }
-  __threadfence_system();  // stores performed before the GradReady post
 }
 
 // ---------------------------------------------------------------------------
@@ -476,21 +434,14 @@ void launch_rs_reduce(const RankTable* T, const CommTile* tiles, int ntiles, int
 
 void launch_z1_adam(const RankTable* T, const CommTile* tiles, int ntiles, int z2, int replicas,
                     const AdamArgs* a, int /*nlocal*/, bool bf16_param, bool dbg, int ctas,
-                    cudaStream_t s, int64_t stage_stride) {
+                    cudaStream_t s) {
   if (ntiles <= 0) return;
   if (bf16_param)
     z1_adam_kernel<true><<<grid_for(ntiles, ctas), kThreads, 0, s>>>(T, tiles, ntiles, z2,
-                                                                     replicas, *a, dbg, stage_stride);
+                                                                     replicas, *a, dbg);
   else
     z1_adam_kernel<false><<<grid_for(ntiles, ctas), kThreads, 0, s>>>(T, tiles, ntiles, z2,
-                                                                      replicas, *a, dbg, stage_stride);
-  HZP_LAUNCH_CHECK();
-}
-
-void launch_replica_push(const RankTable* T, const CommTile* tiles, int ntiles, int64_t stage_stride, int ctas,
-                         cudaStream_t s) {
-  if (ntiles <= 0) return;
-  replica_push_kernel<<<grid_for(ntiles, ctas), kCommThreads, 0, s>>>(T, tiles, ntiles, stage_stride);
+                                                                      replicas, *a, dbg);
   HZP_LAUNCH_CHECK();
 }
 

@@ -47,7 +47,6 @@ struct RankTable {
   float* grad[kMaxRanks];   // fp32 grad shards [s2]
   void* wgrad[kMaxRanks];   // gradient ring buffers [wslots][slot]
   void* ag[kMaxRanks];      // AG ring + reuse cache [depth + cache][slot]
-  float* stage[kMaxRanks];  // DZP replica staging [replicas][s1] (dp / z2 >= 2)
   uint64_t* flags[kMaxRanks];
   // this process's NVLS multicast addresses (multi-process only, else null)
   void* ag_mc;     // Z3 group's AG buffer
@@ -99,10 +98,7 @@ void launch_rs_reduce(const RankTable* dev_table, const CommTile* tiles, int nti
                       FlagGate gate, int ctas, cudaStream_t s);
 void launch_z1_adam(const RankTable* dev_table, const CommTile* tiles, int ntiles, int z2,
                     int replicas, const AdamArgs* per_local, int nlocal, bool bf16_param,
-                    bool dbg, int ctas, cudaStream_t s, int64_t stage_stride = 0);
-// Replica push tiles (tiles.hpp push_layer_off): q's grad -> chunk owner's staging.
-void launch_replica_push(const RankTable* dev_table, const CommTile* tiles, int ntiles, int64_t stage_stride,
-                         int ctas, cudaStream_t s);
+                    bool dbg, int ctas, cudaStream_t s);
 // Post `value` into flags[q][post_kind][me] for every q in post_mask, then
 // wait until flags[me][wait_kind][q] >= wait_value for every q in wait_mask
 // (single CTA; either mask may be 0).

@@ -145,13 +145,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   // gradients over NVLink and must keep up with the backward: collective
   // priority; flat, it is HBM-only and gives way: measured 7B N=4 90.8 vs
   // 90.0 K tokens/s with, 1.3B N=4 404 vs 414 K without)
-  {
-    const char* op = std::getenv("HZP_EXP_OPTPRIO");  // TEMP experiment
-    const bool opt_mid = op ? std::atoi(op) != 0 : geom.replicas() > 1;
-    HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, opt_mid ? mid : lo));
-  }
-  if (geom.replicas() > 1 && std::getenv("HZP_EXP_PUSHSTREAM"))  // TEMP experiment
-    HZP_CUDA(cudaStreamCreateWithPriority(&push_stream, cudaStreamNonBlocking, mid));
+  HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, geom.replicas() > 1 ? mid : lo));
   const int n = static_cast<int>(plan.entries.size());
   done.resize(n);
   for (auto& e : done) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -179,9 +173,7 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   lay.ag_bytes = zero_copy_ag ? 0 : align_up(size_t(depth + cache_slots) * slot_elems * es, al);
   lay.wgrad = lay.ag + lay.ag_bytes;
   lay.wgrad_bytes = direct_grad ? 0 : align_up(size_t(wslots) * slot_elems * es, al);
-  lay.stage = lay.wgrad + lay.wgrad_bytes;
-  lay.stage_bytes = geom.replicas() > 1 ? align_up(size_t(geom.replicas()) * stage_stride() * 4, 256) : 0;
-  lay.total = align_up(lay.stage + lay.stage_bytes, al);
+  lay.total = align_up(lay.wgrad + lay.wgrad_bytes, al);
   arenas.resize(c.par.dp);
   std::vector<int> mine;
   if (emulate) {
@@ -237,7 +229,6 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
     table.grad[r] = arenas[r].grad;
     table.wgrad[r] = arenas[r].wgrad;
     table.ag[r] = arenas[r].ag;
-    table.stage[r] = arenas[r].stage;
     table.flags[r] = arenas[r].flags;
   }
   for (size_t i = 0; i < locals.size(); ++i) {
@@ -261,7 +252,6 @@ void Engine::carve(Arena& a) const {
   a.flags = reinterpret_cast<uint64_t*>(b + lay.flags);
   a.ag = lay.ag_bytes ? b + lay.ag : nullptr;
   a.wgrad = lay.wgrad_bytes ? b + lay.wgrad : nullptr;
-  a.stage = lay.stage_bytes ? reinterpret_cast<float*>(b + lay.stage) : nullptr;
 }
 
 ShareRecord Engine::share_record() const {
@@ -299,7 +289,6 @@ void Engine::open_peers(const ShareRecord* rec, int n) {
     table.grad[r] = a.grad;
     table.wgrad[r] = a.wgrad;
     table.ag[r] = a.ag;
-    table.stage[r] = a.stage;
     table.flags[r] = a.flags;
   }
   // bind this rank's AG / gradient regions into its groups' multicast
@@ -350,7 +339,6 @@ Engine::~Engine() {
   cudaEventDestroy(ev_z1);
   for (auto s : st) cudaStreamDestroy(s);
   if (opt_stream) cudaStreamDestroy(opt_stream);
-  if (push_stream) cudaStreamDestroy(push_stream);
 }
 
 int Engine::local_index(int rank) const {
@@ -370,7 +358,6 @@ void Engine::build_tiles() {
   z1_off = T.z1_off;
   z1_n = T.z1_n;
   z1_layer_off = T.z1_layer_off;
-  push_layer_off = T.push_layer_off;
   z1_wait_mask.assign(layers.size(), 0);
   if (!emulate)
     for (size_t l = 0; l < layers.size(); ++l)
@@ -462,42 +449,23 @@ AdamArgs Engine::next_adam_args() {
 
 void Engine::z1_adam(cudaStream_t s) {
   const AdamArgs a = next_adam_args();
-  if (geom.replicas() > 1) {  // every layer's replica parts into the chunk owners' staging first
-    const int L = static_cast<int>(layers.size());
-    launch_replica_push(dtable, dtiles + push_layer_off[0], push_layer_off[L] - push_layer_off[0], stage_stride(),
-                        kCommCtas, s);
-    barrier(s);  // every peer's pushes landed
-    launches += 1;
-  }
   launch_z1_adam(dtable, dtiles + z1_off, z1_n, geom.z2, geom.replicas(), &a, 1, bf16,
-                 locals.front().dbg != nullptr, kCommCtas, s, stage_stride());  // HBM-bound
+                 locals.front().dbg != nullptr, kCommCtas, s);  // HBM-bound
   ++launches;
-}
-
-void Engine::grad_final(int layer, cudaStream_t s) {
-  if (geom.replicas() > 1) {
-    launch_replica_push(dtable, dtiles + push_layer_off[layer], push_layer_off[layer + 1] - push_layer_off[layer],
-                        stage_stride(), kCommCtas, s);
-    ++launches;
-  }
-  if (!emulate && cfg.par.dp > 1) {
-    launch_flags(dtable, cfg.my_rank, kFlagGradReady, rank_mask(0, cfg.par.dp), ++grad_seq, 0, 0, 0, s);
-    ++launches;
-  }
 }
 
 void Engine::z1_layer(int layer, const AdamArgs& a, cudaStream_t s) {
   if (!emulate && cfg.par.dp > 1) {
-    // wait for the ranks this layer's Z1 reads gradients from (their pushes
-    // into our staging landed) and pushes parameters into (their reads of
-    // their shards for this layer are done): GradReady(l) = grad_seq, posted
-    // by grad_final in the same layer order on every rank
-    launch_flags(dtable, cfg.my_rank, 0, 0, 0, kFlagGradReady, z1_wait_mask[layer], grad_seq, s);
+    // announce "layer final here" to every rank, wait for the ranks this
+    // layer's Z1 reads gradients from / pushes parameters into
+    const uint64_t seq = ++grad_seq;
+    launch_flags(dtable, cfg.my_rank, kFlagGradReady, rank_mask(0, cfg.par.dp), seq, kFlagGradReady,
+                 z1_wait_mask[layer], seq, s);
     ++launches;
   }
   const int t0 = z1_layer_off[layer], nt = z1_layer_off[layer + 1] - t0;
   launch_z1_adam(dtable, dtiles + t0, nt, geom.z2, geom.replicas(), &a, 1, bf16, locals.front().dbg != nullptr,
-                 kCommCtas, s, stage_stride());
+                 kCommCtas, s);
   launches += nt > 0;
 }
 
@@ -546,7 +514,6 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
   HZP_CUDA(cudaStreamWaitEvent(st[1], ev_step0, 0));
   HZP_CUDA(cudaStreamWaitEvent(st[2], ev_step0, 0));
   HZP_CUDA(cudaStreamWaitEvent(opt_stream, ev_step0, 0));
-  if (push_stream) HZP_CUDA(cudaStreamWaitEvent(push_stream, ev_step0, 0));
   const char* in_dev = static_cast<const char*>(inputs);
   if (!on_device) {
     HZP_CUDA(cudaMemcpyAsync(dinputs, inputs, in_total, cudaMemcpyHostToDevice, cs));
@@ -736,15 +703,8 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
                    post_after[e.id], 0, 0, 0, s);
     if (e.kind == TaskKind::OptStep && !early_z1) barrier(s);  // every push landed, every grad pull done
     if (final_of[e.id] >= 0) {  // this task made a layer's gradient final: its Z1 now
-      // replica push + GradReady on the RS stream (the reference's AR-dzp(l)
-      // lives there), the optimizer on its own stream (later RSs never queue
-      // behind it)
-      cudaStream_t rs = push_stream ? push_stream : st[2];
-      if (s != rs) HZP_CUDA(cudaStreamWaitEvent(rs, done[e.id], 0));
-      grad_final(final_of[e.id], rs);
-      HZP_CUDA(cudaEventRecord(ev_z1, rs));
-      cudaStream_t zs = opt_stream;
-      HZP_CUDA(cudaStreamWaitEvent(zs, ev_z1, 0));
+      cudaStream_t zs = opt_stream;  // its own stream: later RSs never queue behind it
+      HZP_CUDA(cudaStreamWaitEvent(zs, done[e.id], 0));
       if (!adam_ready) {
         adam = next_adam_args();
         adam_ready = true;

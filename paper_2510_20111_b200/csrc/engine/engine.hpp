@@ -30,12 +30,10 @@ struct Arena {
   uint64_t* flags = nullptr;
   void* ag = nullptr;     // [depth + cache_slots][slot_elems]: ring, then the reuse cache
   void* wgrad = nullptr;  // [wslots][slot_elems] wire dtype (null when z2 == 1)
-  float* stage = nullptr;  // [replicas][s1] fp32: DZP replicas' gradients of this rank's Z1 chunk
 };
 
 struct ArenaLayout {
-  size_t param = 0, grad = 0, flags = 0, ag = 0, ag_bytes = 0, wgrad = 0, wgrad_bytes = 0, stage = 0,
-         stage_bytes = 0, total = 0;
+  size_t param = 0, grad = 0, flags = 0, ag = 0, ag_bytes = 0, wgrad = 0, wgrad_bytes = 0, total = 0;
 };
 
 struct LocalRank {
@@ -87,7 +85,6 @@ struct Engine {
   std::vector<uint64_t> ag_owners;  // [L] Z3 members owning part of layer l (multi-process)
   int z1_off = 0, z1_n = 0;
   std::vector<int> z1_layer_off;       // [L + 1] Z1 tiles per layer
-  std::vector<int> push_layer_off;     // [L + 1] replica-push tiles per layer (replicas > 1)
   std::vector<uint64_t> z1_wait_mask;  // [L] ranks whose GradReady(l) this rank's Z1(l) needs
   cudaEvent_t ev_z1 = nullptr;         // last per-layer Z1 of the step (async mode)
   ArenaLayout lay;
@@ -138,12 +135,6 @@ struct Engine {
   // Z1 of one layer as soon as its gradient is final everywhere it is read
   // from and its parameters are no longer read anywhere this step
   void z1_layer(int layer, const AdamArgs& a, cudaStream_t s);
-  // after the task that made layer `layer`'s gradient final, on its stream s:
-  // push the replicas' parts (replicas > 1) and post GradReady (multi-process)
-  void grad_final(int layer, cudaStream_t s);
-  // replica slots start 16-byte aligned (s1 need not be a multiple of 4)
-  int64_t stage_stride() const { return geom.replicas() > 1 ? (geom.s1 + 3) / 4 * 4 : 0; }
-  cudaStream_t push_stream = nullptr;  // replica pushes (replicas > 1)
   void barrier(cudaStream_t s);
   GradTarget grad_target(int li, int layer, int wslot, int mb) const;
   const void* layer_params(int li, int layer, int slot) const;

@@ -117,70 +117,42 @@ TileTables build_comm_tiles(const ShardGeom& g, const std::vector<Range64>& laye
   // Z1: each driven rank's chunk ∩ [0, P), cut at Z2 and Z3 segment bounds
   // and at layer bounds; grouped by layer (z1_layer_off) so the optimizer
   // step of a layer can run as soon as that layer's gradient is final.
-  // z1_tiles(r, l, li, emit): rank r's tiles of layer l (li = its local index).
-  auto z1_tiles = [&](int r, int l, int li, auto&& emit) {
-    const int i1 = r % g.z1;
-    int64_t e = std::max(int64_t(i1) * g.s1, layers[l].off);
-    const int64_t end = std::min({int64_t(i1 + 1) * g.s1, g.P, layers[l].off + layers[l].size});
-    while (e < end) {
-      const int j2 = static_cast<int>(e / g.s2), j3 = static_cast<int>(e / g.s3);
-      const int64_t stop = std::min({end, (j2 + 1) * g.s2, (j3 + 1) * g.s3});
-      const int64_t offs[3] = {e - i1 * g.s1, e - j2 * g.s2, e - j3 * g.s3};
-      // master/m/v and grads are fp32 (16-byte float4); the param stream is
-      // stored 4 elements at a time (float4 or 4 x bf16 = 8 bytes), so all
-      // three need offset % 4 == 0: model that as 4-byte elements.
-      const int eb[3] = {4, 4, 4};
-      const uint64_t mask = z1_targets(g, r, j3);
-      split_run(offs, eb, 3, stop - e, 4, [&](int64_t p, int64_t n, bool v) {
-        CommTile t{};
-        t.a_off = offs[0] + p;
-        t.b_off = offs[1] + p;
-        t.c_off = offs[2] + p;
-        t.mask = mask;
-        t.len = static_cast<int32_t>(n);
-        t.local = static_cast<int16_t>(li);
-        t.src = static_cast<int16_t>(j2);
-        t.vec = v;
-        emit(t);
-      }, kZ1TileElems);
-      e = stop;
-    }
-  };
   T.z1_off = static_cast<int>(tiles.size());
   T.z1_layer_off.assign(L + 1, T.z1_off);
   for (int l = 0; l < L; ++l) {
     T.z1_layer_off[l] = static_cast<int>(tiles.size());
-    for (size_t li = 0; li < local_ranks.size(); ++li)
-      z1_tiles(local_ranks[li], l, int(li), [&](const CommTile& t) { tiles.push_back(t); });
-  }
-  T.z1_layer_off[L] = static_cast<int>(tiles.size());
-  // Replica push (DZP replicas, dp / z2 >= 2): after a layer's gradient is
-  // final on rank q (segment j = q % z2 of replica b = q / z2), q stores its
-  // part of every Z1 chunk (in every Z1 group) into that chunk owner's
-  // staging slot b: tile {a_off: offset in r's chunk, b_off: offset in q's segment,
-  // c_off: replica b, src: destination rank r, local: q}.
-  T.push_layer_off.assign(L + 1, static_cast<int>(tiles.size()));
-  if (g.replicas() > 1) {
-    for (int l = 0; l < L; ++l) {
-      T.push_layer_off[l] = static_cast<int>(tiles.size());
-      for (size_t li = 0; li < local_ranks.size(); ++li) {
-        const int q = local_ranks[li];
-        // every Z1 group holds a (z1-way sharded) optimizer copy when z1 < dp:
-        // the chunk owners of q's elements in each of them
-        for (int r = 0; r < g.dp; ++r)
-          z1_tiles(r, l, int(li), [&](const CommTile& z) {
-            if (z.src != q % g.z2) return;
-            CommTile t = z;
-            t.c_off = q / g.z2;
-            t.src = static_cast<int16_t>(r);
-            t.mask = 0;
-            tiles.push_back(t);
-          });
+    for (size_t li = 0; li < local_ranks.size(); ++li) {
+      const int r = local_ranks[li];
+      const int i1 = r % g.z1;
+      int64_t e = std::max(int64_t(i1) * g.s1, layers[l].off);
+      const int64_t end = std::min({int64_t(i1 + 1) * g.s1, g.P, layers[l].off + layers[l].size});
+      while (e < end) {
+        const int j2 = static_cast<int>(e / g.s2), j3 = static_cast<int>(e / g.s3);
+        const int64_t stop = std::min({end, (j2 + 1) * g.s2, (j3 + 1) * g.s3});
+        const int64_t offs[3] = {e - i1 * g.s1, e - j2 * g.s2, e - j3 * g.s3};
+        // master/m/v and grads are fp32 (16-byte float4); the param stream is
+        // stored 4 elements at a time (float4 or 4 x bf16 = 8 bytes), so all
+        // three need offset % 4 == 0: model that as 4-byte elements.
+        const int eb[3] = {4, 4, 4};
+        const uint64_t mask = z1_targets(g, r, j3);
+        split_run(offs, eb, 3, stop - e, 4, [&](int64_t p, int64_t n, bool v) {
+          CommTile t{};
+          t.a_off = offs[0] + p;
+          t.b_off = offs[1] + p;
+          t.c_off = offs[2] + p;
+          t.mask = mask;
+          t.len = static_cast<int32_t>(n);
+          t.local = static_cast<int16_t>(li);
+          t.src = static_cast<int16_t>(j2);
+          t.vec = v;
+          tiles.push_back(t);
+        }, kZ1TileElems);
+        e = stop;
       }
     }
-    T.push_layer_off[L] = static_cast<int>(tiles.size());
   }
-  T.z1_n = T.z1_layer_off[L] - T.z1_off;
+  T.z1_layer_off[L] = static_cast<int>(tiles.size());
+  T.z1_n = static_cast<int>(tiles.size()) - T.z1_off;
   return T;
 }
 

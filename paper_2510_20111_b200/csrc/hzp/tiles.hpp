@@ -31,7 +31,6 @@ struct TileTables {
   std::vector<int> rs_off;  // [L + 1]
   int z1_off = 0, z1_n = 0;
   std::vector<int> z1_layer_off;  // [L + 1]: Z1 tiles of layer l (every driven rank)
-  std::vector<int> push_layer_off;  // [L + 1]: replica-push tiles of layer l (dp / z2 >= 2)
 };
 
 struct Range64 {

@@ -39,11 +39,7 @@ def _tiles(dp, z1, z2, z3, P, layers, rank, es):
     N.check(N.lib.hzp_comm_tiles(C.byref(par), P, offs, sizes, L, rank, es, out, n.value, C.byref(n),
                                  ag, rs, C.byref(z1o), C.byref(z1n)))
     t = [(x.a_off, x.b_off, x.c_off, x.mask, x.len, x.src, x.vec) for x in out[: n.value]]
-    N.check(N.lib.hzp_comm_push_tiles(C.byref(par), P, offs, sizes, L, rank, None, 0, C.byref(n)))
-    pout = (N.hzp_comm_tile * max(1, n.value))()
-    N.check(N.lib.hzp_comm_push_tiles(C.byref(par), P, offs, sizes, L, rank, pout, n.value, C.byref(n)))
-    push = [(x.a_off, x.b_off, x.c_off, x.len, x.src) for x in pout[: n.value]]
-    return {"tiles": t, "ag": list(ag), "rs": list(rs), "z1": (z1o.value, z1n.value), "push": push}
+    return {"tiles": t, "ag": list(ag), "rs": list(rs), "z1": (z1o.value, z1n.value)}
 
 
 def _worker(rank, world, port, z, layers, P, es, q):
@@ -129,25 +125,6 @@ def test_multirank_plans_and_tiles(world, z, dims, es):
                         assert (r % z2) * s2 + a == lo + b  # segment offset <-> layer offset
                         cov[b:b + n] += 1
                 assert np.all(cov == 1), (g0, l)
-    # replica pushes: every element of every Z1 chunk (every Z1 group) arrives
-    # once from the segment owner of each DZP replica b (rank j + b * z2), into
-    # slot b at the element's offset in the chunk
-    R = world // z2
-    got = np.zeros((world, R, s1), np.int32)
-    for q, v in enumerate(allv):
-        if R == 1:
-            assert not v["push"]
-            continue
-        for (a, b, c, n, r) in v["push"]:
-            assert c == q // z2  # replica index
-            e0 = (r % z1) * s1 + a
-            assert (q % z2) * s2 + b == e0  # q's segment offset <-> chunk offset
-            got[r, c, a:a + n] += 1
-    if R > 1:
-        for r in range(world):
-            lo = (r % z1) * s1
-            n_valid = max(0, min(s1, P - lo))
-            assert np.all(got[r, :, :n_valid] == 1) and not got[r, :, n_valid:].any(), r
     for g0 in range(0, world, z1):
         cov = np.zeros(P, np.int32)
         pushed = np.zeros((world, P), np.int32)
