@@ -92,19 +92,24 @@ __device__ __forceinline__ void gate_wait(const RankTable* __restrict__ T, const
 }
 
 // ---------------------------------------------------------------------------
-// AG: owner tile -> slot of every member of the owner's Z3 group.  Raw bits
-// (bit-exact by construction).
-template <int kEB, bool kMC>
+// AG, kMode: 0 = owner push by unicast stores to every member of the owner's
+// Z3 group, 1 = owner push by one multimem.st (NVLS), 2 = reader pull from
+// the owner's shard into the reader's own slot.  Raw bits (bit-exact by
+// construction).
+template <int kEB, int kMode>
 __global__ void __maxnreg__(kCommRegs) ag_push_kernel(const RankTable* __restrict__ T,
                                                       const CommTile* __restrict__ tiles, int ntiles,
                                                       int slot, int64_t slot_elems, int z3, FlagGate gate) {
+  constexpr bool kMC = kMode == 1;
   gate_wait(T, gate);
   const uint64_t pol = l2_evict_first_policy();
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const CommTile t = tiles[ti];
     const char* src = static_cast<const char*>(T->param[t.src]) + t.b_off * kEB;
     const int64_t dst_off = (slot * slot_elems + t.a_off) * kEB;
-    const int base = t.src - t.src % z3;
+    // destination ranks: every member of the owner's group (push), or the reader
+    const int base = kMode == 2 ? T->global_rank[t.local] : t.src - t.src % z3;
+    const int nd = kMode == 2 ? 1 : z3;
     char* const mc = kMC ? static_cast<char*>(T->ag_mc) + dst_off : nullptr;  // hoisted past the asm clobbers
     if (t.vec) {
       const int64_t nv = int64_t(t.len) * kEB / 16;
@@ -124,7 +129,7 @@ __global__ void __maxnreg__(kCommRegs) ag_push_kernel(const RankTable* __restric
           if (kMC) {
             mc_st_v4(mc + j * 16, v[u]);
           } else {
-            for (int q = base; q < base + z3; ++q) st_v4(static_cast<char*>(T->ag[q]) + dst_off + j * 16, v[u]);
+            for (int q = base; q < base + nd; ++q) st_v4(static_cast<char*>(T->ag[q]) + dst_off + j * 16, v[u]);
           }
         }
       }
@@ -133,7 +138,7 @@ __global__ void __maxnreg__(kCommRegs) ag_push_kernel(const RankTable* __restric
       const E* se = reinterpret_cast<const E*>(src);
       for (int64_t i = threadIdx.x; i < t.len; i += kCommThreads) {
         const E v = se[i];
-        for (int q = base; q < base + z3; ++q)
+        for (int q = base; q < base + nd; ++q)
           reinterpret_cast<E*>(static_cast<char*>(T->ag[q]) + dst_off)[i] = v;
       }
     }
@@ -397,16 +402,20 @@ int grid_for(int ntiles, int ctas) { return ntiles < ctas ? (ntiles > 0 ? ntiles
 }  // namespace
 
 void launch_ag_push(const RankTable* T, const CommTile* tiles, int ntiles, int slot, int64_t slot_elems,
-                    int z3, bool bf16, bool multicast, FlagGate gate, int ctas, cudaStream_t s) {
+                    int z3, bool bf16, AgMode mode, FlagGate gate, int ctas, cudaStream_t s) {
   if (ntiles <= 0) return;
   const int grid = grid_for(ntiles, ctas);
+#define HZP_AG(EB, M) ag_push_kernel<EB, M><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate)
   if (bf16) {
-    if (multicast) ag_push_kernel<2, true><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
-    else ag_push_kernel<2, false><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
+    if (mode == kAgMulticast) HZP_AG(2, 1);
+    else if (mode == kAgPull) HZP_AG(2, 2);
+    else HZP_AG(2, 0);
   } else {
-    if (multicast) ag_push_kernel<4, true><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
-    else ag_push_kernel<4, false><<<grid, kCommThreads, 0, s>>>(T, tiles, ntiles, slot, slot_elems, z3, gate);
+    if (mode == kAgMulticast) HZP_AG(4, 1);
+    else if (mode == kAgPull) HZP_AG(4, 2);
+    else HZP_AG(4, 0);
   }
+#undef HZP_AG
   HZP_LAUNCH_CHECK();
 }
 

@@ -7,7 +7,9 @@
 //               owner stores its span once into the group's NVLS multicast
 //               AG slot (multimem.st.v4) and the switch delivers it to every
 //               member's slot — the owner's link carries the layer once, not
-//               (z3 - 1) times, and the readers spend no SM time.
+//               (z3 - 1) times, and the readers spend no SM time.  In a
+//               group of 2 the one reader pulls instead (same single link
+//               crossing, faster unicast loads, no rendezvous).
 //   rs_reduce — gradient reduce-scatter within the Z2 group
 //               (collective.cpp:69-97 + train.cpp:306-323): the member that
 //               owns (layer ∩ its Z2 segment) reduces it and accumulates
@@ -88,10 +90,15 @@ enum RsMode {
   kRsMulticast = 2      // multimem.ld_reduce.add.acc::f32 (bf16 wire, NVLS)
 };
 
-// AG: owner tiles [tiles, +ntiles) into slot `slot` of every member of the
-// owner's Z3 group (z3 members from z3_base(owner)); multicast = NVLS store.
+enum AgMode {
+  kAgUnicastPush = 0,  // owner stores into every member's slot (the unicast model of kAgMulticast)
+  kAgMulticast = 1,    // owner: one multimem.st into the group's NVLS slot
+  kAgPull = 2          // reader copies the owners' spans into its own slot (pull-form tiles)
+};
+// AG of one layer into slot `slot`: owner-push tiles (z3 members from
+// z3_base(owner)) or reader-pull tiles (tiles.hpp ag_pull).
 void launch_ag_push(const RankTable* dev_table, const CommTile* tiles, int ntiles, int slot,
-                    int64_t slot_elems, int z3, bool bf16, bool multicast, FlagGate gate, int ctas,
+                    int64_t slot_elems, int z3, bool bf16, AgMode mode, FlagGate gate, int ctas,
                     cudaStream_t s);
 void launch_rs_reduce(const RankTable* dev_table, const CommTile* tiles, int ntiles, int wslot,
                       int64_t wslot_elems, int z2, bool bf16_wire, RsMode mode, bool assign, float scale,

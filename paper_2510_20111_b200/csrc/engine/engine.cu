@@ -354,6 +354,7 @@ void Engine::build_tiles() {
   for (const auto& l : locals) ranks.push_back(l.rank);
   TileTables T = build_comm_tiles(geom, lr, ranks, bf16 ? 2 : 4, direct_grad);
   ag_off = T.ag_off;
+  ag_pull = T.ag_pull;
   rs_off = T.rs_off;
   z1_off = T.z1_off;
   z1_n = T.z1_n;
@@ -365,6 +366,12 @@ void Engine::build_tiles() {
         const CommTile& t = T.tiles[i];
         for (int b = 0; b < geom.replicas(); ++b) z1_wait_mask[l] |= 1ull << (t.src + b * geom.z2);
         z1_wait_mask[l] |= t.mask;
+        // the owners we push parameters into are read by their whole Z3
+        // group (AG pull): those readers must be past this layer too
+        for (uint64_t m = t.mask; m; m &= m - 1) {
+          const int q = __builtin_ctzll(m);
+          z1_wait_mask[l] |= rank_mask(geom.z3_base(q), geom.z3);
+        }
       }
   // members of this rank's Z3 group whose shard holds part of each layer
   ag_owners.assign(layers.size(), 0);
@@ -387,8 +394,12 @@ void Engine::build_tiles() {
 void Engine::ag_layer(int layer, int slot, cudaStream_t s, bool ready_posted) {
   if (zero_copy_ag) throw std::invalid_argument("z3 == 1: the all-gather is the identity (layers read the shard)");
   const int t0 = ag_off[layer], nt = ag_off[layer + 1] - t0;
-  if (emulate) {
-    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, false, FlagGate{}, kCommCtas, s);
+  if (emulate || ag_pull) {
+    // pull (groups of 2): each reader copies the layer's owner spans into its
+    // own slot; its ring wait is already on this stream and the owners'
+    // shards do not change during the step, so no cross-GPU rendezvous
+    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, ag_pull ? kAgPull : kAgUnicastPush,
+                   FlagGate{}, kCommCtas, s);
     ++launches;
     return;
   }
@@ -399,8 +410,8 @@ void Engine::ag_layer(int layer, int slot, cudaStream_t s, bool ready_posted) {
   const uint64_t grp = rank_mask(geom.z3_base(me), geom.z3);
   launch_flags(dtable, me, kFlagAgReady, ready_posted ? 0 : grp, seq, kFlagAgReady, nt > 0 ? grp : 0, seq, s);
   if (nt > 0)
-    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, ag_multicast(), FlagGate{},
-                   kCommCtas, s);
+    launch_ag_push(dtable, dtiles + t0, nt, slot, slot_elems, geom.z3, bf16, kAgMulticast, FlagGate{}, kCommCtas,
+                   s);
   launch_flags(dtable, me, kFlagAgDone, nt > 0 ? grp : 0, seq, kFlagAgDone, ag_owners[layer], seq, s);
   launches += nt > 0 ? 3 : 2;
 }
@@ -579,7 +590,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
   // so an owner's multicast waits on the members' compute progress only, not
   // on their AG streams.  post_after[t] = AG sequence number to post after
   // compute task t (monotone); AGs with no ring wait are free at step start.
-  const bool post_ready_early = !emulate && !zero_copy_ag && cfg.par.dp > 1;
+  const bool post_ready_early = !emulate && !zero_copy_ag && !ag_pull && cfg.par.dp > 1;
   std::vector<uint64_t> post_after(n, 0);
   uint64_t post_at_start = 0;
   if (post_ready_early) {

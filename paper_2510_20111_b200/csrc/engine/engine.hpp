@@ -83,6 +83,7 @@ struct Engine {
   CommTile* dtiles = nullptr;
   std::vector<int> ag_off, rs_off;  // [L + 1] per layer tile ranges
   std::vector<uint64_t> ag_owners;  // [L] Z3 members owning part of layer l (multi-process)
+  bool ag_pull = false;             // Z3 groups of 2: readers pull (tiles in pull form)
   int z1_off = 0, z1_n = 0;
   std::vector<int> z1_layer_off;       // [L + 1] Z1 tiles per layer
   std::vector<uint64_t> z1_wait_mask;  // [L] ranks whose GradReady(l) this rank's Z1(l) needs
@@ -121,6 +122,7 @@ struct Engine {
   // same choice (multicast groups: the sum rounded to bf16 like the switch).
   bool rs_multicast_group() const { return bf16 && !direct_grad && geom.z2 >= 3; }
   bool ag_multicast() const { return !emulate && cfg.par.dp > 1 && !zero_copy_ag && geom.z3 >= 3; }
+  // (groups of 2 pull: tiles.hpp ag_pull)
   bool rs_multicast() const { return !emulate && cfg.par.dp > 1 && rs_multicast_group(); }
   void carve(Arena& a) const;
   ShareRecord share_record() const;

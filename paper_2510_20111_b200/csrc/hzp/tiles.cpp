@@ -64,8 +64,40 @@ TileTables build_comm_tiles(const ShardGeom& g, const std::vector<Range64>& laye
   // owns (layer ∩ o's Z3 shard).  o stores it into the AG slot of every
   // member of its Z3 group (one multimem.st on NVLS; the union over the
   // group's owners covers the layer once).
+  //
+  // AG (reader pull, Z3 groups of 2): per layer, per driven rank r, the
+  // layer's spans by owner; r copies them from the owners' shards into its
+  // own slot (with one peer the owner's link carries the layer once either
+  // way, and a pull needs no rendezvous: the owner's shard does not change
+  // during the step).
   T.ag_off.assign(L + 1, 0);
-  for (int l = 0; l < L; ++l) {
+  T.ag_pull = g.z3 == 2;
+  for (int l = 0; l < L && T.ag_pull; ++l) {
+    T.ag_off[l] = static_cast<int>(tiles.size());
+    for (size_t li = 0; li < local_ranks.size(); ++li) {
+      const int r = local_ranks[li];
+      int64_t e = layers[l].off;
+      const int64_t end = layers[l].off + layers[l].size;
+      while (e < end) {
+        const int j3 = static_cast<int>(e / g.s3);
+        const int64_t stop = std::min(end, (j3 + 1) * g.s3);
+        const int64_t offs[2] = {e - layers[l].off, e - j3 * g.s3};
+        const int eb[2] = {es, es};
+        split_run(offs, eb, 2, stop - e, 16 / es, [&](int64_t p, int64_t n, bool v) {
+          CommTile t{};
+          t.a_off = offs[0] + p;
+          t.b_off = offs[1] + p;
+          t.len = static_cast<int32_t>(n);
+          t.local = static_cast<int16_t>(li);
+          t.src = static_cast<int16_t>(g.z3_base(r) + j3);
+          t.vec = v;
+          tiles.push_back(t);
+        });
+        e = stop;
+      }
+    }
+  }
+  for (int l = 0; l < L && !T.ag_pull; ++l) {
     T.ag_off[l] = static_cast<int>(tiles.size());
     for (size_t li = 0; li < local_ranks.size(); ++li) {
       const int o = local_ranks[li];

@@ -19,7 +19,8 @@ struct CommTile {
   int64_t c_off;   // Z1: param-shard offset
   uint64_t mask;   // Z1: push targets, bit q = global rank q
   int32_t len;     // elements
-  int16_t local;   // index of the rank among the ctx's driven ranks (AG: the owner; RS / Z1: the destination)
+  int16_t local;   // index of the rank among the ctx's driven ranks (AG push: the owner, AG pull: the reader;
+                   // RS / Z1: the destination)
   int16_t src;     // AG: owner rank | RS: Z2 group base | Z1: Z2 segment index j
   int32_t vec;     // 1 = every address 16-byte aligned and len a multiple of the vector
   int32_t pad_;
@@ -28,6 +29,7 @@ struct CommTile {
 struct TileTables {
   std::vector<CommTile> tiles;
   std::vector<int> ag_off;  // [L + 1]
+  bool ag_pull = false;     // AG tiles in reader-pull form (Z3 groups of 2) instead of owner-push
   std::vector<int> rs_off;  // [L + 1]
   int z1_off = 0, z1_n = 0;
   std::vector<int> z1_layer_off;  // [L + 1]: Z1 tiles of layer l (every driven rank)

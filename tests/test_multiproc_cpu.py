@@ -6,7 +6,8 @@ checks the multi-rank invariants the device kernels rely on:
   * every rank derives the identical launch order / slot plan;
   * AG tiles: rank r pushes exactly the part of each layer inside its own
     Z3 shard (e // s3 == r % z3, train.cpp:229-249); the owners of a Z3
-    group together cover each layer exactly once;
+    group together cover each layer exactly once (groups of 2: pull form,
+    every reader covers each layer once from the elements' owners);
   * RS tiles of a Z2 group partition (layer ∩ segment) across its members;
   * Z1 tiles of a Z1 group partition [0, P), and every element is pushed to
     exactly the group members q with q % z3 == e // s3 (train.cpp:361-379).
@@ -102,7 +103,16 @@ def test_multirank_plans_and_tiles(world, z, dims, es):
         assert p.exitcode == 0
     # identical plans on every rank
     assert all(v["plan"] == allv[0]["plan"] for v in allv)
-    for g0 in range(0, world, z3):
+    if z3 == 2:  # groups of 2: pull form, every reader covers each layer once from the owners
+        for r, v in enumerate(allv):
+            for l, (lo, ln) in enumerate(layers):
+                cov = np.zeros(ln, np.int32)
+                for (a, b, c, m, n, src, vec) in v["tiles"][v["ag"][l]:v["ag"][l + 1]]:
+                    cov[a:a + n] += 1
+                    owner = src - (r - r % z3)
+                    assert 0 <= owner < z3 and owner * s3 + b == lo + a
+                assert np.all(cov == 1), (r, l)
+    for g0 in range(0, world if z3 != 2 else 0, z3):
         for l, (lo, ln) in enumerate(layers):
             cov = np.zeros(ln, np.int32)
             for r in range(g0, g0 + z3):
