@@ -240,30 +240,33 @@ MLP_CASES = {
 }
 
 
+def _ref_mlp_one(arg):
+    """One single-threaded run of the reference's steps (a pool worker)."""
+    import numpy as np
+    from oracle import load_ref
+    case, steps = arg
+    ref = load_ref()
+    d = np.asarray(case["dims"], dtype=np.int32)
+    z1, z2, z3 = case["z"]
+    losses = np.zeros(case["dp"], np.float32)
+    sec = ref.L.ref_time_steps_f32(d, len(d) - 1, case["dp"], z1, z2, z3, case["mbs"], case["batch"], 2024,
+                                   steps, case["prec"], losses)
+    return sec, losses
+
+
 def ref_mlp(case, steps, cores=1):
     """The reference's train_step_hzp<float> (oracle/_ref = its sources
     compiled unmodified) on the same config: rows/s on `cores` concurrent
     single-threaded processes (the reference has no threading)."""
-    import numpy as np
     from oracle import load_ref
-    ref = load_ref()
-    if ref is None:
+    if load_ref() is None:
         return None
-    d = np.asarray(case["dims"], dtype=np.int32)
-    z1, z2, z3 = case["z"]
-
-    def one(_=None):
-        losses = np.zeros(case["dp"], np.float32)
-        sec = ref.L.ref_time_steps_f32(d, len(d) - 1, case["dp"], z1, z2, z3, case["mbs"], case["batch"], 2024,
-                                       steps, case["prec"], losses)
-        return sec, losses
-
     if cores > 1:
         import multiprocessing as mp
         with mp.get_context("fork").Pool(cores) as pool:
-            res = pool.map(one, range(cores))
+            res = pool.map(_ref_mlp_one, [(case, steps)] * cores)
     else:
-        res = [one()]
+        res = [_ref_mlp_one((case, steps))]
     rows = case["dp"] * case["mbs"] * case["batch"]
     return {"value": sum(rows / sec for sec, _ in res), "sec_per_step": res[0][0], "cores": cores,
             "losses": [float(x) for x in res[0][1]]}

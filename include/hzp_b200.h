@@ -399,7 +399,11 @@ int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K,
 int hzp_attention_fwd(const void* qkv, void* O, float* lse, int b, int nh, int S, int h, void* stream);
 int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const float* lse, float* D,
                       void* dqkv, void* dsT, int b, int nh, int S, int h, void* stream);
-/* Same contract, fp32 operands on the CUDA cores (fp32 parity tier). */
+/* Same contract, fp32 operands on the CUDA cores (fp32 parity tier): each
+ * output a left fold over k in ascending order, separately rounded multiply
+ * and add (train.cpp:68-79).  epi 1 = store, 2 = accumulate, 3 = store
+ * tanh(acc) with the host libm's tanhf bit for bit (the hidden-layer
+ * activation of the reference's MLP). */
 int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                  int ldb, int ldc, int a_mn, int b_mn, int epi, void* stream);
 

@@ -98,6 +98,12 @@ void orc_bf16_round_vec(float* v, size_t n) {
   for (size_t k = 0; k < n; ++k) v[k] = orc_bf16_round(v[k]);
 }
 
+/* The host libm's tanhf (what the reference's std::tanh on float calls,
+ * train.cpp:68-79) over a vector: the checker for the device restatement. */
+void orc_tanhf_vec(const float* x, float* y, size_t n) {
+  for (size_t k = 0; k < n; ++k) y[k] = tanhf(x[k]);
+}
+
 /* shard_elems (src/memory.cpp:13-15): ceil(n / parts) */
 int64_t orc_shard_elems(int64_t n, int64_t parts) { return (n + parts - 1) / parts; }
 

@@ -98,6 +98,7 @@ class Oracle:
         L.orc_bf16_round.argtypes = [C.c_float]
         L.orc_bf16_round.restype = C.c_float
         L.orc_bf16_round_vec.argtypes = [_f32p, C.c_size_t]
+        L.orc_tanhf_vec.argtypes = [_f32p, _f32p, C.c_size_t]
         L.orc_fnv1a.argtypes = [C.c_void_p, C.c_size_t]
         L.orc_fnv1a.restype = u64
         for sfx, p in (("f32", _f32p), ("f64", _f64p)):
@@ -138,6 +139,12 @@ class Oracle:
     def bf16_round(self, x: np.ndarray) -> np.ndarray:
         out = np.ascontiguousarray(x, dtype=np.float32).copy()
         self.L.orc_bf16_round_vec(out, out.size)
+        return out
+
+    def tanhf(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.empty_like(x)
+        self.L.orc_tanhf_vec(x, out, x.size)
         return out
 
     def fnv1a(self, a: np.ndarray) -> str:

@@ -931,6 +931,7 @@ int hzp_gemm_f32(const float* A, const float* B, float* C, int M, int N, int K, 
     e.ldc = ldc;
     e.out_bf16 = 0;
     e.mode = epi == 2 ? kEpiAccum : kEpiStore;
+    if (epi == 3) e.act = kActTanh;
     gemm_f32_ordered(A, B, C, s, e, static_cast<cudaStream_t>(stream));
   });
 }

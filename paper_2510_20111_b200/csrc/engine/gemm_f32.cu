@@ -2,12 +2,14 @@
 // tier B).  Each output element accumulates over k in ascending order with
 // separately rounded multiply and add, starting from the bias, which is
 // exactly the reference's loop (train.cpp:68-79 forward; 118-148 backward),
-// so the only fp32 divergence left in a full step is tanhf's last ulp.
+// and the tanh epilogue is the bit-exact restatement of the host libm's tanhf
+// (libm_f32.cuh), so the fp32 step is bitwise the reference's.
 // Tiled through shared memory (32x32 outputs, K chunks of 32): tiling along K
 // keeps each thread's summation order intact.
 #include <cmath>
 
 #include "engine/gemm.cuh"
+#include "engine/libm_f32.cuh"
 
 namespace hzp {
 namespace {
@@ -46,7 +48,7 @@ __global__ void __launch_bounds__(kT* kT) gemm_f32_ordered_kernel(const float* _
   const int64_t ci = int64_t(m) * e.ldc + n;
   float v = acc;
   switch (e.act) {
-    case kActTanh: v = tanhf(acc); break;
+    case kActTanh: v = tanhf_fdlibm(acc); break;
     case kActTanhGrad: {
       const float a = static_cast<const float*>(e.aux)[int64_t(m) * e.ldaux + n];
       v = __fmul_rn(acc, __fsub_rn(1.f, __fmul_rn(a, a)));

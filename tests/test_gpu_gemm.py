@@ -166,3 +166,32 @@ def test_epilogues_match_torch(gpu, M, N, K):
     _ex(As, Bs, C, M, N, K, lda, ldb, N, 0, 0, mode=2, out_bf16=0)
     torch.cuda.synchronize()
     assert (C - acc).abs().max().item() < 1e-3
+
+
+def test_f32_tanh_epilogue_is_libm_tanhf(gpu, oracle):
+    """The fp32 tier's tanh epilogue (libm_f32.cuh) against the host libm's
+    tanhf — what the reference's std::tanh on float calls — bit for bit, on
+    every 61st float of [-12, 12] plus the branch edges of the fdlibm
+    algorithm (2^-55, 2^-25, ln2/2, 1.5 ln2, 1, 27 ln2, 22).  Through the
+    GEMM itself: K = 1, A = 1, so acc = x exactly."""
+    import numpy as np
+    from paper_2510_20111_b200.engine import gemm_f32
+    lo = np.float32(-12.0).view(np.uint32)
+    hi = np.float32(12.0).view(np.uint32)
+    pos = np.arange(61, int(hi), 61, dtype=np.uint32)  # (x = -0 would reach the epilogue as 0 + -0 = +0)
+    edges = np.array([2.0 ** -55, 2.0 ** -25, 0.34657359, 0.5, 1.0, 1.03972077, 18.714973, 22.0, 11.0],
+                     dtype=np.float32)
+    nb = np.concatenate([edges, np.nextafter(edges, np.float32(0)), np.nextafter(edges, np.float32(30))])
+    x = np.concatenate([pos.view(np.float32), nb]).astype(np.float32)
+    x = np.concatenate([x, -x, np.zeros(1, np.float32)])
+    assert int(lo) & 0x80000000
+    want = oracle.tanhf(x)
+    n = x.size  # C [1, n] = 1 x B^T, B = x as [n, 1] (the grid spans n along x)
+    X = torch.from_numpy(x).to(gpu).view(n, 1)
+    one = torch.ones(1, 1, device=gpu)
+    Y = torch.empty(1, n, device=gpu)
+    gemm_f32(one.data_ptr(), X.data_ptr(), Y.data_ptr(), 1, n, 1, 1, 1, n, 0, 0, 3)
+    torch.cuda.synchronize()
+    got = Y.view(-1).cpu().numpy()
+    bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
+    assert bad.size == 0, (bad.size, x[bad[:4]], got[bad[:4]], want[bad[:4]])
