@@ -674,6 +674,7 @@ def run_hzp(args):
     eng.step_async(dev[0].data_ptr(), True)
     eng.sync()
     tl = eng.timeline()
+    z1tl = eng.z1_timeline()
     eng.set_timeline(False)
     idle = max_over_ranks(tl["compute_idle_ms"])
     mk = max_over_ranks(tl["makespan_ms"])
@@ -700,9 +701,24 @@ def run_hzp(args):
             key = {0: "before_fwd", 2: "before_bwd", 1: "before_bwd", 6: "before_opt"}[k]
             gaps[key] += s0 - prev
         prev = max(prev, e0)
+    # the per-layer optimizer on its own stream: when each layer's gradient
+    # was final here, when its cross-rank GradReady waits passed, when it ended
+    z1info = None
+    if z1tl["end_ms"]:
+        last_bwd = max((e0 for _, e0, k in comp if k != 6), default=0.0)
+        busy = sum(e - b for b, e in zip(z1tl["start_ms"], z1tl["end_ms"]))
+        wait = sum(b - r for r, b in zip(z1tl["ready_ms"], z1tl["start_ms"]))
+        z1info = {"busy_ms": round(max_over_ranks(busy), 3), "wait_ms": round(max_over_ranks(wait), 3),
+                  "end_after_last_bwd_ms": round(max_over_ranks(max(z1tl["end_ms"]) - last_bwd), 3),
+                  "layers_rank0": [[l, round(r, 2), round(b, 2), round(e, 2)] for l, (r, b, e) in
+                                   enumerate(zip(z1tl["ready_ms"], z1tl["start_ms"], z1tl["end_ms"]))],
+                  "definition": "per-layer Z1 on the optimizer stream (CUDA events): busy = sum of kernel "
+                                "spans, wait = sum of GradReady waits / queueing, end_after_last_bwd = "
+                                "last Z1 end - last backward end (max over ranks); layers_rank0 = "
+                                "[layer, ready, start, end] ms from step start"}
     sim = simulator_prediction(c, N, z1, z2, z3, nmb, mb, args.depth)
     exposed = {"compute_idle_ms": round(idle, 3), "makespan_ms": round(mk, 3), "simulator": sim,
-               "idle_by_next_task_ms": {k: round(v, 3) for k, v in gaps.items()},
+               "idle_by_next_task_ms": {k: round(v, 3) for k, v in gaps.items()}, "z1_per_layer": z1info,
                "frac": round(idle / mk, 4) if mk else None,
                "definition": "last compute end - sum of compute task times (sched.cpp:341-350), "
                              "CUDA-event timeline of one extra step, max over ranks"}

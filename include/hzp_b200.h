@@ -322,6 +322,11 @@ int hzp_launch_log(const hzp_ctx* ctx, hzp_launch_rec* out, int cap, int* n);
  * (= last compute end - sum compute busy, sched.cpp:341-350). */
 int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, int* n,
                  double* compute_idle_ms, double* compute_busy_ms, double* makespan_ms);
+/* Per-layer optimizer (Z1) times of the last step (requires cfg.timeline;
+ * async mode: *n = layers, vanilla: *n = 0 — one tail kernel): ms from step
+ * start when the layer's gradient was final on this rank, when every rank it
+ * reads from / pushes into had posted GradReady, and when its kernel ended. */
+int hzp_z1_timeline(const hzp_ctx* ctx, double* ready_ms, double* start_ms, double* end_ms, int cap, int* n);
 /* Turn per-task event recording on/off for the following steps (events are
  * created on first use), so a timed run can be measured untouched and one
  * extra step recorded for hzp_timeline. */

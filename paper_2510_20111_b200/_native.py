@@ -148,6 +148,7 @@ SIGNATURES = [
     ("hzp_launch_log", C.c_int, [_vp, _P(hzp_launch_rec), C.c_int, _P(C.c_int)]),
     ("hzp_timeline", C.c_int, [_vp, _P(C.c_double), _P(C.c_double), C.c_int, _P(C.c_int),
                                _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
+    ("hzp_z1_timeline", C.c_int, [_vp, _P(C.c_double), _P(C.c_double), _P(C.c_double), C.c_int, _P(C.c_int)]),
     ("hzp_set_timeline", C.c_int, [_vp, C.c_int]),
     ("hzp_ctx_launch_count", C.c_int, [_vp, _P(C.c_int64)]),
     ("hzp_kernel_launches", C.c_uint64, []),

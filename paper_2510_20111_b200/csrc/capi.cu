@@ -607,15 +607,7 @@ int hzp_set_timeline(hzp_ctx* ctx, int on) {
     Engine& e = *ctx->e;
     HZP_CUDA(cudaSetDevice(e.cfg.device));
     HZP_CUDA(cudaDeviceSynchronize());
-    const int n = static_cast<int>(e.plan.entries.size());
-    if (on && static_cast<int>(e.tev0.size()) != n) {
-      e.tev0.resize(n);
-      e.tev1.resize(n);
-      for (int i = 0; i < n; ++i) {
-        HZP_CUDA(cudaEventCreate(&e.tev0[i]));
-        HZP_CUDA(cudaEventCreate(&e.tev1[i]));
-      }
-    }
+    e.timeline_events(on != 0);
     e.cfg.timeline = on ? 1 : 0;
   });
 }
@@ -647,6 +639,24 @@ int hzp_timeline(const hzp_ctx* ctx, double* start_ms, double* end_ms, int cap, 
     if (compute_idle_ms) *compute_idle_ms = last_c - busy;
     if (compute_busy_ms) *compute_busy_ms = busy;
     if (makespan_ms) *makespan_ms = mk;
+  });
+}
+
+int hzp_z1_timeline(const hzp_ctx* ctx, double* ready_ms, double* start_ms, double* end_ms, int cap, int* n) {
+  if (!ctx || !n) return HZP_ERR_ARG;
+  return guarded([&] {
+    const Engine& e = *ctx->e;
+    HZP_CUDA(cudaEventSynchronize(e.ev_step1));
+    *n = e.z1_timed ? static_cast<int>(e.layers.size()) : 0;
+    for (int l = 0; l < *n && l < cap; ++l) {
+      float a = 0, b = 0, c = 0;
+      HZP_CUDA(cudaEventElapsedTime(&a, e.ev_step0, e.zev_ready[l]));
+      HZP_CUDA(cudaEventElapsedTime(&b, e.ev_step0, e.zev_start[l]));
+      HZP_CUDA(cudaEventElapsedTime(&c, e.ev_step0, e.zev_end[l]));
+      if (ready_ms) ready_ms[l] = a;
+      if (start_ms) start_ms[l] = b;
+      if (end_ms) end_ms[l] = c;
+    }
   });
 }
 

@@ -419,14 +419,13 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
     for (int j = 0; j < nj; ++j) {
       mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
-      // Two passes over S_j in TMEM (32 columns at a time keeps the register
-      // footprint small): the row max, then P = 2^(s c - mref) packed to bf16
-      // and stored over S_j's first 64 columns — chunk c's P lands on columns
-      // [16c, 16c+16), already consumed.
+      // Two passes over the row's 128 scores, read from TMEM once into
+      // registers: the row max, then P = 2^(s c - mref) packed to bf16 and
+      // stored over S_j's first 64 columns (chunk c's P on [16c, 16c+16)).
       const bool diag = j == nj - 1;
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      uint32_t r[128];  // the row's scores, kept for pass 2 (S is read from TMEM once)
       {  // pass 1: all 128 scores in flight at once, one wait
-        uint32_t r[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32_nw(tmem + lane_off + s_col + c * 32, r + 32 * c);
         tmem_wait_ld32(r);
@@ -449,27 +448,17 @@ __global__ void __launch_bounds__(kThreads2, 1) attn_fwd2_kernel(const __grid_co
       const float mref = bump ? mx : m;
       const float corr = bump ? exp2_fast(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
       // pass 2: P = 2^(s c - mref), FFMA2 per pair; 2 of every 8 pairs' exp2
-      // on the FMA pipe so MUFU (16/clk/SM) stops bounding the tile.  Chunk
-      // c+1's scores are loaded while chunk c is exponentiated.
+      // on the FMA pipe so MUFU (16/clk/SM) stops bounding the tile.
       const uint64_t nm2 = f2_pack(-mref, -mref);
       uint64_t acc[4] = {0, 0, 0, 0};
-      uint32_t rb[2][32];
-      tmem_ld32_nw(tmem + lane_off + s_col, rb[0]);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t* r = rb[c & 1];
-        tmem_wait_ld32(r);
-        if (c + 1 < 4) tmem_ld32_nw(tmem + lane_off + s_col + (c + 1) * 32, rb[(c + 1) & 1]);
+        const uint32_t* rc = r + 32 * c;  // (the diagonal mask was applied in pass 1)
         uint32_t pw[16];
-        if (diag) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i > row) r[i] = 0xff800000u;
-        }
 #pragma unroll
         for (int ii = 0; ii < 16; ++ii) {
           const int i = c * 16 + ii;
-          const uint64_t x = f2_fma(f2_pack(__uint_as_float(r[2 * ii]), __uint_as_float(r[2 * ii + 1])), sc2, nm2);
+          const uint64_t x = f2_fma(f2_pack(__uint_as_float(rc[2 * ii]), __uint_as_float(rc[2 * ii + 1])), sc2, nm2);
           uint64_t e;
           if ((i & 7) >= HZP_ATTN_POLY_FROM) {
             e = exp2_poly2(x);
@@ -557,6 +546,7 @@ constexpr int kBQ2 = 64;  // query rows per backward sub-tile
 constexpr int kThreadsB = 320;  // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 struct AttnBwdParams {
   CUtensorMap tmQ, tmK, tmV, tmdO;
+  CUtensorMap tmdS;  // dS^T as {q, key, head, seq}, box {64, 128}, SW128 (TMA store)
   const float* V;    // [2][z][S]: -rowsum(dO * O) / sqrt(d) | -lse log2(e)
   int64_t zS;        // z * S (offset of the second vector)
   uint16_t* dqkv;    // [b, S, 3h]: dK, dV written into the k / v thirds
@@ -576,7 +566,12 @@ constexpr int kQStages = 4;
 constexpr int kBOffQ = 2 * kTileBytes;                 // 4 x 16 KB
 constexpr int kBOffdO = kBOffQ + kQStages * kQTile;    // 4 x 16 KB
 constexpr int kBOffVec = kBOffdO + kQStages * kQTile;  // 4 x (-lse log2 e [64] | -D/sqrt(d) [64])
-constexpr int kBOffBar = kBOffVec + kQStages * 512;
+// dS^T of one sub-tile (128 keys x 64 queries bf16, the SW128 image of the
+// TMA box) staged for one bulk tensor store: a thread's 64 bytes of a key
+// row as direct global stores were 32 rows per warp instruction (~1 K L1
+// wavefronts per sub-tile, holding the softmax warps' registers).
+constexpr int kBOffDs = kBOffVec + kQStages * 512;      // 16 KB (1024-aligned)
+constexpr int kBOffBar = kBOffDs + kQTile;
 constexpr size_t kBSmem = size_t(kBOffBar) + 256 + 1024;
 static_assert(kBSmem <= 232448, "attention backward smem budget");
 
@@ -762,13 +757,28 @@ __global__ void __launch_bounds__(kThreadsB, 1) attn_bwd_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
-      if (p.dsT) {  // legacy dQ path (dQ = dS K as a GEMM over dS^T in HBM)
-        uint4* dsg = reinterpret_cast<uint4*>(p.dsT + (int64_t(z) * p.S + k0 + row) * p.S + q0 + half * 32);
+      if (p.dsT) {  // dQ = dS K as a GEMM over dS^T in HBM
+        // the previous sub-tile's store has finished reading the buffer
+        const bool issuer = warp == 2 && lane == 0;
+        if (issuer && it > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const uint32_t rb = smem_u32(smem + kBOffDs) + row * 128;
 #pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4)
-          dsg[j4] = make_uint4(dsw[4 * j4], dsw[4 * j4 + 1], dsw[4 * j4 + 2], dsw[4 * j4 + 3]);
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const uint32_t c = (half * 4 + j4) ^ (row & 7);  // SW128: 16-byte chunk ^ row % 8
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rb + c * 16), "r"(dsw[4 * j4]),
+                       "r"(dsw[4 * j4 + 1]), "r"(dsw[4 * j4 + 2]), "r"(dsw[4 * j4 + 3])
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (issuer) {
+          tma_store_4d(&p.tmdS, smem + kBOffDs, q0, k0, head, seq);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     }
+    if (p.dsT && warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     mbar_wait(acc_done, 0);
     tc_fence_after();
     const int64_t rowbase = (int64_t(seq) * p.S + k0 + row) * (3 * int64_t(p.h)) + int64_t(head) * kHd;
@@ -1127,6 +1137,7 @@ void attention_bwd_tc(const uint16_t* qkv, const uint16_t* dO, const float* lse,
   p.zS = int64_t(b) * nh * S;
   p.dqkv = dqkv;
   p.dsT = dsT;
+  if (dsT) p.tmdS = make_tma_map_bf16(dsT, S, S, S, 128, nh, b, int64_t(S) * S, int64_t(S) * S * nh);
   p.S = S;
   p.h = h;
   p.nh = nh;

@@ -136,27 +136,20 @@ Engine::Engine(const hzp_engine_config& c) : cfg(c) {
   // compute highest, so a pending persistent GEMM takes every SM it needs
   // before any queued collective / optimizer CTA (those then fill the space
   // beside the resident GEMM CTAs, one per SM); collectives next; the
-  // per-layer optimizer lowest (it has the most slack).
+  // per-layer optimizer lowest: its grids are thousands of CTAs, and at the
+  // collectives' priority a rank's later RS kernels queued behind them, so
+  // its GradReady reached the other ranks late (MoE N = 4: 238 K -> 265 K
+  // tokens/s at the lowest priority, 7B N = 4: 94.7 K -> 96.1 K;
+  // profiles/r02_optprio_*.jsonl).
   const int mid = hi < lo ? std::min(lo, hi + 1) : hi;
   HZP_CUDA(cudaStreamCreateWithPriority(&st[0], cudaStreamNonBlocking, hi));
   HZP_CUDA(cudaStreamCreateWithPriority(&st[1], cudaStreamNonBlocking, mid));
   HZP_CUDA(cudaStreamCreateWithPriority(&st[2], cudaStreamNonBlocking, mid));
-  // (with DZP replicas the per-layer optimizer also moves the replicas'
-  // gradients over NVLink and must keep up with the backward: collective
-  // priority; flat, it is HBM-only and gives way: measured 7B N=4 90.8 vs
-  // 90.0 K tokens/s with, 1.3B N=4 404 vs 414 K without)
-  HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, geom.replicas() > 1 ? mid : lo));
+  HZP_CUDA(cudaStreamCreateWithPriority(&opt_stream, cudaStreamNonBlocking, lo));
   const int n = static_cast<int>(plan.entries.size());
   done.resize(n);
   for (auto& e : done) HZP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  if (c.timeline) {
-    tev0.resize(n);
-    tev1.resize(n);
-    for (int i = 0; i < n; ++i) {
-      HZP_CUDA(cudaEventCreate(&tev0[i]));
-      HZP_CUDA(cudaEventCreate(&tev1[i]));
-    }
-  }
+  if (c.timeline) timeline_events(true);
   HZP_CUDA(cudaEventCreate(&ev_step0));
   HZP_CUDA(cudaEventCreate(&ev_step1));
   HZP_CUDA(cudaEventCreateWithFlags(&ev_opt, cudaEventDisableTiming));
@@ -311,6 +304,21 @@ void Engine::open_peers(const ShareRecord* rec, int n) {
   peers_open = true;
 }
 
+void Engine::timeline_events(bool on) {
+  const size_t n = plan.entries.size(), nl = layers.size();
+  if (!on || tev0.size() == n) return;
+  tev0.resize(n);
+  tev1.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    HZP_CUDA(cudaEventCreate(&tev0[i]));
+    HZP_CUDA(cudaEventCreate(&tev1[i]));
+  }
+  for (auto* v : {&zev_ready, &zev_start, &zev_end}) {
+    v->resize(nl);
+    for (auto& e : *v) HZP_CUDA(cudaEventCreate(&e));
+  }
+}
+
 Engine::~Engine() {
   cudaDeviceSynchronize();
   for (auto& l : locals) {
@@ -333,6 +341,8 @@ Engine::~Engine() {
   for (auto e : done) cudaEventDestroy(e);
   for (auto e : tev0) cudaEventDestroy(e);
   for (auto e : tev1) cudaEventDestroy(e);
+  for (auto* v : {&zev_ready, &zev_start, &zev_end})
+    for (auto e : *v) cudaEventDestroy(e);
   cudaEventDestroy(ev_step0);
   cudaEventDestroy(ev_step1);
   cudaEventDestroy(ev_opt);
@@ -465,15 +475,25 @@ void Engine::z1_adam(cudaStream_t s) {
   ++launches;
 }
 
-void Engine::z1_layer(int layer, const AdamArgs& a, cudaStream_t s) {
+void Engine::z1_layer(int layer, const AdamArgs& a, cudaStream_t s, cudaStream_t post) {
   if (!emulate && cfg.par.dp > 1) {
-    // announce "layer final here" to every rank, wait for the ranks this
+    // announce "layer final here" to every rank from the stream of the task
+    // that made it final (not from the optimizer stream, where it would queue
+    // behind this rank's earlier layers' Z1 and hold back every rank that
+    // waits for it), then wait on the optimizer stream for the ranks this
     // layer's Z1 reads gradients from / pushes parameters into
     const uint64_t seq = ++grad_seq;
-    launch_flags(dtable, cfg.my_rank, kFlagGradReady, rank_mask(0, cfg.par.dp), seq, kFlagGradReady,
-                 z1_wait_mask[layer], seq, s);
-    ++launches;
+    const uint64_t all = rank_mask(0, cfg.par.dp);
+    if (post && post != s) {
+      launch_flags(dtable, cfg.my_rank, kFlagGradReady, all, seq, 0, 0, 0, post);
+      launch_flags(dtable, cfg.my_rank, 0, 0, 0, kFlagGradReady, z1_wait_mask[layer], seq, s);
+      launches += 2;
+    } else {
+      launch_flags(dtable, cfg.my_rank, kFlagGradReady, all, seq, kFlagGradReady, z1_wait_mask[layer], seq, s);
+      ++launches;
+    }
   }
+  if (cfg.timeline && !zev_start.empty()) HZP_CUDA(cudaEventRecord(zev_start[layer], s));
   const int t0 = z1_layer_off[layer], nt = z1_layer_off[layer + 1] - t0;
   launch_z1_adam(dtable, dtiles + t0, nt, geom.z2, geom.replicas(), &a, 1, bf16, locals.front().dbg != nullptr,
                  kCommCtas, s);
@@ -716,11 +736,14 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
     if (final_of[e.id] >= 0) {  // this task made a layer's gradient final: its Z1 now
       cudaStream_t zs = opt_stream;  // its own stream: later RSs never queue behind it
       HZP_CUDA(cudaStreamWaitEvent(zs, done[e.id], 0));
+      const bool zt = cfg.timeline && !zev_ready.empty();
+      if (zt) HZP_CUDA(cudaEventRecord(zev_ready[final_of[e.id]], zs));
       if (!adam_ready) {
         adam = next_adam_args();
         adam_ready = true;
       }
-      z1_layer(final_of[e.id], adam, zs);
+      z1_layer(final_of[e.id], adam, zs, s);
+      if (zt) HZP_CUDA(cudaEventRecord(zev_end[final_of[e.id]], zs));
       HZP_CUDA(cudaEventRecord(ev_z1, zs));
       ++z1_issued;
     }
@@ -732,6 +755,7 @@ void Engine::step(const void* inputs, bool on_device, float* losses_out) {
     }
   }
   rs_seq = seq0 + rs_ids.size();
+  z1_timed = cfg.timeline && !zev_ready.empty() && z1_issued == static_cast<int>(layers.size());
   // join the comm streams back into the compute stream
   for (int k = 1; k < 3; ++k)
     if (last_comm_ev[k] >= 0) HZP_CUDA(cudaStreamWaitEvent(cs, done[last_comm_ev[k]], 0));

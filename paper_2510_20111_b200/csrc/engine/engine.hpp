@@ -73,6 +73,11 @@ struct Engine {
   cudaStream_t opt_stream = nullptr;  // per-layer Z1 kernels (async mode)
   std::vector<cudaEvent_t> done;
   std::vector<cudaEvent_t> tev0, tev1;
+  // per-layer Z1 on the optimizer stream (timeline, async mode): gradient
+  // final here / every GradReady wait passed / kernel done
+  std::vector<cudaEvent_t> zev_ready, zev_start, zev_end;
+  bool z1_timed = false;  // the last step recorded them
+  void timeline_events(bool on);
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr, ev_opt = nullptr;
 
   std::vector<Arena> arenas;  // [dp]
@@ -136,7 +141,7 @@ struct Engine {
   AdamArgs next_adam_args();     // advances the Adam step of every driven rank
   // Z1 of one layer as soon as its gradient is final everywhere it is read
   // from and its parameters are no longer read anywhere this step
-  void z1_layer(int layer, const AdamArgs& a, cudaStream_t s);
+  void z1_layer(int layer, const AdamArgs& a, cudaStream_t s, cudaStream_t post = nullptr);
   void barrier(cudaStream_t s);
   GradTarget grad_target(int li, int layer, int wslot, int mb) const;
   const void* layer_params(int li, int layer, int slot) const;

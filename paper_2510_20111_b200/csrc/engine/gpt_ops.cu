@@ -585,6 +585,122 @@ __global__ void __launch_bounds__(256) colred_kernel(const uint16_t* __restrict_
   }
 }
 
+// LayerNorm backward with its column reductions fused: one CTA per chunk of
+// rows, taken 8 at a time.  Phase 1: warp w reduces row r0 + w to
+// mean(dy g) and mean(dy g xhat) (lane-strided 16-byte vectors, then a warp
+// sum: the same order as ln_bwd_dx_kernel); phase 2: thread t owns column
+// vectors t, t + 256, ... and walks the 8 rows (L1 / L2 hits), writing
+// dx (+ resid) and accumulating, in registers, the chunk's column sums
+// dgamma = sum dy xhat, dbeta = sum dy and (prev) sum of the bf16 dx written
+// — the bias gradient of the projection whose output gradient dx is.  So dy
+// and x cross HBM once (the unfused path re-read both for dgamma / dbeta, and
+// dx again for that bias), and no cross-thread fold is needed.
+template <int NV>
+__global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const uint16_t* __restrict__ dy,
+                                                           const uint16_t* __restrict__ x,
+                                                           const uint16_t* __restrict__ g,
+                                                           const float* __restrict__ mu,
+                                                           const float* __restrict__ rs,
+                                                           const uint16_t* __restrict__ resid,
+                                                           uint16_t* __restrict__ dx, int rows, int h, int per,
+                                                           float* __restrict__ part, float* __restrict__ prev) {
+  __shared__ float st[8][4];
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int nvec = h / 8;
+  const int rb = blockIdx.x * per, re = min(rows, rb + per);
+  float ab[NV][8], ag[NV][8], ap[NV][8], gv[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ab[k][j] = ag[k][j] = ap[k][j] = 0.f;
+    const int v = t + 256 * k;
+    if (v < nvec) unpack8(__ldg(reinterpret_cast<const uint4*>(g) + v), gv[k]);
+  }
+  for (int r0 = rb; r0 < re; r0 += 8) {
+    const int r = r0 + w;
+    if (r < re) {
+      const float m = mu[r], rstd = rs[r];
+      const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
+      const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
+      float s1 = 0.f, s2 = 0.f;
+      for (int v = lane; v < nvec; v += 32) {
+        float d[8], xv[8], gg[8];
+        unpack8(__ldg(dyr + v), d);
+        unpack8(__ldg(xr + v), xv);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + v), gg);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xv[j] - m) * rstd, dg = d[j] * gg[j];
+          s1 += dg;
+          s2 += dg * xh;
+        }
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        st[w][0] = s1 / h;
+        st[w][1] = s2 / h;
+        st[w][2] = m;
+        st[w][3] = rstd;
+      }
+    }
+    __syncthreads();
+    const int nr = min(8, re - r0);
+#pragma unroll 2
+    for (int q = 0; q < nr; ++q) {
+      const int64_t rq = int64_t(r0 + q) * h;
+      const float a1 = st[q][0], a2 = st[q][1], m = st[q][2], rstd = st[q][3];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int v = t + 256 * k;
+        if (v >= nvec) continue;
+        float d[8], xv[8], o[8];
+        unpack8(__ldg(reinterpret_cast<const uint4*>(dy + rq) + v), d);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(x + rq) + v), xv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xv[j] - m) * rstd;
+          o[j] = rstd * (d[j] * gv[k][j] - a1 - xh * a2);
+          ab[k][j] += d[j];
+          ag[k][j] += d[j] * xh;
+        }
+        if (resid) {
+          float rv[8];
+          unpack8(__ldg(reinterpret_cast<const uint4*>(resid + rq) + v), rv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] += rv[j];
+        }
+        const uint4 pk = pack8(o);
+        reinterpret_cast<uint4*>(dx + rq)[v] = pk;
+        if (prev) {
+          float ob[8];
+          unpack8(pk, ob);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ap[k][j] += ob[j];
+        }
+      }
+    }
+    __syncthreads();  // st is rewritten by the next group
+  }
+  const int64_t cb = int64_t(blockIdx.x) * h, slab = int64_t(gridDim.x) * h;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int v = t + 256 * k;
+    if (v >= nvec) continue;
+    float4* pg = reinterpret_cast<float4*>(part + cb + 8 * v);
+    float4* pb = reinterpret_cast<float4*>(part + slab + cb + 8 * v);
+    pg[0] = make_float4(ag[k][0], ag[k][1], ag[k][2], ag[k][3]);
+    pg[1] = make_float4(ag[k][4], ag[k][5], ag[k][6], ag[k][7]);
+    pb[0] = make_float4(ab[k][0], ab[k][1], ab[k][2], ab[k][3]);
+    pb[1] = make_float4(ab[k][4], ab[k][5], ab[k][6], ab[k][7]);
+    if (prev) {
+      float4* pp = reinterpret_cast<float4*>(prev + cb + 8 * v);
+      pp[0] = make_float4(ap[k][0], ap[k][1], ap[k][2], ap[k][3]);
+      pp[1] = make_float4(ap[k][4], ap[k][5], ap[k][6], ap[k][7]);
+    }
+  }
+}
+
 // out[c] (mode) = sum_k part[k][c]; 4 threads per column, 64 columns per CTA.
 __global__ void __launch_bounds__(256) colsum_finalize4_kernel(const float* __restrict__ part, int chunks,
                                                                int cols, void* out, int out_bf16, int mode) {
@@ -780,6 +896,22 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
   }
   HZP_LAUNCH_CHECK();
 }
+int layernorm_bwd_chunks(int rows) { return (rows + kLnRowsPerChunk - 1) / kLnRowsPerChunk; }
+
+void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
+                         const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, float* prev,
+                         int rows, int h, cudaStream_t s) {
+  if (h % 8 || h > 2 * 256 * 8) throw std::invalid_argument("layernorm_bwd_fused: h % 8 != 0 or h > 4096");
+  const int chunks = layernorm_bwd_chunks(rows);
+  if (h <= 256 * 8)
+    ln_bwd_fused_kernel<1><<<chunks, 256, 0, s>>>(dy, x, g, mu, rstd, resid, dx, rows, h, kLnRowsPerChunk, part,
+                                                  prev);
+  else
+    ln_bwd_fused_kernel<2><<<chunks, 256, 0, s>>>(dy, x, g, mu, rstd, resid, dx, rows, h, kLnRowsPerChunk, part,
+                                                  prev);
+  HZP_LAUNCH_CHECK();
+}
+
 void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s) {
   if (cols % 8) throw std::invalid_argument("colsum: cols % 8 != 0");
   colred_kernel<false><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(d, nullptr, nullptr, nullptr, rows, cols,

@@ -30,6 +30,17 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
                    const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
                    int rows, int h, cudaStream_t s);
 
+// Same dx, with the column reductions fused into the one pass over dy / x:
+// part [2][chunks][h] = (sum dy xhat, sum dy) per chunk of kLnRowsPerChunk
+// rows, and, if prev != nullptr, prev [chunks][h] = sum of the bf16 dx
+// written (the bias gradient of the projection whose output gradient dx is).
+// chunks = layernorm_bwd_chunks(rows); h <= 4096.
+constexpr int kLnRowsPerChunk = 32;
+int layernorm_bwd_chunks(int rows);
+void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
+                         const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, float* prev,
+                         int rows, int h, cudaStream_t s);
+
 // Column sums of a bf16 [rows, cols] matrix into fp32 partials [chunks][cols].
 void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s);
 // out[c] (mode, dtype) <- sum over chunks of part[k][c]  (+ optional 2nd slab)

@@ -62,6 +62,10 @@ struct GptBuffers {
   uint16_t *dln = nullptr, *dqkv = nullptr, *dattn = nullptr, *dfc1 = nullptr, *dxm = nullptr;
   uint16_t* dact = nullptr;  // SwiGLU: grad of the activation [T, f] (dfc1 is [T, 2f])
   float* part = nullptr;       // column-sum partials
+  // fused LayerNorm-backward partials, each slab [layernorm_bwd_chunks(T)][h]:
+  // 0-1 ln2 (dgamma, dbeta), 2-3 ln1, 4 ln2's dx sum (b_o), 5-6 ln1's / the
+  // final LN's dx sum = the next-lower block's b_fc2, by that block's parity
+  float* lnpart = nullptr;
   // weight gradients of a block run on a side stream (they are leaves of the
   // backward DAG), so they fill the SMs the dgrad chain's tail waves leave
   // idle; own column-sum partials, fork/join by events.
@@ -237,6 +241,7 @@ class GptModel final : public Model {
     B->dxm = bf(T_ * h_);
     B->part = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
     B->part_side = f32(2 * int64_t(kChunks) * std::max<int64_t>(f_, 3 * int64_t(h_)));
+    B->lnpart = f32(7 * lnslab());
     {  // weight-gradient GEMMs: compute, at the compute stream's (highest) priority
       int lo = 0, hi = 0;
       HZP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -265,7 +270,7 @@ class GptModel final : public Model {
     for (void* q : {(void*)B->lnf, (void*)B->muf, (void*)B->rsf, (void*)B->logits, (void*)B->S,
                     (void*)B->dS, (void*)B->D, (void*)B->dx[0], (void*)B->dx[1], (void*)B->dln,
                     (void*)B->dqkv, (void*)B->dattn, (void*)B->dfc1, (void*)B->dxm, (void*)B->part,
-                    (void*)B->part_side, (void*)B->moe_dy, (void*)B->moe_dh, (void*)B->moe_dxp,
+                    (void*)B->part_side, (void*)B->lnpart, (void*)B->moe_dy, (void*)B->moe_dh, (void*)B->moe_dxp,
                     (void*)B->moe_dlogits, (void*)B->moe_dgate,
                     (void*)B->emb, B->emb_ws, (void*)B->row_loss, (void*)B->loss})
       cudaFree(q);
@@ -312,13 +317,22 @@ class GptModel final : public Model {
     return g.bf16 ? static_cast<void*>(static_cast<uint16_t*>(g.ptr) + off)
                   : static_cast<void*>(static_cast<float*>(g.ptr) + off);
   }
-  // LN gamma / beta gradients from layernorm_bwd's column partials `part`
-  // ([2][kChunks][h]; B->part by default)
+  // fused LayerNorm backward partials (see GptBuffers::lnpart)
+  int64_t lnslab() const { return int64_t(layernorm_bwd_chunks(int(T_))) * h_; }
+  float* lnp(GptBuffers* B, int slab) const { return B->lnpart + slab * lnslab(); }
+  // dense FFN with biases: its b_fc2 gradient is the column sum of the
+  // block-output gradient, i.e. of the next block's LN1 (or the final LN) dx
+  bool fc2_bias() const { return E_ == 0 && !sw_; }
+  float* fc2b_part(GptBuffers* B, int block) const { return lnp(B, 5 + (block & 1)); }
+  // LN gamma / beta gradients from layernorm_bwd_fused's partials
   void ln_param_grads(GptBuffers* B, const GradTarget& g, int64_t g_off, int64_t b_off, cudaStream_t s,
-                      const float* part = nullptr) const {
-    if (!part) part = B->part;
-    colsum_finalize(part, kChunks, h_, gptr(g, g_off), g.bf16, g.mode, s);
-    colsum_finalize(part + int64_t(kChunks) * h_, kChunks, h_, gptr(g, b_off), g.bf16, g.mode, s);
+                      const float* part) const {
+    const int ch = layernorm_bwd_chunks(int(T_));
+    colsum_finalize(part, ch, h_, gptr(g, g_off), g.bf16, g.mode, s);
+    colsum_finalize(part + lnslab(), ch, h_, gptr(g, b_off), g.bf16, g.mode, s);
+  }
+  void bias_from_ln(GptBuffers* B, const float* part, const GradTarget& g, int64_t b_off, cudaStream_t s) const {
+    colsum_finalize(part, layernorm_bwd_chunks(int(T_)), h_, gptr(g, b_off), g.bf16, g.mode, s);
   }
   // batched attention shapes over z = (sequence b, head)
   GemmShape attn_shape(int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int64_t a_sh,
@@ -556,9 +570,9 @@ class GptModel final : public Model {
       Epilogue e;
       linear_dgrad(B->logits, W + 2 * h_, B->dln, V_, h_, e, s);
       B->cur = 0;
-      layernorm_bwd(B->dln, B->x[l], W, B->muf, B->rsf, nullptr, B->dx[0], B->part, kChunks,
-                    int(T_), h_, s);
-      ln_param_grads(B, g, 0, h_, s);
+      layernorm_bwd_fused(B->dln, B->x[l], W, B->muf, B->rsf, nullptr, B->dx[0], lnp(B, 0),
+                          fc2_bias() ? fc2b_part(B, L_) : nullptr, int(T_), h_, s);
+      ln_param_grads(B, g, 0, h_, s, lnp(B, 0));
       HZP_CUDA(cudaEventRecord(B->ev[1], B->side));
       HZP_CUDA(cudaStreamWaitEvent(s, B->ev[1], 0));
       return;
@@ -584,14 +598,17 @@ class GptModel final : public Model {
     cudaStream_t ws = B->side;
     if (E_ > 0) {
       moe_bwd(B, a, W, g, dout, s, ws, to_side);
-      layernorm_bwd(B->dattn, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_), h_,
-                    s);
+      layernorm_bwd_fused(B->dattn, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, lnp(B, 0), lnp(B, 4),
+                          int(T_), h_, s);
       to_side();  // the LN parameter reductions are leaves too
-      ln_param_grads(B, g, o.ln2_g, o.ln2_b, ws, B->part);
+      ln_param_grads(B, g, o.ln2_g, o.ln2_b, ws, lnp(B, 0));
+      bias_from_ln(B, lnp(B, 4), g, o.b_o, ws);
     } else {
     // MLP
     to_side();
-    linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, o.b_fc2, B, ws);
+    // b_fc2 = column sum of dout, accumulated by the LN backward that made it
+    if (fc2_bias()) bias_from_ln(B, fc2b_part(B, l), g, o.b_fc2, ws);
+    linear_wgrad(dout, a.fact, h_, f_, g, o.w_fc2, -1, B, ws);
     if (sw_) {
       linear_dgrad(dout, W + o.w_fc2, B->dact, h_, f_, Epilogue{}, s);
       swiglu_bwd(a.fpre, B->dact, B->dfc1, T_, f_, s);
@@ -608,14 +625,15 @@ class GptModel final : public Model {
       Epilogue e;
       linear_dgrad(B->dfc1, W + o.w_fc1, B->dln, f1_, h_, e, s);
     }
-    layernorm_bwd(B->dln, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, B->part, kChunks, int(T_),
-                  h_, s);
+    layernorm_bwd_fused(B->dln, a.xm, W + o.ln2_g, a.mu2, a.rs2, dout, B->dxm, lnp(B, 0), lnp(B, 4), int(T_),
+                        h_, s);
     to_side();  // the LN parameter reductions are leaves too
-    ln_param_grads(B, g, o.ln2_g, o.ln2_b, ws, B->part);
+    ln_param_grads(B, g, o.ln2_g, o.ln2_b, ws, lnp(B, 0));
+    bias_from_ln(B, lnp(B, 4), g, o.b_o, ws);  // b_o = column sum of dxm
     }
     // attention output projection
     to_side();
-    linear_wgrad(B->dxm, a.attn, h_, h_, g, o.w_o, o.b_o, B, ws);
+    linear_wgrad(B->dxm, a.attn, h_, h_, g, o.w_o, -1, B, ws);
     {
       Epilogue e;
       linear_dgrad(B->dxm, W + o.w_o, B->dattn, h_, h_, e, s);
@@ -635,10 +653,11 @@ class GptModel final : public Model {
       linear_dgrad(B->dqkv, W + o.w_qkv, B->dln, int(h3), h_, e, s);
     }
     // ln1's partials in their own region: the side stream may still be
-    // reducing ln2's
-    float* part1 = B->part + 2 * int64_t(kChunks) * h_;
-    layernorm_bwd(B->dln, B->x[l], W + o.ln1_g, a.mu1, a.rs1, B->dxm, din, part1, kChunks,
-                  int(T_), h_, s);
+    // reducing ln2's; its dx sum is block l-1's b_fc2 (consumed at the start
+    // of that block's backward, double-buffered by parity)
+    float* part1 = lnp(B, 2);
+    layernorm_bwd_fused(B->dln, B->x[l], W + o.ln1_g, a.mu1, a.rs1, B->dxm, din, part1,
+                        fc2_bias() && l > 1 ? fc2b_part(B, l - 1) : nullptr, int(T_), h_, s);
     to_side();
     ln_param_grads(B, g, o.ln1_g, o.ln1_b, ws, part1);
     // join: the block's task ends when its weight gradients are written (the

@@ -265,6 +265,16 @@ class HzpEngine:
                 "compute_idle_ms": idle.value, "compute_busy_ms": busy.value,
                 "makespan_ms": mk.value}
 
+    def z1_timeline(self):
+        """Per-layer optimizer times of the last recorded step (async mode):
+        ready / start / end ms from step start (hzp_z1_timeline)."""
+        n = C.c_int()
+        cap = 4096
+        a, b, c = (C.c_double * cap)(), (C.c_double * cap)(), (C.c_double * cap)()
+        N.check(N.lib.hzp_z1_timeline(self._h, a, b, c, cap, C.byref(n)))
+        k = min(n.value, cap)
+        return {"ready_ms": list(a)[:k], "start_ms": list(b)[:k], "end_ms": list(c)[:k]}
+
     def set_timeline(self, on: bool) -> None:
         N.check(N.lib.hzp_set_timeline(self._h, 1 if on else 0))
 

@@ -102,7 +102,7 @@ def main():
         ref_losses, _ = o.train_step_hzp(st, x, batch, bool(prec))
         losses = eng.step(np.ascontiguousarray(x[rank:rank + 1]))
     eng.sync()
-    tol = 1e-5 if prec == 0 else 1e-2
+    tol = 0.0 if prec == 0 else 1e-2  # fp32 tier: bitwise (ordered RS, libm tanhf restatement)
 
     def rel(a, b):
         return float(np.max(np.abs(a.astype(np.float64) - b)) / max(np.max(np.abs(b)), 1e-30))

@@ -21,6 +21,9 @@ CFG_BENCH = dict(layers=1, hidden=2048, heads=16, ffn=8192, vocab=50304, seq=204
 
 
 # SwiGLU FFN (BASELINE configs[2] / [3]): fc1 [2f, h] = gate | up, no FFN biases
+# the 7B width (h = 4096: the fused LayerNorm backward's two-vector path, the
+# two-warp LayerNorm rows), GELU FFN so the b_fc2 hand-over is exercised
+CFG_H4096 = dict(layers=2, hidden=4096, heads=32, ffn=1024, vocab=512, seq=256, batch=1)
 CFG_SWIGLU = dict(layers=2, hidden=256, heads=2, ffn=704, vocab=512, seq=256, batch=2, swiglu=1)
 
 
@@ -105,7 +108,8 @@ def _bf16_bits(x):
             ((np.ascontiguousarray(x, np.float32).view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("c", [CFG, CFG_WIDE, CFG_BENCH, CFG_SWIGLU], ids=["small", "wide", "bench", "swiglu"])
+@pytest.mark.parametrize("c", [CFG, CFG_WIDE, CFG_BENCH, CFG_SWIGLU, CFG_H4096],
+                         ids=["small", "wide", "bench", "swiglu", "h4096"])
 def test_gpt_gradient_matches_torch(gpu, c):
     eng = _engine(c)
     master = init_params(c)
