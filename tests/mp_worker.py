@@ -75,9 +75,58 @@ def kernels(z1, z2, z3, prec):
     return ok
 
 
+def gpt_race(z1, z2, z3):
+    """Race check of the device-flag protocol without a sanitizer (closed on
+    this pool): the bf16 GPT step (dense GELU and MoE) on every rank, three
+    times — async twice, then with HZP_DEBUG_SYNC (every task serialised on
+    the device and followed by a cross-rank barrier) — must give bitwise the
+    same parameters, optimizer state and losses.  A missing wait anywhere in
+    the AG / RS / GradReady / Z1 protocol lets some run read a buffer early."""
+    from paper_2510_20111_b200.engine import make_tokens
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    c = dict(layers=3, hidden=256, heads=2, ffn=1024, vocab=512, seq=256, batch=2)
+    ok = True
+    for experts in (0, 8):
+        runs = []
+        for mode in ("async", "async", "serial"):
+            if mode == "serial":
+                os.environ["HZP_DEBUG_SYNC"] = "1"
+            eng = HzpEngine(EngineConfig(model=1, precision=1, gpt_layers=c["layers"], gpt_hidden=c["hidden"],
+                                         gpt_heads=c["heads"], gpt_ffn=c["ffn"], gpt_vocab=c["vocab"],
+                                         gpt_seq=c["seq"], batch=c["batch"], num_microbatches=2,
+                                         gpt_experts=experts,
+                                         par=ParallelConfig(dp=world, z1=z1, z2=z2, z3=z3), device=local,
+                                         my_rank=rank))
+            os.environ.pop("HZP_DEBUG_SYNC", None)
+            eng.connect()
+            eng.init_seeded(2024, 0.02)
+            dist.barrier()
+            losses = []
+            for step in range(3):
+                tok = np.stack([make_tokens(2024, step, rank, mb, c["batch"] * (c["seq"] + 1), c["vocab"])
+                                .reshape(c["batch"], c["seq"] + 1) for mb in range(2)])[None]
+                losses.append(np.asarray(eng.step(np.ascontiguousarray(tok, np.int32))))
+            eng.sync()
+            runs.append((np.concatenate(losses), eng.param_f32(rank), eng.download(rank, 2),
+                         eng.download(rank, 3), eng.download(rank, 4)))
+            dist.barrier()
+            eng.close()
+        same = [all(np.array_equal(a, b) for a, b in zip(runs[0], r)) for r in runs[1:]]
+        print(f"rank {rank}: experts {experts}: async == async {same[0]}, async == serialised {same[1]}", flush=True)
+        ok &= all(same)
+    print(f"rank {rank}: {'OK' if ok else 'FAIL'} gpt race", flush=True)
+    return ok
+
+
 def main():
     z1, z2, z3, prec = (int(x) for x in sys.argv[1:5])
     dist.init_process_group("gloo")
+    if len(sys.argv) > 5 and sys.argv[5] == "gpt_race":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", dist.get_rank())))
+        ok = gpt_race(z1, z2, z3)
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     if len(sys.argv) > 5 and sys.argv[5] == "kernels":
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", dist.get_rank())))
         ok = kernels(z1, z2, z3, prec)

@@ -68,3 +68,20 @@ def test_multiprocess_ragged_shards_match_oracle(n, z):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert r.stdout.count(": OK") == n
+
+
+@pytest.mark.parametrize("n,z", [(2, (2, 2, 2)), (4, (4, 2, 2)), (4, (4, 4, 4))])
+def test_multiprocess_gpt_async_equals_serialised(n, z):
+    """Race check of the cross-GPU flag protocol (compute-sanitizer is closed
+    on this pool): the bf16 GPT step, dense and MoE, async twice and fully
+    serialised (HZP_DEBUG_SYNC) once — bitwise the same parameters, Adam state
+    and losses on every rank (tests/mp_worker.py gpt_race)."""
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + n * 10 + z[1]),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *map(str, z), "1", "gpt_race"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count("OK gpt race") == n

@@ -5,8 +5,12 @@ Opt-in: one tool per run, selected with HZP_SANITIZER=memcheck|racecheck|
 synccheck (B200_PROFILING.md: at most one sanitizer tool per GPU session;
 several in one call have left a GPU unusable).  With >= 2 GPUs the tool wraps
 a 2-process step (multicast AG / RS, GradReady / AgReady / RsDone flags,
-fused Z1 over NVLink); on one GPU it wraps the emulated 2-rank step.  The
-logs of the runs are kept under profiles/ (r02_sanitizer_*.txt)."""
+fused Z1 over NVLink); on one GPU it wraps the emulated 2-rank step.
+Round 2: compute-sanitizer is closed on this GPU pool (the first memcheck call
+was refused, profiles/r02_sanitizer_closed.txt); the flag protocol's race
+check is test_gpu_multi.py::test_multiprocess_gpt_async_equals_serialised
+(async vs fully serialised runs, bitwise), and memory safety rests on the
+bitwise parity tests against the oracle (every shard, ragged sizes)."""
 import os
 import subprocess
 import sys
