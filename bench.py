@@ -449,6 +449,37 @@ def collectives(eng, N, local, max_over_ranks, barrier, z2, z3, iters=5):
     return out
 
 
+def z1_link_bytes(N, P, z1, z2, z3, pbytes=2):
+    """Per-rank NVLink egress / ingress (bytes) of one whole Z1 stage, from the
+    layout alone: rank r's chunk [i1 s1, +s1) (i1 = r % z1) needs the gradient
+    of every DZP replica of its Z2 segment (ranks g z2 + j2, g < N / z2; fp32)
+    and pushes the bf16 result to the Z3 owner in every Z3 group of its Z1
+    group (b1 + t z3 + j3, t < z1 / z3).  Every byte between two ranks crosses
+    the sender's egress and the receiver's ingress once."""
+    s1, s2, s3 = -(-P // z1), -(-P // z2), -(-P // z3)
+    eg, ing = [0] * N, [0] * N
+    for r in range(N):
+        lo, hi = (r % z1) * s1, min(P, (r % z1 + 1) * s1)
+        b1 = r - r % z1
+        x = lo
+        while x < hi:
+            j2, j3 = x // s2, x // s3
+            y = min(hi, (j2 + 1) * s2, (j3 + 1) * s3)
+            n = y - x
+            for g in range(N // z2):
+                s = g * z2 + j2
+                if s != r:
+                    eg[s] += 4 * n
+                    ing[r] += 4 * n
+            for t in range(z1 // z3):
+                q = b1 + t * z3 + j3
+                if q != r:
+                    eg[r] += pbytes * n
+                    ing[q] += pbytes * n
+            x = y
+    return eg, ing
+
+
 def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, z1=1, z2=1, z3=1, iters=3):
     """Fused Z1 stage (replica pull-reduce + Adam + bf16 push) timed through
     hzp_z1_adam_step on the step's own state (after the timed region), vs
@@ -470,16 +501,20 @@ def z1_roofline(eng, N, local, max_over_ranks, barrier, hbm_gbps, z1=1, z2=1, z3
     ms = max_over_ranks(e0.elapsed_time(e1) / iters)
     R, k = max(1, N // z2), max(1, z1 // z3)
     per = 4 * R + 24 + 2 * k
-    remote = 4 * (R - 1) + 2 * (k - 1)  # at least R-1 replica reads and k-1 owner pushes cross NVLink
+    eg, ing = z1_link_bytes(N, eng.P, z1, z2, z3) if N > 1 else ([0], [0])
+    link = max(max(eg), max(ing))  # the busiest rank's busier link direction
     t_hbm = per * eng.s1 / (hbm_gbps * 1e9)
-    t_nvl = remote * eng.s1 / (NVLINK_GBPS * 1e9)
+    t_nvl = link / (NVLINK_GBPS * 1e9)
     bound = "nvlink" if t_nvl > t_hbm else "hbm"
     floor_ms = max(t_hbm, t_nvl) * 1e3
     return {"ms": round(ms, 3), "elems": int(eng.s1), "replicas": R, "owners": k, "bytes_per_elem": per,
-            "remote_bytes_per_elem": remote, "GBps": round(per * eng.s1 / (ms / 1e3) / 1e9, 1),
+            "link_bytes_busiest_rank": int(link), "link_bytes_per_elem_busiest": round(link / eng.s1, 2),
+            "GBps": round(per * eng.s1 / (ms / 1e3) / 1e9, 1),
             "bound": bound, "roofline_ms": round(floor_ms, 3), "frac": round(floor_ms / ms, 3),
+            "frac_of_measured_link": round(link / (NVLINK_MEASURED_GBPS * 1e9) * 1e3 / ms, 3) if link else None,
             "peak_GBps": {"hbm": hbm_gbps, "nvlink": NVLINK_GBPS},
-            "note": "includes the two device-wide barriers around the kernel (no-op at N=1)"}
+            "note": "includes the two device-wide barriers around the kernel (no-op at N=1); link bytes: "
+                    "z1_link_bytes (replica gradients fp32 + bf16 pushes, per-rank egress / ingress)"}
 
 
 def memory_report(eng, tl, N, z1, z2, z3, nmb, args):

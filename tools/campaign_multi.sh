@@ -1,8 +1,8 @@
 #!/bin/bash
-# Multi-GPU measurement campaign (run under gpurun --gpus 4): multi-GPU
-# parity tests, the three BASELINE models at N = 2 and 4, the async / vanilla
-# x prefetch-depth ablation (BASELINE configs[4]), and the
-# AG / RS sweep.  Outputs under gpurun_out/<tag>_*.
+# Multi-GPU measurement campaign (run under gpurun --gpus 4): the three
+# BASELINE models at N = 2 and 4, the async / vanilla x prefetch-depth
+# ablation (BASELINE configs[4]), the AG / RS sweep, and
+# (MULTI_TESTS=1) the multi-GPU parity tests.  Outputs under gpurun_out/<tag>_*.
 tag=${1:-r02m}
 mkdir -p gpurun_out
 run() {  # run <name> <nproc> <bench args...>
@@ -21,19 +21,21 @@ except Exception as ex:
     print(sys.argv[1], "unparsed", ex)
 PY
 }
-timeout 1200 python -m pytest tests/test_gpu_multi.py -q > gpurun_out/${tag}_multi.log 2>&1; echo "multi rc=$?"; tail -1 gpurun_out/${tag}_multi.log
+[ "${MULTI_TESTS:-0}" = 1 ] && { timeout 1500 python -m pytest tests/test_gpu_multi.py -q > gpurun_out/${tag}_multi.log 2>&1; echo "multi rc=$?"; tail -1 gpurun_out/${tag}_multi.log; }
 for n in 2 4; do
   run 13b_n$n $n
   run 7b_n$n $n --model 7b
   run moe_n$n $n --model moe
 done
-for m in async vanilla; do
-  for d in 1 2 4; do run 13b_n4_${m}_d$d 4 --mode $m --depth $d; done
-  run 7b_n4_${m} 4 --model 7b --mode $m
-done
-for n in 2 4; do
-  timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
-    --master-port 29950 tools/bench_collectives.py --sizes-mb 1,4,16,64,256,1024 --depths 1,2,4 --precs 1,0 \
-    > gpurun_out/${tag}_sweep_n$n.jsonl 2> gpurun_out/${tag}_sweep_n$n.err
-  echo "sweep n$n rc=$? rows $(wc -l < gpurun_out/${tag}_sweep_n$n.jsonl)"
-done
+# scheduler ablation (BASELINE configs[4]): async (= the model runs above at
+# depth 2) vs vanilla, prefetch depth 1 / 4, at N = 2 and 4
+run 13b_n2_vanilla_d2 2 --mode vanilla
+run 13b_n4_vanilla_d2 4 --mode vanilla
+run 13b_n4_async_d1 4 --depth 1
+run 13b_n4_async_d4 4 --depth 4
+run 13b_n4_vanilla_d1 4 --mode vanilla --depth 1
+run 7b_n4_vanilla 4 --model 7b --mode vanilla
+timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+  --master-port 29950 tools/bench_collectives.py --sizes-mb 64,256,1024 --depths 2 --precs 1,0 \
+  > gpurun_out/${tag}_sweep_n4.jsonl 2> gpurun_out/${tag}_sweep_n4.err
+echo "sweep n4 rc=$? rows $(wc -l < gpurun_out/${tag}_sweep_n4.jsonl)"
