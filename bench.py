@@ -444,6 +444,19 @@ def collectives(eng, N, local, max_over_ranks, barrier, z2, z3, iters=5):
             bw = (N - 1) / N * full.numel() * 2 / (ms / 1e3) / 1e9
             out[name] = {"ms": round(ms, 4), "busbw_GBps": round(bw, 1)}
         dist.destroy_process_group(g)
+        # the same traffic as ours: NCCL broadcast from / reduce to ONE owner
+        # of the whole layer, inside the same Z3 / Z2 groups
+        rank = dist.get_rank()
+        layer = torch.empty(n, dtype=torch.bfloat16, device=f"cuda:{local}")
+        for name, gs, op in (("nccl_broadcast_from_owner", z3, "bcast"), ("nccl_reduce_to_owner", z2, "reduce")):
+            if gs <= 1:
+                continue
+            groups = [dist.new_group(list(range(b, b + gs)), backend="nccl") for b in range(0, N, gs)]
+            mine, root = groups[rank // gs], rank - rank % gs
+            fn = ((lambda: dist.broadcast(layer, root, group=mine)) if op == "bcast" else
+                  (lambda: dist.reduce(layer, root, group=mine)))
+            ms = timed(fn)
+            out[name] = {"group": gs, "ms": round(ms, 4), "owner_link_GBps": round(n * 2 / (ms / 1e3) / 1e9, 1)}
     except Exception as exc:  # noqa: BLE001
         out["nccl"] = f"unavailable: {exc}"[:200]
     return out
