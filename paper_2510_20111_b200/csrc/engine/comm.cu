@@ -33,7 +33,7 @@ constexpr int kCommThreads = 128;
 constexpr int kCommRegs = 80;
 constexpr int kUnroll = 8;    // AG: 16-byte vectors in flight per thread
 constexpr int kUnrollRS = 4;  // RS: per source
-constexpr int kUnrollMC = 8;  // RS through multimem.ld_reduce
+constexpr int kUnrollMC = 4;  // RS through multimem.ld_reduce (+ the fp32 shard's 2 x 16 B each)
 
 __device__ __forceinline__ void fadd4(float4& a, const float4& b) {
   a.x = __fadd_rn(a.x, b.x);
@@ -166,14 +166,20 @@ __global__ void __maxnreg__(kCommRegs) rs_reduce_kernel(const RankTable* __restr
     const char* const mcw = kMode == kRsMulticast ? static_cast<const char*>(T->wgrad_mc) + woff : nullptr;
     if (kMode == kRsMulticast && t.vec) {
       // one in-switch reduction per 16 bytes: 8 bf16 of every member summed
-      // (fp32 accumulate), returned as 8 bf16; kUnrollMC in flight per thread
+      // (fp32 accumulate), returned as 8 bf16; kUnrollMC in flight per thread,
+      // each with the 32 bytes of the fp32 shard it is added into (issued
+      // together: the local read no longer waits for the switch round trip)
       const int64_t nv = t.len / 8;
       for (int64_t i0 = threadIdx.x; i0 < nv; i0 += int64_t(kUnrollMC) * kCommThreads) {
         uint4 v[kUnrollMC];
+        float4 ga[kUnrollMC], gb[kUnrollMC];
 #pragma unroll
         for (int u = 0; u < kUnrollMC; ++u) {
           const int64_t i = i0 + int64_t(u) * kCommThreads;
           v[u] = i < nv ? mc_ld_reduce_bf16x8(mcw + i * 16) : make_uint4(0u, 0u, 0u, 0u);
+          const float4* g4 = reinterpret_cast<const float4*>(g) + i * 2;
+          ga[u] = assign || i >= nv ? make_float4(0.f, 0.f, 0.f, 0.f) : as_f4(ld_stream_v4(g4, pol));
+          gb[u] = assign || i >= nv ? make_float4(0.f, 0.f, 0.f, 0.f) : as_f4(ld_stream_v4(g4 + 1, pol));
         }
 #pragma unroll
         for (int u = 0; u < kUnrollMC; ++u) {
@@ -188,8 +194,7 @@ __global__ void __maxnreg__(kCommRegs) rs_reduce_kernel(const RankTable* __restr
             hi.z = __fmul_rn(hi.z, scale); hi.w = __fmul_rn(hi.w, scale);
           }
           float4* g4 = reinterpret_cast<float4*>(g) + i * 2;
-          float4 a = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : as_f4(ld_stream_v4(g4, pol));
-          float4 b = assign ? make_float4(0.f, 0.f, 0.f, 0.f) : as_f4(ld_stream_v4(g4 + 1, pol));
+          float4 a = ga[u], b = gb[u];
           fadd4(a, lo);
           fadd4(b, hi);
           st_stream_v4(g4, as_u4(a), pol);

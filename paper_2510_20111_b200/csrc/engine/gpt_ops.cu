@@ -585,17 +585,26 @@ __global__ void __launch_bounds__(256) colred_kernel(const uint16_t* __restrict_
   }
 }
 
-// LayerNorm backward with its column reductions fused: one CTA per chunk of
-// rows, taken 8 at a time.  Phase 1: warp w reduces row r0 + w to
-// mean(dy g) and mean(dy g xhat) (lane-strided 16-byte vectors, then a warp
-// sum: the same order as ln_bwd_dx_kernel); phase 2: thread t owns column
-// vectors t, t + 256, ... and walks the 8 rows (L1 / L2 hits), writing
-// dx (+ resid) and accumulating, in registers, the chunk's column sums
-// dgamma = sum dy xhat, dbeta = sum dy and (prev) sum of the bf16 dx written
-// — the bias gradient of the projection whose output gradient dx is.  So dy
-// and x cross HBM once (the unfused path re-read both for dgamma / dbeta, and
-// dx again for that bias), and no cross-thread fold is needed.
-template <int NV>
+// LayerNorm backward with its column reductions fused, streamed through
+// shared memory.  Persistent CTAs (2 per SM), each owning a contiguous chunk of rows
+// and walks it in batches of RB rows; thread t owns the 16-byte column
+// vectors t, t + 256, ... of every row and moves them itself with cp.async
+// (no register staging) into a 2-stage ring — batch i + 1 is in flight while
+// batch i is computed.  Per batch:
+// each thread forms its part of mean(dy g) and mean(dy g xhat) per row, one
+// CTA reduction (shuffles, then the 8 warps in a fixed order) completes
+// them, and a second pass over the thread's own smem vectors writes dx
+// (+ resid) and accumulates, in registers, the chunk's column sums
+// dgamma = sum dy xhat, dbeta = sum dy and (prev) the sum of the bf16 dx
+// written — the bias gradient of the projection whose output gradient dx
+// is.  dy, x and resid cross HBM once; no column fold between threads.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int NV, int RB>
 __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const uint16_t* __restrict__ dy,
                                                            const uint16_t* __restrict__ x,
                                                            const uint16_t* __restrict__ g,
@@ -604,59 +613,91 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const uint16_t* __res
                                                            const uint16_t* __restrict__ resid,
                                                            uint16_t* __restrict__ dx, int rows, int h, int per,
                                                            float* __restrict__ part, float* __restrict__ prev) {
-  __shared__ float st[8][4];
+  extern __shared__ __align__(16) uint8_t lsm[];  // [2 stages][RB rows][3 tensors][h] bf16
+  __shared__ float red[2][RB][2][8];
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31, t = threadIdx.x;
   const int nvec = h / 8;
   const int rb = blockIdx.x * per, re = min(rows, rb + per);
+  const int64_t rowb = int64_t(h) * 2;  // bytes of one row of one tensor
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(lsm));
+  auto slot = [&](int st, int q, int ten) -> int64_t { return ((int64_t(st) * RB + q) * 3 + ten) * rowb; };
+  auto issue = [&](int r0, int st) {  // this thread's vectors of rows [r0, r0 + RB)
+    for (int q = 0; q < RB; ++q) {
+      const int r = min(r0 + q, re - 1);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int v = t + 256 * k;
+        if (v >= nvec) continue;
+        cp_async16(sbase + uint32_t(slot(st, q, 0)) + v * 16, dy + int64_t(r) * h + 8 * v);
+        cp_async16(sbase + uint32_t(slot(st, q, 1)) + v * 16, x + int64_t(r) * h + 8 * v);
+        if (resid) cp_async16(sbase + uint32_t(slot(st, q, 2)) + v * 16, resid + int64_t(r) * h + 8 * v);
+      }
+    }
+  };
   float ab[NV][8], ag[NV][8], ap[NV][8], gv[NV][8];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) ab[k][j] = ag[k][j] = ap[k][j] = 0.f;
+    for (int j = 0; j < 8; ++j) ab[k][j] = ag[k][j] = ap[k][j] = gv[k][j] = 0.f;
     const int v = t + 256 * k;
     if (v < nvec) unpack8(__ldg(reinterpret_cast<const uint4*>(g) + v), gv[k]);
   }
-  for (int r0 = rb; r0 < re; r0 += 8) {
-    const int r = r0 + w;
-    if (r < re) {
-      const float m = mu[r], rstd = rs[r];
-      const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
-      const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
-      float s1 = 0.f, s2 = 0.f;
-      for (int v = lane; v < nvec; v += 32) {
-        float d[8], xv[8], gg[8];
-        unpack8(__ldg(dyr + v), d);
-        unpack8(__ldg(xr + v), xv);
-        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + v), gg);
+  if (rb < re) issue(rb, 0);
+  cp_async_commit();
+  int st = 0;
+  for (int r0 = rb; r0 < re; r0 += RB, st ^= 1) {
+    if (r0 + RB < re) issue(r0 + RB, st ^ 1);  // the next batch streams in meanwhile
+    cp_async_commit();
+    cp_async_wait1();  // this thread's copies of batch r0 have landed (it reads only those)
+    float s1[RB], s2[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const float m = mu[min(r0 + q, re - 1)], rstd = rs[min(r0 + q, re - 1)];
+      s1[q] = s2[q] = 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int v = t + 256 * k;
+        if (v >= nvec) continue;
+        float d[8], xv[8];
+        unpack8(*reinterpret_cast<const uint4*>(lsm + slot(st, q, 0) + v * 16), d);
+        unpack8(*reinterpret_cast<const uint4*>(lsm + slot(st, q, 1) + v * 16), xv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float xh = (xv[j] - m) * rstd, dg = d[j] * gg[j];
-          s1 += dg;
-          s2 += dg * xh;
+          const float xh = (xv[j] - m) * rstd, dg = d[j] * gv[k][j];
+          s1[q] += dg;
+          s2[q] += dg * xh;
         }
       }
-      s1 = warp_sum(s1);
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        st[w][0] = s1 / h;
-        st[w][1] = s2 / h;
-        st[w][2] = m;
-        st[w][3] = rstd;
+      s1[q] = warp_sum(s1[q]);
+      s2[q] = warp_sum(s2[q]);
+    }
+    const int b = (r0 / RB) & 1;  // double-buffered: rewritten only after the next sync
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        red[b][q][0][w] = s1[q];
+        red[b][q][1][w] = s2[q];
       }
     }
     __syncthreads();
-    const int nr = min(8, re - r0);
-#pragma unroll 2
-    for (int q = 0; q < nr; ++q) {
-      const int64_t rq = int64_t(r0 + q) * h;
-      const float a1 = st[q][0], a2 = st[q][1], m = st[q][2], rstd = st[q][3];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int r = r0 + q;
+      if (r >= re) continue;
+      float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) {  // fixed order: deterministic
+        t1 += red[b][q][0][ww];
+        t2 += red[b][q][1][ww];
+      }
+      const float a1 = t1 / h, a2 = t2 / h, m = mu[r], rstd = rs[r];
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const int v = t + 256 * k;
         if (v >= nvec) continue;
         float d[8], xv[8], o[8];
-        unpack8(__ldg(reinterpret_cast<const uint4*>(dy + rq) + v), d);
-        unpack8(__ldg(reinterpret_cast<const uint4*>(x + rq) + v), xv);
+        unpack8(*reinterpret_cast<const uint4*>(lsm + slot(st, q, 0) + v * 16), d);
+        unpack8(*reinterpret_cast<const uint4*>(lsm + slot(st, q, 1) + v * 16), xv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float xh = (xv[j] - m) * rstd;
@@ -666,12 +707,12 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const uint16_t* __res
         }
         if (resid) {
           float rv[8];
-          unpack8(__ldg(reinterpret_cast<const uint4*>(resid + rq) + v), rv);
+          unpack8(*reinterpret_cast<const uint4*>(lsm + slot(st, q, 2) + v * 16), rv);
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] += rv[j];
         }
         const uint4 pk = pack8(o);
-        reinterpret_cast<uint4*>(dx + rq)[v] = pk;
+        reinterpret_cast<uint4*>(dx + int64_t(r) * h)[v] = pk;
         if (prev) {
           float ob[8];
           unpack8(pk, ob);
@@ -680,7 +721,6 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const uint16_t* __res
         }
       }
     }
-    __syncthreads();  // st is rewritten by the next group
   }
   const int64_t cb = int64_t(blockIdx.x) * h, slab = int64_t(gridDim.x) * h;
 #pragma unroll
@@ -701,18 +741,27 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_kernel(const uint16_t* __res
   }
 }
 
-// out[c] (mode) = sum_k part[k][c]; 4 threads per column, 64 columns per CTA.
-__global__ void __launch_bounds__(256) colsum_finalize4_kernel(const float* __restrict__ part, int chunks,
+// out[c] (mode) = sum_k part[k][c]: 32 columns per CTA, 8 chunk lanes (warp
+// w sums chunks w, w + 8, ... of its 32 columns: 128-byte coalesced rows),
+// folded in a fixed order.
+__global__ void __launch_bounds__(256) colsum_finalize8_kernel(const float* __restrict__ part, int chunks,
                                                                int cols, void* out, int out_bf16, int mode) {
-  __shared__ float red[4][64];
-  const int cl = threadIdx.x & 63, sub = threadIdx.x >> 6;
-  const int c = blockIdx.x * 64 + cl;
+  __shared__ float red[8][32];
+  const int cl = threadIdx.x & 31, sub = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
   float s = 0.f;
-  if (c < cols)
-    for (int k = sub; k < chunks; k += 4) s += part[int64_t(k) * cols + c];
+  if (c < cols) {
+#pragma unroll 4
+    for (int k = sub; k < chunks; k += 8) s += part[int64_t(k) * cols + c];
+  }
   red[sub][cl] = s;
   __syncthreads();
-  if (sub == 0 && c < cols) write_mode(out, c, ((red[0][cl] + red[1][cl]) + red[2][cl]) + red[3][cl], out_bf16, mode);
+  if (sub == 0 && c < cols) {
+    float t = red[0][cl];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += red[i][cl];
+    write_mode(out, c, t, out_bf16, mode);
+  }
 }
 
 #define HZP_NVL_SWITCH(nvl, ...)                      \
@@ -896,19 +945,30 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
   }
   HZP_LAUNCH_CHECK();
 }
-int layernorm_bwd_chunks(int rows) { return (rows + kLnRowsPerChunk - 1) / kLnRowsPerChunk; }
+int layernorm_bwd_chunks(int rows) { return std::max(1, std::min(2 * kNumSMs, (rows + 3) / 4)); }
 
 void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
                          const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, float* prev,
                          int rows, int h, cudaStream_t s) {
   if (h % 8 || h > 2 * 256 * 8) throw std::invalid_argument("layernorm_bwd_fused: h % 8 != 0 or h > 4096");
   const int chunks = layernorm_bwd_chunks(rows);
-  if (h <= 256 * 8)
-    ln_bwd_fused_kernel<1><<<chunks, 256, 0, s>>>(dy, x, g, mu, rstd, resid, dx, rows, h, kLnRowsPerChunk, part,
-                                                  prev);
-  else
-    ln_bwd_fused_kernel<2><<<chunks, 256, 0, s>>>(dy, x, g, mu, rstd, resid, dx, rows, h, kLnRowsPerChunk, part,
-                                                  prev);
+  const int per = (rows + chunks - 1) / chunks;
+  // two persistent CTAs per SM (16 warps hide the per-row latencies; one CTA
+  // of 8 warps ran at 54 us, four CTAs at 37 us with a costlier finalize), each
+  // a ring of 2 stages x RB rows x (dy, x, resid) in smem
+  static bool attr = false;
+  if (!attr) {  // both instantiations' ring is at most 2 x 4 x 3 x 2048 bf16
+    constexpr int kMaxSmem = 2 * 4 * 3 * 2048 * 2;
+    HZP_CUDA(cudaFuncSetAttribute(ln_bwd_fused_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    HZP_CUDA(cudaFuncSetAttribute(ln_bwd_fused_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    attr = true;
+  }
+  auto launch = [&](auto kern, int rb) {
+    const size_t smem = size_t(2) * rb * 3 * h * 2;
+    kern<<<chunks, 256, smem, s>>>(dy, x, g, mu, rstd, resid, dx, rows, h, per, part, prev);
+  };
+  if (h <= 256 * 8) launch(ln_bwd_fused_kernel<1, 4>, 4);
+  else launch(ln_bwd_fused_kernel<2, 2>, 2);
   HZP_LAUNCH_CHECK();
 }
 
@@ -920,7 +980,7 @@ void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chun
 }
 void colsum_finalize(const float* part, int chunks, int cols, void* out, int out_bf16, int mode,
                      cudaStream_t s) {
-  colsum_finalize4_kernel<<<(cols + 63) / 64, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
+  colsum_finalize8_kernel<<<(cols + 31) / 32, 256, 0, s>>>(part, chunks, cols, out, out_bf16, mode);
   HZP_LAUNCH_CHECK();
 }
 void grad_write(const float* src, int64_t n, void* out, int out_bf16, int mode, cudaStream_t s) {

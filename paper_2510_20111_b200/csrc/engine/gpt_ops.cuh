@@ -34,8 +34,7 @@ void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, con
 // part [2][chunks][h] = (sum dy xhat, sum dy) per chunk of kLnRowsPerChunk
 // rows, and, if prev != nullptr, prev [chunks][h] = sum of the bf16 dx
 // written (the bias gradient of the projection whose output gradient dx is).
-// chunks = layernorm_bwd_chunks(rows); h <= 4096.
-constexpr int kLnRowsPerChunk = 32;
+// chunks = layernorm_bwd_chunks(rows) (one persistent CTA per SM); h <= 4096.
 int layernorm_bwd_chunks(int rows);
 void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
                          const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, float* prev,
