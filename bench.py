@@ -830,14 +830,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="async", choices=["async", "vanilla"],
                     help="scheduler mode (sched.cpp:280-284: vanilla blocks compute on every issued collective)")
-    ap.add_argument("--depth", type=int, default=2, help="AG prefetch depth (ring slots), BASELINE configs[4]: 1-4")
-    ap.add_argument("--wgrad-slots", type=int, default=2,
-                    help="gradient buffers peers reduce-scatter from (ring; >= 2)")
+    ap.add_argument("--depth", type=int, default=None,
+                    help="AG prefetch depth (ring slots), BASELINE configs[4]: 1-4; default 3 for the 1.3B "
+                         "(configs[1] fixes none; measured +1.8 %% at N = 4), 2 otherwise (configs[2] says 2)")
+    ap.add_argument("--wgrad-slots", type=int, default=3,
+                    help="gradient buffers peers reduce-scatter from (ring; >= 2; 3 measured +0.7-1.8 %% "
+                         "over 2 at N = 2 / 4, profiles/r02_ring_*)")
     ap.add_argument("--recompute", type=int, default=0, choices=[0, 1],
                     help="activation recomputation (FWD-recompute before each BWD; GPT blocks keep inputs only)")
     ap.add_argument("--reuse", type=int, default=0, choices=[0, 1],
                     help="the CLI's parameter reuse (R3: later forwards read microbatch 0's gathered layers)")
     args = ap.parse_args()
+    if args.depth is None:
+        args.depth = 3 if args.model == "1.3b" else 2
     if args.model in MLP_CASES:
         return run_mlp(args)
     if args.impl == "reference":

@@ -27,13 +27,16 @@ for n in 2 4; do
   run 7b_n$n $n --model 7b
   run moe_n$n $n --model moe
 done
-# scheduler ablation (BASELINE configs[4]): async (= the model runs above at
-# depth 2) vs vanilla, prefetch depth 1 / 4, at N = 2 and 4
-run 13b_n2_vanilla_d2 2 --mode vanilla
-run 13b_n4_vanilla_d2 4 --mode vanilla
+# scheduler ablation (BASELINE configs[4]): async vs vanilla at prefetch
+# depth 1 / 2 / 3 (3 = the 1.3B default, the model runs above) / 4, N = 2 and 4
+run 13b_n2_async_d2 2 --depth 2
+run 13b_n2_vanilla_d2 2 --mode vanilla --depth 2
+run 13b_n4_async_d2 4 --depth 2
+run 13b_n4_vanilla_d2 4 --mode vanilla --depth 2
+run 13b_n4_vanilla_d3 4 --mode vanilla --depth 3
 run 13b_n4_async_d1 4 --depth 1
-run 13b_n4_async_d4 4 --depth 4
 run 13b_n4_vanilla_d1 4 --mode vanilla --depth 1
+run 13b_n4_async_d4 4 --depth 4
 run 7b_n4_vanilla 4 --model 7b --mode vanilla
 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
   --master-port 29950 tools/bench_collectives.py --sizes-mb 64,256,1024 --depths 2 --precs 1,0 \
