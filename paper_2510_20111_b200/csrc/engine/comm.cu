@@ -32,6 +32,13 @@ constexpr int kThreads = 128;
 constexpr int kCommThreads = 128;
 constexpr int kCommRegs = 80;
 constexpr int kUnroll = 8;    // AG: 16-byte vectors in flight per thread
+// Z1: one float4 group per thread per pass at 48 registers — ten CTAs (40
+// warps) per SM hide the IEEE div / sqrt chains and the loads better than
+// two groups at 80 registers (six CTAs): 1.3B N = 1 Z1 8.4 -> 7.1 ms (0.91
+// of its HBM roofline), MoE 51.0 -> 43.1 ms; 4 groups at 128 registers was
+// slower still (11.5 ms).
+constexpr int kZ1U = 1;
+constexpr int kZ1Regs = 48;
 constexpr int kUnrollRS = 4;  // RS: per source
 constexpr int kUnrollMC = 4;  // RS through multimem.ld_reduce (+ the fp32 shard's 2 x 16 B each)
 
@@ -300,7 +307,7 @@ __device__ __forceinline__ float adam_one(float g, float& m, float& v, float& w,
 }
 
 template <bool kBf16Param>
-__global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
+__global__ void __maxnreg__(kZ1Regs) z1_adam_kernel(const RankTable* __restrict__ T,
                                                            const CommTile* __restrict__ tiles,
                                                            int ntiles, int z2, int replicas,
                                                            AdamArgs a, int dbg) {
@@ -312,14 +319,14 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
     float* mv = T->var[t.local] + t.a_off;
     float* gd = dbg ? T->z1_grad_dbg[t.local] + t.a_off : nullptr;
     if (t.vec) {
-      // two float4 per thread per pass: all ten 16-byte loads issued before
+      // kZ1U float4 per thread per pass, all its 16-byte loads issued before
       // the (IEEE div / sqrt heavy) Adam math
       const int64_t nv = t.len / 4;
-      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += 2 * kThreads) {
-        float4 g[2], m[2], v[2], w[2];
-        bool ok[2];
+      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += kZ1U * kThreads) {
+        float4 g[kZ1U], m[kZ1U], v[kZ1U], w[kZ1U];
+        bool ok[kZ1U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kZ1U; ++u) {
           const int64_t i = i0 + int64_t(u) * kThreads;
           ok[u] = i < nv;
           if (!ok[u]) continue;
@@ -331,7 +338,7 @@ __global__ void __maxnreg__(80) z1_adam_kernel(const RankTable* __restrict__ T,
           w[u] = as_f4(ld_stream_v4(mw + 4 * i, pol));
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kZ1U; ++u) {
           if (!ok[u]) continue;
           const int64_t i = i0 + int64_t(u) * kThreads;
           if (gd) reinterpret_cast<float4*>(gd)[i] = g[u];
