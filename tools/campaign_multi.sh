@@ -4,6 +4,7 @@
 # ablation (BASELINE configs[4]), the AG / RS sweep, and
 # (MULTI_TESTS=1) the multi-GPU parity tests.  Outputs under gpurun_out/<tag>_*.
 tag=${1:-r02m}
+what=${2:-all}  # all | models (the N = 2 / 4 model lines and the depth-2 / 3 ablation pair only)
 mkdir -p gpurun_out
 run() {  # run <name> <nproc> <bench args...>
   local name=$1 n=$2; shift 2
@@ -34,10 +35,11 @@ run 13b_n2_vanilla_d2 2 --mode vanilla --depth 2
 run 13b_n4_async_d2 4 --depth 2
 run 13b_n4_vanilla_d2 4 --mode vanilla --depth 2
 run 13b_n4_vanilla_d3 4 --mode vanilla --depth 3
+run 7b_n4_vanilla 4 --model 7b --mode vanilla
+[ "$what" = models ] && exit 0
 run 13b_n4_async_d1 4 --depth 1
 run 13b_n4_vanilla_d1 4 --mode vanilla --depth 1
 run 13b_n4_async_d4 4 --depth 4
-run 7b_n4_vanilla 4 --model 7b --mode vanilla
 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
   --master-port 29950 tools/bench_collectives.py --sizes-mb 64,256,1024 --depths 2 --precs 1,0 \
   > gpurun_out/${tag}_sweep_n4.jsonl 2> gpurun_out/${tag}_sweep_n4.err
