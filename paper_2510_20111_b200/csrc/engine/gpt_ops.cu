@@ -419,41 +419,69 @@ __global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
 // ---- LayerNorm / column reductions for h a multiple of 256 -------------------
 // NVL = h / 256: 16-byte vectors per lane, so every array below is sized at
 // compile time and lives in registers.
-template <int NVL>
+// WPR warps per row (h > 2048 uses 2: a warp holding a whole 4096-wide row
+// needed 255 registers, one CTA of 8 warps per SM; at h = 2048 two warps per
+// row measured no faster: 16 us per launch either way), each
+// owning NVL / WPR of the row's 16-byte vectors; the two row sums (mean,
+// then the centred square sum) are combined across the row's warps through
+// shared memory in a fixed order.
+template <int NVL, int WPR = 1>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const uint16_t* __restrict__ x,
                                                      const uint16_t* __restrict__ g,
                                                      const uint16_t* __restrict__ be, uint16_t* __restrict__ y,
                                                      float* __restrict__ mu, float* __restrict__ rs, int rows,
                                                      int h) {
-  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
-  float v[NVL][8];
+  constexpr int kV = NVL / WPR > 0 ? NVL / WPR : 1;
+  __shared__ float red[2][8];
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (8 / WPR) + w / WPR, part = w % WPR;
+  const bool live = r < rows;
+  if (WPR == 1 && !live) return;
+  const int rr = live ? r : rows - 1;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(rr) * h);
+  float v[kV][8];
   float s = 0.f;
 #pragma unroll
-  for (int k = 0; k < NVL; ++k) {
-    unpack8(__ldg(xr + lane + 32 * k), v[k]);
+  for (int k = 0; k < kV; ++k) {
+    unpack8(__ldg(xr + lane + 32 * (part + WPR * k)), v[k]);
 #pragma unroll
     for (int j = 0; j < 8; ++j) s += v[k][j];
   }
-  const float mean = warp_sum(s) / h;
-  float q = 0.f;
+  s = warp_sum(s);
+  if (WPR > 1) {
+    if (lane == 0) red[0][w] = s;
+    __syncthreads();
+    s = 0.f;
 #pragma unroll
-  for (int k = 0; k < NVL; ++k)
+    for (int q = 0; q < WPR; ++q) s += red[0][w - part + q];
+  }
+  const float mean = s / h;
+  float q2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < kV; ++k)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float d = v[k][j] - mean;
-      q += d * d;
+      q2 += d * d;
     }
-  const float rstd = rsqrtf(warp_sum(q) / h + 1e-5f);
-  if (lane == 0) {
+  q2 = warp_sum(q2);
+  if (WPR > 1) {
+    if (lane == 0) red[1][w] = q2;
+    __syncthreads();
+    q2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < WPR; ++q) q2 += red[1][w - part + q];
+    if (!live) return;
+  }
+  const float rstd = rsqrtf(q2 / h + 1e-5f);
+  if (lane == 0 && part == 0) {
     mu[r] = mean;
     rs[r] = rstd;
   }
   uint4* yr = reinterpret_cast<uint4*>(y + int64_t(r) * h);
 #pragma unroll
-  for (int k = 0; k < NVL; ++k) {
-    const int i = lane + 32 * k;
+  for (int k = 0; k < kV; ++k) {
+    const int i = lane + 32 * (part + WPR * k);
     float gg[8], bb[8], o[8];
     unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i), gg);
     unpack8(__ldg(reinterpret_cast<const uint4*>(be) + i), bb);
@@ -904,7 +932,11 @@ void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, u
   if (h % 8) throw std::invalid_argument("layernorm: h % 8 != 0");
   bool handled = h % 256 == 0;
   if (handled) {
-    HZP_NVL_SWITCH(h / 256, (ln_fwd_kernel<NVL><<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h)));
+    if (h / 256 > 8) {  // two warps per row beyond h = 2048 (255 registers with one)
+      HZP_NVL_SWITCH(h / 256, (ln_fwd_kernel<NVL, 2><<<(rows + 3) / 4, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h)));
+    } else {
+      HZP_NVL_SWITCH(h / 256, (ln_fwd_kernel<NVL><<<(rows + 7) / 8, 256, 0, s>>>(x, g, beta, y, mu, rstd, rows, h)));
+    }
   }
   if (!handled) {
     if (h > 32 * 8 * kWV) throw std::invalid_argument("layernorm: h > 4096 must be 256 x {12, 16}");
