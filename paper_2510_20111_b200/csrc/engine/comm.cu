@@ -32,13 +32,13 @@ constexpr int kThreads = 128;
 constexpr int kCommThreads = 128;
 constexpr int kCommRegs = 80;
 constexpr int kUnroll = 8;    // AG: 16-byte vectors in flight per thread
-// Z1: one float4 group per thread per pass at 48 registers — ten CTAs (40
-// warps) per SM hide the IEEE div / sqrt chains and the loads better than
-// two groups at 80 registers (six CTAs): 1.3B N = 1 Z1 8.4 -> 7.1 ms (0.91
-// of its HBM roofline), MoE 51.0 -> 43.1 ms; 4 groups at 128 registers was
-// slower still (11.5 ms).
+// Z1: one float4 group per thread per pass at 40 registers — twelve CTAs
+// (48 warps) per SM hide the IEEE div / sqrt chains and the loads better
+// than two groups at 80 registers (six CTAs): 1.3B N = 1 Z1 8.4 -> 6.8 ms
+// (0.95 of its HBM roofline), MoE 51.0 -> 40.9 ms (48 registers: 7.1 / 43.1;
+// 32 spills; 4 groups at 128 registers: 11.5 ms).
 constexpr int kZ1U = 1;
-constexpr int kZ1Regs = 48;
+constexpr int kZ1Regs = 40;
 constexpr int kUnrollRS = 4;  // RS: per source
 constexpr int kUnrollMC = 4;  // RS through multimem.ld_reduce (+ the fp32 shard's 2 x 16 B each)
 
