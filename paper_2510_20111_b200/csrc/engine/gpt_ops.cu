@@ -117,76 +117,6 @@ __global__ void __launch_bounds__(kT) embed_wpe_grad_kernel(const uint16_t* __re
 }
 
 
-__global__ void __launch_bounds__(kT) layernorm_bwd_kernel(
-    const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
-    const float* __restrict__ mu, const float* __restrict__ rs, const uint16_t* __restrict__ resid,
-    uint16_t* __restrict__ dx, float* __restrict__ part, int chunks, int rows, int h) {
-  __shared__ float red[32];
-  const int nv = h / 8;
-  const int per = (rows + chunks - 1) / chunks;
-  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
-  float pg[kMaxVec][8], pb[kMaxVec][8], gg[kMaxVec][8];
-#pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = threadIdx.x + k * kT;
-    for (int j = 0; j < 8; ++j) pg[k][j] = pb[k][j] = 0.f;
-    if (i < nv) unpack8(reinterpret_cast<const uint4*>(g)[i], gg[k]);
-  }
-  for (int r = r0; r < r1; ++r) {
-    const float m = mu[r], rstd = rs[r];
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
-    const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
-    float xh[kMaxVec][8], dg[kMaxVec][8];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int i = threadIdx.x + k * kT;
-      if (i < nv) {
-        float d[8];
-        unpack8(dyr[i], d);
-        unpack8(xr[i], xh[k]);
-        for (int j = 0; j < 8; ++j) {
-          xh[k][j] = (xh[k][j] - m) * rstd;
-          dg[k][j] = d[j] * gg[k][j];
-          s1 += dg[k][j];
-          s2 += dg[k][j] * xh[k][j];
-          pg[k][j] += d[j] * xh[k][j];
-          pb[k][j] += d[j];
-        }
-      }
-    }
-    const float a1 = block_sum(s1, red) / h;
-    const float a2 = block_sum(s2, red) / h;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
-    const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + int64_t(r) * h) : nullptr;
-#pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int i = threadIdx.x + k * kT;
-      if (i < nv) {
-        float o[8], rv[8];
-        if (rr) unpack8(rr[i], rv);
-        for (int j = 0; j < 8; ++j) {
-          o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
-          if (rr) o[j] += rv[j];
-        }
-        dxr[i] = pack8(o);
-      }
-    }
-  }
-  float* pgo = part + int64_t(blockIdx.x) * h;
-  float* pbo = part + int64_t(chunks + blockIdx.x) * h;
-#pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = threadIdx.x + k * kT;
-    if (i < nv)
-      for (int j = 0; j < 8; ++j) {
-        pgo[8 * i + j] = pg[k][j];
-        pbo[8 * i + j] = pb[k][j];
-      }
-  }
-}
-
-
 __device__ __forceinline__ void write_mode(void* out, int64_t i, float v, int out_bf16, int mode) {
   if (out_bf16) {
     static_cast<uint16_t*>(out)[i] = f32_to_bf16_bits(v);
@@ -339,82 +269,6 @@ __global__ void __launch_bounds__(256) layernorm_fwd_warp_kernel(
   }
 }
 
-// dg / dbeta partial column sums: each warp accumulates its rows into a
-// private smem slab (plain read-modify-write, no atomics), reduced across the
-// 8 warps once per CTA into part[2][gridDim.x][h].
-constexpr int kWVB = 8;  // h <= 2048
-
-__global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
-    const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
-    const float* __restrict__ mu, const float* __restrict__ rs, const uint16_t* __restrict__ resid,
-    uint16_t* __restrict__ dx, float* __restrict__ part, int rows, int h) {
-  extern __shared__ float acc[];  // [8 warps][2][h]
-  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
-  const int nv = h / 8;
-  float* ag = acc + size_t(w) * 2 * h;
-  float* ab = ag + h;
-  for (int i = lane; i < 2 * h; i += 32) ag[i] = 0.f;
-  __syncwarp();
-  float gg[kWVB][8];
-#pragma unroll
-  for (int k = 0; k < kWVB; ++k)
-    if (lane + 32 * k < nv) unpack8(reinterpret_cast<const uint4*>(g)[lane + 32 * k], gg[k]);
-  for (int r = blockIdx.x * 8 + w; r < rows; r += gridDim.x * 8) {
-    const float m = mu[r], rstd = rs[r];
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(r) * h);
-    const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(r) * h);
-    float xh[kWVB][8], dg[kWVB][8];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < kWVB; ++k) {
-      const int i = lane + 32 * k;
-      if (i < nv) {
-        float d[8];
-        unpack8(dyr[i], d);
-        unpack8(xr[i], xh[k]);
-        float4* pg = reinterpret_cast<float4*>(ag + 8 * i);
-        float4* pb = reinterpret_cast<float4*>(ab + 8 * i);
-        float4 g0 = pg[0], g1 = pg[1], b0 = pb[0], b1 = pb[1];
-        for (int j = 0; j < 8; ++j) {
-          xh[k][j] = (xh[k][j] - m) * rstd;
-          dg[k][j] = d[j] * gg[k][j];
-          s1 += dg[k][j];
-          s2 += dg[k][j] * xh[k][j];
-        }
-        g0.x += d[0] * xh[k][0]; g0.y += d[1] * xh[k][1]; g0.z += d[2] * xh[k][2]; g0.w += d[3] * xh[k][3];
-        g1.x += d[4] * xh[k][4]; g1.y += d[5] * xh[k][5]; g1.z += d[6] * xh[k][6]; g1.w += d[7] * xh[k][7];
-        b0.x += d[0]; b0.y += d[1]; b0.z += d[2]; b0.w += d[3];
-        b1.x += d[4]; b1.y += d[5]; b1.z += d[6]; b1.w += d[7];
-        pg[0] = g0; pg[1] = g1; pb[0] = b0; pb[1] = b1;
-      }
-    }
-    const float a1 = warp_sum(s1) / h, a2 = warp_sum(s2) / h;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
-    const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + int64_t(r) * h) : nullptr;
-#pragma unroll
-    for (int k = 0; k < kWVB; ++k) {
-      const int i = lane + 32 * k;
-      if (i < nv) {
-        float o[8], rv[8];
-        if (rr) unpack8(rr[i], rv);
-        for (int j = 0; j < 8; ++j) {
-          o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
-          if (rr) o[j] += rv[j];
-        }
-        dxr[i] = pack8(o);
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) {
-    float t = 0.f;
-    for (int ww = 0; ww < 8; ++ww) t += acc[size_t(ww) * 2 * h + i];
-    if (i < h) part[int64_t(blockIdx.x) * h + i] = t;
-    else part[int64_t(gridDim.x + blockIdx.x) * h + (i - h)] = t;
-  }
-}
-
-
 
 // ---- LayerNorm / column reductions for h a multiple of 256 -------------------
 // NVL = h / 256: 16-byte vectors per lane, so every array below is sized at
@@ -491,125 +345,36 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const uint16_t* __restrict_
   }
 }
 
-// dx = rstd (dy g - mean(dy g) - xhat mean(dy g xhat)) (+ resid); warp per row.
-// WPR warps per row (h = 4096 uses 2: one warp holding 16 x 2 x 8 floats of a
-// row would spill), each owning NVL / WPR of the row's 16-byte vectors; the
-// two row sums are combined across the row's warps through shared memory.
-template <int NVL, int WPR = 1>
-__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const uint16_t* __restrict__ dy,
-                                                        const uint16_t* __restrict__ x,
-                                                        const uint16_t* __restrict__ g,
-                                                        const float* __restrict__ mu, const float* __restrict__ rs,
-                                                        const uint16_t* __restrict__ resid,
-                                                        uint16_t* __restrict__ dx, int rows, int h) {
-  constexpr int kV = NVL / WPR > 0 ? NVL / WPR : 1;  // vectors per lane (dispatched with WPR | NVL)
-  __shared__ float red[8][2];
-  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (8 / WPR) + w / WPR, part = w % WPR;
-  const bool live = r < rows;
-  if (WPR == 1 && !live) return;
-  const int rr = live ? r : rows - 1;
-  const float m = mu[rr], rstd = rs[rr];
-  const uint4* dyr = reinterpret_cast<const uint4*>(dy + int64_t(rr) * h);
-  const uint4* xr = reinterpret_cast<const uint4*>(x + int64_t(rr) * h);
-  float xh[kV][8], dg[kV][8];
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < kV; ++k) {
-    const int i = lane + 32 * (part + WPR * k);
-    float d[8], gg[8];
-    unpack8(__ldg(dyr + i), d);
-    unpack8(__ldg(xr + i), xh[k]);
-    unpack8(__ldg(reinterpret_cast<const uint4*>(g) + i), gg);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      xh[k][j] = (xh[k][j] - m) * rstd;
-      dg[k][j] = d[j] * gg[j];
-      s1 += dg[k][j];
-      s2 += dg[k][j] * xh[k][j];
-    }
-  }
-  float t1 = warp_sum(s1), t2 = warp_sum(s2);
-  if (WPR > 1) {
-    if (lane == 0) {
-      red[w][0] = t1;
-      red[w][1] = t2;
-    }
-    __syncthreads();
-    t1 = t2 = 0.f;
-#pragma unroll
-    for (int q = 0; q < WPR; ++q) {  // fixed order: deterministic
-      t1 += red[w - part + q][0];
-      t2 += red[w - part + q][1];
-    }
-    if (!live) return;
-  }
-  const float a1 = t1 / h, a2 = t2 / h;
-  uint4* dxr = reinterpret_cast<uint4*>(dx + int64_t(r) * h);
-#pragma unroll
-  for (int k = 0; k < kV; ++k) {
-    const int i = lane + 32 * (part + WPR * k);
-    float o[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = rstd * (dg[k][j] - a1 - xh[k][j] * a2);
-    if (resid) {
-      float rv[8];
-      unpack8(__ldg(reinterpret_cast<const uint4*>(resid + int64_t(r) * h) + i), rv);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] += rv[j];
-    }
-    dxr[i] = pack8(o);
-  }
-}
-
 // Column partial sums over a chunk of rows: part[chunk][c] = sum_r d[r][c]
-// and, with LN, part2[chunk][c] = sum_r d[r][c] * xhat[r][c] (dgamma; part
-// then holds dbeta).  CTA = 8 warps x 256 columns (8 per lane), the warps
-// interleaving the chunk's rows; registers, then one smem fold.
-template <bool LN>
-__global__ void __launch_bounds__(256) colred_kernel(const uint16_t* __restrict__ d,
-                                                     const uint16_t* __restrict__ x,
-                                                     const float* __restrict__ mu, const float* __restrict__ rs,
-                                                     int rows, int cols, float* __restrict__ part,
-                                                     float* __restrict__ part2, int chunks) {
-  __shared__ float red[LN ? 2 : 1][8][257];
+// (the bias gradients of b_qkv / b_fc1 / the MoE experts).  CTA = 8 warps x
+// 256 columns (8 per lane), the warps interleaving the chunk's rows;
+// registers, then one smem fold.
+__global__ void __launch_bounds__(256) colred_kernel(const uint16_t* __restrict__ d, int rows, int cols,
+                                                     float* __restrict__ part, int chunks) {
+  __shared__ float red[8][257];
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
   const int c0 = blockIdx.x * 256 + lane * 8;
   const int per = (rows + chunks - 1) / chunks;
   const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
-  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (c0 < cols) {
 #pragma unroll 2
     for (int r = r0 + w; r < r1; r += 8) {
       float f[8];
       unpack8(__ldg(reinterpret_cast<const uint4*>(d + int64_t(r) * cols + c0)), f);
-      if (LN) {
-        float xv[8];
-        unpack8(__ldg(reinterpret_cast<const uint4*>(x + int64_t(r) * cols + c0)), xv);
-        const float m = mu[r], rstd = rs[r];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) b[j] += f[j] * ((xv[j] - m) * rstd);
-      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[j] += f[j];
     }
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    red[0][w][lane * 8 + j] = a[j];
-    if (LN) red[LN ? 1 : 0][w][lane * 8 + j] = b[j];
-  }
+  for (int j = 0; j < 8; ++j) red[w][lane * 8 + j] = a[j];
   __syncthreads();
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c < cols) {
-    float t = 0.f, u = 0.f;
+    float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      t += red[0][i][threadIdx.x];
-      if (LN) u += red[LN ? 1 : 0][i][threadIdx.x];
-    }
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
     part[int64_t(blockIdx.y) * cols + c] = t;
-    if (LN) part2[int64_t(blockIdx.y) * cols + c] = u;
   }
 }
 
@@ -944,39 +709,6 @@ void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, u
   }
   HZP_LAUNCH_CHECK();
 }
-void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
-                   const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
-                   int rows, int h, cudaStream_t s) {
-  bool handled = h % 256 == 0;
-  if (handled) {  // dx pass (warp per row) + column pass for dgamma / dbeta
-    if (h / 256 > 8) {  // two warps per row beyond h = 2048 (no spills)
-      HZP_NVL_SWITCH(h / 256, (ln_bwd_dx_kernel<NVL, 2><<<(rows + 3) / 4, 256, 0, s>>>(dy, x, g, mu, rstd, resid,
-                                                                                         dx, rows, h)));
-    } else {
-      HZP_NVL_SWITCH(h / 256, (ln_bwd_dx_kernel<(NVL > 8 ? 8 : NVL)><<<(rows + 7) / 8, 256, 0, s>>>(
-                                   dy, x, g, mu, rstd, resid, dx, rows, h)));
-    }
-  }
-  if (handled) {
-    HZP_LAUNCH_CHECK();
-    colred_kernel<true><<<dim3(h / 256, chunks), 256, 0, s>>>(dy, x, mu, rstd, rows, h,
-                                                              part + int64_t(chunks) * h, part, chunks);
-    HZP_LAUNCH_CHECK();
-    return;
-  }
-  if (h <= 32 * 8 * kWVB) {
-    const size_t smem = size_t(16) * h * sizeof(float);  // 8 warps x (dg, dbeta)
-    static bool attr = false;
-    if (!attr) {
-      HZP_CUDA(cudaFuncSetAttribute(layernorm_bwd_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
-      attr = true;
-    }
-    layernorm_bwd_warp_kernel<<<chunks, 256, smem, s>>>(dy, x, g, mu, rstd, resid, dx, part, rows, h);
-  } else {
-    layernorm_bwd_kernel<<<chunks, kT, 0, s>>>(dy, x, g, mu, rstd, resid, dx, part, chunks, rows, h);
-  }
-  HZP_LAUNCH_CHECK();
-}
 int layernorm_bwd_chunks(int rows) { return std::max(1, std::min(2 * kNumSMs, (rows + 3) / 4)); }
 
 void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
@@ -1006,8 +738,7 @@ void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* 
 
 void colsum_partial(const uint16_t* d, int rows, int cols, float* part, int chunks, cudaStream_t s) {
   if (cols % 8) throw std::invalid_argument("colsum: cols % 8 != 0");
-  colred_kernel<false><<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(d, nullptr, nullptr, nullptr, rows, cols,
-                                                                        part, nullptr, chunks);
+  colred_kernel<<<dim3((cols + 255) / 256, chunks), 256, 0, s>>>(d, rows, cols, part, chunks);
   HZP_LAUNCH_CHECK();
 }
 void colsum_finalize(const float* part, int chunks, int cols, void* out, int out_bf16, int mode,

@@ -24,17 +24,12 @@ void embed_bwd(const int* tokens, const uint16_t* dx, float* dwte, float* dwpe, 
 // LayerNorm over h (eps 1e-5): y = (x - mu) * rstd * g + beta; saves mu, rstd.
 void layernorm_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* beta, uint16_t* y,
                    float* mu, float* rstd, int rows, int h, cudaStream_t s);
-// dx = resid + rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)); per-chunk
-// partial column sums of dy*xhat (dg) and dy (dbeta) into part[2][chunks][h].
-void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
-                   const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, int chunks,
-                   int rows, int h, cudaStream_t s);
-
-// Same dx, with the column reductions fused into the one pass over dy / x:
-// part [2][chunks][h] = (sum dy xhat, sum dy) per chunk of kLnRowsPerChunk
-// rows, and, if prev != nullptr, prev [chunks][h] = sum of the bf16 dx
-// written (the bias gradient of the projection whose output gradient dx is).
-// chunks = layernorm_bwd_chunks(rows) (one persistent CTA per SM); h <= 4096.
+// LayerNorm backward: dx = resid + rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)),
+// with the column reductions fused into the one pass over dy / x:
+// part [2][chunks][h] = (sum dy xhat, sum dy) per chunk of rows, and, if
+// prev != nullptr, prev [chunks][h] = sum of the bf16 dx written (the bias
+// gradient of the projection whose output gradient dx is).
+// chunks = layernorm_bwd_chunks(rows) (two persistent CTAs per SM); h <= 4096.
 int layernorm_bwd_chunks(int rows);
 void layernorm_bwd_fused(const uint16_t* dy, const uint16_t* x, const uint16_t* g, const float* mu,
                          const float* rstd, const uint16_t* resid, uint16_t* dx, float* part, float* prev,
