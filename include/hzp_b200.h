@@ -398,9 +398,10 @@ int hzp_gemm_bf16_ex(const void* A, const void* B, void* C, int M, int N, int K,
  * O [b,S,h], lse [b*nh,S] fp32; backward from dO [b,S,h] and
  * workspace D [2,b*nh,S] fp32 (filled here with -rowsum(dO*O)/sqrt(128) and
  * -lse*log2(e), the backward's per-query vectors) writes dQ, dK, dV into
- * dqkv [b,S,3h].  dsT = NULL (production): dQ by a query-tile pass that
- * recomputes P / dS in TMEM; dsT = a [b*nh,S,S] bf16 buffer: the legacy path
- * (dS^T through HBM, dQ as one causal GEMM), kept for A/B measurement. */
+ * dqkv [b,S,3h].  dsT = a [b*nh,S,S] bf16 buffer: dS^T leaves the backward
+ * kernel by TMA stores and dQ is one causal GEMM over it (what the GPT step
+ * uses: 0.28 ms at b 4, 16 heads, S 2048); dsT = NULL: dQ by a query-tile
+ * pass that recomputes P / dS in TMEM, no S^2 buffer (0.34 ms). */
 int hzp_attention_fwd(const void* qkv, void* O, float* lse, int b, int nh, int S, int h, void* stream);
 int hzp_attention_bwd(const void* qkv, const void* O, const void* dO, const float* lse, float* D,
                       void* dqkv, void* dsT, int b, int nh, int S, int h, void* stream);
